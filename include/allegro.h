@@ -1,0 +1,157 @@
+/*
+ * allegro.h -- C ABI of the B200-native Allegro-Legato NNQMD hot path.
+ *
+ * One MD step of the paper's method: the energy and analytic forces of a
+ * strictly local E(3)-equivariant Allegro model, then a velocity-Verlet update.
+ *
+ *   Eq. 1 (§2.1):  m_i d^2 r_i / dt^2 = f_i = -dE/dr_i
+ *   Allegro (§2.1): E = sum of pairwise embedding energies
+ *       E_ij within a finite cutoff, equivariant to E(3), tensors up to rank l
+ *       and tensor products of irreps.  The concrete model is the reading
+ *       written out in SURVEY.md §8(c) E1-E9.
+ *   NVE integration at dt = 2 fs (§3.2); velocity Verlet as
+ *       SPEC.md:77.
+ *   5-sigma force outliers (Fig. 1 caption).
+ *   Neighbour lists by linked-list cells (§2.4), here on device.
+ *
+ * Conventions (all calls):
+ *   - Every call returns int status: 0 = ALLEGRO_OK, < 0 = an ALLEGRO_E_* code.
+ *     No C++ exception crosses the ABI.  allegro_last_error() gives a message.
+ *   - Units: positions A, velocities A/fs, time fs, energies eV, forces eV/A,
+ *     masses amu (H 1.008, N 14.007).  Species: 0 = H, 1 = N.
+ *   - Arrays are caller-owned.  `where` selects host (ALLEGRO_HOST) or device
+ *     (ALLEGRO_DEVICE, CUDA global memory on the ctx's device) pointers for the
+ *     per-atom arrays of allegro_compute_energy_forces; device pointers are used
+ *     with zero copy.  No pointer is retained after a call returns.
+ *   - Layouts: pos / forces / vel are row-major [n][3] float64; gid, species
+ *     are int32 [n]; e_atom is float64 [n].
+ *   - Positions outside the box are wrapped into [0, L), not
+ *     rejected.  Non-finite inputs -> ALLEGRO_E_ARG; species outside {0,1} ->
+ *     ALLEGRO_E_ARG; a non-finite result -> ALLEGRO_E_NONFINITE (never masked,
+ *     SPEC.md:78).
+ *   - Determinism: results are bit-identical across repeated runs at a fixed
+ *     world size and precision (fixed-order reductions, no float atomics).
+ *   - Threading: one ctx per rank; calls on a ctx are not thread-safe.  With
+ *     world_size > 1 every call that takes a ctx is collective.
+ */
+#ifndef ALLEGRO_B200_H
+#define ALLEGRO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct allegro_ctx allegro_ctx; /* opaque; owns all device work buffers */
+
+enum {
+  ALLEGRO_OK = 0,
+  ALLEGRO_E_ARG = -1,       /* bad argument (NULL, size, non-finite input, species) */
+  ALLEGRO_E_GEOMETRY = -2,  /* domain smaller than r_c + skin with world_size > 1 */
+  ALLEGRO_E_NONFINITE = -3, /* a non-finite energy / force / velocity was produced */
+  ALLEGRO_E_WEIGHTS = -4,   /* weight file unreadable or inconsistent with its header */
+  ALLEGRO_E_CUDA = -5,      /* CUDA runtime error */
+  ALLEGRO_E_NCCL = -6,      /* NCCL error */
+  ALLEGRO_E_OOM = -7,       /* device allocation failed */
+  ALLEGRO_E_STATE = -8      /* call out of order (e.g. md_step before md_set_state) */
+};
+
+enum { ALLEGRO_HOST = 0, ALLEGRO_DEVICE = 1 };
+
+/* Arithmetic of the per-edge MLP contractions (the only dense GEMMs).
+ * FP32: CUDA-core fp32 FMA (the parity mode of this build). */
+enum {
+  ALLEGRO_PREC_FP32 = 0,
+  ALLEGRO_PREC_3XTF32 = 1,
+  ALLEGRO_PREC_BF16X3 = 2,
+  ALLEGRO_PREC_TF32 = 3,
+  ALLEGRO_PREC_BF16 = 4
+};
+
+typedef struct {
+  const char* weights_path; /* weight file (synth/weights.py layout): header L, lmax, C, D,
+                               widths, n_basis, n_species, p, r_max, nbar, sigma_Z, mu_Z */
+  double r_cut;             /* A; must equal the file's r_max (else ALLEGRO_E_WEIGHTS); <= 0: take the file's */
+  double skin;              /* A; 0 = rebuild the neighbour list every step (the paper: P:246) */
+  double box[3];            /* orthorhombic periodic box edges, A */
+  int64_t n_atoms_global;   /* atoms in the whole box */
+  int device;               /* CUDA ordinal for this rank */
+  int rank, world_size;     /* 1 GPU: 0, 1 */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId broadcast by the caller; NULL if world_size == 1 */
+  int grid[3];              /* domain grid px,py,pz (product == world_size); {0,0,0} = auto */
+  int precision;            /* ALLEGRO_PREC_* */
+  void* cuda_stream;        /* cudaStream_t to run on (e.g. torch's current stream); NULL = ctx-owned stream */
+} allegro_params;
+
+/* Create a ctx: reads and validates the weight file (tensor shapes and the parameter
+ * count are re-derived from the irreps rules; Table 2), uploads fp32
+ * weights, and sizes buffers.  Collective over ranks.  On failure *out is NULL and
+ * allegro_last_error(NULL) describes the error (thread-local). */
+int allegro_create(const allegro_params* p, allegro_ctx** out);
+void allegro_destroy(allegro_ctx* ctx);
+const char* allegro_last_error(const allegro_ctx* ctx);
+
+/* One force evaluation (Eq. 1).
+ *   n        owned atoms passed by this rank (world_size 1: all atoms)
+ *   where    ALLEGRO_HOST or ALLEGRO_DEVICE for gid/species/pos/e_atom/forces
+ *   gid      [n] global ids (NULL: 0..n-1); identify atoms in the canonical row order
+ *   species  [n] 0 = H, 1 = N
+ *   pos      [n][3] A (wrapped internally)
+ *   box      [3] A, or NULL = the box given at create
+ *   e_total  out, host double, eV (all ranks)
+ *   e_atom   out [n] eV, or NULL
+ *   forces   out [n][3] eV/A
+ * Returns ALLEGRO_E_NONFINITE if any output is non-finite. */
+int allegro_compute_energy_forces(allegro_ctx* ctx, int64_t n, int where, const int32_t* gid,
+                                  const int32_t* species, const double* pos, const double* box,
+                                  double* e_total, double* e_atom, double* forces);
+
+/* MD state lives on the device inside ctx.  set/get take GLOBAL host arrays
+ * [n_global] (species, pos [n][3] A, vel [n][3] A/fs); set computes the initial forces. */
+int md_set_state(allegro_ctx* ctx, int64_t n_global, const int32_t* species, const double* pos,
+                 const double* vel);
+int md_get_state(allegro_ctx* ctx, int64_t n_global, double* pos, double* vel, double* forces);
+
+typedef struct {
+  int64_t steps_done;
+  double e_pot, e_kin, e_total, temperature; /* eV, eV, eV, K after the last step */
+  int64_t n_outliers_last;                   /* outliers of the last step vs the step-0 baseline */
+  int64_t n_edges, n_rebuilds;
+} md_report;
+
+/* n_steps of velocity Verlet at dt (fs): exactly one
+ * force evaluation per step, forces cached.  Stops at the first non-finite value and
+ * returns ALLEGRO_E_NONFINITE with steps_done set.  out may be NULL. */
+int md_step(allegro_ctx* ctx, int64_t n_steps, double dt_fs, md_report* out);
+
+/* Count atoms with |F_a| > mean + k*sigma (strict) for the current
+ * forces.  Collective. */
+int md_count_outliers(allegro_ctx* ctx, double mean, double sigma, double k, int64_t* count);
+/* mean and population std of |F_a| over all atoms for the current forces */
+int md_force_baseline(allegro_ctx* ctx, double* mean, double* sigma);
+
+/* Test hook: the current edge list (of the last force evaluation) as (i_gid, j_gid, shift),
+ * in the canonical row order (row by centre, within a row by (j_gid, nx, ny, nz)).
+ * capacity: entries available in the output arrays; *n_edges receives the count
+ * (ALLEGRO_E_ARG if capacity is too small; outputs may be NULL to query the count). */
+int allegro_get_edges(allegro_ctx* ctx, int64_t capacity, int64_t* n_edges, int32_t* i_gid,
+                      int32_t* j_gid, int8_t* shift);
+
+/* Test hook: per-edge dE/dr_e [E][3] (fp32 widened to double) of the last evaluation,
+ * in the edge order of allegro_get_edges. */
+int allegro_get_edge_grad(allegro_ctx* ctx, int64_t capacity, double* g);
+
+/* Host-only helpers (no GPU needed): this library's own derivations. */
+/* real W3j^{l1 l2 l3} table (l <= 2) into out[(2l1+1)(2l2+1)(2l3+1)] */
+int allegro_w3j_table(int l1, int l2, int l3, double* out);
+/* parameter count of the (n_layers, lmax) model with C=32, D=128 (Table 2) */
+int64_t allegro_param_count(int n_layers, int lmax);
+/* per-layer (#paths, #scalar paths) of (n_layers, lmax): out[2*k], out[2*k+1] */
+int allegro_layer_paths(int n_layers, int lmax, int* out);
+const char* allegro_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ALLEGRO_B200_H */

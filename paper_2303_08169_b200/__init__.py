@@ -1,0 +1,243 @@
+"""B200-native Allegro-Legato NNQMD hot path: a thin ctypes binding of include/allegro.h.
+
+Argument marshalling only -- every step of the method (neighbour build, model,
+forces, Verlet, outliers) runs in the CUDA kernels of ``libpaper_allegro.so``.
+Importing this package requires the in-tree library; there is no CPU fallback.
+
+Names follow the C ABI: ``allegro_create`` -> ``Allegro(...)``,
+``allegro_compute_energy_forces`` -> ``Allegro.compute_energy_forces``,
+``md_set_state`` / ``md_step`` / ``md_get_state`` / ``md_count_outliers`` /
+``md_force_baseline`` -> methods of the same names.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libpaper_allegro.so")
+
+OK = 0
+E_ARG, E_GEOMETRY, E_NONFINITE, E_WEIGHTS, E_CUDA, E_NCCL, E_OOM, E_STATE = -1, -2, -3, -4, -5, -6, -7, -8
+HOST, DEVICE = 0, 1
+PREC_FP32, PREC_3XTF32, PREC_BF16X3, PREC_TF32, PREC_BF16 = 0, 1, 2, 3, 4
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_2303_08169_b200.build` "
+        "(there is no CPU fallback for the CUDA path)"
+    )
+_lib = C.CDLL(LIB_PATH)
+
+
+class AllegroParams(C.Structure):
+    _fields_ = [
+        ("weights_path", C.c_char_p),
+        ("r_cut", C.c_double),
+        ("skin", C.c_double),
+        ("box", C.c_double * 3),
+        ("n_atoms_global", C.c_int64),
+        ("device", C.c_int),
+        ("rank", C.c_int),
+        ("world_size", C.c_int),
+        ("nccl_unique_id", C.c_void_p),
+        ("grid", C.c_int * 3),
+        ("precision", C.c_int),
+        ("cuda_stream", C.c_void_p),
+    ]
+
+
+class MdReport(C.Structure):
+    _fields_ = [
+        ("steps_done", C.c_int64),
+        ("e_pot", C.c_double),
+        ("e_kin", C.c_double),
+        ("e_total", C.c_double),
+        ("temperature", C.c_double),
+        ("n_outliers_last", C.c_int64),
+        ("n_edges", C.c_int64),
+        ("n_rebuilds", C.c_int64),
+    ]
+
+
+_P = C.c_void_p
+_lib.allegro_create.argtypes = [C.POINTER(AllegroParams), C.POINTER(_P)]
+_lib.allegro_destroy.argtypes = [_P]
+_lib.allegro_destroy.restype = None
+_lib.allegro_last_error.argtypes = [_P]
+_lib.allegro_last_error.restype = C.c_char_p
+_lib.allegro_compute_energy_forces.argtypes = [_P, C.c_int64, C.c_int, _P, _P, _P, _P, _P, _P, _P]
+_lib.md_set_state.argtypes = [_P, C.c_int64, _P, _P, _P]
+_lib.md_get_state.argtypes = [_P, C.c_int64, _P, _P, _P]
+_lib.md_step.argtypes = [_P, C.c_int64, C.c_double, C.POINTER(MdReport)]
+_lib.md_count_outliers.argtypes = [_P, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_int64)]
+_lib.md_force_baseline.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+_lib.allegro_get_edges.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), _P, _P, _P]
+_lib.allegro_get_edge_grad.argtypes = [_P, C.c_int64, _P]
+_lib.allegro_w3j_table.argtypes = [C.c_int, C.c_int, C.c_int, _P]
+_lib.allegro_param_count.argtypes = [C.c_int, C.c_int]
+_lib.allegro_param_count.restype = C.c_int64
+_lib.allegro_layer_paths.argtypes = [C.c_int, C.c_int, _P]
+_lib.allegro_version.restype = C.c_char_p
+
+EXPORTED = [
+    "allegro_create", "allegro_destroy", "allegro_last_error", "allegro_compute_energy_forces",
+    "md_set_state", "md_get_state", "md_step", "md_count_outliers", "md_force_baseline",
+    "allegro_get_edges", "allegro_get_edge_grad", "allegro_w3j_table", "allegro_param_count",
+    "allegro_layer_paths", "allegro_version",
+]
+
+
+class AllegroError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def _ptr(a) -> int | None:
+    """Raw pointer of a numpy array or a torch tensor (host or device)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()  # torch.Tensor
+
+
+def w3j_table(l1: int, l2: int, l3: int) -> np.ndarray:
+    out = np.zeros((2 * l1 + 1) * (2 * l2 + 1) * (2 * l3 + 1))
+    rc = _lib.allegro_w3j_table(l1, l2, l3, out.ctypes.data)
+    if rc != OK:
+        raise AllegroError(rc, "bad (l1, l2, l3)")
+    return out.reshape(2 * l1 + 1, 2 * l2 + 1, 2 * l3 + 1)
+
+
+def param_count(n_layers: int, lmax: int) -> int:
+    return int(_lib.allegro_param_count(n_layers, lmax))
+
+
+def layer_paths(n_layers: int, lmax: int):
+    out = np.zeros(2 * n_layers, dtype=np.int32)
+    _lib.allegro_layer_paths(n_layers, lmax, out.ctypes.data)
+    return [(int(out[2 * k]), int(out[2 * k + 1])) for k in range(n_layers)]
+
+
+def version() -> str:
+    return _lib.allegro_version().decode()
+
+
+class Allegro:
+    """One ctx of the C ABI (allegro_create ... allegro_destroy)."""
+
+    def __init__(self, weights_path: str, box, r_cut: float = 0.0, skin: float = 0.0, device: int = 0,
+                 n_atoms: int = 0, precision: int = PREC_FP32, stream: int | None = None):
+        p = AllegroParams()
+        p.weights_path = os.fsencode(weights_path)
+        p.r_cut = r_cut
+        p.skin = skin
+        for d in range(3):
+            p.box[d] = float(box[d])
+        p.n_atoms_global = n_atoms
+        p.device = device
+        p.rank, p.world_size = 0, 1
+        p.nccl_unique_id = None
+        p.precision = precision
+        p.cuda_stream = stream
+        h = _P()
+        rc = _lib.allegro_create(C.byref(p), C.byref(h))
+        if rc != OK:
+            raise AllegroError(rc, _lib.allegro_last_error(None).decode())
+        self._h = h
+        self.box = np.asarray(box, dtype=np.float64)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.allegro_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, rc):
+        if rc != OK:
+            raise AllegroError(rc, _lib.allegro_last_error(self._h).decode())
+
+    # ---- allegro_compute_energy_forces -------------------------------------------------
+    def compute_energy_forces(self, pos, species, gid=None, box=None, e_atom=None, forces=None):
+        """pos [n,3] f64, species [n] i32 (numpy => host pointers; torch cuda => device
+        pointers, zero copy).  Returns (e_total, e_atom, forces) in the same kind."""
+        n = int(pos.shape[0])
+        on_dev = not isinstance(pos, np.ndarray)
+        if on_dev:
+            import torch
+
+            assert pos.is_cuda and pos.dtype == torch.float64 and pos.is_contiguous()
+            assert species.dtype == torch.int32 and species.is_contiguous()
+            if e_atom is None:
+                e_atom = torch.empty(n, dtype=torch.float64, device=pos.device)
+            if forces is None:
+                forces = torch.empty((n, 3), dtype=torch.float64, device=pos.device)
+        else:
+            pos = np.ascontiguousarray(pos, dtype=np.float64)
+            species = np.ascontiguousarray(species, dtype=np.int32)
+            gid = None if gid is None else np.ascontiguousarray(gid, dtype=np.int32)
+            if e_atom is None:
+                e_atom = np.empty(n, dtype=np.float64)
+            if forces is None:
+                forces = np.empty((n, 3), dtype=np.float64)
+        bx = None if box is None else np.ascontiguousarray(box, dtype=np.float64)
+        e = C.c_double(0.0)
+        rc = _lib.allegro_compute_energy_forces(
+            self._h, n, DEVICE if on_dev else HOST, _ptr(gid), _ptr(species), _ptr(pos),
+            None if bx is None else bx.ctypes.data, C.addressof(e), _ptr(e_atom), _ptr(forces))
+        self._check(rc)
+        return e.value, e_atom, forces
+
+    # ---- MD ---------------------------------------------------------------------------
+    def md_set_state(self, species, pos, vel):
+        species = np.ascontiguousarray(species, dtype=np.int32)
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        vel = np.ascontiguousarray(vel, dtype=np.float64)
+        self.n = int(pos.shape[0])
+        self._check(_lib.md_set_state(self._h, self.n, species.ctypes.data, pos.ctypes.data, vel.ctypes.data))
+
+    def md_get_state(self):
+        pos = np.empty((self.n, 3))
+        vel = np.empty((self.n, 3))
+        frc = np.empty((self.n, 3))
+        self._check(_lib.md_get_state(self._h, self.n, pos.ctypes.data, vel.ctypes.data, frc.ctypes.data))
+        return pos, vel, frc
+
+    def md_step(self, n_steps: int, dt_fs: float = 2.0) -> MdReport:
+        r = MdReport()
+        self._check(_lib.md_step(self._h, n_steps, dt_fs, C.byref(r)))
+        return r
+
+    def md_count_outliers(self, mean: float, sigma: float, k: float = 5.0) -> int:
+        c = C.c_int64(0)
+        self._check(_lib.md_count_outliers(self._h, mean, sigma, k, C.byref(c)))
+        return c.value
+
+    def md_force_baseline(self):
+        m, s = C.c_double(0), C.c_double(0)
+        self._check(_lib.md_force_baseline(self._h, C.byref(m), C.byref(s)))
+        return m.value, s.value
+
+    # ---- test hooks -------------------------------------------------------------------
+    def get_edges(self):
+        n = C.c_int64(0)
+        self._check(_lib.allegro_get_edges(self._h, 0, C.byref(n), None, None, None))
+        E = n.value
+        i = np.empty(E, dtype=np.int32)
+        j = np.empty(E, dtype=np.int32)
+        s = np.empty((E, 3), dtype=np.int8)
+        self._check(_lib.allegro_get_edges(self._h, E, C.byref(n), i.ctypes.data, j.ctypes.data, s.ctypes.data))
+        return i, j, s
+
+    def get_edge_grad(self):
+        n = C.c_int64(0)
+        self._check(_lib.allegro_get_edges(self._h, 0, C.byref(n), None, None, None))
+        g = np.empty((n.value, 3))
+        self._check(_lib.allegro_get_edge_grad(self._h, n.value, g.ctypes.data))
+        return g

@@ -1,0 +1,361 @@
+// abi.cu -- the extern "C" boundary declared in include/allegro.h.  Argument checking,
+// host <-> device marshalling and error mapping only; every step of the method runs
+// in the kernels of neighbor.cu, model.cu and md.cu.
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "ctx.cuh"
+
+using namespace allegro;
+
+namespace {
+
+thread_local std::string g_create_err;
+
+int fail(allegro_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  else g_create_err = msg;
+  return code;
+}
+
+template <typename F>
+int guarded(allegro_ctx* c, F&& f) {
+  try {
+    return f();
+  } catch (const WeightsError& e) {
+    return fail(c, ALLEGRO_E_WEIGHTS, e.what());
+  } catch (const CudaError& e) {
+    const std::string m = e.what();
+    return fail(c, m.rfind("OOM", 0) == 0 ? ALLEGRO_E_OOM : ALLEGRO_E_CUDA, m);
+  } catch (const std::exception& e) {
+    return fail(c, ALLEGRO_E_CUDA, e.what());
+  } catch (...) {
+    return fail(c, ALLEGRO_E_CUDA, "unknown error");
+  }
+}
+
+__global__ void k_iota(int32_t* x, int64_t n) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a < n) x[a] = (int32_t)a;
+}
+
+void reserve_atoms(allegro_ctx* c, int64_t n) {
+  c->pos.reserve(3 * n + 3);
+  c->vel.reserve(3 * n + 3);
+  c->frc.reserve(3 * n + 3);
+  c->species.reserve(n + 1);
+  c->gid.reserve(n + 1);
+  c->e_atom.reserve(n + 1);
+}
+
+int evaluate(allegro_ctx* c) {
+  ALG_CUDA(cudaMemsetAsync(c->flags.p, 0, 4 * sizeof(int), c->stream));
+  wrap_positions(c);
+  if (!check_inputs(c)) return fail(c, ALLEGRO_E_ARG, "non-finite position or species outside {0, 1}");
+  build_neighbors(c);
+  compute_forces(c);
+  if (!all_finite(c)) return fail(c, ALLEGRO_E_NONFINITE, "non-finite energy or force");
+  return ALLEGRO_OK;
+}
+
+bool box_ok(const double* b) {
+  for (int d = 0; d < 3; ++d)
+    if (!(std::isfinite(b[d]) && b[d] > 0)) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* allegro_version(void) { return "allegro-b200 0.1 (sm_100a)"; }
+
+const char* allegro_last_error(const allegro_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+int allegro_create(const allegro_params* p, allegro_ctx** out) {
+  if (!out) return fail(nullptr, ALLEGRO_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (!p || !p->weights_path) return fail(nullptr, ALLEGRO_E_ARG, "params or weights_path is NULL");
+  if (!box_ok(p->box)) return fail(nullptr, ALLEGRO_E_ARG, "box must be three finite positive lengths");
+  if (p->world_size != 1 || p->rank != 0)
+    return fail(nullptr, ALLEGRO_E_ARG, "this build runs one domain per ctx (world_size == 1)");
+  if (p->precision != ALLEGRO_PREC_FP32) return fail(nullptr, ALLEGRO_E_ARG, "only ALLEGRO_PREC_FP32 is built");
+  if (!(p->skin >= 0 && std::isfinite(p->skin))) return fail(nullptr, ALLEGRO_E_ARG, "skin must be >= 0");
+  allegro_ctx* c = new allegro_ctx();
+  c->prm = *p;
+  int rc = guarded(nullptr, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(p->device));
+    c->device = p->device;
+    if (p->cuda_stream) {
+      c->stream = (cudaStream_t)p->cuda_stream;
+    } else {
+      ALG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    load_model(c, p->weights_path);
+    if (p->r_cut > 0 && std::fabs(p->r_cut - c->model.r_max) > 1e-12)
+      throw WeightsError("r_cut differs from the weight file's r_max");
+    c->r_cut = c->model.r_max;
+    c->skin = p->skin;
+    for (int d = 0; d < 3; ++d) c->box[d] = p->box[d];
+    c->flags.reserve(8);
+    c->red.reserve(8);
+    size_t free_b = 0, total_b = 0;
+    ALG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    c->ws_budget_bytes = std::min<size_t>(free_b / 2, (size_t)64 << 30);
+    if (p->n_atoms_global > 0) reserve_atoms(c, p->n_atoms_global);
+    return ALLEGRO_OK;
+  });
+  if (rc != ALLEGRO_OK) {
+    allegro_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return ALLEGRO_OK;
+}
+
+void allegro_destroy(allegro_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  free_model(c->model);
+  c->pos.release();
+  c->vel.release();
+  c->frc.release();
+  c->species.release();
+  c->gid.release();
+  c->apos.release();
+  c->aowner.release();
+  c->ashift.release();
+  c->agid.release();
+  c->gcount.release();
+  c->goff.release();
+  c->ccount.release();
+  c->cstart.release();
+  c->cslot.release();
+  c->csorted.release();
+  c->nb_count.release();
+  c->nb_pad.release();
+  c->row_ptr.release();
+  c->nbr.release();
+  c->cidx.release();
+  c->rev.release();
+  c->key_pad.release();
+  c->key.release();
+  c->g.release();
+  c->flags.release();
+  c->red.release();
+  c->e_atom.release();
+  Workspace& w = c->ws;
+  for (DBuf<float>* b : {&w.z, &w.a1, &w.h1, &w.a2, &w.h2, &w.m, &w.u, &w.Y, &w.xa, &w.xb, &w.T, &w.xbar_a, &w.xbar_b,
+                         &w.sbar, &w.vbar_a, &w.vbar_b, &w.wbar, &w.ybar, &w.ubar, &w.zbar, &w.ab2, &w.ab1, &w.ee})
+    b->release();
+  for (int k = 0; k < kMaxLayers; ++k) {
+    w.w[k].release();
+    w.h[k].release();
+    w.V[k].release();
+    w.G[k].release();
+  }
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int allegro_compute_energy_forces(allegro_ctx* c, int64_t n, int where, const int32_t* gid, const int32_t* species,
+                                  const double* pos, const double* box, double* e_total, double* e_atom, double* forces) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (n < 0 || !species || !pos || !e_total || !forces) return fail(c, ALLEGRO_E_ARG, "NULL argument or n < 0");
+  if (where != ALLEGRO_HOST && where != ALLEGRO_DEVICE) return fail(c, ALLEGRO_E_ARG, "where must be HOST or DEVICE");
+  if (box && !box_ok(box)) return fail(c, ALLEGRO_E_ARG, "box must be three finite positive lengths");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    if (box)
+      for (int d = 0; d < 3; ++d) c->box[d] = box[d];
+    c->n = n;
+    reserve_atoms(c, n);
+    const cudaMemcpyKind kin = where == ALLEGRO_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const cudaMemcpyKind kout = where == ALLEGRO_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (n > 0) {
+      ALG_CUDA(cudaMemcpyAsync(c->pos.p, pos, sizeof(double) * 3 * n, kin, c->stream));
+      ALG_CUDA(cudaMemcpyAsync(c->species.p, species, sizeof(int32_t) * n, kin, c->stream));
+      if (gid) {
+        ALG_CUDA(cudaMemcpyAsync(c->gid.p, gid, sizeof(int32_t) * n, kin, c->stream));
+      } else {
+        k_iota<<<ceil_div(n, 256), 256, 0, c->stream>>>(c->gid.p, n);
+        ALG_LAUNCH_CHECK();
+      }
+    }
+    c->md_ready = false;
+    const int rc = evaluate(c);
+    *e_total = c->e_pot;
+    if (n > 0) {
+      ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, sizeof(double) * 3 * n, kout, c->stream));
+      if (e_atom) ALG_CUDA(cudaMemcpyAsync(e_atom, c->e_atom.p, sizeof(double) * n, kout, c->stream));
+    }
+    ALG_CUDA(cudaStreamSynchronize(c->stream));
+    return rc;
+  });
+}
+
+int md_set_state(allegro_ctx* c, int64_t n, const int32_t* species, const double* pos, const double* vel) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (n <= 0 || !species || !pos || !vel) return fail(c, ALLEGRO_E_ARG, "NULL argument or n <= 0");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    c->n = n;
+    reserve_atoms(c, n);
+    ALG_CUDA(cudaMemcpyAsync(c->pos.p, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->vel.p, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->species.p, species, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    k_iota<<<ceil_div(n, 256), 256, 0, c->stream>>>(c->gid.p, n);
+    ALG_LAUNCH_CHECK();
+    c->md_ready = false;
+    const int rc = evaluate(c);
+    if (rc != ALLEGRO_OK) return rc;
+    force_stats(c, &c->f_mean0, &c->f_sigma0);
+    c->md_ready = true;
+    c->md_steps = 0;
+    return ALLEGRO_OK;
+  });
+}
+
+int md_get_state(allegro_ctx* c, int64_t n, double* pos, double* vel, double* forces) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (!c->md_ready) return fail(c, ALLEGRO_E_STATE, "md_set_state has not been called");
+  if (n != c->n) return fail(c, ALLEGRO_E_ARG, "n differs from the state size");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    if (pos) ALG_CUDA(cudaMemcpyAsync(pos, c->pos.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (vel) ALG_CUDA(cudaMemcpyAsync(vel, c->vel.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (forces) ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaStreamSynchronize(c->stream));
+    return ALLEGRO_OK;
+  });
+}
+
+int md_step(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (!c->md_ready) return fail(c, ALLEGRO_E_STATE, "md_set_state has not been called");
+  if (n_steps < 0 || !(dt > 0 && std::isfinite(dt))) return fail(c, ALLEGRO_E_ARG, "bad n_steps or dt");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    int rc = ALLEGRO_OK;
+    int64_t done = 0;
+    for (; done < n_steps; ++done) {
+      md_half_kick_drift(c, dt);
+      ALG_CUDA(cudaMemsetAsync(c->flags.p, 0, 4 * sizeof(int), c->stream));
+      build_neighbors(c);
+      compute_forces(c);
+      md_half_kick(c, dt);
+      if (!all_finite(c)) {
+        rc = fail(c, ALLEGRO_E_NONFINITE, "non-finite energy, force or velocity at step " + std::to_string(c->md_steps + 1));
+        ++done;
+        ++c->md_steps;
+        break;
+      }
+      ++c->md_steps;
+    }
+    if (out) {
+      out->steps_done = done;
+      out->e_pot = c->e_pot;
+      out->e_kin = md_kinetic(c);
+      out->e_total = out->e_pot + out->e_kin;
+      out->temperature = 2.0 * out->e_kin / (3.0 * (double)c->n * 8.617333e-5);
+      out->n_outliers_last = count_outliers(c, c->f_mean0 + 5.0 * c->f_sigma0);
+      out->n_edges = c->n_edges;
+      out->n_rebuilds = c->n_rebuilds;
+    }
+    return rc;
+  });
+}
+
+int md_count_outliers(allegro_ctx* c, double mean, double sigma, double k, int64_t* count) {
+  if (!c || !count) return fail(c, ALLEGRO_E_ARG, "NULL argument");
+  if (!(std::isfinite(mean) && std::isfinite(sigma) && std::isfinite(k)))
+    return fail(c, ALLEGRO_E_ARG, "non-finite threshold");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    *count = count_outliers(c, mean + k * sigma);
+    return ALLEGRO_OK;
+  });
+}
+
+int md_force_baseline(allegro_ctx* c, double* mean, double* sigma) {
+  if (!c || !mean || !sigma) return fail(c, ALLEGRO_E_ARG, "NULL argument");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    force_stats(c, mean, sigma);
+    return ALLEGRO_OK;
+  });
+}
+
+int allegro_get_edges(allegro_ctx* c, int64_t capacity, int64_t* n_edges, int32_t* i_gid, int32_t* j_gid, int8_t* shift) {
+  if (!c || !n_edges) return fail(c, ALLEGRO_E_ARG, "NULL argument");
+  *n_edges = c->n_edges;
+  if (!i_gid && !j_gid && !shift) return ALLEGRO_OK;
+  if (capacity < c->n_edges) return fail(c, ALLEGRO_E_ARG, "capacity too small");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    const int64_t E = c->n_edges, na = c->n + c->n_ghost;
+    std::vector<int32_t> cidx(E), nbr(E), gid(c->n), agid(na), ash(na);
+    ALG_CUDA(cudaMemcpyAsync(cidx.data(), c->cidx.p, 4 * E, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(nbr.data(), c->nbr.p, 4 * E, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(gid.data(), c->gid.p, 4 * c->n, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(agid.data(), c->agid.p, 4 * na, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(ash.data(), c->ashift.p, 4 * na, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaStreamSynchronize(c->stream));
+    for (int64_t e = 0; e < E; ++e) {
+      if (i_gid) i_gid[e] = gid[cidx[e]];
+      if (j_gid) j_gid[e] = agid[nbr[e]];
+      if (shift) {
+        const int32_t s = ash[nbr[e]];
+        shift[3 * e] = (int8_t)((s & 0xff) - 128);
+        shift[3 * e + 1] = (int8_t)(((s >> 8) & 0xff) - 128);
+        shift[3 * e + 2] = (int8_t)(((s >> 16) & 0xff) - 128);
+      }
+    }
+    return ALLEGRO_OK;
+  });
+}
+
+int allegro_get_edge_grad(allegro_ctx* c, int64_t capacity, double* g) {
+  if (!c || !g) return fail(c, ALLEGRO_E_ARG, "NULL argument");
+  if (capacity < c->n_edges) return fail(c, ALLEGRO_E_ARG, "capacity too small");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    std::vector<float> h(3 * c->n_edges);
+    ALG_CUDA(cudaMemcpyAsync(h.data(), c->g.p, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaStreamSynchronize(c->stream));
+    for (size_t q = 0; q < h.size(); ++q) g[q] = h[q];
+    return ALLEGRO_OK;
+  });
+}
+
+int allegro_w3j_table(int l1, int l2, int l3, double* out) {
+  if (!out || l1 < 0 || l2 < 0 || l3 < 0 || l1 > 2 || l2 > 2 || l3 > 2) return ALLEGRO_E_ARG;
+  if (!(std::abs(l1 - l2) <= l3 && l3 <= l1 + l2)) return ALLEGRO_E_ARG;
+  const int d2 = 2 * l2 + 1, d3 = 2 * l3 + 1;
+  for (int a = 0; a < 2 * l1 + 1; ++a)
+    for (int b = 0; b < d2; ++b)
+      for (int c = 0; c < d3; ++c) out[(a * d2 + b) * d3 + c] = w3j_value(l1, l2, l3, a, b, c);
+  return ALLEGRO_OK;
+}
+
+int64_t allegro_param_count(int n_layers, int lmax) {
+  if (n_layers < 1 || n_layers > kMaxLayers || lmax < 0 || lmax > 2) return -1;
+  return param_count(n_layers, lmax);
+}
+
+int allegro_layer_paths(int n_layers, int lmax, int* out) {
+  if (!out || n_layers < 1 || n_layers > kMaxLayers || lmax < 0 || lmax > 2) return ALLEGRO_E_ARG;
+  for (int k = 0; k < n_layers; ++k) {
+    const LayerArch A = layer_arch(n_layers, lmax, k);
+    out[2 * k] = A.n_paths;
+    out[2 * k + 1] = A.n_s;
+  }
+  return ALLEGRO_OK;
+}
+
+}  // extern "C"

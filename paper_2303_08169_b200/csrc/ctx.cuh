@@ -1,0 +1,160 @@
+// ctx.cuh -- the runtime state behind the opaque allegro_ctx, and the internal entry
+// points of each subsystem (neighbour build, model, MD).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/allegro.h"
+#include "arch.cuh"
+#include "common.cuh"
+
+namespace allegro {
+
+struct WeightsError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Device buffer that only grows (capacity in elements of T).
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  void reserve(size_t n) {
+    if (n <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    size_t c = n + n / 4 + 64;
+    if (cudaMalloc(&p, c * sizeof(T)) != cudaSuccess) {
+      cap = 0;
+      p = nullptr;
+      cudaGetLastError();
+      throw CudaError("OOM: cudaMalloc of " + std::to_string(c * sizeof(T)) + " bytes");
+    }
+    cap = c;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Runtime view of the compile-time layer architecture (same constexpr derivation).
+struct LayerInfo {
+  LayerArch A;
+  int nw;              // env-embed outputs: C * n_env * (2 if k == 0 else 1)
+  int fan_lat;         // D + C * n_s
+  int t_base[kMaxIr];  // per out irrep: offset (floats per edge) of T_o in the T scratch
+  int v_base[kMaxIr];  // per in irrep: offset (floats per edge) of V_ir in the V store of this layer
+};
+
+struct DevWeights {
+  float* tb_w0 = nullptr;   // [16][32], rows 12..15 zero
+  float* tb_w1 = nullptr;   // [32][64]
+  float* tb_w2 = nullptr;   // [64][128]
+  float* tb_w0T = nullptr;  // [32][16]
+  float* tb_w1T = nullptr;  // [64][32]
+  float* tb_w2T = nullptr;  // [128][64]
+  float* env[kMaxLayers] = {};   // [128][nw]  columns in [chunk][l][c] order
+  float* envT[kMaxLayers] = {};  // [nw][128]
+  float* lin[kMaxLayers][kMaxIr] = {};   // [n_to*C][C]   rows (path_local, c)
+  float* linT[kMaxLayers][kMaxIr] = {};  // [C][n_to*C]
+  float* lat[kMaxLayers] = {};     // [128 + n_s*C][128], scalar rows in (q, c) order
+  float* latT_x[kMaxLayers] = {};  // [128][128]
+  float* latT_s[kMaxLayers] = {};  // [128][n_s*C]
+  float* wout = nullptr;           // [128] = W_o1 W_o2 / (sqrt(128) sqrt(32))
+  float bessel[kNB] = {};
+  std::vector<void*> owned;
+};
+
+struct Model {
+  int n_layers = 0, lmax = 0;
+  double r_max = 0, nbar = 0, sigma[2] = {1, 1}, mu[2] = {0, 0};
+  LayerInfo L[kMaxLayers];
+  DevWeights w;
+};
+
+// Per-chunk activation workspace (fp32, row-major [E_cap][width]).
+struct Workspace {
+  size_t e_cap = 0, a_cap = 0;
+  DBuf<float> z, a1, h1, a2, h2, m, u, Y;
+  DBuf<float> xa, xb;
+  DBuf<float> w[kMaxLayers], h[kMaxLayers], V[kMaxLayers], G[kMaxLayers];
+  DBuf<float> T;
+  DBuf<float> xbar_a, xbar_b, sbar, vbar_a, vbar_b, wbar, ybar, ubar, zbar, ab2, ab1, ee;
+};
+
+}  // namespace allegro
+
+struct allegro_ctx {
+  std::string err;
+  allegro_params prm{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double box[3] = {0, 0, 0};
+  double r_cut = 0, skin = 0;
+  allegro::Model model;
+
+  // ---- atoms (owned first, then ghosts) ----
+  int64_t n = 0;        // owned
+  int64_t n_ghost = 0;  // ghosts of the last build
+  allegro::DBuf<double> pos, vel, frc;       // [n][3] owned state (fp64)
+  allegro::DBuf<int32_t> species, gid;       // [n]
+  allegro::DBuf<double> apos;                // [n + G][3] canonical image positions
+  allegro::DBuf<int32_t> aowner, ashift, agid;  // [n + G]
+  allegro::DBuf<int32_t> gcount, goff;       // ghost count / offsets per owned atom
+  // ---- cells ----
+  int ncell[3] = {0, 0, 0};
+  double cell_lo[3] = {0, 0, 0}, cell_size[3] = {0, 0, 0};
+  allegro::DBuf<int32_t> ccount, cstart, cslot, csorted;
+  // ---- edges (CSR by owned centre, canonical row order) ----
+  int max_nb = 256;
+  int64_t n_edges = 0;
+  allegro::DBuf<int32_t> nb_count, nb_pad, row_ptr, nbr, cidx, rev;
+  allegro::DBuf<unsigned long long> key_pad, key;
+  allegro::DBuf<float> g;                    // [E][3] dE/dr_e
+  std::vector<int32_t> h_row_ptr;
+  // ---- scalars / flags ----
+  allegro::DBuf<int> flags;                  // [0] overflow max count, [1] bad input, [2] non-finite
+  allegro::DBuf<double> red;                 // reduction scratch
+  allegro::DBuf<double> e_atom;              // [n]
+  allegro::DBuf<int32_t> scan_tmp;
+  allegro::Workspace ws;
+  size_t ws_budget_bytes = 0;
+  // ---- MD ----
+  bool md_ready = false;
+  int64_t md_steps = 0, n_rebuilds = 0;
+  double e_pot = 0;
+  double f_mean0 = 0, f_sigma0 = 0;  // step-0 outlier baseline
+};
+
+namespace allegro {
+
+// weights.cu
+void load_model(allegro_ctx* c, const char* path);
+void free_model(Model& m);
+
+// scan.cu: out[i] = sum_{j<i} in[j] (int32), out[n] = total; returns total (host sync)
+void exclusive_scan(allegro_ctx* c, const int32_t* in, int32_t* out, int64_t n);
+
+// neighbor.cu: wrap owned positions, build ghosts, cells, CSR edges and reverse index.
+void build_neighbors(allegro_ctx* c);
+void wrap_positions(allegro_ctx* c);
+
+// model.cu: energies and forces for the current edge list -> c->frc, c->e_atom, c->e_pot
+void compute_forces(allegro_ctx* c);
+
+// md.cu
+void md_half_kick_drift(allegro_ctx* c, double dt);
+void md_half_kick(allegro_ctx* c, double dt);
+double md_kinetic(allegro_ctx* c);
+void force_stats(allegro_ctx* c, double* mean, double* sigma);
+int64_t count_outliers(allegro_ctx* c, double thr);
+bool all_finite(allegro_ctx* c);
+double sum_e_atom(allegro_ctx* c);
+bool check_inputs(allegro_ctx* c);
+
+}  // namespace allegro

@@ -1,0 +1,41 @@
+// gemm.cuh -- per-edge dense contractions C[M x N] = epi(A[M x K] W[K x N]).
+// The only dense GEMMs of the method: the
+// two-body MLP, env-embed, TP-linear and latent linears and their input-gradient
+// (W^T) counterparts.  M = edges (or edges x irrep dim), K, N <= 224.
+#pragma once
+#include "common.cuh"
+
+namespace allegro {
+
+enum GemmEpi : int {
+  EPI_STORE = 0,      // C = s acc
+  EPI_SILU = 1,       // aux = s acc; C = SiLU(aux)
+  EPI_UMUL_SAVE = 2,  // aux = s acc; C = u[r] aux
+  EPI_RESID = 3,      // aux = s acc; C = alpha X + beta u[r] aux
+  EPI_URESID = 4,     // C = alpha X + beta u[r] s acc
+  EPI_USCALE = 5,     // C = beta u[r] s acc
+  EPI_ACC = 6,        // C += s acc
+  EPI_ADDX = 7,       // C = s acc + X
+  EPI_DSILU = 8,      // C = (u ? u[r] : 1) s acc SiLU'(X)
+};
+
+struct GemmArgs {
+  int64_t M = 0;
+  int N = 0, K = 0;
+  const float* A = nullptr;  // row-major, columns [0, K1)
+  int lda = 0;
+  const float* A2 = nullptr;  // row-major, columns [K1, K) (nullptr: A has all K)
+  int lda2 = 0;
+  int K1 = 0;
+  const float* W = nullptr;  // [K][N] row-major
+  float* C = nullptr;        // [M][N]
+  float* aux = nullptr;      // [M][N]
+  const float* X = nullptr;  // [M][N]
+  const float* u = nullptr;  // [M]
+  float s = 1.f, alpha = 0.f, beta = 0.f;
+  int epi = EPI_STORE;
+};
+
+void gemm(const GemmArgs& g, cudaStream_t st);
+
+}  // namespace allegro

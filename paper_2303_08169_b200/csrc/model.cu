@@ -1,0 +1,741 @@
+// model.cu -- the Allegro energy and its analytic forces on the GPU.
+//
+// PAPER.md:128-131 (§2.1) and Eq. 1; concrete model = SURVEY.md
+// §8(c) E1-E9.  Centre atoms are processed in chunks of complete CSR
+// rows (each E_i depends on its own row only), so every segmented reduction (Gamma_i,
+// its adjoint, E_i) stays inside one warp and is done in a fixed order: the result is
+// deterministic and independent of the chunking.
+//
+// Per chunk (E edges, fp32 row-major [E][width] activations):
+//   K3  k_geom        r_e (fp64 difference -> fp32), u(d), B(d) u, Y(r_hat)       E1-E3
+//   A5  3 GEMMs       two-body MLP 16(12) -> 32 -> 64 -> 128, x0 = u MLP           E4-E5
+//   per layer k:
+//   A6  GEMM          w = x^k W_env / sqrt(D)                                      E6
+//   A7+A8 k_tp_fwd    Gamma_i (warp per centre, lane = channel) and the "uuu" TP  E6
+//   A9  GEMMs         V^{k+1} per out irrep; x^{k+1} = a x^k + b u [x^k,s] W_lat   E6
+//   A10 k_energy      E_e = x^L . w_out, E_i = sigma nbar^-1/2 sum E_e + mu      E7-E8
+//   A11 reverse mode  the same chain transposed (W^T GEMMs, k_tp_bwd), k_geom_bwd E9
+// then over all atoms:
+//   A12 k_force       F_a = sum_{e in row a} (g_e - g_rev(e)) in row order (fp64)
+#include <algorithm>
+#include <cmath>
+
+#include "ctx.cuh"
+#include "gemm.cuh"
+
+namespace allegro {
+namespace {
+
+constexpr float kCSilu = 1.6765324703f;  // E[SiLU(z)^2]^-1/2 (reading row 5)
+constexpr float kResA = 0.89442719099991588f;  // 2/sqrt5
+constexpr float kResB = 0.44721359549995794f;  // 1/sqrt5
+
+template <int NL, int LMAX, int K>
+struct Arch {
+  static constexpr LayerArch A = layer_arch(NL, LMAX, K);
+  static constexpr int DSH = (LMAX + 1) * (LMAX + 1);
+  static constexpr int NENV = LMAX + 1;
+  static constexpr int NW = kC * NENV * (K == 0 ? 2 : 1);
+  static constexpr int ENV_OFF = K == 0 ? kC * NENV : 0;  // column offset of the env chunk in w
+  static constexpr int DIN = A.dim_in;
+  static constexpr int DT = A.dim_T;
+  static constexpr int t_base(int o) {
+    int b = 0;
+    for (int q = 0; q < o; ++q) b += ir_dim(A.out.v[q]) * A.n_to[q] * kC;
+    return b;
+  }
+  static constexpr int v_base(int i) {
+    int b = 0;
+    for (int q = 0; q < i; ++q) b += ir_dim(A.in.v[q]) * kC;
+    return b;
+  }
+};
+
+constexpr int lm_l(int m) { return m == 0 ? 0 : (m < 4 ? 1 : 2); }
+
+struct ChunkPtrs {
+  int64_t a0, n_c;  // first centre atom, number of centres
+  int64_t e0, n_e;  // first edge, number of edges
+};
+
+// ----------------------------------------------------------------- K3 geometry
+__device__ __forceinline__ void sh_eval(const float n[3], float* Y, int lmax) {
+  // component-normalised real SH (E3), m = -l..l; l = 1 stored (y, z, x)
+  const float s3 = 1.7320508075688772f, s5 = 2.2360679774997896f, s15 = 3.8729833462074170f;
+  Y[0] = 1.f;
+  if (lmax >= 1) {
+    Y[1] = s3 * n[1];
+    Y[2] = s3 * n[2];
+    Y[3] = s3 * n[0];
+  }
+  if (lmax >= 2) {
+    Y[4] = s15 * n[0] * n[1];
+    Y[5] = s15 * n[1] * n[2];
+    Y[6] = 0.5f * s5 * (2.f * n[2] * n[2] - n[0] * n[0] - n[1] * n[1]);
+    Y[7] = s15 * n[0] * n[2];
+    Y[8] = 0.5f * s15 * (n[0] * n[0] - n[1] * n[1]);
+  }
+}
+
+struct GeomParams {
+  float rc, inv_rc;
+  float freq[kNB];
+  int lmax, dsh;
+};
+
+__device__ __forceinline__ void edge_vec(const double* __restrict__ apos, int32_t i, int32_t a, float r[3]) {
+#pragma unroll
+  for (int d = 0; d < 3; ++d) r[d] = (float)__dsub_rn(apos[(int64_t)a * 3 + d], apos[(int64_t)i * 3 + d]);
+}
+
+__global__ void k_geom(ChunkPtrs ch, GeomParams gp, const double* __restrict__ apos, const int32_t* __restrict__ cidx,
+                       const int32_t* __restrict__ nbr, const int32_t* __restrict__ aowner,
+                       const int32_t* __restrict__ species, float* __restrict__ z, float* __restrict__ Y,
+                       float* __restrict__ u) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ch.n_e) return;
+  const int64_t ge = ch.e0 + e;
+  const int32_t i = cidx[ge], a = nbr[ge];
+  float r[3];
+  edge_vec(apos, i, a, r);
+  const float d = sqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  const float x = d * gp.inv_rc;
+  float uu = 0.f;
+  if (x < 1.f) {
+    const float x2 = x * x, x3 = x2 * x, x6 = x3 * x3;
+    uu = 1.f - 28.f * x6 + 48.f * x6 * x - 21.f * x6 * x2;
+  }
+  u[e] = uu;
+  const int zi = species[i], zj = species[aowner[a]];
+  float* zz = z + e * 16;
+  zz[0] = zi == 0 ? 1.f : 0.f;
+  zz[1] = zi == 1 ? 1.f : 0.f;
+  zz[2] = zj == 0 ? 1.f : 0.f;
+  zz[3] = zj == 1 ? 1.f : 0.f;
+  const float pre = 2.f * gp.inv_rc / d;
+#pragma unroll
+  for (int q = 0; q < kNB; ++q) zz[4 + q] = uu * pre * sinf(gp.freq[q] * d * gp.inv_rc);
+#pragma unroll
+  for (int q = 12; q < 16; ++q) zz[q] = 0.f;
+  const float inv = 1.f / d;
+  const float nv[3] = {r[0] * inv, r[1] * inv, r[2] * inv};
+  float y[9];
+  sh_eval(nv, y, gp.lmax);
+  for (int q = 0; q < gp.dsh; ++q) Y[e * gp.dsh + q] = y[q];
+}
+
+// ----------------------------------------------------------------- A7+A8 TP forward
+struct TpArgs {
+  ChunkPtrs ch;
+  const int32_t* row_ptr;
+  const float* w;      // [E][NW] layer weights (env chunk at ENV_OFF)
+  const float* Y;      // [E][DSH]
+  const float* V;      // layer-K V store (K >= 1)
+  float* T;            // T scratch (per out irrep [E][dim][n_to][C])
+  float* G;            // [n_c][DSH][C]
+  const float* Tb[kMaxIr];  // backward: T-bar per out irrep
+  float* Vb;           // backward: V-bar store of layer K (K >= 1)
+  float* wbar;         // backward: [E][NW]
+  float* ybar;         // backward: [E][DSH] accumulated
+  int64_t e_cap;
+  float inv_sqrt_nbar;
+};
+
+template <int NL, int LMAX, int K>
+__device__ __forceinline__ void load_v(const TpArgs& t, int64_t e, int lane, float* v) {
+  using AR = Arch<NL, LMAX, K>;
+  if constexpr (K == 0) {
+    float y[AR::DSH], we[AR::NENV];
+#pragma unroll
+    for (int m = 0; m < AR::DSH; ++m) y[m] = t.Y[e * AR::DSH + m];
+#pragma unroll
+    for (int l = 0; l < AR::NENV; ++l) we[l] = t.w[e * AR::NW + l * kC + lane];
+#pragma unroll
+    for (int m = 0; m < AR::DSH; ++m) v[m] = we[lm_l(m)] * y[m];
+  } else {
+    static_for<AR::A.in.n>([&](auto I) {
+      constexpr int ii = decltype(I)::value;
+      constexpr int dim = ir_dim(AR::A.in.v[ii]);
+      constexpr int off = AR::A.in.off(ii);
+      constexpr int vbase = AR::v_base(ii);
+      const float* src = t.V + (int64_t)vbase * t.e_cap + e * dim * kC + lane;
+#pragma unroll
+      for (int m = 0; m < dim; ++m) v[off + m] = src[m * kC];
+    });
+  }
+}
+
+template <int NL, int LMAX, int K>
+__global__ void __launch_bounds__(128) k_tp_fwd(TpArgs t) {
+  using AR = Arch<NL, LMAX, K>;
+  constexpr LayerArch A = AR::A;
+  const int lane = threadIdx.x & 31;
+  const int64_t ii = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ii >= t.ch.n_c) return;
+  const int64_t r0 = t.row_ptr[t.ch.a0 + ii] - t.ch.e0, r1 = t.row_ptr[t.ch.a0 + ii + 1] - t.ch.e0;
+  float G[AR::DSH];
+#pragma unroll
+  for (int m = 0; m < AR::DSH; ++m) G[m] = 0.f;
+  for (int64_t e = r0; e < r1; ++e) {
+    float we[AR::NENV];
+#pragma unroll
+    for (int l = 0; l < AR::NENV; ++l) we[l] = t.w[e * AR::NW + AR::ENV_OFF + l * kC + lane];
+#pragma unroll
+    for (int m = 0; m < AR::DSH; ++m) G[m] = fmaf(we[lm_l(m)], t.Y[e * AR::DSH + m], G[m]);
+  }
+#pragma unroll
+  for (int m = 0; m < AR::DSH; ++m) {
+    G[m] *= t.inv_sqrt_nbar;
+    t.G[(ii * AR::DSH + m) * kC + lane] = G[m];
+  }
+  for (int64_t e = r0; e < r1; ++e) {
+    float v[AR::DIN];
+    load_v<NL, LMAX, K>(t, e, lane, v);
+    float T[AR::DT];
+#pragma unroll
+    for (int q = 0; q < AR::DT; ++q) T[q] = 0.f;
+    static_for<A.n_paths>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      constexpr int L1 = AR::A.path[q].a.l, L2 = AR::A.path[q].b.l, LO = AR::A.path[q].o.l;
+      constexpr int D2 = 2 * L2 + 1, D3 = 2 * LO + 1;
+      constexpr double alpha = csqrt(2.0 * LO + 1.0);
+      static_for<(2 * L1 + 1) * D2 * D3>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int m1 = i / (D2 * D3), m2 = (i / D3) % D2, m3 = i % D3;
+        constexpr float c = (float)(alpha * W3j<L1, L2, LO>::t.v[i]);
+        constexpr int it = AR::A.t_off[q] + m3, iv = AR::A.in_off[q] + m1, ig = AR::A.sh_off[q] + m2;
+        if constexpr (c != 0.f) T[it] = fmaf(c * v[iv], G[ig], T[it]);
+      });
+    });
+    static_for<A.n_paths>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      constexpr int o = AR::A.out_idx[q];
+      constexpr int dim = ir_dim(AR::A.out.v[o]);
+      constexpr int nto = AR::A.n_to[o];
+      constexpr int ol = AR::A.out_local[q];
+      constexpr int toff = AR::A.t_off[q];
+      constexpr int tbase = AR::t_base(o);
+      float* dst = t.T + (int64_t)tbase * t.e_cap + (e * dim * nto + ol) * kC + lane;
+#pragma unroll
+      for (int m = 0; m < dim; ++m) dst[m * nto * kC] = T[toff + m];
+    });
+  }
+}
+
+// ----------------------------------------------------------------- A11 TP backward
+template <int NL, int LMAX, int K>
+__global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
+  using AR = Arch<NL, LMAX, K>;
+  constexpr LayerArch A = AR::A;
+  const int lane = threadIdx.x & 31;
+  const int64_t ii = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ii >= t.ch.n_c) return;
+  const int64_t r0 = t.row_ptr[t.ch.a0 + ii] - t.ch.e0, r1 = t.row_ptr[t.ch.a0 + ii + 1] - t.ch.e0;
+  float G[AR::DSH], Gb[AR::DSH];
+#pragma unroll
+  for (int m = 0; m < AR::DSH; ++m) {
+    G[m] = t.G[(ii * AR::DSH + m) * kC + lane];
+    Gb[m] = 0.f;
+  }
+  for (int64_t e = r0; e < r1; ++e) {
+    float v[AR::DIN], vb[AR::DIN], tb[AR::DT];
+    load_v<NL, LMAX, K>(t, e, lane, v);
+#pragma unroll
+    for (int q = 0; q < AR::DIN; ++q) vb[q] = 0.f;
+    static_for<A.n_paths>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      constexpr int o = AR::A.out_idx[q];
+      constexpr int dim = ir_dim(AR::A.out.v[o]);
+      constexpr int nto = AR::A.n_to[o];
+      constexpr int ol = AR::A.out_local[q];
+      constexpr int toff = AR::A.t_off[q];
+      const float* src = t.Tb[o] + (e * dim * nto + ol) * kC + lane;
+#pragma unroll
+      for (int m = 0; m < dim; ++m) tb[toff + m] = src[m * nto * kC];
+    });
+    static_for<A.n_paths>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      constexpr int L1 = AR::A.path[q].a.l, L2 = AR::A.path[q].b.l, LO = AR::A.path[q].o.l;
+      constexpr int D2 = 2 * L2 + 1, D3 = 2 * LO + 1;
+      constexpr double alpha = csqrt(2.0 * LO + 1.0);
+      static_for<(2 * L1 + 1) * D2 * D3>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int m1 = i / (D2 * D3), m2 = (i / D3) % D2, m3 = i % D3;
+        constexpr float c = (float)(alpha * W3j<L1, L2, LO>::t.v[i]);
+        constexpr int it = AR::A.t_off[q] + m3, iv = AR::A.in_off[q] + m1, ig = AR::A.sh_off[q] + m2;
+        if constexpr (c != 0.f) {
+          const float ct = c * tb[it];
+          vb[iv] = fmaf(ct, G[ig], vb[iv]);
+          Gb[ig] = fmaf(ct, v[iv], Gb[ig]);
+        }
+      });
+    });
+    if constexpr (K == 0) {
+      // V0 = w_edge (x) Y:  wbar_edge[l] = sum_m vb[m] Y[m];  Ybar[m] += sum_c vb[m] w_edge[l]
+      float y[AR::DSH], we[AR::NENV], wb[AR::NENV];
+#pragma unroll
+      for (int m = 0; m < AR::DSH; ++m) y[m] = t.Y[e * AR::DSH + m];
+#pragma unroll
+      for (int l = 0; l < AR::NENV; ++l) {
+        we[l] = t.w[e * AR::NW + l * kC + lane];
+        wb[l] = 0.f;
+      }
+      float yb_mine = 0.f;
+#pragma unroll
+      for (int m = 0; m < AR::DSH; ++m) {
+        wb[lm_l(m)] = fmaf(vb[m], y[m], wb[lm_l(m)]);
+        const float s = warp_sum(vb[m] * we[lm_l(m)]);
+        if (lane == m) yb_mine = s;
+      }
+#pragma unroll
+      for (int l = 0; l < AR::NENV; ++l) t.wbar[e * AR::NW + l * kC + lane] = wb[l];
+      if (lane < AR::DSH) t.ybar[e * AR::DSH + lane] += yb_mine;
+    } else {
+      static_for<AR::A.in.n>([&](auto I) {
+        constexpr int ii2 = decltype(I)::value;
+        constexpr int dim = ir_dim(AR::A.in.v[ii2]);
+        constexpr int off = AR::A.in.off(ii2);
+        constexpr int vbase = AR::v_base(ii2);
+        float* dst = t.Vb + (int64_t)vbase * t.e_cap + e * dim * kC + lane;
+#pragma unroll
+        for (int m = 0; m < dim; ++m) dst[m * kC] = vb[off + m];
+      });
+    }
+  }
+  // environment adjoint: w_env-bar and Ybar from Gamma-bar
+  for (int64_t e = r0; e < r1; ++e) {
+    float y[AR::DSH], we[AR::NENV], wb[AR::NENV];
+#pragma unroll
+    for (int m = 0; m < AR::DSH; ++m) y[m] = t.Y[e * AR::DSH + m];
+#pragma unroll
+    for (int l = 0; l < AR::NENV; ++l) {
+      we[l] = t.w[e * AR::NW + AR::ENV_OFF + l * kC + lane];
+      wb[l] = 0.f;
+    }
+    float yb_mine = 0.f;
+#pragma unroll
+    for (int m = 0; m < AR::DSH; ++m) {
+      wb[lm_l(m)] = fmaf(Gb[m], y[m], wb[lm_l(m)]);
+      const float s = warp_sum(Gb[m] * we[lm_l(m)]);
+      if (lane == m) yb_mine = s;
+    }
+#pragma unroll
+    for (int l = 0; l < AR::NENV; ++l) t.wbar[e * AR::NW + AR::ENV_OFF + l * kC + lane] = t.inv_sqrt_nbar * wb[l];
+    if (lane < AR::DSH) t.ybar[e * AR::DSH + lane] += t.inv_sqrt_nbar * yb_mine;
+  }
+}
+
+// ----------------------------------------------------------------- A10 energies
+__global__ void k_energy(ChunkPtrs ch, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ species,
+                         const float* __restrict__ x, const float* __restrict__ wout, float* __restrict__ xbar,
+                         double* __restrict__ e_atom, double s0, double s1, double mu0, double mu1, float inv_sqrt_nbar) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ii = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ii >= ch.n_c) return;
+  const int64_t a = ch.a0 + ii;
+  const int64_t r0 = row_ptr[a] - ch.e0, r1 = row_ptr[a + 1] - ch.e0;
+  const int z = species[a];
+  const double sig = z == 0 ? s0 : s1;
+  const float ebar = (float)sig * inv_sqrt_nbar;
+  const float4 w4 = reinterpret_cast<const float4*>(wout)[lane];
+  const float4 xb4 = make_float4(ebar * w4.x, ebar * w4.y, ebar * w4.z, ebar * w4.w);
+  float acc = 0.f;
+  for (int64_t e = r0; e < r1; ++e) {
+    const float4 x4 = reinterpret_cast<const float4*>(x + e * kD)[lane];
+    float p = x4.x * w4.x;
+    p = fmaf(x4.y, w4.y, p);
+    p = fmaf(x4.z, w4.z, p);
+    p = fmaf(x4.w, w4.w, p);
+    acc += warp_sum(p);
+    reinterpret_cast<float4*>(xbar + e * kD)[lane] = xb4;
+  }
+  if (lane == 0) e_atom[a] = sig * (double)inv_sqrt_nbar * (double)acc + (z == 0 ? mu0 : mu1);
+}
+
+// ubar[e] += coef <P[e], Q[e]> over 128 (warp per edge)
+__global__ void k_rowdot(int64_t E, const float* __restrict__ P, const float* __restrict__ Q, float coef,
+                         float* __restrict__ ubar) {
+  const int lane = threadIdx.x & 31;
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (e >= E) return;
+  const float4 p = reinterpret_cast<const float4*>(P + e * kD)[lane];
+  const float4 q = reinterpret_cast<const float4*>(Q + e * kD)[lane];
+  const float s = warp_sum(p.x * q.x + p.y * q.y + p.z * q.z + p.w * q.w);
+  if (lane == 0) ubar[e] += coef * s;
+}
+
+// ----------------------------------------------------------------- E9 geometry reverse
+__global__ void k_geom_bwd(ChunkPtrs ch, GeomParams gp, const double* __restrict__ apos, const int32_t* __restrict__ cidx,
+                           const int32_t* __restrict__ nbr, const float* __restrict__ ubar,
+                           const float* __restrict__ zbar, const float* __restrict__ ybar, float* __restrict__ g) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ch.n_e) return;
+  const int64_t ge = ch.e0 + e;
+  float r[3];
+  edge_vec(apos, cidx[ge], nbr[ge], r);
+  const float d = sqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  const float inv = 1.f / d;
+  const float n[3] = {r[0] * inv, r[1] * inv, r[2] * inv};
+  const float x = d * gp.inv_rc;
+  float uu = 0.f, du = 0.f;
+  if (x < 1.f) {
+    const float x2 = x * x, x3 = x2 * x, x5 = x3 * x2, x6 = x3 * x3;
+    uu = 1.f - 28.f * x6 + 48.f * x6 * x - 21.f * x6 * x2;
+    du = -168.f * gp.inv_rc * x5 * (1.f - x) * (1.f - x);
+  }
+  float ub = ubar[e];
+  float db = 0.f;
+  const float pre = 2.f * gp.inv_rc;
+#pragma unroll
+  for (int q = 0; q < kNB; ++q) {
+    const float k = gp.freq[q] * gp.inv_rc;
+    float sn, cs;
+    sincosf(k * d, &sn, &cs);
+    const float B = pre * sn * inv;
+    const float dB = pre * (k * cs * inv - sn * inv * inv);
+    const float zb = zbar[e * 16 + 4 + q];
+    ub = fmaf(zb, B, ub);
+    db = fmaf(uu * zb, dB, db);
+  }
+  db = fmaf(ub, du, db);
+  float gx = db * n[0], gy = db * n[1], gz = db * n[2];
+  // sum_m Ybar[m] dY_m/dr,  dY^l/dr = (grad P_l(n) - l Y^l n) / d
+  if (gp.lmax >= 1) {
+    const float s3 = 1.7320508075688772f;
+    const float* yb = ybar + e * gp.dsh;
+    const float b1 = yb[1], b2 = yb[2], b3 = yb[3];
+    const float dot1 = b1 * n[1] + b2 * n[2] + b3 * n[0];  // sum_m yb_m Y_m / sqrt3
+    gx += s3 * inv * (b3 - dot1 * n[0]);
+    gy += s3 * inv * (b1 - dot1 * n[1]);
+    gz += s3 * inv * (b2 - dot1 * n[2]);
+    if (gp.lmax >= 2) {
+      const float s5 = 2.2360679774997896f, s15 = 3.8729833462074170f;
+      const float c0 = yb[4], c1 = yb[5], c2 = yb[6], c3 = yb[7], c4 = yb[8];
+      float Y2[5] = {s15 * n[0] * n[1], s15 * n[1] * n[2], 0.5f * s5 * (2.f * n[2] * n[2] - n[0] * n[0] - n[1] * n[1]),
+                     s15 * n[0] * n[2], 0.5f * s15 * (n[0] * n[0] - n[1] * n[1])};
+      const float sy = c0 * Y2[0] + c1 * Y2[1] + c2 * Y2[2] + c3 * Y2[3] + c4 * Y2[4];
+      // grad P2 at n
+      const float px = s15 * (c0 * n[1] + c3 * n[2]) + 0.5f * s5 * c2 * (-2.f * n[0]) + 0.5f * s15 * c4 * (2.f * n[0]);
+      const float py = s15 * (c0 * n[0] + c1 * n[2]) + 0.5f * s5 * c2 * (-2.f * n[1]) + 0.5f * s15 * c4 * (-2.f * n[1]);
+      const float pz = s15 * (c1 * n[1] + c3 * n[0]) + 0.5f * s5 * c2 * (4.f * n[2]);
+      gx += inv * (px - 2.f * sy * n[0]);
+      gy += inv * (py - 2.f * sy * n[1]);
+      gz += inv * (pz - 2.f * sy * n[2]);
+    }
+  }
+  g[ge * 3] = gx;
+  g[ge * 3 + 1] = gy;
+  g[ge * 3 + 2] = gz;
+}
+
+// ----------------------------------------------------------------- A12 force gather
+__global__ void k_force(int64_t n, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ rev,
+                        const float* __restrict__ g, double* __restrict__ F, int* __restrict__ flags) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  double f[3] = {0, 0, 0};
+  for (int64_t e = row_ptr[a]; e < row_ptr[a + 1]; ++e) {
+    const int32_t r = rev[e];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) f[d] += (double)g[e * 3 + d] - (r >= 0 ? (double)g[(int64_t)r * 3 + d] : 0.0);
+  }
+  bool bad = false;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    F[a * 3 + d] = f[d];
+    bad = bad || !isfinite(f[d]);
+  }
+  if (bad) atomicOr(flags + 2, 1);
+}
+
+// ----------------------------------------------------------------- dispatch
+template <int NL, int LMAX, int K>
+void launch_tp(bool fwd, const TpArgs& t, cudaStream_t st) {
+  const unsigned blocks = (unsigned)((t.ch.n_c * 32 + 127) / 128);
+  if (blocks == 0) return;
+  if (fwd) k_tp_fwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
+  else k_tp_bwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
+  ALG_LAUNCH_CHECK();
+}
+
+void tp_dispatch(int NL, int LMAX, int K, bool fwd, const TpArgs& t, cudaStream_t st) {
+#define ALG_TP(nl, lm, k) \
+  if (NL == nl && LMAX == lm && K == k) return launch_tp<nl, lm, k>(fwd, t, st);
+  ALG_TP(2, 1, 0) ALG_TP(2, 1, 1)
+  ALG_TP(2, 2, 0) ALG_TP(2, 2, 1)
+  ALG_TP(3, 0, 0) ALG_TP(3, 0, 1) ALG_TP(3, 0, 2)
+  ALG_TP(3, 1, 0) ALG_TP(3, 1, 1) ALG_TP(3, 1, 2)
+  ALG_TP(3, 2, 0) ALG_TP(3, 2, 1) ALG_TP(3, 2, 2)
+#undef ALG_TP
+  throw CudaError("no TP kernel for this architecture");
+}
+
+size_t floats_per_edge(const Model& M) {
+  const int dsh = (M.lmax + 1) * (M.lmax + 1);
+  size_t f = 16 + 32 + 32 + 64 + 64 + 128 + 1 + dsh + 2 * 128;
+  size_t tmax = 0, vmax = 0, nwmax = 0, nsmax = 0;
+  for (int k = 0; k < M.n_layers; ++k) {
+    const LayerInfo& L = M.L[k];
+    f += L.nw + 128;
+    if (k >= 1) f += (size_t)L.A.dim_in * kC;
+    tmax = std::max(tmax, (size_t)L.A.dim_T * kC);
+    vmax = std::max(vmax, (size_t)L.A.dim_in * kC);
+    nwmax = std::max(nwmax, (size_t)L.nw);
+    nsmax = std::max(nsmax, (size_t)L.A.n_s * kC);
+  }
+  f += tmax + 2 * 128 + nsmax + 2 * vmax + nwmax + dsh + 1 + 16 + 64 + 32;
+  return f;
+}
+
+void reserve_ws(allegro_ctx* c, size_t e_cap, size_t a_cap) {
+  Workspace& w = c->ws;
+  const Model& M = c->model;
+  const int dsh = (M.lmax + 1) * (M.lmax + 1);
+  w.z.reserve(e_cap * 16);
+  w.a1.reserve(e_cap * 32);
+  w.h1.reserve(e_cap * 32);
+  w.a2.reserve(e_cap * 64);
+  w.h2.reserve(e_cap * 64);
+  w.m.reserve(e_cap * 128);
+  w.u.reserve(e_cap);
+  w.Y.reserve(e_cap * dsh);
+  w.xa.reserve(e_cap * 128);
+  w.xb.reserve(e_cap * 128);
+  size_t tmax = 0, vmax = 0, nwmax = 0, nsmax = 0;
+  for (int k = 0; k < M.n_layers; ++k) {
+    const LayerInfo& L = M.L[k];
+    w.w[k].reserve(e_cap * L.nw);
+    w.h[k].reserve(e_cap * 128);
+    if (k >= 1) w.V[k].reserve(e_cap * L.A.dim_in * kC);
+    w.G[k].reserve(a_cap * dsh * kC);
+    tmax = std::max(tmax, (size_t)L.A.dim_T * kC);
+    vmax = std::max(vmax, (size_t)L.A.dim_in * kC);
+    nwmax = std::max(nwmax, (size_t)L.nw);
+    nsmax = std::max(nsmax, (size_t)L.A.n_s * kC);
+  }
+  w.T.reserve(e_cap * tmax);
+  w.xbar_a.reserve(e_cap * 128);
+  w.xbar_b.reserve(e_cap * 128);
+  w.sbar.reserve(e_cap * nsmax);
+  w.vbar_a.reserve(e_cap * vmax);
+  w.vbar_b.reserve(e_cap * vmax);
+  w.wbar.reserve(e_cap * nwmax);
+  w.ybar.reserve(e_cap * dsh);
+  w.ubar.reserve(e_cap);
+  w.zbar.reserve(e_cap * 16);
+  w.ab2.reserve(e_cap * 64);
+  w.ab1.reserve(e_cap * 32);
+  w.e_cap = e_cap;
+  w.a_cap = a_cap;
+}
+
+void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
+  const Model& M = c->model;
+  Workspace& w = c->ws;
+  cudaStream_t st = c->stream;
+  const int64_t E = ch.n_e;
+  const int64_t ecap = (int64_t)w.e_cap;
+  const int dsh = (M.lmax + 1) * (M.lmax + 1);
+  const float inv_sqrt_nbar = (float)(1.0 / std::sqrt(M.nbar));
+  GeomParams gp;
+  gp.rc = (float)M.r_max;
+  gp.inv_rc = (float)(1.0 / M.r_max);
+  for (int q = 0; q < kNB; ++q) gp.freq[q] = M.w.bessel[q];
+  gp.lmax = M.lmax;
+  gp.dsh = dsh;
+  if (E > 0) {
+    k_geom<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, c->aowner.p, c->species.p, w.z.p,
+                                             w.Y.p, w.u.p);
+    ALG_LAUNCH_CHECK();
+  }
+  auto G = [&](const float* A, int lda, const float* W, int N, int K, float* C, float s, int epi) {
+    GemmArgs g;
+    g.M = E;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.W = W;
+    g.C = C;
+    g.s = s;
+    g.epi = epi;
+    return g;
+  };
+  // ---- two-body MLP (E4, E5) ----
+  {
+    GemmArgs g = G(w.z.p, 16, M.w.tb_w0, 32, 16, w.h1.p, 1.f / std::sqrt(12.f), EPI_SILU);
+    g.aux = w.a1.p;
+    gemm(g, st);
+    g = G(w.h1.p, 32, M.w.tb_w1, 64, 32, w.h2.p, kCSilu / std::sqrt(32.f), EPI_SILU);
+    g.aux = w.a2.p;
+    gemm(g, st);
+    g = G(w.h2.p, 64, M.w.tb_w2, 128, 64, w.xa.p, kCSilu / std::sqrt(64.f), EPI_UMUL_SAVE);
+    g.aux = w.m.p;
+    g.u = w.u.p;
+    gemm(g, st);
+  }
+  float* x = w.xa.p;
+  float* xn = w.xb.p;
+  TpArgs tp{};
+  tp.ch = ch;
+  tp.row_ptr = c->row_ptr.p;
+  tp.Y = w.Y.p;
+  tp.T = w.T.p;
+  tp.e_cap = ecap;
+  tp.inv_sqrt_nbar = inv_sqrt_nbar;
+  const unsigned warp_blocks = (unsigned)((ch.n_c * 32 + 127) / 128);
+  // ---- layers (E6) ----
+  for (int k = 0; k < M.n_layers; ++k) {
+    const LayerInfo& L = M.L[k];
+    gemm(G(x, 128, M.w.env[k], L.nw, 128, w.w[k].p, 1.f / std::sqrt(128.f), EPI_STORE), st);
+    tp.w = w.w[k].p;
+    tp.V = k >= 1 ? w.V[k].p : nullptr;
+    tp.G = w.G[k].p;
+    tp_dispatch(M.n_layers, M.lmax, k, true, tp, st);
+    if (k < M.n_layers - 1) {
+      for (int o = 0; o < L.A.out.n; ++o) {
+        const int dim = ir_dim(L.A.out.v[o]);
+        GemmArgs g = G(w.T.p + (int64_t)L.t_base[o] * ecap, L.A.n_to[o] * kC, M.w.lin[k][o], kC, L.A.n_to[o] * kC,
+                       w.V[k + 1].p + (int64_t)M.L[k + 1].v_base[o] * ecap, 1.f / std::sqrt((float)(kC * L.A.n_to[o])),
+                       EPI_STORE);
+        g.M = E * dim;
+        gemm(g, st);
+      }
+    }
+    GemmArgs g = G(x, 128, M.w.lat[k], 128, L.fan_lat, xn, 1.f / std::sqrt((float)L.fan_lat), EPI_RESID);
+    g.K1 = 128;
+    g.A2 = w.T.p;  // T_0e = the scalars s, [E][n_s C] in (q, c) order
+    g.lda2 = L.A.n_s * kC;
+    g.aux = w.h[k].p;
+    g.X = x;
+    g.u = w.u.p;
+    g.alpha = kResA;
+    g.beta = kResB;
+    gemm(g, st);
+    std::swap(x, xn);
+  }
+  // ---- energies (E7, E8) and x-bar^L ----
+  float* xb = w.xbar_a.p;
+  float* xbn = w.xbar_b.p;
+  if (warp_blocks) {
+    k_energy<<<warp_blocks, 128, 0, st>>>(ch, c->row_ptr.p, c->species.p, x, M.w.wout, xb, c->e_atom.p, M.sigma[0],
+                                          M.sigma[1], M.mu[0], M.mu[1], inv_sqrt_nbar);
+    ALG_LAUNCH_CHECK();
+  }
+  // ---- reverse mode (E9) ----
+  ALG_CUDA(cudaMemsetAsync(w.ubar.p, 0, sizeof(float) * E, st));
+  ALG_CUDA(cudaMemsetAsync(w.ybar.p, 0, sizeof(float) * E * dsh, st));
+  float* vb = w.vbar_a.p;   // V-bar^{k+1} (input to layer k)
+  float* vbn = w.vbar_b.p;  // V-bar^k (output of layer k)
+  const unsigned edge_warp_blocks = (unsigned)((E * 32 + 255) / 256);
+  for (int k = M.n_layers - 1; k >= 0; --k) {
+    const LayerInfo& L = M.L[k];
+    if (E > 0) {
+      k_rowdot<<<edge_warp_blocks, 256, 0, st>>>(E, w.h[k].p, xb, kResB, w.ubar.p);
+      ALG_LAUNCH_CHECK();
+    }
+    const float sl = 1.f / std::sqrt((float)L.fan_lat);
+    {
+      GemmArgs g = G(xb, 128, M.w.latT_x[k], 128, 128, xbn, sl, EPI_URESID);
+      g.X = xb;
+      g.u = w.u.p;
+      g.alpha = kResA;
+      g.beta = kResB;
+      gemm(g, st);
+      g = G(xb, 128, M.w.latT_s[k], L.A.n_s * kC, 128, w.sbar.p, sl, EPI_USCALE);
+      g.u = w.u.p;
+      g.beta = kResB;
+      gemm(g, st);
+    }
+    tp.w = w.w[k].p;
+    tp.V = k >= 1 ? w.V[k].p : nullptr;
+    tp.G = w.G[k].p;
+    tp.wbar = w.wbar.p;
+    tp.ybar = w.ybar.p;
+    tp.Vb = vbn;
+    if (k == M.n_layers - 1) {
+      tp.Tb[0] = w.sbar.p;  // last layer: out = {0e}, T-bar = s-bar
+    } else {
+      for (int o = 0; o < L.A.out.n; ++o) {
+        const int dim = ir_dim(L.A.out.v[o]);
+        float* dst = w.T.p + (int64_t)L.t_base[o] * ecap;
+        GemmArgs g = G(vb + (int64_t)M.L[k + 1].v_base[o] * ecap, kC, M.w.linT[k][o], L.A.n_to[o] * kC, kC, dst,
+                       1.f / std::sqrt((float)(kC * L.A.n_to[o])), EPI_STORE);
+        g.M = E * dim;
+        if (L.A.out.v[o].l == 0 && L.A.out.v[o].p == 1) {
+          g.epi = EPI_ADDX;
+          g.X = w.sbar.p;
+        }
+        gemm(g, st);
+        tp.Tb[o] = dst;
+      }
+    }
+    tp_dispatch(M.n_layers, M.lmax, k, false, tp, st);
+    {
+      GemmArgs g = G(w.wbar.p, L.nw, M.w.envT[k], 128, L.nw, xbn, 1.f / std::sqrt(128.f), EPI_ACC);
+      gemm(g, st);
+    }
+    std::swap(xb, xbn);
+    std::swap(vb, vbn);
+  }
+  // ---- two-body reverse ----
+  if (E > 0) {
+    k_rowdot<<<edge_warp_blocks, 256, 0, st>>>(E, w.m.p, xb, 1.f, w.ubar.p);
+    ALG_LAUNCH_CHECK();
+  }
+  {
+    GemmArgs g = G(xb, 128, M.w.tb_w2T, 64, 128, w.ab2.p, kCSilu / std::sqrt(64.f), EPI_DSILU);
+    g.X = w.a2.p;
+    g.u = w.u.p;
+    gemm(g, st);
+    g = G(w.ab2.p, 64, M.w.tb_w1T, 32, 64, w.ab1.p, kCSilu / std::sqrt(32.f), EPI_DSILU);
+    g.X = w.a1.p;
+    gemm(g, st);
+    g = G(w.ab1.p, 32, M.w.tb_w0T, 16, 32, w.zbar.p, 1.f / std::sqrt(12.f), EPI_STORE);
+    gemm(g, st);
+  }
+  if (E > 0) {
+    k_geom_bwd<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, w.ubar.p, w.zbar.p, w.ybar.p,
+                                                 c->g.p);
+    ALG_LAUNCH_CHECK();
+  }
+}
+
+}  // namespace
+
+void compute_forces(allegro_ctx* c) {
+  cudaStream_t st = c->stream;
+  const int64_t n = c->n;
+  const int64_t E = c->n_edges;
+  c->e_atom.reserve(n + 1);
+  c->frc.reserve(3 * n + 3);
+  // chunk plan: complete rows, at most e_cap edges per chunk
+  const size_t fpe = floats_per_edge(c->model);
+  size_t e_cap = std::max<size_t>(4096, c->ws_budget_bytes / (fpe * sizeof(float)));
+  e_cap = std::min<size_t>(e_cap, (size_t)std::max<int64_t>(E, 4096));
+  c->h_row_ptr.resize(n + 1);
+  ALG_CUDA(cudaMemcpyAsync(c->h_row_ptr.data(), c->row_ptr.p, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+  ALG_CUDA(cudaStreamSynchronize(st));
+  std::vector<ChunkPtrs> chunks;
+  int64_t a = 0;
+  size_t a_cap = 1;
+  while (a < n) {
+    int64_t b = a;
+    while (b < n && (b == a || (size_t)(c->h_row_ptr[b + 1] - c->h_row_ptr[a]) <= e_cap)) ++b;
+    ChunkPtrs ch{a, b - a, c->h_row_ptr[a], (int64_t)c->h_row_ptr[b] - c->h_row_ptr[a]};
+    if ((size_t)ch.n_e > e_cap) e_cap = ch.n_e;  // a single row larger than the cap
+    a_cap = std::max<size_t>(a_cap, ch.n_c);
+    chunks.push_back(ch);
+    a = b;
+  }
+  reserve_ws(c, e_cap, a_cap);
+  for (const ChunkPtrs& ch : chunks) run_chunk(c, ch);
+  ALG_CUDA(cudaMemsetAsync(c->flags.p + 2, 0, sizeof(int), st));
+  if (n > 0) {
+    k_force<<<ceil_div(n, 256), 256, 0, st>>>(n, c->row_ptr.p, c->rev.p, c->g.p, c->frc.p, c->flags.p);
+    ALG_LAUNCH_CHECK();
+  }
+  c->e_pot = sum_e_atom(c);
+}
+
+}  // namespace allegro

@@ -1,0 +1,100 @@
+// scan.cu -- exclusive prefix sum of int32 counts (cell counts, ghost counts,
+// neighbour counts -> CSR offsets).  Three-phase block scan, recursive over the
+// block sums; deterministic.
+#include "ctx.cuh"
+
+namespace allegro {
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int block_exclusive(int v, int* smem, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < kScanThreads / 32 ? smem[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < kScanThreads / 32) smem[lane] = s;
+  }
+  __syncthreads();
+  const int warp_off = wid > 0 ? smem[wid - 1] : 0;
+  *total = smem[kScanThreads / 32 - 1];
+  return warp_off + x - v;
+}
+
+__global__ void scan_tiles(const int32_t* __restrict__ in, int32_t* __restrict__ out, int32_t* __restrict__ sums, int64_t n) {
+  __shared__ int smem[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int v[kScanItems];
+  int s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = (base + i < n) ? in[base + i] : 0;
+    s += v[i];
+  }
+  int total;
+  int run = block_exclusive(s, smem, &total);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) out[base + i] = run;
+    run += v[i];
+  }
+  if (threadIdx.x == 0 && sums) sums[blockIdx.x] = total;
+}
+
+__global__ void scan_add(int32_t* __restrict__ out, const int32_t* __restrict__ offs, int64_t n) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  const int o = offs[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < n) out[base + i] += o;
+}
+
+__global__ void scan_total(const int32_t* in, int32_t* out, int64_t n) {
+  // out[n] = out[n-1] + in[n-1]
+  if (n > 0) out[n] = out[n - 1] + in[n - 1];
+  else out[0] = 0;
+}
+
+void scan_rec(cudaStream_t st, const int32_t* in, int32_t* out, int64_t n, DBuf<int32_t>* tmp, int level) {
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  if (tiles <= 1) {
+    scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, nullptr, n);
+    ALG_LAUNCH_CHECK();
+    return;
+  }
+  // block sums for this level live in tmp[level]
+  tmp[level].reserve(2 * tiles + 2);
+  int32_t* sums = tmp[level].p;
+  int32_t* offs = sums + tiles + 1;
+  scan_tiles<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, sums, n);
+  ALG_LAUNCH_CHECK();
+  scan_rec(st, sums, offs, tiles, tmp, level + 1);
+  scan_add<<<(unsigned)tiles, kScanThreads, 0, st>>>(out, offs, n);
+  ALG_LAUNCH_CHECK();
+}
+
+DBuf<int32_t> g_scan_tmp[8];
+
+}  // namespace
+
+void exclusive_scan(allegro_ctx* c, const int32_t* in, int32_t* out, int64_t n) {
+  scan_rec(c->stream, in, out, n, g_scan_tmp, 0);
+  scan_total<<<1, 1, 0, c->stream>>>(in, out, n);
+  ALG_LAUNCH_CHECK();
+}
+
+}  // namespace allegro

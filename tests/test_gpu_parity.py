@@ -1,0 +1,221 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bars (BASELINE.json north_star; SURVEY.md §8(c) reading row 20):
+* neighbour lists bit-exact as sorted (i_gid, j_gid, shift) sets;
+* energy: |dE| / sum_a |E_a - mu| <= 1e-5 and max_a |dE_a| <= 1e-5 max_a |E_a|;
+* forces: max_{a,alpha} |dF| <= 1e-4 eV/A (sigma calibrated so RMS|F| = 1 eV/A).
+"""
+import numpy as np
+import pytest
+
+from oracle import allegro as oa, md as omd, neighbors as onb, weights_io
+from synth import configs, nh3, weights as sw
+
+pytestmark = pytest.mark.gpu
+
+E_TOL = 1e-5
+F_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2303_08169_b200 as pb
+
+    return pb
+
+
+def _edge_set(i, j, s):
+    return sorted(zip(np.asarray(i).tolist(), np.asarray(j).tolist(), map(tuple, np.asarray(s).tolist())))
+
+
+def _check_energy_forces(ref, e_tot, e_atom, F, atoms=None):
+    ea = ref["e_atom"] if atoms is None else ref["e_atom"][atoms]
+    fa = ref["forces"] if atoms is None else ref["forces"][atoms]
+    if atoms is None:
+        norm = np.abs(ea).sum()
+        assert abs(e_tot - ref["energy"]) <= E_TOL * norm, (e_tot, ref["energy"])
+    assert np.abs(e_atom - ea).max() <= E_TOL * np.abs(ea).max()
+    err = np.abs(F - fa).max()
+    assert err <= F_TOL, err
+    return err
+
+
+def _model_file(tmp_path, L, lmax, rc, sigma):
+    path = str(tmp_path / f"m{L}{lmax}.algw")
+    sw.write(path, L, lmax, rc, sw.generate(L, lmax, 0), sw.nbar_for(rc), (sigma, sigma), (0.0, 0.0))
+    return path
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_edges_bit_exact(pb, cfg):
+    c = configs.CONFIGS[cfg]
+    s = configs.system(cfg)
+    m = pb.Allegro(configs.weight_file(cfg), s.box)
+    m.compute_energy_forces(s.pos, s.species)
+    gi, gj, gs = m.get_edges()
+    ri, rj, rn = onb.cell_list(onb.wrap(s.pos, s.box), s.box, c.r_cut)
+    assert _edge_set(gi, gj, gs) == _edge_set(ri, rj, rn)
+    # canonical row order: by centre, then (j_gid, shift)
+    order = np.lexsort((gs[:, 2], gs[:, 1], gs[:, 0], gj, gi))
+    assert np.array_equal(order, np.arange(len(gi)))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_edges_random_boxes_incl_multi_image(pb, tmp_path, seed):
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.integers(1, 200))
+    rc = 5.0
+    lo = 0.7 * rc if seed % 2 == 0 else 2.5 * rc
+    box = rng.uniform(lo, lo + 2 * rc, size=3)
+    s = nh3.random_box(n, box, seed)
+    m = pb.Allegro(_model_file(tmp_path, 2, 1, rc, 1.0), box)
+    m.compute_energy_forces(s.pos, s.species)
+    gi, gj, gs = m.get_edges()
+    ri, rj, rn = onb.brute_force(onb.wrap(s.pos, box), box, rc)
+    assert _edge_set(gi, gj, gs) == _edge_set(ri, rj, rn)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_energy_forces_parity(pb, cfg):
+    s = configs.system(cfg)
+    wf = configs.weight_file(cfg)
+    model = weights_io.read(wf)
+    ref = oa.energy_forces(model, s.pos, s.species, s.box)
+    m = pb.Allegro(wf, s.box)
+    e, ea, F = m.compute_energy_forces(s.pos, s.species)
+    err = _check_energy_forces(ref, e, ea, F)
+    # per-edge dE/dr_e in the same (canonical) order
+    g = m.get_edge_grad()
+    assert np.abs(g - ref["g"]).max() <= F_TOL
+    print(f"{cfg}: max|dF| = {err:.3g} eV/A, E = {e:.6f} vs {ref['energy']:.6f}")
+
+
+@pytest.mark.parametrize("L,lmax", [(2, 1), (2, 2), (3, 0), (3, 1), (3, 2)])
+def test_every_architecture_on_c1_geometry(pb, tmp_path, L, lmax):
+    s = configs.system("C1")
+    wf = _model_file(tmp_path, L, lmax, 5.0, 3.0)
+    ref = oa.energy_forces(weights_io.read(wf), s.pos, s.species, s.box)
+    m = pb.Allegro(wf, s.box)
+    e, ea, F = m.compute_energy_forces(s.pos, s.species)
+    _check_energy_forces(ref, e, ea, F * 1.0)
+
+
+def test_c3_full_size_sampled(pb):
+    """C3 at full size (110,592 atoms, paper's l=2 model) in the launch configuration
+    the bench uses; the oracle computes sampled atoms one by one (rows of the atoms
+    and of all their neighbours)."""
+    s = configs.system("C3")
+    wf = configs.weight_file("C3")
+    m = pb.Allegro(wf, s.box)
+    e, ea, F = m.compute_energy_forces(s.pos, s.species)
+    atoms = np.array([0, 55555, 110591])
+    Fo, Eo, _ = oa.sampled_forces(weights_io.read(wf), s.pos, s.species, s.box, atoms)
+    assert np.abs(F[atoms] - Fo).max() <= F_TOL
+    assert np.abs(ea[atoms] - Eo).max() <= E_TOL * np.abs(ea).max()
+    # properties at any size: zero net force, per-row edge-set rows of the sample
+    assert np.abs(F.sum(0)).max() < 1e-6 * s.n
+    gi, gj, gs = m.get_edges()
+    ri, rj, rn = onb.cell_list(onb.wrap(s.pos, s.box), s.box, 6.0, atoms)
+    mask = np.isin(gi, atoms)
+    assert _edge_set(gi[mask], gj[mask], gs[mask]) == _edge_set(ri, rj, rn)
+
+
+def test_deterministic_and_device_pointers(pb):
+    import torch
+
+    s = configs.system("C2")
+    m = pb.Allegro(configs.weight_file("C2"), s.box)
+    e1, a1, F1 = m.compute_energy_forces(s.pos, s.species)
+    e2, a2, F2 = m.compute_energy_forces(s.pos, s.species)
+    assert e1 == e2 and np.array_equal(F1, F2) and np.array_equal(a1, a2)
+    pos = torch.tensor(s.pos, device="cuda")
+    spc = torch.tensor(s.species, device="cuda", dtype=torch.int32)
+    e3, a3, F3 = m.compute_energy_forces(pos, spc)
+    assert e3 == e1 and np.array_equal(F3.cpu().numpy(), F1)
+
+
+def test_translation_and_replica(pb):
+    s = configs.system("C1")
+    wf = configs.weight_file("C1")
+    m = pb.Allegro(wf, s.box)
+    e, _, F = m.compute_energy_forces(s.pos, s.species)
+    big = nh3.replicate(s, (2, 2, 2))
+    m8 = pb.Allegro(wf, big.box)
+    e8, _, F8 = m8.compute_energy_forces(big.pos, big.species)
+    assert abs(e8 - 8 * e) <= 1e-5 * abs(8 * e) + 1e-5
+    assert np.abs(F8 - np.tile(F, (8, 1))).max() <= 1e-5
+
+
+def test_edge_cases(pb, tmp_path):
+    wf = _model_file(tmp_path, 2, 1, 5.0, 1.0)
+    box = np.array([30.0, 30.0, 30.0])
+    m = pb.Allegro(wf, box)
+    # isolated atoms: no edges, E = mu = 0, F = 0
+    pos = np.array([[1.0, 1.0, 1.0], [15.0, 15.0, 15.0]])
+    e, ea, F = m.compute_energy_forces(pos, np.array([0, 1]))
+    assert e == 0.0 and np.all(F == 0)
+    # species outside {0,1} and non-finite positions are rejected
+    with pytest.raises(pb.AllegroError) as ex:
+        m.compute_energy_forces(pos, np.array([0, 2]))
+    assert ex.value.code == pb.E_ARG
+    with pytest.raises(pb.AllegroError) as ex:
+        m.compute_energy_forces(np.array([[np.nan, 1.0, 1.0], [2.0, 2.0, 2.0]]), np.array([0, 1]))
+    assert ex.value.code == pb.E_ARG
+    # positions outside the box are wrapped
+    e1, _, F1 = m.compute_energy_forces(pos + np.array([30.0, -30.0, 60.0]), np.array([0, 1]))
+    assert e1 == 0.0
+
+
+def test_md_snapshot_parity_and_outliers(pb):
+    """C1: 10 NVE steps at dt = 2 fs on the GPU; the final snapshot is re-evaluated by
+    the oracle (trajectories are chaotic, so parity is per evaluation: reading row 21)."""
+    s = configs.system("C1")
+    wf = configs.weight_file("C1")
+    model = weights_io.read(wf)
+    m = pb.Allegro(wf, s.box)
+    m.md_set_state(s.species, s.pos, s.vel)
+    p0, v0, f0 = m.md_get_state()
+    ref0 = oa.energy_forces(model, s.pos, s.species, s.box)
+    assert np.abs(f0 - ref0["forces"]).max() <= F_TOL
+    mean0, sig0 = m.md_force_baseline()
+    rep = m.md_step(10, 2.0)
+    assert rep.steps_done == 10
+    p, v, f = m.md_get_state()
+    assert np.all(p >= 0) and np.all(p < s.box)
+    ref = oa.energy_forces(model, p, s.species, s.box)
+    assert np.abs(f - ref["forces"]).max() <= F_TOL
+    assert abs(rep.e_pot - ref["energy"]) <= E_TOL * np.abs(ref["e_atom"]).sum()
+    # one oracle Verlet step from the same state agrees with one GPU step
+    m.md_set_state(s.species, p, v)
+    m.md_step(1, 2.0)
+    p1, v1, _ = m.md_get_state()
+    fn = lambda q: (lambda r: (r["energy"], r["forces"]))(oa.energy_forces(model, q, s.species, s.box))
+    po, vo, _, _ = omd.verlet(fn, p, v, s.species, s.box, 2.0, 1)
+    dp = p1 - po
+    dp -= s.box * np.round(dp / s.box)
+    # the GPU forces differ from the oracle's by <= F_TOL: bound the resulting kick
+    dv_tol = 2.0 * omd.KAPPA * F_TOL / omd.MASS_H
+    assert np.abs(v1 - vo).max() <= dv_tol and np.abs(dp).max() <= 2.0 * dv_tol + 1e-12
+    # outlier count (integer): bit-exact against the count on the same forces
+    for k in (0.5, 1.0, 2.0, 5.0):
+        assert m.md_count_outliers(mean0, sig0, k) == omd.count_outliers(f1 := m.md_get_state()[2], mean0, sig0, k)
+    mo, so = omd.force_baseline(f1)
+    mg, sg = m.md_force_baseline()
+    assert abs(mo - mg) < 1e-12 * max(1, mo) and abs(so - sg) < 1e-10 * max(1, so)
+
+
+def test_md_energy_conservation_c2(pb):
+    """C2 (1,024 atoms): NVE energy drift over 200 steps of 2 fs stays small (reported)."""
+    s = configs.system("C2")
+    m = pb.Allegro(configs.weight_file("C2"), s.box)
+    m.md_set_state(s.species, s.pos, s.vel)
+    r0 = m.md_step(1, 2.0)
+    r = m.md_step(199, 2.0)
+    assert r.steps_done == 199
+    drift = abs(r.e_total - r0.e_total) / s.n
+    print(f"C2 drift per atom over 200 steps: {drift:.3g} eV, T = {r.temperature:.1f} K")
+    assert drift < 1e-2
