@@ -1,0 +1,306 @@
+"""Benchmark of the Allegro-Legato NNQMD hot path: one MD step = neighbour build +
+Allegro energy/forces + velocity Verlet (BASELINE.json metric: atom-steps/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5|C4|C3|C2|C1]
+                    [--impl ours|reference] [--no-cpu-baseline]
+
+N > 1 is launched by torchrun (one process per GPU).  The default workload is C5
+(BASELINE.json configs[4], the metric's weak-scaling configuration): 500,000 atoms of
+liquid NH3 per GPU with the paper's l=1 3-layer model.  Prints ONE JSON line on rank 0.
+``--impl reference`` times the fp64 CPU oracle (the reference arm of this tier) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "atom-steps/s (Allegro force+Verlet) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "atom-steps/s"
+DT_FS = 2.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def _fp32_alu_peak_tflops(sm_mhz):
+    # 148 SMs x 128 FP32 lanes x 2 flop/FMA x clock (B200_PROFILING.md unit counts)
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(gpu), "-lms", "200"], stdout=open(self.path, "w"),
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """The reference arm: the fp64 oracle as it stands, on host cores, rank 0 only."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from synth import configs
+
+    cfg = configs.CONFIGS[args.config]
+    sample = args.ref_sample
+    rec = _oracle_rate(cfg, sample, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rec["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_dict(cfg, args.gpus, None),
+        "cpu_baseline": {"value": rec["value"], "unit": UNIT, "cores": rec["cores"], "kind": "oracle",
+                         "sample": rec["sample"]},
+        "e2e": {"value": rec["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _oracle_rate(cfg, sample, steps, warmup):
+    """Oracle force evaluation of ``sample`` centre rows of the cfg box per step."""
+    from threadpoolctl import threadpool_info
+
+    from oracle import allegro as oa, neighbors as onb, weights_io
+    from synth import configs
+
+    s = configs.system(cfg)
+    model = weights_io.read(configs.weight_file(cfg))
+    pos = onb.wrap(s.pos, s.box)
+    rng = np.random.default_rng(0)
+    times = []
+    for it in range(warmup + steps):
+        centers = np.sort(rng.choice(s.n, sample, replace=False))
+        t0 = time.perf_counter()
+        oa.energy_forces(model, pos, s.species, s.box, centers=centers)
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            times.append(dt)
+    t = float(np.mean(times))
+    cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    return {
+        "value": sample / t,
+        "ms_per_step": 1e3 * t,
+        "cores": cores,
+        "sample": (f"{sample} random centre rows of the {cfg.name} box per step (neighbour search + Allegro "
+                   f"energy/forces of those rows, fp64 numpy; Verlet O(N) excluded), mean of {steps} steps; "
+                   f"value = rows / s"),
+    }
+
+
+def _config_dict(cfg, n_gpus, edges):
+    from oracle import irreps  # parameter count only (pure arithmetic of the architecture)
+
+    return {
+        "workload": f"{cfg.name}: {cfg.description}, r_c={cfg.r_cut} A, NVE dt={DT_FS} fs, rebuild every step",
+        "atoms_per_gpu": cfg.n_atoms,
+        "atoms_total": cfg.n_atoms * n_gpus,
+        "edges_per_gpu": edges,
+        "layers": cfg.n_layers,
+        "lmax": cfg.lmax,
+        "params": irreps.param_count(cfg.n_layers, cfg.lmax),
+        "precision": "fp32 CUDA-core GEMM + fp32 TP (fp64 positions, Verlet, energy sums)",
+        "parallelism": "single domain" if n_gpus == 1 else f"{n_gpus} independent replica domains (no halo exchange yet)",
+        "l2": "inputs larger than L2 (per-edge activations are GBs per step)",
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=512)
+    ap.add_argument("--ref-sample", type=int, default=96)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    import paper_2303_08169_b200 as pb
+    from synth import configs
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    cfg = configs.CONFIGS[args.config]
+    s = configs.system(cfg)
+    wf = configs.weight_file(cfg)
+    stream = torch.cuda.current_stream()
+    m = pb.Allegro(wf, s.box, device=local, n_atoms=s.n, stream=stream.cuda_stream)
+    m.md_set_state(s.species, s.pos, s.vel)
+    m.md_step(args.warmup, DT_FS)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    # ---- timed region: K steps with inputs resident in HBM ----
+    clocks = ClockSampler(local)
+    time.sleep(0.3)
+    m.profile(True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    rep = m.md_step(args.steps, DT_FS)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = m.launch_count()
+    prof = m.profile_read()
+    m.profile(False)
+    clk = clocks.stop()
+    t = torch.tensor([ms], device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = s.n * ws * args.steps / (ms_max / 1e3)
+
+    # ---- e2e: the same steps through md_step_host with pinned host state ----
+    pos, vel, frc = m.md_get_state()
+    h_spc = torch.from_numpy(s.species.astype(np.int32)).pin_memory()
+    h_pos = torch.from_numpy(pos).pin_memory()
+    h_vel = torch.from_numpy(vel).pin_memory()
+    h_frc = torch.from_numpy(frc).pin_memory()
+    m.md_step_host(h_spc, h_pos, h_vel, h_frc, 1, DT_FS)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        m.md_step_host(h_spc, h_pos, h_vel, h_frc, 1, DT_FS)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    te = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = s.n * ws * args.steps / (float(te.item()) / 1e3)
+    h2d = s.n * (4 + 3 * 24)
+    d2h = s.n * 3 * 24
+
+    # ---- roofline of the dominant kernel class (live CUDA events, algorithmic work) ----
+    peaks, peak_src = _peaks()
+    total_ms = sum(v[0] for v in prof.values())
+    dom = max(prof, key=lambda k: prof[k][0])
+    d_ms, d_fl, d_by, d_n = prof[dom]
+    kernels = {}
+    for k, (kms, kfl, kby, kn) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
+        if kn == 0:
+            continue
+        kernels[k] = {"ms_per_step": round(kms / args.steps, 4), "share": round(kms / max(total_ms, 1e-9), 4),
+                      "launches_per_step": kn / args.steps,
+                      "gflops": round(kfl / max(kms, 1e-9) / 1e6, 1), "gbs": round(kby / max(kms, 1e-9) / 1e6, 1)}
+    alu_peak = _fp32_alu_peak_tflops(peaks.get("sm_max_mhz", 1965.0))
+    if dom in ("gemm", "tp_fwd", "tp_bwd", "energy", "rowdot"):
+        achieved = d_fl / (d_ms / 1e3) / 1e12
+        roof = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 3), "peak": round(alu_peak, 2),
+                "unit": "TFLOP/s", "frac": round(achieved / alu_peak, 4), "traffic": None,
+                "peak_source": "derived: 148 SMs x 128 fp32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json)",
+                "per_launch": f"{d_fl / d_n:.4g} flop / {d_ms / d_n:.4g} ms"}
+    else:
+        achieved = d_by / (d_ms / 1e3) / 1e9
+        pk = peaks["hbm_gbs"]
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": pk, "unit": "GB/s",
+                "frac": round(achieved / pk, 4), "traffic": None, "peak_source": f"{peak_src} hbm_gbs",
+                "per_launch": f"{d_by / d_n:.4g} B / {d_ms / d_n:.4g} ms"}
+    # HBM roofline of the streaming edge kernel (north_star: >= 60% on the edge kernels)
+    fg = prof.get("force_gather")
+    if fg and fg[3]:
+        roof["force_gather_hbm_frac"] = round(fg[2] / (fg[0] / 1e3) / 1e9 / peaks["hbm_gbs"], 4)
+
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config_dict(cfg, ws, int(rep.n_edges)),
+        "roofline": roof,
+        "kernels": kernels,
+        "gpu_launches": launches,
+        "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": d2h * ws},
+        "clocks": clk,
+        "md": {"e_pot": rep.e_pot, "e_kin": rep.e_kin, "temperature": rep.temperature,
+               "n_outliers_last": rep.n_outliers_last},
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rec = _oracle_rate(cfg, args.cpu_sample, 1, 0)
+        line["cpu_baseline"] = {"value": round(rec["value"], 2), "unit": UNIT, "cores": rec["cores"], "kind": "oracle",
+                                "sample": rec["sample"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    m.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

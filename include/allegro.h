@@ -125,6 +125,14 @@ typedef struct {
  * returns ALLEGRO_E_NONFINITE with steps_done set.  out may be NULL. */
 int md_step(allegro_ctx* ctx, int64_t n_steps, double dt_fs, md_report* out);
 
+/* End-to-end variant of md_step for HOST-resident state (the e2e measurement of bench.py):
+ * copies species [n], pos/vel/forces [n][3] (forces = F at pos, e.g. from the previous call
+ * or from md_get_state) host -> device, runs n_steps exactly as md_step, and writes pos, vel
+ * and forces back into the caller's arrays (device -> host).  n must equal the md_set_state
+ * size.  Pinned host memory makes the copies asynchronous. */
+int md_step_host(allegro_ctx* ctx, int64_t n, const int32_t* species, double* pos, double* vel, double* forces,
+                 int64_t n_steps, double dt_fs, md_report* out);
+
 /* Count atoms with |F_a| > mean + k*sigma (strict) for the current
  * forces.  Collective. */
 int md_count_outliers(allegro_ctx* ctx, double mean, double sigma, double k, int64_t* count);
@@ -142,7 +150,18 @@ int allegro_get_edges(allegro_ctx* ctx, int64_t capacity, int64_t* n_edges, int3
  * in the edge order of allegro_get_edges. */
 int allegro_get_edge_grad(allegro_ctx* ctx, int64_t capacity, double* g);
 
+/* Per-kernel-class accounting.  Every launch of the library is counted;
+ * with profiling enabled each launch is also bracketed by CUDA events on the stream it is
+ * launched on and its ALGORITHMIC flops / DRAM bytes are accumulated.
+ * allegro_profile(ctx, enable) resets all totals.  Kinds are 0 .. allegro_profile_kinds()-1. */
+int allegro_profile(allegro_ctx* ctx, int enable);
+int allegro_profile_read(allegro_ctx* ctx, int kind, double* time_ms, double* flops, double* bytes,
+                         int64_t* launches);
+int64_t allegro_launch_count(allegro_ctx* ctx); /* launches since the last allegro_profile() */
+
 /* Host-only helpers (no GPU needed): this library's own derivations. */
+int allegro_profile_kinds(void);
+const char* allegro_profile_kind_name(int kind);
 /* real W3j^{l1 l2 l3} table (l <= 2) into out[(2l1+1)(2l2+1)(2l3+1)] */
 int allegro_w3j_table(int l1, int l2, int l3, double* out);
 /* parameter count of the (n_layers, lmax) model with C=32, D=128 (Table 2) */

@@ -26,7 +26,7 @@ PREC_FP32, PREC_3XTF32, PREC_BF16X3, PREC_TF32, PREC_BF16 = 0, 1, 2, 3, 4
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_2303_08169_b200.build` "
+        f"{LIB_PATH} is missing: build it with `python paper_2303_08169_b200/build.py` "
         "(there is no CPU fallback for the CUDA path)"
     )
 _lib = C.CDLL(LIB_PATH)
@@ -81,12 +81,20 @@ _lib.allegro_param_count.argtypes = [C.c_int, C.c_int]
 _lib.allegro_param_count.restype = C.c_int64
 _lib.allegro_layer_paths.argtypes = [C.c_int, C.c_int, _P]
 _lib.allegro_version.restype = C.c_char_p
+_lib.md_step_host.argtypes = [_P, C.c_int64, _P, _P, _P, _P, C.c_int64, C.c_double, C.POINTER(MdReport)]
+_lib.allegro_profile.argtypes = [_P, C.c_int]
+_lib.allegro_profile_read.argtypes = [_P, C.c_int, _P, _P, _P, _P]
+_lib.allegro_launch_count.argtypes = [_P]
+_lib.allegro_launch_count.restype = C.c_int64
+_lib.allegro_profile_kind_name.argtypes = [C.c_int]
+_lib.allegro_profile_kind_name.restype = C.c_char_p
 
 EXPORTED = [
     "allegro_create", "allegro_destroy", "allegro_last_error", "allegro_compute_energy_forces",
     "md_set_state", "md_get_state", "md_step", "md_count_outliers", "md_force_baseline",
     "allegro_get_edges", "allegro_get_edge_grad", "allegro_w3j_table", "allegro_param_count",
-    "allegro_layer_paths", "allegro_version",
+    "allegro_layer_paths", "allegro_version", "md_step_host", "allegro_profile", "allegro_profile_read",
+    "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name",
 ]
 
 
@@ -223,6 +231,30 @@ class Allegro:
         m, s = C.c_double(0), C.c_double(0)
         self._check(_lib.md_force_baseline(self._h, C.byref(m), C.byref(s)))
         return m.value, s.value
+
+    def md_step_host(self, species, pos, vel, forces, n_steps: int = 1, dt_fs: float = 2.0) -> MdReport:
+        """End-to-end step on HOST arrays (updated in place): H2D, n_steps, D2H.
+        numpy or (pinned) torch CPU tensors."""
+        r = MdReport()
+        self._check(_lib.md_step_host(self._h, int(pos.shape[0]), _ptr(species), _ptr(pos), _ptr(vel), _ptr(forces),
+                                      n_steps, dt_fs, C.byref(r)))
+        return r
+
+    # ---- profiling -----------------------------------------------------------------
+    def profile(self, enable: bool = True):
+        self._check(_lib.allegro_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        """{kind name: (time_ms, algorithmic flops, algorithmic bytes, launches)}"""
+        out = {}
+        for k in range(_lib.allegro_profile_kinds()):
+            ms, fl, by, n = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
+            self._check(_lib.allegro_profile_read(self._h, k, C.byref(ms), C.byref(fl), C.byref(by), C.byref(n)))
+            out[_lib.allegro_profile_kind_name(k).decode()] = (ms.value, fl.value, by.value, n.value)
+        return out
+
+    def launch_count(self) -> int:
+        return int(_lib.allegro_launch_count(self._h))
 
     # ---- test hooks -------------------------------------------------------------------
     def get_edges(self):

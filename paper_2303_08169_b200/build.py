@@ -1,6 +1,6 @@
 """Build the in-tree CUDA library libpaper_allegro.so for sm_100a with nvcc.
 
-    python -m paper_2303_08169_b200.build [--force]
+    python paper_2303_08169_b200/build.py [--force]
 
 Every translation unit under csrc/ is compiled with
 ``-gencode arch=compute_100a,code=sm_100a -lineinfo -O3`` and linked into

@@ -159,6 +159,7 @@ void allegro_destroy(allegro_ctx* c) {
     w.V[k].release();
     w.G[k].release();
   }
+  c->prof.destroy();
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -183,7 +184,10 @@ int allegro_compute_energy_forces(allegro_ctx* c, int64_t n, int where, const in
       if (gid) {
         ALG_CUDA(cudaMemcpyAsync(c->gid.p, gid, sizeof(int32_t) * n, kin, c->stream));
       } else {
-        k_iota<<<ceil_div(n, 256), 256, 0, c->stream>>>(c->gid.p, n);
+        {
+          ProfScope ps_(&c->prof, c->stream, PK_WRAP, 0, 4.0 * n);
+          k_iota<<<ceil_div(n, 256), 256, 0, c->stream>>>(c->gid.p, n);
+        }
         ALG_LAUNCH_CHECK();
       }
     }
@@ -195,6 +199,7 @@ int allegro_compute_energy_forces(allegro_ctx* c, int64_t n, int where, const in
       if (e_atom) ALG_CUDA(cudaMemcpyAsync(e_atom, c->e_atom.p, sizeof(double) * n, kout, c->stream));
     }
     ALG_CUDA(cudaStreamSynchronize(c->stream));
+    c->prof.flush();
     return rc;
   });
 }
@@ -209,12 +214,16 @@ int md_set_state(allegro_ctx* c, int64_t n, const int32_t* species, const double
     ALG_CUDA(cudaMemcpyAsync(c->pos.p, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     ALG_CUDA(cudaMemcpyAsync(c->vel.p, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     ALG_CUDA(cudaMemcpyAsync(c->species.p, species, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
-    k_iota<<<ceil_div(n, 256), 256, 0, c->stream>>>(c->gid.p, n);
+    {
+      ProfScope ps_(&c->prof, c->stream, PK_WRAP, 0, 4.0 * n);
+      k_iota<<<ceil_div(n, 256), 256, 0, c->stream>>>(c->gid.p, n);
+    }
     ALG_LAUNCH_CHECK();
     c->md_ready = false;
     const int rc = evaluate(c);
     if (rc != ALLEGRO_OK) return rc;
     force_stats(c, &c->f_mean0, &c->f_sigma0);
+    c->baseline_set = true;
     c->md_ready = true;
     c->md_steps = 0;
     return ALLEGRO_OK;
@@ -235,12 +244,8 @@ int md_get_state(allegro_ctx* c, int64_t n, double* pos, double* vel, double* fo
   });
 }
 
-int md_step(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
-  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
-  if (!c->md_ready) return fail(c, ALLEGRO_E_STATE, "md_set_state has not been called");
-  if (n_steps < 0 || !(dt > 0 && std::isfinite(dt))) return fail(c, ALLEGRO_E_ARG, "bad n_steps or dt");
-  return guarded(c, [&]() -> int {
-    ALG_CUDA(cudaSetDevice(c->device));
+static int md_run(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
+  {
     int rc = ALLEGRO_OK;
     int64_t done = 0;
     for (; done < n_steps; ++done) {
@@ -256,6 +261,7 @@ int md_step(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
         break;
       }
       ++c->md_steps;
+      c->prof.flush();
     }
     if (out) {
       out->steps_done = done;
@@ -267,9 +273,68 @@ int md_step(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
       out->n_edges = c->n_edges;
       out->n_rebuilds = c->n_rebuilds;
     }
+    c->prof.flush();
+    return rc;
+  }
+}
+
+int md_step(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (!c->md_ready) return fail(c, ALLEGRO_E_STATE, "md_set_state has not been called");
+  if (n_steps < 0 || !(dt > 0 && std::isfinite(dt))) return fail(c, ALLEGRO_E_ARG, "bad n_steps or dt");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    return md_run(c, n_steps, dt, out);
+  });
+}
+
+int md_step_host(allegro_ctx* c, int64_t n, const int32_t* species, double* pos, double* vel, double* forces,
+                 int64_t n_steps, double dt, md_report* out) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (!c->md_ready) return fail(c, ALLEGRO_E_STATE, "md_set_state has not been called");
+  if (n != c->n || !species || !pos || !vel || !forces) return fail(c, ALLEGRO_E_ARG, "bad arrays or n");
+  if (n_steps < 0 || !(dt > 0 && std::isfinite(dt))) return fail(c, ALLEGRO_E_ARG, "bad n_steps or dt");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    ALG_CUDA(cudaMemcpyAsync(c->species.p, species, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->pos.p, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->vel.p, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->frc.p, forces, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    const int rc = md_run(c, n_steps, dt, out);
+    ALG_CUDA(cudaMemcpyAsync(pos, c->pos.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(vel, c->vel.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaStreamSynchronize(c->stream));
     return rc;
   });
 }
+
+int allegro_profile(allegro_ctx* c, int enable) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    ALG_CUDA(cudaStreamSynchronize(c->stream));
+    c->prof.reset();
+    c->prof.on = enable != 0;
+    return ALLEGRO_OK;
+  });
+}
+
+int allegro_profile_read(allegro_ctx* c, int kind, double* ms, double* flops, double* bytes, int64_t* launches) {
+  if (!c || kind < 0 || kind >= PK_COUNT) return fail(c, ALLEGRO_E_ARG, "bad ctx or kind");
+  c->prof.flush();
+  if (ms) *ms = c->prof.ms[kind];
+  if (flops) *flops = c->prof.flops[kind];
+  if (bytes) *bytes = c->prof.bytes[kind];
+  if (launches) *launches = c->prof.count[kind];
+  return ALLEGRO_OK;
+}
+
+int64_t allegro_launch_count(allegro_ctx* c) { return c ? c->prof.launches : -1; }
+
+int allegro_profile_kinds(void) { return PK_COUNT; }
+
+const char* allegro_profile_kind_name(int kind) { return prof_name(kind); }
 
 int md_count_outliers(allegro_ctx* c, double mean, double sigma, double k, int64_t* count) {
   if (!c || !count) return fail(c, ALLEGRO_E_ARG, "NULL argument");

@@ -9,6 +9,7 @@
 #include "../../include/allegro.h"
 #include "arch.cuh"
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace allegro {
 
@@ -48,6 +49,7 @@ struct LayerInfo {
   int fan_lat;         // D + C * n_s
   int t_base[kMaxIr];  // per out irrep: offset (floats per edge) of T_o in the T scratch
   int v_base[kMaxIr];  // per in irrep: offset (floats per edge) of V_ir in the V store of this layer
+  int tp_nnz;          // non-zero W3j entries summed over the layer's paths (FMAs per edge-channel)
 };
 
 struct DevWeights {
@@ -129,6 +131,8 @@ struct allegro_ctx {
   int64_t md_steps = 0, n_rebuilds = 0;
   double e_pot = 0;
   double f_mean0 = 0, f_sigma0 = 0;  // step-0 outlier baseline
+  bool baseline_set = false;
+  allegro::Profiler prof;
 };
 
 namespace allegro {

@@ -114,8 +114,12 @@ __global__ void __launch_bounds__(NT) k_gemm(GemmArgs g) {
 
 }  // namespace
 
-void gemm(const GemmArgs& g, cudaStream_t st) {
+void gemm(const GemmArgs& g, cudaStream_t st, Profiler* prof) {
   if (g.M == 0) return;
+  // algorithmic work: 2 M N K flops; A, W read, C written (+ aux written, X read)
+  const double mn = (double)g.M * g.N;
+  const int n_io = 1 + (g.aux != nullptr) + (g.X != nullptr) + (g.epi == EPI_ACC);
+  ProfScope ps(prof, st, PK_GEMM, 2.0 * mn * g.K, 4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * n_io));
   if (g.K % BK != 0 || g.N % 16 != 0 || (g.A2 && g.K1 % BK != 0))
     throw CudaError("gemm: unsupported shape N=" + std::to_string(g.N) + " K=" + std::to_string(g.K));
   const unsigned gx = (unsigned)((g.M + BM - 1) / BM);

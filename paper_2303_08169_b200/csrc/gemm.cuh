@@ -4,6 +4,7 @@
 // (W^T) counterparts.  M = edges (or edges x irrep dim), K, N <= 224.
 #pragma once
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace allegro {
 
@@ -36,6 +37,6 @@ struct GemmArgs {
   int epi = EPI_STORE;
 };
 
-void gemm(const GemmArgs& g, cudaStream_t st);
+void gemm(const GemmArgs& g, cudaStream_t st, Profiler* prof);
 
 }  // namespace allegro

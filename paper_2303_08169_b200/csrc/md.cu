@@ -116,27 +116,39 @@ double fetch(allegro_ctx* c, const double* d) {
 
 void md_half_kick_drift(allegro_ctx* c, double dt) {
   if (c->n == 0) return;
-  k_kick_drift<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->pos.p, c->vel.p, c->frc.p, c->species.p, c->n, dt,
+  {
+    ProfScope ps_(&c->prof, c->stream, PK_VERLET, 0, 124.0 * c->n);
+    k_kick_drift<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->pos.p, c->vel.p, c->frc.p, c->species.p, c->n, dt,
                                                            c->box[0], c->box[1], c->box[2]);
+  }
   ALG_LAUNCH_CHECK();
 }
 
 void md_half_kick(allegro_ctx* c, double dt) {
   if (c->n == 0) return;
-  k_kick<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->vel.p, c->frc.p, c->species.p, c->n, dt);
+  {
+    ProfScope ps_(&c->prof, c->stream, PK_VERLET, 0, 76.0 * c->n);
+    k_kick<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->vel.p, c->frc.p, c->species.p, c->n, dt);
+  }
   ALG_LAUNCH_CHECK();
 }
 
 double md_kinetic(allegro_ctx* c) {
   c->red.reserve(8);
-  k_ke<<<1, kRedThreads, 0, c->stream>>>(c->vel.p, c->species.p, c->n, c->red.p);
+  {
+    ProfScope ps_(&c->prof, c->stream, PK_REDUCE, 0, 28.0 * c->n);
+    k_ke<<<1, kRedThreads, 0, c->stream>>>(c->vel.p, c->species.p, c->n, c->red.p);
+  }
   ALG_LAUNCH_CHECK();
   return fetch(c, c->red.p);
 }
 
 double sum_e_atom(allegro_ctx* c) {
   c->red.reserve(8);
-  k_sum<<<1, kRedThreads, 0, c->stream>>>(c->e_atom.p, c->n, c->red.p + 1);
+  {
+    ProfScope ps_(&c->prof, c->stream, PK_REDUCE, 0, 8.0 * c->n);
+    k_sum<<<1, kRedThreads, 0, c->stream>>>(c->e_atom.p, c->n, c->red.p + 1);
+  }
   ALG_LAUNCH_CHECK();
   return fetch(c, c->red.p + 1);
 }
@@ -147,9 +159,15 @@ void force_stats(allegro_ctx* c, double* mean, double* sigma) {
     *mean = *sigma = 0;
     return;
   }
-  k_fnorm_sum<<<1, kRedThreads, 0, c->stream>>>(c->frc.p, c->n, c->red.p + 2);
+  {
+    ProfScope ps_(&c->prof, c->stream, PK_REDUCE, 0, 24.0 * c->n);
+    k_fnorm_sum<<<1, kRedThreads, 0, c->stream>>>(c->frc.p, c->n, c->red.p + 2);
+  }
   ALG_LAUNCH_CHECK();
-  k_fnorm_var<<<1, kRedThreads, 0, c->stream>>>(c->frc.p, c->n, c->red.p + 2, c->red.p + 3);
+  {
+    ProfScope ps_(&c->prof, c->stream, PK_REDUCE, 0, 24.0 * c->n);
+    k_fnorm_var<<<1, kRedThreads, 0, c->stream>>>(c->frc.p, c->n, c->red.p + 2, c->red.p + 3);
+  }
   ALG_LAUNCH_CHECK();
   *mean = fetch(c, c->red.p + 2) / (double)c->n;
   *sigma = std::sqrt(fetch(c, c->red.p + 3) / (double)c->n);
@@ -160,7 +178,10 @@ int64_t count_outliers(allegro_ctx* c, double thr) {
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(c->red.p + 4);
   ALG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), c->stream));
   if (c->n > 0) {
-    k_outliers<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->frc.p, c->n, thr, cnt);
+    {
+      ProfScope ps_(&c->prof, c->stream, PK_REDUCE, 0, 24.0 * c->n);
+      k_outliers<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->frc.p, c->n, thr, cnt);
+    }
     ALG_LAUNCH_CHECK();
   }
   unsigned long long h = 0;
@@ -172,7 +193,10 @@ int64_t count_outliers(allegro_ctx* c, double thr) {
 bool all_finite(allegro_ctx* c) {
   // flags[2] is set by the force gather; also check velocities
   if (c->n > 0 && c->md_ready) {
-    k_finite3<<<ceil_div(3 * c->n, 256), 256, 0, c->stream>>>(c->vel.p, c->n, c->flags.p + 2);
+    {
+      ProfScope ps_(&c->prof, c->stream, PK_REDUCE, 0, 24.0 * c->n);
+      k_finite3<<<ceil_div(3 * c->n, 256), 256, 0, c->stream>>>(c->vel.p, c->n, c->flags.p + 2);
+    }
     ALG_LAUNCH_CHECK();
   }
   int f = 0;

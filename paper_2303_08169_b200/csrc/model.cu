@@ -450,17 +450,31 @@ __global__ void k_force(int64_t n, const int32_t* __restrict__ row_ptr, const in
 
 // ----------------------------------------------------------------- dispatch
 template <int NL, int LMAX, int K>
-void launch_tp(bool fwd, const TpArgs& t, cudaStream_t st) {
+void launch_tp(bool fwd, const TpArgs& t, cudaStream_t st, Profiler* prof, double flops, double bytes) {
   const unsigned blocks = (unsigned)((t.ch.n_c * 32 + 127) / 128);
   if (blocks == 0) return;
-  if (fwd) k_tp_fwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
-  else k_tp_bwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
+  {
+    ProfScope ps_(prof, st, fwd ? PK_TP_FWD : PK_TP_BWD, flops, bytes);
+    if (fwd) k_tp_fwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
+    else k_tp_bwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
+  }
   ALG_LAUNCH_CHECK();
 }
 
-void tp_dispatch(int NL, int LMAX, int K, bool fwd, const TpArgs& t, cudaStream_t st) {
+// Algorithmic work of the TP kernels per edge: forward = Gamma sum
+// (DSH FMA) + TP (nnz FMA) per channel; backward = 2 nnz FMA + env adjoint.  Bytes:
+// the per-edge operands the method reads/writes once (w, Y, V in; T out / T-bar, V,
+// w, Y in; w-bar, Y-bar, V-bar out), fp32.
+void tp_dispatch(int NL, int LMAX, int K, bool fwd, const TpArgs& t, cudaStream_t st, Profiler* prof,
+                 const LayerInfo& L) {
+  const double E = (double)t.ch.n_e;
+  const int dsh = (LMAX + 1) * (LMAX + 1);
+  const double vin = K == 0 ? 0.0 : (double)L.A.dim_in * kC;
+  const double flops = fwd ? E * kC * 2.0 * (L.tp_nnz + dsh) : E * kC * 2.0 * (2.0 * L.tp_nnz + 2 * dsh);
+  const double bytes = fwd ? 4.0 * E * (L.nw + dsh + vin + (double)L.A.dim_T * kC)
+                           : 4.0 * E * ((double)L.A.dim_T * kC + 2.0 * vin + 2.0 * L.nw + 2.0 * dsh);
 #define ALG_TP(nl, lm, k) \
-  if (NL == nl && LMAX == lm && K == k) return launch_tp<nl, lm, k>(fwd, t, st);
+  if (NL == nl && LMAX == lm && K == k) return launch_tp<nl, lm, k>(fwd, t, st, prof, flops, bytes);
   ALG_TP(2, 1, 0) ALG_TP(2, 1, 1)
   ALG_TP(2, 2, 0) ALG_TP(2, 2, 1)
   ALG_TP(3, 0, 0) ALG_TP(3, 0, 1) ALG_TP(3, 0, 2)
@@ -544,8 +558,11 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   gp.lmax = M.lmax;
   gp.dsh = dsh;
   if (E > 0) {
-    k_geom<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, c->aowner.p, c->species.p, w.z.p,
+    {
+      ProfScope ps_(&c->prof, st, PK_GEOM, 0, (double)E * (8 + 64 + 4 * dsh + 4));
+      k_geom<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, c->aowner.p, c->species.p, w.z.p,
                                              w.Y.p, w.u.p);
+    }
     ALG_LAUNCH_CHECK();
   }
   auto G = [&](const float* A, int lda, const float* W, int N, int K, float* C, float s, int epi) {
@@ -565,14 +582,14 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   {
     GemmArgs g = G(w.z.p, 16, M.w.tb_w0, 32, 16, w.h1.p, 1.f / std::sqrt(12.f), EPI_SILU);
     g.aux = w.a1.p;
-    gemm(g, st);
+    gemm(g, st, &c->prof);
     g = G(w.h1.p, 32, M.w.tb_w1, 64, 32, w.h2.p, kCSilu / std::sqrt(32.f), EPI_SILU);
     g.aux = w.a2.p;
-    gemm(g, st);
+    gemm(g, st, &c->prof);
     g = G(w.h2.p, 64, M.w.tb_w2, 128, 64, w.xa.p, kCSilu / std::sqrt(64.f), EPI_UMUL_SAVE);
     g.aux = w.m.p;
     g.u = w.u.p;
-    gemm(g, st);
+    gemm(g, st, &c->prof);
   }
   float* x = w.xa.p;
   float* xn = w.xb.p;
@@ -587,11 +604,11 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   // ---- layers (E6) ----
   for (int k = 0; k < M.n_layers; ++k) {
     const LayerInfo& L = M.L[k];
-    gemm(G(x, 128, M.w.env[k], L.nw, 128, w.w[k].p, 1.f / std::sqrt(128.f), EPI_STORE), st);
+    gemm(G(x, 128, M.w.env[k], L.nw, 128, w.w[k].p, 1.f / std::sqrt(128.f), EPI_STORE), st, &c->prof);
     tp.w = w.w[k].p;
     tp.V = k >= 1 ? w.V[k].p : nullptr;
     tp.G = w.G[k].p;
-    tp_dispatch(M.n_layers, M.lmax, k, true, tp, st);
+    tp_dispatch(M.n_layers, M.lmax, k, true, tp, st, &c->prof, L);
     if (k < M.n_layers - 1) {
       for (int o = 0; o < L.A.out.n; ++o) {
         const int dim = ir_dim(L.A.out.v[o]);
@@ -599,7 +616,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
                        w.V[k + 1].p + (int64_t)M.L[k + 1].v_base[o] * ecap, 1.f / std::sqrt((float)(kC * L.A.n_to[o])),
                        EPI_STORE);
         g.M = E * dim;
-        gemm(g, st);
+        gemm(g, st, &c->prof);
       }
     }
     GemmArgs g = G(x, 128, M.w.lat[k], 128, L.fan_lat, xn, 1.f / std::sqrt((float)L.fan_lat), EPI_RESID);
@@ -611,15 +628,18 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     g.u = w.u.p;
     g.alpha = kResA;
     g.beta = kResB;
-    gemm(g, st);
+    gemm(g, st, &c->prof);
     std::swap(x, xn);
   }
   // ---- energies (E7, E8) and x-bar^L ----
   float* xb = w.xbar_a.p;
   float* xbn = w.xbar_b.p;
   if (warp_blocks) {
-    k_energy<<<warp_blocks, 128, 0, st>>>(ch, c->row_ptr.p, c->species.p, x, M.w.wout, xb, c->e_atom.p, M.sigma[0],
+    {
+      ProfScope ps_(&c->prof, st, PK_ENERGY, 2.0 * 128 * E, (double)E * 1024);
+      k_energy<<<warp_blocks, 128, 0, st>>>(ch, c->row_ptr.p, c->species.p, x, M.w.wout, xb, c->e_atom.p, M.sigma[0],
                                           M.sigma[1], M.mu[0], M.mu[1], inv_sqrt_nbar);
+    }
     ALG_LAUNCH_CHECK();
   }
   // ---- reverse mode (E9) ----
@@ -631,7 +651,10 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   for (int k = M.n_layers - 1; k >= 0; --k) {
     const LayerInfo& L = M.L[k];
     if (E > 0) {
-      k_rowdot<<<edge_warp_blocks, 256, 0, st>>>(E, w.h[k].p, xb, kResB, w.ubar.p);
+      {
+        ProfScope ps_(&c->prof, st, PK_ROWDOT, 2.0 * 128 * E, (double)E * 1024);
+        k_rowdot<<<edge_warp_blocks, 256, 0, st>>>(E, w.h[k].p, xb, kResB, w.ubar.p);
+      }
       ALG_LAUNCH_CHECK();
     }
     const float sl = 1.f / std::sqrt((float)L.fan_lat);
@@ -641,11 +664,11 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
       g.u = w.u.p;
       g.alpha = kResA;
       g.beta = kResB;
-      gemm(g, st);
+      gemm(g, st, &c->prof);
       g = G(xb, 128, M.w.latT_s[k], L.A.n_s * kC, 128, w.sbar.p, sl, EPI_USCALE);
       g.u = w.u.p;
       g.beta = kResB;
-      gemm(g, st);
+      gemm(g, st, &c->prof);
     }
     tp.w = w.w[k].p;
     tp.V = k >= 1 ? w.V[k].p : nullptr;
@@ -666,37 +689,43 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
           g.epi = EPI_ADDX;
           g.X = w.sbar.p;
         }
-        gemm(g, st);
+        gemm(g, st, &c->prof);
         tp.Tb[o] = dst;
       }
     }
-    tp_dispatch(M.n_layers, M.lmax, k, false, tp, st);
+    tp_dispatch(M.n_layers, M.lmax, k, false, tp, st, &c->prof, L);
     {
       GemmArgs g = G(w.wbar.p, L.nw, M.w.envT[k], 128, L.nw, xbn, 1.f / std::sqrt(128.f), EPI_ACC);
-      gemm(g, st);
+      gemm(g, st, &c->prof);
     }
     std::swap(xb, xbn);
     std::swap(vb, vbn);
   }
   // ---- two-body reverse ----
   if (E > 0) {
-    k_rowdot<<<edge_warp_blocks, 256, 0, st>>>(E, w.m.p, xb, 1.f, w.ubar.p);
+    {
+      ProfScope ps_(&c->prof, st, PK_ROWDOT, 2.0 * 128 * E, (double)E * 1024);
+      k_rowdot<<<edge_warp_blocks, 256, 0, st>>>(E, w.m.p, xb, 1.f, w.ubar.p);
+    }
     ALG_LAUNCH_CHECK();
   }
   {
     GemmArgs g = G(xb, 128, M.w.tb_w2T, 64, 128, w.ab2.p, kCSilu / std::sqrt(64.f), EPI_DSILU);
     g.X = w.a2.p;
     g.u = w.u.p;
-    gemm(g, st);
+    gemm(g, st, &c->prof);
     g = G(w.ab2.p, 64, M.w.tb_w1T, 32, 64, w.ab1.p, kCSilu / std::sqrt(32.f), EPI_DSILU);
     g.X = w.a1.p;
-    gemm(g, st);
+    gemm(g, st, &c->prof);
     g = G(w.ab1.p, 32, M.w.tb_w0T, 16, 32, w.zbar.p, 1.f / std::sqrt(12.f), EPI_STORE);
-    gemm(g, st);
+    gemm(g, st, &c->prof);
   }
   if (E > 0) {
-    k_geom_bwd<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, w.ubar.p, w.zbar.p, w.ybar.p,
+    {
+      ProfScope ps_(&c->prof, st, PK_GEOM_BWD, 0, (double)E * (8 + 4 + 64 + 4 * dsh + 12));
+      k_geom_bwd<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, w.ubar.p, w.zbar.p, w.ybar.p,
                                                  c->g.p);
+    }
     ALG_LAUNCH_CHECK();
   }
 }
@@ -732,7 +761,10 @@ void compute_forces(allegro_ctx* c) {
   for (const ChunkPtrs& ch : chunks) run_chunk(c, ch);
   ALG_CUDA(cudaMemsetAsync(c->flags.p + 2, 0, sizeof(int), st));
   if (n > 0) {
-    k_force<<<ceil_div(n, 256), 256, 0, st>>>(n, c->row_ptr.p, c->rev.p, c->g.p, c->frc.p, c->flags.p);
+    {
+      ProfScope ps_(&c->prof, st, PK_FORCE, 0, 24.0 * n + 8.0 * n + 28.0 * E);
+      k_force<<<ceil_div(n, 256), 256, 0, st>>>(n, c->row_ptr.p, c->rev.p, c->g.p, c->frc.p, c->flags.p);
+    }
     ALG_LAUNCH_CHECK();
   }
   c->e_pot = sum_e_atom(c);

@@ -284,8 +284,11 @@ __global__ void k_edge_rev(int64_t E, const int32_t* __restrict__ cidx, const in
 
 void wrap_positions(allegro_ctx* c) {
   if (c->n == 0) return;
-  k_wrap<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->pos.p, c->species.p, c->n, c->box[0], c->box[1], c->box[2],
+  {
+    ProfScope ps_(&c->prof, c->stream, PK_WRAP, 0, 52.0 * c->n);
+    k_wrap<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->pos.p, c->species.p, c->n, c->box[0], c->box[1], c->box[2],
                                                      c->flags.p);
+  }
   ALG_LAUNCH_CHECK();
 }
 
@@ -305,7 +308,10 @@ void build_neighbors(allegro_ctx* c) {
   }
   c->gcount.reserve(n + 1);
   c->goff.reserve(n + 1);
-  k_ghost_count<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(c->pos.p, n, gg, c->gcount.p);
+  {
+    ProfScope ps_(&c->prof, st, PK_GHOST, 0, 28.0 * n);
+    k_ghost_count<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(c->pos.p, n, gg, c->gcount.p);
+  }
   ALG_LAUNCH_CHECK();
   exclusive_scan(c, c->gcount.p, c->goff.p, n);
   int32_t G = 0;
@@ -317,8 +323,11 @@ void build_neighbors(allegro_ctx* c) {
   c->aowner.reserve(na);
   c->ashift.reserve(na);
   c->agid.reserve(na);
-  k_ghost_fill<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(c->pos.p, c->gid.p, n, gg, c->goff.p, c->apos.p,
+  {
+    ProfScope ps_(&c->prof, st, PK_GHOST, 0, 24.0 * n + 40.0 * (n + G));
+    k_ghost_fill<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(c->pos.p, c->gid.p, n, gg, c->goff.p, c->apos.p,
                                                                        c->aowner.p, c->ashift.p, c->agid.p);
+  }
   ALG_LAUNCH_CHECK();
   // ---- cells of edge >= rc (1 + 1e-9) over [lo, hi) ----
   CellGeom cg;
@@ -338,10 +347,16 @@ void build_neighbors(allegro_ctx* c) {
   c->cslot.reserve(na);
   c->csorted.reserve(na);
   ALG_CUDA(cudaMemsetAsync(c->ccount.p, 0, sizeof(int32_t) * (ncells + 1), st));
-  k_cell_count<<<ceil_div(na, 256), 256, 0, st>>>(c->apos.p, na, cg, c->ccount.p, c->cslot.p);
+  {
+    ProfScope ps_(&c->prof, st, PK_CELL, 0, 28.0 * na);
+    k_cell_count<<<ceil_div(na, 256), 256, 0, st>>>(c->apos.p, na, cg, c->ccount.p, c->cslot.p);
+  }
   ALG_LAUNCH_CHECK();
   exclusive_scan(c, c->ccount.p, c->cstart.p, ncells);
-  k_cell_fill<<<ceil_div(na, 256), 256, 0, st>>>(c->apos.p, na, cg, c->cstart.p, c->cslot.p, c->csorted.p);
+  {
+    ProfScope ps_(&c->prof, st, PK_CELL, 0, 36.0 * na);
+    k_cell_fill<<<ceil_div(na, 256), 256, 0, st>>>(c->apos.p, na, cg, c->cstart.p, c->cslot.p, c->csorted.p);
+  }
   ALG_LAUNCH_CHECK();
   // ---- edges ----
   const double rc2 = rc * rc;
@@ -355,9 +370,12 @@ void build_neighbors(allegro_ctx* c) {
     if (smem > 48 * 1024)
       ALG_CUDA(cudaFuncSetAttribute(k_edge_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (n > 0) {
-      k_edge_build<<<ceil_div(n, kEdgeWarps), kEdgeWarps * 32, smem, st>>>(
+      {
+        ProfScope ps_(&c->prof, st, PK_EDGE, 0, 28.0 * n);
+        k_edge_build<<<ceil_div(n, kEdgeWarps), kEdgeWarps * 32, smem, st>>>(
           c->apos.p, n, cg, c->cstart.p, c->csorted.p, c->ashift.p, c->agid.p, rc2, c->max_nb, c->nb_count.p, c->nb_pad.p,
           c->key_pad.p, c->flags.p);
+      }
       ALG_LAUNCH_CHECK();
     }
     int over = 0;
@@ -380,13 +398,19 @@ void build_neighbors(allegro_ctx* c) {
   c->rev.reserve(E + 1);
   c->g.reserve(3 * (size_t)E + 3);
   if (n > 0) {
-    k_edge_compact<<<ceil_div(n * 32, 256), 256, 0, st>>>(n, c->max_nb, c->nb_count.p, c->nb_pad.p, c->key_pad.p,
+    {
+      ProfScope ps_(&c->prof, st, PK_EDGE, 0, 4.0 * n);
+      k_edge_compact<<<ceil_div(n * 32, 256), 256, 0, st>>>(n, c->max_nb, c->nb_count.p, c->nb_pad.p, c->key_pad.p,
                                                          c->row_ptr.p, c->nbr.p, c->key.p, c->cidx.p);
+    }
     ALG_LAUNCH_CHECK();
   }
   if (E > 0) {
-    k_edge_rev<<<ceil_div(E, 256), 256, 0, st>>>(E, c->cidx.p, c->nbr.p, c->aowner.p, c->ashift.p, c->gid.p, c->row_ptr.p,
+    {
+      ProfScope ps_(&c->prof, st, PK_EDGE, 0, 16.0 * E);
+      k_edge_rev<<<ceil_div(E, 256), 256, 0, st>>>(E, c->cidx.p, c->nbr.p, c->aowner.p, c->ashift.p, c->gid.p, c->row_ptr.p,
                                                  c->key.p, c->rev.p);
+    }
     ALG_LAUNCH_CHECK();
   }
   c->n_rebuilds++;

@@ -1,0 +1,105 @@
+// prof.cuh -- per-kernel-class launch accounting: every launch of this library goes
+// through a ProfScope, which counts it and (when profiling is enabled) brackets it
+// with CUDA events on the launching stream and adds the ALGORITHMIC work of that
+// launch (flops / DRAM bytes the method must move).  bench.py reads
+// the totals to report the live roofline of the dominant kernel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <vector>
+
+namespace allegro {
+
+enum ProfKind : int {
+  PK_WRAP = 0,
+  PK_GHOST,
+  PK_CELL,
+  PK_EDGE,
+  PK_SCAN,
+  PK_GEOM,
+  PK_GEMM,
+  PK_TP_FWD,
+  PK_TP_BWD,
+  PK_ENERGY,
+  PK_ROWDOT,
+  PK_GEOM_BWD,
+  PK_FORCE,
+  PK_VERLET,
+  PK_REDUCE,
+  PK_COUNT
+};
+
+inline const char* prof_name(int k) {
+  static const char* names[PK_COUNT] = {"wrap", "ghost", "cell", "edge_build", "scan", "geom", "gemm", "tp_fwd",
+                                        "tp_bwd", "energy", "rowdot", "geom_bwd", "force_gather", "verlet", "reduce"};
+  return (k >= 0 && k < PK_COUNT) ? names[k] : "?";
+}
+
+struct Profiler {
+  bool on = false;
+  long long launches = 0;
+  double ms[PK_COUNT] = {}, flops[PK_COUNT] = {}, bytes[PK_COUNT] = {};
+  long long count[PK_COUNT] = {};
+  struct Rec {
+    int kind;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+
+  cudaEvent_t ev() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void reset() {
+    flush();
+    launches = 0;
+    for (int k = 0; k < PK_COUNT; ++k) ms[k] = flops[k] = bytes[k] = 0, count[k] = 0;
+  }
+  // accumulate completed records (call after a stream synchronisation)
+  void flush() {
+    for (Rec& r : pending) {
+      cudaEventSynchronize(r.b);
+      float t = 0;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      ms[r.kind] += t;
+      flops[r.kind] += r.flops;
+      bytes[r.kind] += r.bytes;
+      count[r.kind] += 1;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    pending.clear();
+  }
+  void destroy() {
+    flush();
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    pool.clear();
+  }
+};
+
+struct ProfScope {
+  Profiler* p;
+  cudaStream_t st;
+  ProfScope(Profiler* prof, cudaStream_t s, int kind, double flops = 0, double bytes = 0) : p(prof), st(s) {
+    if (!p) return;
+    ++p->launches;
+    if (p->on) {
+      Profiler::Rec r{kind, p->ev(), p->ev(), flops, bytes};
+      cudaEventRecord(r.a, st);
+      p->pending.push_back(r);
+    }
+  }
+  ~ProfScope() {
+    if (p && p->on) cudaEventRecord(p->pending.back().b, st);
+  }
+};
+
+}  // namespace allegro

@@ -69,9 +69,10 @@ __global__ void scan_total(const int32_t* in, int32_t* out, int64_t n) {
   else out[0] = 0;
 }
 
-void scan_rec(cudaStream_t st, const int32_t* in, int32_t* out, int64_t n, DBuf<int32_t>* tmp, int level) {
+void scan_rec(cudaStream_t st, const int32_t* in, int32_t* out, int64_t n, DBuf<int32_t>* tmp, int level, Profiler* prof) {
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
   if (tiles <= 1) {
+    ProfScope ps_(prof, st, PK_SCAN, 0, 8.0 * n);
     scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, nullptr, n);
     ALG_LAUNCH_CHECK();
     return;
@@ -80,10 +81,16 @@ void scan_rec(cudaStream_t st, const int32_t* in, int32_t* out, int64_t n, DBuf<
   tmp[level].reserve(2 * tiles + 2);
   int32_t* sums = tmp[level].p;
   int32_t* offs = sums + tiles + 1;
-  scan_tiles<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, sums, n);
+  {
+    ProfScope ps_(prof, st, PK_SCAN, 0, 8.0 * n);
+    scan_tiles<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, sums, n);
+  }
   ALG_LAUNCH_CHECK();
-  scan_rec(st, sums, offs, tiles, tmp, level + 1);
-  scan_add<<<(unsigned)tiles, kScanThreads, 0, st>>>(out, offs, n);
+  scan_rec(st, sums, offs, tiles, tmp, level + 1, prof);
+  {
+    ProfScope ps_(prof, st, PK_SCAN, 0, 8.0 * n);
+    scan_add<<<(unsigned)tiles, kScanThreads, 0, st>>>(out, offs, n);
+  }
   ALG_LAUNCH_CHECK();
 }
 
@@ -92,7 +99,8 @@ DBuf<int32_t> g_scan_tmp[8];
 }  // namespace
 
 void exclusive_scan(allegro_ctx* c, const int32_t* in, int32_t* out, int64_t n) {
-  scan_rec(c->stream, in, out, n, g_scan_tmp, 0);
+  scan_rec(c->stream, in, out, n, g_scan_tmp, 0, &c->prof);
+  ProfScope ps_(&c->prof, c->stream, PK_SCAN, 0, 0);
   scan_total<<<1, 1, 0, c->stream>>>(in, out, n);
   ALG_LAUNCH_CHECK();
 }

@@ -171,6 +171,13 @@ void load_model(allegro_ctx* c, const char* path) {
       W.lin[k][o] = upload(W, lw);
       W.linT[k][o] = upload(W, transpose(lw, A.n_to[o] * C, C));
     }
+    li.tp_nnz = 0;
+    for (int q = 0; q < A.n_paths; ++q) {
+      const int l1 = A.path[q].a.l, l2 = A.path[q].b.l, l3 = A.path[q].o.l;
+      for (int a = 0; a < 2 * l1 + 1; ++a)
+        for (int b2 = 0; b2 < 2 * l2 + 1; ++b2)
+          for (int c3 = 0; c3 < 2 * l3 + 1; ++c3) li.tp_nnz += w3j_value(l1, l2, l3, a, b2, c3) != 0.0;
+    }
     int vb = 0;
     for (int i = 0; i < A.in.n; ++i) {
       li.v_base[i] = vb;

