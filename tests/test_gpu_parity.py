@@ -215,7 +215,7 @@ def test_md_energy_conservation_dt2_c2(pb):
     s = configs.system("C2")
     m = pb.Allegro(configs.weight_file("C2"), s.box)
 
-    def fluct(dt, t_total=20.0):
+    def fluct(dt, t_total=5.0):
         m.md_set_state(s.species, s.pos, s.vel)
         e = []
         for _ in range(int(round(t_total / dt))):
@@ -223,8 +223,8 @@ def test_md_energy_conservation_dt2_c2(pb):
         return max(e) - min(e)
 
     f1, f2 = fluct(0.5), fluct(0.25)
-    print(f"C2 energy fluctuation over 20 fs: dt=0.5 -> {f1:.3g} eV, dt=0.25 -> {f2:.3g} eV, ratio {f1 / f2:.2f}")
-    assert 2.5 < f1 / f2 < 6.0
+    print(f"C2 energy fluctuation over 5 fs: dt=0.5 -> {f1:.3g} eV, dt=0.25 -> {f2:.3g} eV, ratio {f1 / f2:.2f}")
+    assert 3.0 < f1 / f2 < 5.0
 
 
 def test_md_step_host_matches_device(pb):
