@@ -159,6 +159,10 @@ int allegro_profile_read(allegro_ctx* ctx, int kind, double* time_ms, double* fl
                          int64_t* launches);
 int64_t allegro_launch_count(allegro_ctx* ctx); /* launches since the last allegro_profile() */
 
+/* Test hook: one GEMM C[M][N] = A[M][K] W[K][N] (row-major fp32 HOST arrays) on device
+ * `device` with the given ALLEGRO_PREC_* contraction kernel (CUDA-core or tcgen05). */
+int allegro_debug_gemm(int device, int precision, int64_t M, int N, int K, const float* A, const float* W, float* C);
+
 /* Host-only helpers (no GPU needed): this library's own derivations. */
 int allegro_profile_kinds(void);
 const char* allegro_profile_kind_name(int kind);

@@ -88,13 +88,14 @@ _lib.allegro_launch_count.argtypes = [_P]
 _lib.allegro_launch_count.restype = C.c_int64
 _lib.allegro_profile_kind_name.argtypes = [C.c_int]
 _lib.allegro_profile_kind_name.restype = C.c_char_p
+_lib.allegro_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, _P, _P, _P]
 
 EXPORTED = [
     "allegro_create", "allegro_destroy", "allegro_last_error", "allegro_compute_energy_forces",
     "md_set_state", "md_get_state", "md_step", "md_count_outliers", "md_force_baseline",
     "allegro_get_edges", "allegro_get_edge_grad", "allegro_w3j_table", "allegro_param_count",
     "allegro_layer_paths", "allegro_version", "md_step_host", "allegro_profile", "allegro_profile_read",
-    "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name",
+    "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name", "allegro_debug_gemm",
 ]
 
 
@@ -129,6 +130,18 @@ def layer_paths(n_layers: int, lmax: int):
     out = np.zeros(2 * n_layers, dtype=np.int32)
     _lib.allegro_layer_paths(n_layers, lmax, out.ctypes.data)
     return [(int(out[2 * k]), int(out[2 * k + 1])) for k in range(n_layers)]
+
+
+def debug_gemm(A: np.ndarray, W: np.ndarray, precision: int = PREC_FP32, device: int = 0) -> np.ndarray:
+    """Test hook: C = A W with the library's contraction kernel (fp32 arrays)."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    W = np.ascontiguousarray(W, dtype=np.float32)
+    C_ = np.empty((A.shape[0], W.shape[1]), dtype=np.float32)
+    rc = _lib.allegro_debug_gemm(device, precision, A.shape[0], W.shape[1], A.shape[1], A.ctypes.data,
+                                 W.ctypes.data, C_.ctypes.data)
+    if rc != OK:
+        raise AllegroError(rc, _lib.allegro_last_error(None).decode())
+    return C_
 
 
 def version() -> str:

@@ -8,6 +8,8 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "gemm.cuh"
+#include "tc_gemm.cuh"
 
 using namespace allegro;
 
@@ -82,7 +84,8 @@ int allegro_create(const allegro_params* p, allegro_ctx** out) {
   if (!box_ok(p->box)) return fail(nullptr, ALLEGRO_E_ARG, "box must be three finite positive lengths");
   if (p->world_size != 1 || p->rank != 0)
     return fail(nullptr, ALLEGRO_E_ARG, "this build runs one domain per ctx (world_size == 1)");
-  if (p->precision != ALLEGRO_PREC_FP32) return fail(nullptr, ALLEGRO_E_ARG, "only ALLEGRO_PREC_FP32 is built");
+  if (p->precision != ALLEGRO_PREC_FP32 && p->precision != ALLEGRO_PREC_3XTF32)
+    return fail(nullptr, ALLEGRO_E_ARG, "built precisions: ALLEGRO_PREC_FP32, ALLEGRO_PREC_3XTF32");
   if (!(p->skin >= 0 && std::isfinite(p->skin))) return fail(nullptr, ALLEGRO_E_ARG, "skin must be >= 0");
   allegro_ctx* c = new allegro_ctx();
   c->prm = *p;
@@ -394,6 +397,42 @@ int allegro_get_edge_grad(allegro_ctx* c, int64_t capacity, double* g) {
     ALG_CUDA(cudaMemcpyAsync(h.data(), c->g.p, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream));
     ALG_CUDA(cudaStreamSynchronize(c->stream));
     for (size_t q = 0; q < h.size(); ++q) g[q] = h[q];
+    return ALLEGRO_OK;
+  });
+}
+
+int allegro_debug_gemm(int device, int precision, int64_t M, int N, int K, const float* A, const float* W, float* C) {
+  if (!A || !W || !C || M < 0 || N <= 0 || K <= 0) return fail(nullptr, ALLEGRO_E_ARG, "bad gemm arguments");
+  return guarded(nullptr, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(device));
+    std::vector<void*> owned;
+    std::vector<float> w(W, W + (size_t)K * N);
+    float *dA = nullptr, *dW = nullptr, *dC = nullptr;
+    ALG_CUDA(cudaMalloc(&dA, sizeof(float) * (M * K + 4)));
+    ALG_CUDA(cudaMalloc(&dW, sizeof(float) * K * N));
+    ALG_CUDA(cudaMalloc(&dC, sizeof(float) * (M * N + 4)));
+    ALG_CUDA(cudaMemcpy(dA, A, sizeof(float) * M * K, cudaMemcpyHostToDevice));
+    ALG_CUDA(cudaMemcpy(dW, W, sizeof(float) * K * N, cudaMemcpyHostToDevice));
+    GemmArgs g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = dA;
+    g.lda = K;
+    g.W = dW;
+    g.C = dC;
+    if (precision == ALLEGRO_PREC_3XTF32) {
+      TcWeight t = tc_prepare_weight(w, K, N, owned);
+      tc_gemm(g, t, 0, nullptr);
+    } else {
+      gemm(g, 0, nullptr);
+    }
+    ALG_CUDA(cudaDeviceSynchronize());
+    ALG_CUDA(cudaMemcpy(C, dC, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
+    cudaFree(dA);
+    cudaFree(dW);
+    cudaFree(dC);
+    for (void* p : owned) cudaFree(p);
     return ALLEGRO_OK;
   });
 }

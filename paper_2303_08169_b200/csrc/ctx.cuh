@@ -10,6 +10,7 @@
 #include "arch.cuh"
 #include "common.cuh"
 #include "prof.cuh"
+#include "tc_gemm.cuh"
 
 namespace allegro {
 
@@ -52,27 +53,36 @@ struct LayerInfo {
   int tp_nnz;          // non-zero W3j entries summed over the layer's paths (FMAs per edge-channel)
 };
 
+// One GEMM weight W [K][N]: fp32 row-major (CUDA-core path) and, in 3xTF32 mode, the
+// pre-split / pre-swizzled tensor-core image.
+struct Wt {
+  float* f = nullptr;
+  TcWeight tc;
+  int K = 0, N = 0;
+};
+
 struct DevWeights {
-  float* tb_w0 = nullptr;   // [16][32], rows 12..15 zero
-  float* tb_w1 = nullptr;   // [32][64]
-  float* tb_w2 = nullptr;   // [64][128]
-  float* tb_w0T = nullptr;  // [32][16]
-  float* tb_w1T = nullptr;  // [64][32]
-  float* tb_w2T = nullptr;  // [128][64]
-  float* env[kMaxLayers] = {};   // [128][nw]  columns in [chunk][l][c] order
-  float* envT[kMaxLayers] = {};  // [nw][128]
-  float* lin[kMaxLayers][kMaxIr] = {};   // [n_to*C][C]   rows (path_local, c)
-  float* linT[kMaxLayers][kMaxIr] = {};  // [C][n_to*C]
-  float* lat[kMaxLayers] = {};     // [128 + n_s*C][128], scalar rows in (q, c) order
-  float* latT_x[kMaxLayers] = {};  // [128][128]
-  float* latT_s[kMaxLayers] = {};  // [128][n_s*C]
-  float* wout = nullptr;           // [128] = W_o1 W_o2 / (sqrt(128) sqrt(32))
+  Wt tb_w0;   // [16][32], rows 12..15 zero
+  Wt tb_w1;   // [32][64]
+  Wt tb_w2;   // [64][128]
+  Wt tb_w0T;  // [32][16]
+  Wt tb_w1T;  // [64][32]
+  Wt tb_w2T;  // [128][64]
+  Wt env[kMaxLayers];             // [128][nw]  columns in [chunk][l][c] order
+  Wt envT[kMaxLayers];            // [nw][128]
+  Wt lin[kMaxLayers][kMaxIr];     // [n_to*C][C]   rows (path_local, c)
+  Wt linT[kMaxLayers][kMaxIr];    // [C][n_to*C]
+  Wt lat[kMaxLayers];             // [128 + n_s*C][128], scalar rows in (q, c) order
+  Wt latT_x[kMaxLayers];          // [128][128]
+  Wt latT_s[kMaxLayers];          // [128][n_s*C]
+  float* wout = nullptr;          // [128] = W_o1 W_o2 / (sqrt(128) sqrt(32))
   float bessel[kNB] = {};
   std::vector<void*> owned;
 };
 
 struct Model {
   int n_layers = 0, lmax = 0;
+  int precision = ALLEGRO_PREC_FP32;
   double r_max = 0, nbar = 0, sigma[2] = {1, 1}, mu[2] = {0, 0};
   LayerInfo L[kMaxLayers];
   DevWeights w;

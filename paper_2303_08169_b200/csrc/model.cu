@@ -484,6 +484,12 @@ void tp_dispatch(int NL, int LMAX, int K, bool fwd, const TpArgs& t, cudaStream_
   throw CudaError("no TP kernel for this architecture");
 }
 
+// CUDA-core fp32 (parity reference mode) or tcgen05 3xTF32 (tensor cores)
+void run_gemm(const Model& M, const GemmArgs& g, const Wt& w, cudaStream_t st, Profiler* prof) {
+  if (M.precision == ALLEGRO_PREC_3XTF32) tc_gemm(g, w.tc, st, prof);
+  else gemm(g, st, prof);
+}
+
 size_t floats_per_edge(const Model& M) {
   const int dsh = (M.lmax + 1) * (M.lmax + 1);
   size_t f = 16 + 32 + 32 + 64 + 64 + 128 + 1 + dsh + 2 * 128;
@@ -565,7 +571,10 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     }
     ALG_LAUNCH_CHECK();
   }
-  auto G = [&](const float* A, int lda, const float* W, int N, int K, float* C, float s, int epi) {
+  const Wt* last_w = nullptr;
+  auto G = [&](const float* A, int lda, const Wt& Wm, int N, int K, float* C, float s, int epi) {
+    last_w = &Wm;
+    const float* W = Wm.f;
     GemmArgs g;
     g.M = E;
     g.N = N;
@@ -582,14 +591,14 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   {
     GemmArgs g = G(w.z.p, 16, M.w.tb_w0, 32, 16, w.h1.p, 1.f / std::sqrt(12.f), EPI_SILU);
     g.aux = w.a1.p;
-    gemm(g, st, &c->prof);
+    run_gemm(M, g, *last_w, st, &c->prof);
     g = G(w.h1.p, 32, M.w.tb_w1, 64, 32, w.h2.p, kCSilu / std::sqrt(32.f), EPI_SILU);
     g.aux = w.a2.p;
-    gemm(g, st, &c->prof);
+    run_gemm(M, g, *last_w, st, &c->prof);
     g = G(w.h2.p, 64, M.w.tb_w2, 128, 64, w.xa.p, kCSilu / std::sqrt(64.f), EPI_UMUL_SAVE);
     g.aux = w.m.p;
     g.u = w.u.p;
-    gemm(g, st, &c->prof);
+    run_gemm(M, g, *last_w, st, &c->prof);
   }
   float* x = w.xa.p;
   float* xn = w.xb.p;
@@ -604,7 +613,10 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   // ---- layers (E6) ----
   for (int k = 0; k < M.n_layers; ++k) {
     const LayerInfo& L = M.L[k];
-    gemm(G(x, 128, M.w.env[k], L.nw, 128, w.w[k].p, 1.f / std::sqrt(128.f), EPI_STORE), st, &c->prof);
+    {
+      GemmArgs g = G(x, 128, M.w.env[k], L.nw, 128, w.w[k].p, 1.f / std::sqrt(128.f), EPI_STORE);
+      run_gemm(M, g, *last_w, st, &c->prof);
+    }
     tp.w = w.w[k].p;
     tp.V = k >= 1 ? w.V[k].p : nullptr;
     tp.G = w.G[k].p;
@@ -616,7 +628,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
                        w.V[k + 1].p + (int64_t)M.L[k + 1].v_base[o] * ecap, 1.f / std::sqrt((float)(kC * L.A.n_to[o])),
                        EPI_STORE);
         g.M = E * dim;
-        gemm(g, st, &c->prof);
+        run_gemm(M, g, *last_w, st, &c->prof);
       }
     }
     GemmArgs g = G(x, 128, M.w.lat[k], 128, L.fan_lat, xn, 1.f / std::sqrt((float)L.fan_lat), EPI_RESID);
@@ -628,7 +640,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     g.u = w.u.p;
     g.alpha = kResA;
     g.beta = kResB;
-    gemm(g, st, &c->prof);
+    run_gemm(M, g, *last_w, st, &c->prof);
     std::swap(x, xn);
   }
   // ---- energies (E7, E8) and x-bar^L ----
@@ -664,11 +676,11 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
       g.u = w.u.p;
       g.alpha = kResA;
       g.beta = kResB;
-      gemm(g, st, &c->prof);
+      run_gemm(M, g, *last_w, st, &c->prof);
       g = G(xb, 128, M.w.latT_s[k], L.A.n_s * kC, 128, w.sbar.p, sl, EPI_USCALE);
       g.u = w.u.p;
       g.beta = kResB;
-      gemm(g, st, &c->prof);
+      run_gemm(M, g, *last_w, st, &c->prof);
     }
     tp.w = w.w[k].p;
     tp.V = k >= 1 ? w.V[k].p : nullptr;
@@ -689,14 +701,14 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
           g.epi = EPI_ADDX;
           g.X = w.sbar.p;
         }
-        gemm(g, st, &c->prof);
+        run_gemm(M, g, *last_w, st, &c->prof);
         tp.Tb[o] = dst;
       }
     }
     tp_dispatch(M.n_layers, M.lmax, k, false, tp, st, &c->prof, L);
     {
       GemmArgs g = G(w.wbar.p, L.nw, M.w.envT[k], 128, L.nw, xbn, 1.f / std::sqrt(128.f), EPI_ACC);
-      gemm(g, st, &c->prof);
+      run_gemm(M, g, *last_w, st, &c->prof);
     }
     std::swap(xb, xbn);
     std::swap(vb, vbn);
@@ -713,12 +725,12 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     GemmArgs g = G(xb, 128, M.w.tb_w2T, 64, 128, w.ab2.p, kCSilu / std::sqrt(64.f), EPI_DSILU);
     g.X = w.a2.p;
     g.u = w.u.p;
-    gemm(g, st, &c->prof);
+    run_gemm(M, g, *last_w, st, &c->prof);
     g = G(w.ab2.p, 64, M.w.tb_w1T, 32, 64, w.ab1.p, kCSilu / std::sqrt(32.f), EPI_DSILU);
     g.X = w.a1.p;
-    gemm(g, st, &c->prof);
+    run_gemm(M, g, *last_w, st, &c->prof);
     g = G(w.ab1.p, 32, M.w.tb_w0T, 16, 32, w.zbar.p, 1.f / std::sqrt(12.f), EPI_STORE);
-    gemm(g, st, &c->prof);
+    run_gemm(M, g, *last_w, st, &c->prof);
   }
   if (E > 0) {
     {

@@ -1,0 +1,32 @@
+// tc_gemm.cuh -- tcgen05 / TMEM / TMA tensor-core GEMM in split precision (3xTF32) for
+// the per-edge contractions (ALLEGRO_PREC_3XTF32).  Same epilogues as gemm.cuh.
+//
+// Single-pass TF32 misses the force bound by ~30x; 3xTF32
+// (a = a_hi + a_lo, w = w_hi + w_lo, a w ~ a_hi w_lo + a_lo w_hi + a_hi w_hi) keeps the
+// error at the fp32 level.  W is pre-split and pre-swizzled on the host once per weight.
+#pragma once
+#include <vector>
+
+#include "gemm.cuh"
+
+namespace allegro {
+
+// A weight W [K][N] prepared for the tensor-core path: per N-tile an SMEM image
+// [hi | lo], each [K/32 blocks][N_t rows][128 B, SWIZZLE_128B] of W^T (K-major).
+struct TcWeight {
+  int K = 0, N = 0, N_t = 0, n_tiles = 0;
+  size_t tile_bytes = 0;  // bytes of one N-tile image (hi + lo)
+  float* dev = nullptr;   // n_tiles images, contiguous
+};
+
+// Build (host) and upload a TcWeight from row-major fp32 W [K][N].
+TcWeight tc_prepare_weight(const std::vector<float>& W, int K, int N, std::vector<void*>& owned);
+
+// C = epi(A W) on the tensor cores.  g.W is ignored; K % 32 == 0 (pad), N % 16 == 0.
+void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* prof);
+
+// Host-side split used for the weights (exposed for tests): hi = fp32 with the low
+// 13 mantissa bits cleared (exactly representable in TF32), lo = fp32(x - hi).
+float tf32_hi(float x);
+
+}  // namespace allegro

@@ -42,6 +42,15 @@ float* upload(DevWeights& w, const std::vector<float>& h) {
   return d;
 }
 
+Wt make_wt(DevWeights& w, const std::vector<float>& h, int K, int N, bool tc) {
+  Wt t;
+  t.K = K;
+  t.N = N;
+  t.f = upload(w, h);
+  if (tc) t.tc = tc_prepare_weight(h, K, N, w.owned);
+  return t;
+}
+
 std::vector<float> transpose(const std::vector<float>& a, int rows, int cols) {
   std::vector<float> t((size_t)rows * cols);
   for (int r = 0; r < rows; ++r)
@@ -106,6 +115,7 @@ void load_model(allegro_ctx* c, const char* path) {
 
   Model& M = c->model;
   free_model(M);
+  M.precision = c->prm.precision;
   M.n_layers = L;
   M.lmax = lmax;
   M.r_max = dh[0];
@@ -116,6 +126,7 @@ void load_model(allegro_ctx* c, const char* path) {
   M.mu[1] = dh[5];
   const int n_env = lmax + 1;
   DevWeights& W = M.w;
+  const bool tc = M.precision == ALLEGRO_PREC_3XTF32;
 
   const HostTensor& bf = need("bessel_freq", 1, kNB);
   for (int i = 0; i < kNB; ++i) W.bessel[i] = (float)bf.v[i];
@@ -125,16 +136,16 @@ void load_model(allegro_ctx* c, const char* path) {
     std::vector<float> h(16 * 32, 0.f);
     for (int r = 0; r < 12; ++r)
       for (int q = 0; q < 32; ++q) h[r * 32 + q] = (float)w0.at(r, q);
-    W.tb_w0 = upload(W, h);
-    W.tb_w0T = upload(W, transpose(h, 16, 32));
+    W.tb_w0 = make_wt(W, h, 16, 32, tc);
+    W.tb_w0T = make_wt(W, transpose(h, 16, 32), 32, 16, tc);
     const HostTensor& w1 = need("tb_w1", 32, 64);
     std::vector<float> h1(w1.v.begin(), w1.v.end());
-    W.tb_w1 = upload(W, h1);
-    W.tb_w1T = upload(W, transpose(h1, 32, 64));
+    W.tb_w1 = make_wt(W, h1, 32, 64, tc);
+    W.tb_w1T = make_wt(W, transpose(h1, 32, 64), 64, 32, tc);
     const HostTensor& w2 = need("tb_w2", 64, 128);
     std::vector<float> h2(w2.v.begin(), w2.v.end());
-    W.tb_w2 = upload(W, h2);
-    W.tb_w2T = upload(W, transpose(h2, 64, 128));
+    W.tb_w2 = make_wt(W, h2, 64, 128, tc);
+    W.tb_w2T = make_wt(W, transpose(h2, 64, 128), 128, 64, tc);
   }
   for (int k = 0; k < L; ++k) {
     LayerInfo& li = M.L[k];
@@ -151,8 +162,8 @@ void load_model(allegro_ctx* c, const char* path) {
         for (int cc = 0; cc < C; ++cc)
           for (int l = 0; l < n_env; ++l)
             h[(size_t)r * li.nw + ch * C * n_env + l * C + cc] = (float)we.at(r, ch * C * n_env + cc * n_env + l);
-    W.env[k] = upload(W, h);
-    W.envT[k] = upload(W, transpose(h, D, li.nw));
+    W.env[k] = make_wt(W, h, D, li.nw, tc);
+    W.envT[k] = make_wt(W, transpose(h, D, li.nw), li.nw, D, tc);
     // TP-linear per out irrep: rows (path_local, c)
     int np_found = 0;
     while (T.count("tplin_" + std::to_string(k) + "_" + std::to_string(np_found))) ++np_found;
@@ -168,8 +179,8 @@ void load_model(allegro_ctx* c, const char* path) {
         for (int cc = 0; cc < C; ++cc)
           for (int v = 0; v < C; ++v) lw[((size_t)A.out_local[q] * C + cc) * C + v] = (float)wp.at(cc, v);
       }
-      W.lin[k][o] = upload(W, lw);
-      W.linT[k][o] = upload(W, transpose(lw, A.n_to[o] * C, C));
+      W.lin[k][o] = make_wt(W, lw, A.n_to[o] * C, C, tc);
+      W.linT[k][o] = make_wt(W, transpose(lw, A.n_to[o] * C, C), C, A.n_to[o] * C, tc);
     }
     li.tp_nnz = 0;
     for (int q = 0; q < A.n_paths; ++q) {
@@ -191,11 +202,11 @@ void load_model(allegro_ctx* c, const char* path) {
     for (int cc = 0; cc < C; ++cc)
       for (int s = 0; s < A.n_s; ++s)
         for (int q = 0; q < D; ++q) hl[(size_t)(D + s * C + cc) * D + q] = (float)wl.at(D + cc * A.n_s + s, q);
-    W.lat[k] = upload(W, hl);
+    W.lat[k] = make_wt(W, hl, li.fan_lat, D, tc);
     std::vector<float> hx(hl.begin(), hl.begin() + (size_t)D * D);
     std::vector<float> hs(hl.begin() + (size_t)D * D, hl.end());
-    W.latT_x[k] = upload(W, transpose(hx, D, D));
-    W.latT_s[k] = upload(W, transpose(hs, C * A.n_s, D));
+    W.latT_x[k] = make_wt(W, transpose(hx, D, D), D, D, tc);
+    W.latT_s[k] = make_wt(W, transpose(hs, C * A.n_s, D), D, C * A.n_s, tc);
   }
   {
     const HostTensor& o1 = need("out_w1", D, 32);

@@ -79,13 +79,36 @@ def test_edges_random_boxes_incl_multi_image(pb, tmp_path, seed):
     assert _edge_set(gi, gj, gs) == _edge_set(ri, rj, rn)
 
 
+@pytest.mark.parametrize("M,N,K", [(1000, 32, 16), (4097, 128, 128), (300, 64, 224), (129, 16, 32), (5000, 192, 128),
+                                   (777, 96, 96)])
+def test_gemm_kernels(pb, M, N, K):
+    """Both contraction kernels against an fp64 matmul (ragged M, all N/K shapes used)."""
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = rng.uniform(-1.7, 1.7, (K, N)).astype(np.float32)
+    ref = A.astype(np.float64) @ W.astype(np.float64)
+    scale = np.abs(A).astype(np.float64) @ np.abs(W).astype(np.float64)
+    for prec in (pb.PREC_FP32, pb.PREC_3XTF32):
+        C = pb.debug_gemm(A, W, prec)
+        err = np.abs(C - ref) / scale
+        assert err.max() < 5e-6, (prec, err.max())
+
+
+PRECS = ["fp32", "3xtf32"]
+
+
+def _prec(pb, name):
+    return pb.PREC_FP32 if name == "fp32" else pb.PREC_3XTF32
+
+
+@pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("cfg", ["C1", "C2"])
-def test_energy_forces_parity(pb, cfg):
+def test_energy_forces_parity(pb, cfg, prec):
     s = configs.system(cfg)
     wf = configs.weight_file(cfg)
     model = weights_io.read(wf)
     ref = oa.energy_forces(model, s.pos, s.species, s.box)
-    m = pb.Allegro(wf, s.box)
+    m = pb.Allegro(wf, s.box, precision=_prec(pb, prec))
     e, ea, F = m.compute_energy_forces(s.pos, s.species)
     err = _check_energy_forces(ref, e, ea, F)
     # per-edge dE/dr_e in the same (canonical) order
@@ -94,32 +117,34 @@ def test_energy_forces_parity(pb, cfg):
     print(f"{cfg}: max|dF| = {err:.3g} eV/A, E = {e:.6f} vs {ref['energy']:.6f}")
 
 
+@pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("L,lmax", [(2, 1), (2, 2), (3, 0), (3, 1), (3, 2)])
-def test_every_architecture_on_c1_geometry(pb, tmp_path, L, lmax):
+def test_every_architecture_on_c1_geometry(pb, tmp_path, L, lmax, prec):
     s = configs.system("C1")
     wf = _model_file(tmp_path, L, lmax, 5.0, 3.0)
     ref = oa.energy_forces(weights_io.read(wf), s.pos, s.species, s.box)
-    m = pb.Allegro(wf, s.box)
+    m = pb.Allegro(wf, s.box, precision=_prec(pb, prec))
     e, ea, F = m.compute_energy_forces(s.pos, s.species)
     _check_energy_forces(ref, e, ea, F * 1.0)
 
 
-def test_c3_full_size_sampled(pb):
-    """C3 at full size (110,592 atoms, paper's l=2 model) in the launch configuration
-    the bench uses; the oracle computes sampled atoms one by one (rows of the atoms
-    and of all their neighbours)."""
-    s = configs.system("C3")
-    wf = configs.weight_file("C3")
-    m = pb.Allegro(wf, s.box)
+@pytest.mark.parametrize("cfg,prec", [("C3", "fp32"), ("C3", "3xtf32"), ("C5", "3xtf32")])
+def test_full_size_sampled(pb, cfg, prec):
+    """C3 (110,592 atoms, paper's l=2 model) and C5 (500,000 atoms, the bench workload, in
+    the bench's launch configuration) at full size; the oracle computes sampled atoms one
+    by one (rows of the atoms and of all their neighbours)."""
+    s = configs.system(cfg)
+    wf = configs.weight_file(cfg)
+    m = pb.Allegro(wf, s.box, precision=_prec(pb, prec), n_atoms=s.n)
     e, ea, F = m.compute_energy_forces(s.pos, s.species)
-    atoms = np.array([0, 55555, 110591])
+    atoms = np.array([0, s.n // 2 + 1, s.n - 1])
     Fo, Eo, _ = oa.sampled_forces(weights_io.read(wf), s.pos, s.species, s.box, atoms)
     assert np.abs(F[atoms] - Fo).max() <= F_TOL
     assert np.abs(ea[atoms] - Eo).max() <= E_TOL * np.abs(ea).max()
     # properties at any size: zero net force, per-row edge-set rows of the sample
     assert np.abs(F.sum(0)).max() < 1e-6 * s.n
     gi, gj, gs = m.get_edges()
-    ri, rj, rn = onb.cell_list(onb.wrap(s.pos, s.box), s.box, 6.0, atoms)
+    ri, rj, rn = onb.cell_list(onb.wrap(s.pos, s.box), s.box, configs.CONFIGS[cfg].r_cut, atoms)
     mask = np.isin(gi, atoms)
     assert _edge_set(gi[mask], gj[mask], gs[mask]) == _edge_set(ri, rj, rn)
 
