@@ -163,6 +163,11 @@ int64_t allegro_launch_count(allegro_ctx* ctx); /* launches since the last alleg
  * `device` with the given ALLEGRO_PREC_* contraction kernel (CUDA-core or tcgen05). */
 int allegro_debug_gemm(int device, int precision, int64_t M, int N, int K, const float* A, const float* W, float* C);
 
+/* Test hook: time `iters` launches of one contraction shape on device buffers (CUDA events);
+ * epi = internal epilogue id; tma_store / max_stages / diag tune the tcgen05 kernel. */
+int allegro_debug_gemm_bench(int device, int precision, int64_t M, int N, int K, int epi, int iters, int tma_store,
+                             int max_stages, int diag, double* ms_per_iter);
+
 /* Host-only helpers (no GPU needed): this library's own derivations. */
 int allegro_profile_kinds(void);
 const char* allegro_profile_kind_name(int kind);

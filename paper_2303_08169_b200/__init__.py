@@ -89,6 +89,8 @@ _lib.allegro_launch_count.restype = C.c_int64
 _lib.allegro_profile_kind_name.argtypes = [C.c_int]
 _lib.allegro_profile_kind_name.restype = C.c_char_p
 _lib.allegro_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, _P, _P, _P]
+_lib.allegro_debug_gemm_bench.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          C.c_int, C.c_int, C.POINTER(C.c_double)]
 
 EXPORTED = [
     "allegro_create", "allegro_destroy", "allegro_last_error", "allegro_compute_energy_forces",
@@ -96,6 +98,7 @@ EXPORTED = [
     "allegro_get_edges", "allegro_get_edge_grad", "allegro_w3j_table", "allegro_param_count",
     "allegro_layer_paths", "allegro_version", "md_step_host", "allegro_profile", "allegro_profile_read",
     "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name", "allegro_debug_gemm",
+    "allegro_debug_gemm_bench",
 ]
 
 
@@ -142,6 +145,16 @@ def debug_gemm(A: np.ndarray, W: np.ndarray, precision: int = PREC_FP32, device:
     if rc != OK:
         raise AllegroError(rc, _lib.allegro_last_error(None).decode())
     return C_
+
+
+def debug_gemm_bench(M, N, K, epi=0, precision=PREC_3XTF32, iters=10, tma_store=1, max_stages=4, diag=0,
+                     device=0) -> float:
+    """Test hook: ms per launch of one contraction shape (device buffers, CUDA events)."""
+    ms = C.c_double(0)
+    rc = _lib.allegro_debug_gemm_bench(device, precision, M, N, K, epi, iters, tma_store, max_stages, diag, C.byref(ms))
+    if rc != OK:
+        raise AllegroError(rc, _lib.allegro_last_error(None).decode())
+    return ms.value
 
 
 def version() -> str:

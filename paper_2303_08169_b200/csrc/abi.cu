@@ -437,6 +437,68 @@ int allegro_debug_gemm(int device, int precision, int64_t M, int N, int K, const
   });
 }
 
+int allegro_debug_gemm_bench(int device, int precision, int64_t M, int N, int K, int epi, int iters, int tma_store,
+                             int max_stages, int diag, double* ms_per_iter) {
+  if (!ms_per_iter || M <= 0 || N <= 0 || K <= 0 || iters <= 0) return fail(nullptr, ALLEGRO_E_ARG, "bad arguments");
+  return guarded(nullptr, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(device));
+    std::vector<void*> owned;
+    std::vector<float> w((size_t)K * N);
+    for (size_t i = 0; i < w.size(); ++i) w[i] = (float)((i * 2654435761u) % 1000) / 1000.f - 0.5f;
+    float *dA = nullptr, *dW = nullptr, *dC = nullptr, *dX = nullptr, *dAux = nullptr, *du = nullptr;
+    ALG_CUDA(cudaMalloc(&dA, sizeof(float) * M * K));
+    ALG_CUDA(cudaMalloc(&dW, sizeof(float) * K * N));
+    ALG_CUDA(cudaMalloc(&dC, sizeof(float) * M * N));
+    ALG_CUDA(cudaMalloc(&dX, sizeof(float) * M * N));
+    ALG_CUDA(cudaMalloc(&dAux, sizeof(float) * M * N));
+    ALG_CUDA(cudaMalloc(&du, sizeof(float) * M));
+    ALG_CUDA(cudaMemset(dA, 0, sizeof(float) * M * K));
+    ALG_CUDA(cudaMemset(dX, 0, sizeof(float) * M * N));
+    ALG_CUDA(cudaMemset(du, 0, sizeof(float) * M));
+    ALG_CUDA(cudaMemcpy(dW, w.data(), sizeof(float) * K * N, cudaMemcpyHostToDevice));
+    GemmArgs g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = dA;
+    g.lda = K;
+    g.W = dW;
+    g.C = dC;
+    g.epi = epi;
+    if (epi == EPI_RESID || epi == EPI_SILU || epi == EPI_UMUL_SAVE) g.aux = dAux;
+    if (epi == EPI_RESID || epi == EPI_URESID || epi == EPI_ADDX || epi == EPI_DSILU) g.X = dX;
+    if (epi == EPI_RESID || epi == EPI_URESID || epi == EPI_UMUL_SAVE || epi == EPI_USCALE) g.u = du;
+    const TcTuning saved = g_tc_tuning;
+    g_tc_tuning.tma_store = tma_store;
+    g_tc_tuning.max_stages = max_stages;
+    g_tc_tuning.diag = diag;
+    TcWeight t;
+    if (precision == ALLEGRO_PREC_3XTF32) t = tc_prepare_weight(w, K, N, owned);
+    auto run = [&]() {
+      if (precision == ALLEGRO_PREC_3XTF32) tc_gemm(g, t, 0, nullptr);
+      else gemm(g, 0, nullptr);
+    };
+    run();
+    ALG_CUDA(cudaDeviceSynchronize());
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, 0);
+    for (int i = 0; i < iters; ++i) run();
+    cudaEventRecord(e1, 0);
+    ALG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *ms_per_iter = ms / iters;
+    g_tc_tuning = saved;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (void* q : {(void*)dA, (void*)dW, (void*)dC, (void*)dX, (void*)dAux, (void*)du}) cudaFree(q);
+    for (void* q : owned) cudaFree(q);
+    return ALLEGRO_OK;
+  });
+}
+
 int allegro_w3j_table(int l1, int l2, int l3, double* out) {
   if (!out || l1 < 0 || l2 < 0 || l3 < 0 || l1 > 2 || l2 > 2 || l3 > 2) return ALLEGRO_E_ARG;
   if (!(std::abs(l1 - l2) <= l3 && l3 <= l1 + l2)) return ALLEGRO_E_ARG;

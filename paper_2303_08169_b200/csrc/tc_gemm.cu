@@ -1,18 +1,20 @@
 // tc_gemm.cu -- tcgen05 tensor-core GEMM (3xTF32) with TMA-fed operands, TMEM
 // accumulators and the fused epilogues of gemm.cuh.
 //
-// One CTA per SM walks 128-row tiles of A (persistent).  Warp roles (256 threads):
-//   warp 0      TMA producer: A[128 x 32] fp32 K-blocks (SWIZZLE_128B) into a ring of
-//               stages; the W image of this N-tile once (cp.async.bulk).
-//   warps 2-3   split workers: a_hi = a with the low 13 mantissa bits cleared (in place),
-//               a_lo = a - a_hi into the stage's lo buffer; fence.proxy.async; arrive.
-//   warp 1      MMA issuer (one lane): per K-block 4 x K=8 steps of
-//               tcgen05.mma.kind::tf32  D += a_hi w_lo;  D += a_lo w_hi;  D += a_hi w_hi
+// One CTA per SM walks 128-row tiles of A (persistent).  Warp roles (320 threads):
+//   warp 8      TMA producer: A[128 x 32] fp32 K-blocks (SWIZZLE_128B) into a ring of raw
+//               SMEM stages; the W image of this N-tile once (cp.async.bulk).
+//   warps 0-3   split warpgroup (thread = row = TMEM lane): reads its row of a raw stage,
+//               a_hi = a with the low 13 mantissa bits cleared, a_lo = a - a_hi, and writes
+//               both into a TMEM A stage with tcgen05.st (the raw stage is freed at once).
+//   warp 9      MMA issuer (one lane): per K-block 4 x K=8 steps of
+//               tcgen05.mma.kind::tf32 (A from TMEM, W from SMEM)
+//                 D += a_hi w_lo;  D += a_lo w_hi;  D += a_hi w_hi
 //               into one of two TMEM accumulators [128 lanes x N_t fp32 columns];
-//               tcgen05.commit frees the stage / publishes the accumulator.
-//   warps 4-7   epilogue warpgroup: tcgen05.ld 32x32b (thread = row), fused epilogue,
-//               vectorised stores; releases the accumulator.
-// SMEM descriptors: K-major, SWIZZLE_128B, SBO = 1024 B, version 1 (sm_100).
+//               tcgen05.commit frees the TMEM A stage / publishes the accumulator.
+//   warps 4-7   epilogue warpgroup: tcgen05.ld 32x32b (thread = row), fused epilogue, and a
+//               per-warp swizzled SMEM transpose so global loads/stores are 4 x 128 B lines.
+// W SMEM descriptors: K-major, SWIZZLE_128B, SBO = 1024 B, version 1 (sm_100).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -24,13 +26,15 @@
 namespace allegro {
 namespace {
 
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 320;              // 10 warps
 constexpr int BLK_K = 32;                    // fp32 per 128-byte K-block
 constexpr int ROWS = 128;                    // UMMA M
-constexpr int A_BLOCK_BYTES = ROWS * 128;    // 16 KB
-constexpr int STAGE_BYTES = 2 * A_BLOCK_BYTES;
+constexpr int A_BLOCK_BYTES = ROWS * 128;    // 16 KB raw A K-block (TMA, SWIZZLE_128B)
+constexpr int STAGE_BYTES = A_BLOCK_BYTES;
+constexpr int A_TMEM_COLS = 64;              // one TMEM A stage: hi (32 cols) + lo (32 cols)
 constexpr size_t SMEM_LIMIT = 227 * 1024;
 constexpr size_t SMEM_RESERVE = 2048;        // barriers + alignment slack
+constexpr int STAGE_OUT_BYTES = 32 * 128;    // per epilogue warp: [32 rows x 32 fp32] transpose tile
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -61,6 +65,29 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"((uint64_t)map), "r"(c0),
+               "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,"
+      "%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -76,11 +103,23 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+// D[tmem] (+)= A[tmem] B[smem]
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p; }" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -115,38 +154,110 @@ struct TcParams {
   int N_t;             // tile width (multiple of 16)
   int nK;              // K-blocks of 32
   int nK1;             // K-blocks coming from A (rest from A2)
-  int stages;
+  int stages;          // raw SMEM ring depth
+  int a_stages;        // TMEM A ring depth
   uint32_t w_bytes;    // bytes of the W image (hi + lo)
   int n_mtiles;
+  int acc_cols;        // TMEM columns per accumulator (>= N_t, multiple of 32)
+  uint32_t tmem_cols;  // allocated TMEM columns
+  int diag;            // diagnostics: bit0 skip MMAs, bit1 skip global stores
 };
 
+// v <- s v (the saved pre-activation "aux"); out <- epilogue(v, xin) (xin = X, or old C for EPI_ACC)
+template <int NV, int EPI>
+__device__ __forceinline__ void epi_apply(const GemmArgs& g, float* v, const float* xin, float ur, float* out) {
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const float pv = g.s * v[j];
+    v[j] = pv;
+    switch (EPI) {
+      case EPI_STORE: out[j] = pv; break;
+      case EPI_SILU: out[j] = silu(pv); break;
+      case EPI_UMUL_SAVE: out[j] = ur * pv; break;
+      case EPI_RESID: out[j] = g.alpha * xin[j] + g.beta * ur * pv; break;
+      case EPI_URESID: out[j] = g.alpha * xin[j] + g.beta * ur * pv; break;
+      case EPI_USCALE: out[j] = g.beta * ur * pv; break;
+      case EPI_ACC: out[j] = xin[j] + pv; break;
+      case EPI_ADDX: out[j] = pv + xin[j]; break;
+      case EPI_DSILU: out[j] = ur * pv * dsilu(xin[j]); break;
+      default: out[j] = pv; break;
+    }
+  }
+}
+
+// Per-warp transpose tile [32 rows][32 fp32] with 16-byte chunks XOR-swizzled by row % 8:
+// a thread writing / reading its own row and a warp reading / writing 4 rows x 128 B are
+// both bank-conflict free.
+__device__ __forceinline__ float4* tile_at(unsigned char* buf, int row, int chunk) {
+  return reinterpret_cast<float4*>(buf + row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+// coalesced global [32 rows x 32 cols] (row stride ld floats) -> thread-row registers
+// nc = valid 16-byte chunks per row (8 for 32 columns, 4 for a 16-column tile)
+__device__ __forceinline__ void gather_rows(unsigned char* buf, const float* src, int64_t ld, int64_t row0, int64_t M,
+                                            int lane, float* dst, int nc) {
+  float4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {  // all 8 coalesced loads in flight before any use
+    const int r = (lane >> 3) + 4 * i, c = lane & 7;
+    v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row0 + r < M && c < nc) v[i] = __ldg(reinterpret_cast<const float4*>(src + (row0 + r) * ld + 4 * c));
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) *tile_at(buf, (lane >> 3) + 4 * i, lane & 7) = v[i];
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 w = *tile_at(buf, lane, c);
+    dst[4 * c] = w.x, dst[4 * c + 1] = w.y, dst[4 * c + 2] = w.z, dst[4 * c + 3] = w.w;
+  }
+  __syncwarp();
+}
+// thread-row registers -> coalesced global
+__device__ __forceinline__ void scatter_rows(unsigned char* buf, float* dst, int64_t ld, int64_t row0, int64_t M, int lane,
+                                             const float* src, int nc) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) *tile_at(buf, lane, c) = make_float4(src[4 * c], src[4 * c + 1], src[4 * c + 2], src[4 * c + 3]);
+  __syncwarp();
+  float4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = *tile_at(buf, (lane >> 3) + 4 * i, lane & 7);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = (lane >> 3) + 4 * i, c = lane & 7;
+    if (row0 + r < M && c < nc) __stcs(reinterpret_cast<float4*>(dst + (row0 + r) * ld + 4 * c), v[i]);
+  }
+  __syncwarp();
+}
+
+template <int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2, TcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
-  // 1024-align the dynamic smem base (SWIZZLE_128B atoms)
-  unsigned char* base = (unsigned char*)(((uintptr_t)smem_dyn + 1023) & ~(uintptr_t)1023);
+  // 1024-align inside the __shared__ array (pointer arithmetic keeps the shared address space)
+  unsigned char* base = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
   unsigned char* w_hi = base;
   unsigned char* w_lo = base + p.w_bytes / 2;
   unsigned char* stage0 = base + ((p.w_bytes + 1023) & ~1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + (size_t)p.stages * STAGE_BYTES);
-  uint64_t* full = bars;                    // [stages] TMA landed
-  uint64_t* split = bars + p.stages;        // [stages] hi/lo written
-  uint64_t* empty = bars + 2 * p.stages;    // [stages] MMAs done with the stage
-  uint64_t* acc_full = bars + 3 * p.stages; // [2]
-  uint64_t* acc_empty = acc_full + 2;       // [2]
+  unsigned char* out_stage = stage0 + (size_t)p.stages * STAGE_BYTES;  // [4 warps][4 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(out_stage + 4 * STAGE_OUT_BYTES);
+  uint64_t* raw_full = bars;                          // [stages]  TMA landed
+  uint64_t* raw_empty = raw_full + p.stages;          // [stages]  split warps read it
+  uint64_t* a_full = raw_empty + p.stages;            // [a_stages] hi/lo in TMEM
+  uint64_t* a_empty = a_full + p.a_stages;            // [a_stages] MMAs done with it
+  uint64_t* acc_full = a_empty + p.a_stages;          // [2]
+  uint64_t* acc_empty = acc_full + 2;                 // [2]
   uint64_t* w_full = acc_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int acc_cols = p.N_t;
-  uint32_t tmem_cols = 32;
-  while (tmem_cols < 2u * acc_cols) tmem_cols <<= 1;
-
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(split + s, 64);
-      mbar_init(empty + s, 1);
+      mbar_init(raw_full + s, 1);
+      mbar_init(raw_empty + s, 4);
+    }
+    for (int s = 0; s < p.a_stages; ++s) {
+      mbar_init(a_full + s, 4);
+      mbar_init(a_empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(acc_full + a, 1);
@@ -155,15 +266,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     mbar_init(w_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
+  if (warp == 9) tmem_alloc(tmem_slot, p.tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_a = tmem + 2u * (uint32_t)p.acc_cols;  // A ring after the two accumulators
 
   const int n_my = p.n_mtiles > (int)blockIdx.x ? (p.n_mtiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
-  if (warp == 0) {
+  if (warp == 8) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       mbar_expect_tx(w_full, p.w_bytes);
@@ -177,143 +289,143 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int t = 0; t < n_my; ++t) {
         const int m0 = ((int)blockIdx.x + t * (int)gridDim.x) * ROWS;
         for (int kb = 0; kb < p.nK; ++kb) {
-          mbar_wait(empty + s, ph ^ 1);
+          mbar_wait(raw_empty + s, ph ^ 1);
           unsigned char* dst = stage0 + (size_t)s * STAGE_BYTES;
-          mbar_expect_tx(full + s, A_BLOCK_BYTES);
-          if (kb < p.nK1) tma_load_2d(dst, &mapA, kb * BLK_K, m0, full + s);
-          else tma_load_2d(dst, &mapA2, (kb - p.nK1) * BLK_K, m0, full + s);
+          mbar_expect_tx(raw_full + s, A_BLOCK_BYTES);
+          if (kb < p.nK1) tma_load_2d(dst, &mapA, kb * BLK_K, m0, raw_full + s);
+          else tma_load_2d(dst, &mapA2, (kb - p.nK1) * BLK_K, m0, raw_full + s);
           if (++s == p.stages) s = 0, ph ^= 1;
         }
       }
     }
-  } else if (warp == 2 || warp == 3) {
-    // ---------------- split workers ----------------
-    const int t64 = threadIdx.x - 64;
-    int s = 0;
-    uint32_t ph = 0;
+  } else if (warp < 4) {
+    // ---------------- split warpgroup: raw smem row -> (hi, lo) TMEM ----------------
+    const int row = warp * 32 + lane;  // TMEM lane quarter = warp
+    int s = 0, j = 0;
+    uint32_t ph = 0, aph = 0;
     for (int t = 0; t < n_my; ++t) {
       for (int kb = 0; kb < p.nK; ++kb) {
-        mbar_wait(full + s, ph);
-        float4* hi = reinterpret_cast<float4*>(stage0 + (size_t)s * STAGE_BYTES);
-        float4* lo = reinterpret_cast<float4*>(stage0 + (size_t)s * STAGE_BYTES + A_BLOCK_BYTES);
-#pragma unroll 4
-        for (int i = t64; i < A_BLOCK_BYTES / 16; i += 64) {
-          float4 v = hi[i];
-          float4 h, l;
-          h.x = __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
-          h.y = __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
-          h.z = __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
-          h.w = __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
-          l.x = v.x - h.x;
-          l.y = v.y - h.y;
-          l.z = v.z - h.z;
-          l.w = v.w - h.w;
-          hi[i] = h;
-          lo[i] = l;
+        mbar_wait(raw_full + s, ph);
+        const unsigned char* raw = stage0 + (size_t)s * STAGE_BYTES;
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 v = *reinterpret_cast<const float4*>(raw + row * 128 + ((c ^ (row & 7)) << 4));
+          const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t h = __float_as_uint(x[e]) & 0xffffe000u;
+            hi[4 * c + e] = h;
+            lo[4 * c + e] = __float_as_uint(x[e] - __uint_as_float(h));
+          }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(split + s);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(raw_empty + s);
         if (++s == p.stages) s = 0, ph ^= 1;
+        mbar_wait(a_empty + j, aph ^ 1);
+        tc_fence_after();
+        const uint32_t ta = tmem_a + (uint32_t)(j * A_TMEM_COLS) + ((uint32_t)(warp * 32) << 16);
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full + j);
+        if (++j == p.a_stages) j = 0, aph ^= 1;
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 9) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.N_t >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
     mbar_wait(w_full, 0);
     tc_fence_after();
     const uint32_t whi = smem_u32(w_hi), wlo = smem_u32(w_lo);
     const uint32_t wblk = (uint32_t)p.N_t * 128;  // bytes of one W K-block
-    int s = 0;
-    uint32_t ph = 0;
+    int j = 0;
+    uint32_t aph = 0;
     for (int t = 0; t < n_my; ++t) {
       const int a = t & 1;
-      const uint32_t aph = (t >> 1) & 1;
-      mbar_wait(acc_empty + a, aph ^ 1);
+      const uint32_t acph = (t >> 1) & 1;
+      mbar_wait(acc_empty + a, acph ^ 1);
       tc_fence_after();
-      const uint32_t d = tmem + (uint32_t)(a * acc_cols);
+      const uint32_t d = tmem + (uint32_t)(a * p.acc_cols);
       for (int kb = 0; kb < p.nK; ++kb) {
-        mbar_wait(split + s, ph);
+        mbar_wait(a_full + j, aph);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t ahi = smem_u32(stage0 + (size_t)s * STAGE_BYTES);
-          const uint32_t alo = ahi + A_BLOCK_BYTES;
+          const uint32_t ahi = tmem_a + (uint32_t)(j * A_TMEM_COLS), alo = ahi + 32;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint32_t ko = k * 32;
-            const uint64_t dah = sdesc(ahi + ko), dal = sdesc(alo + ko);
+            if (p.diag & 1) break;
+            const uint32_t ko = k * 32;  // 8 tf32 = 32 bytes of a W row
             const uint64_t dwh = sdesc(whi + kb * wblk + ko), dwl = sdesc(wlo + kb * wblk + ko);
-            mma_tf32(d, dah, dwl, idesc, (kb | k) ? 1u : 0u);
-            mma_tf32(d, dal, dwh, idesc, 1u);
-            mma_tf32(d, dah, dwh, idesc, 1u);
+            mma_tf32_ts(d, ahi + 8 * k, dwl, idesc, (kb | k) ? 1u : 0u);
+            mma_tf32_ts(d, alo + 8 * k, dwh, idesc, 1u);
+            mma_tf32_ts(d, ahi + 8 * k, dwh, idesc, 1u);
           }
-          mma_commit(empty + s);
+          mma_commit(a_empty + j);
           if (kb == p.nK - 1) mma_commit(acc_full + a);
         }
         __syncwarp();
-        if (++s == p.stages) s = 0, ph ^= 1;
+        if (++j == p.a_stages) j = 0, aph ^= 1;
       }
     }
   } else {
     // ---------------- epilogue warpgroup (warps 4..7) ----------------
     const int q = warp & 3;  // TMEM lane quarter
-    const int row_in_tile = q * 32 + lane;
     const GemmArgs& g = p.g;
+    constexpr bool kX = EPI == EPI_RESID || EPI == EPI_URESID || EPI == EPI_ADDX || EPI == EPI_DSILU;
+    constexpr bool kAuxEpi = EPI == EPI_SILU || EPI == EPI_UMUL_SAVE || EPI == EPI_RESID;
+    const bool want_aux = kAuxEpi && g.aux != nullptr;
+    unsigned char* buf = out_stage + (size_t)q * STAGE_OUT_BYTES;
+    constexpr bool kIn = kX || EPI == EPI_ACC;  // epilogue reads a [M][N] input (X or old C)
+    const float* in_ptr = kX ? g.X : g.C;
+    float4 xn[8];  // prefetched input chunk (coalesced layout: rows lane/8 + 4i, chunk lane%8)
+    auto issue = [&](int64_t row0, int c0) {
+      const int nc = (p.N_t - c0) >= 32 ? 8 : (p.N_t - c0) / 4;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = (lane >> 3) + 4 * i, cc = lane & 7;
+        xn[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row0 + rr < g.M && cc < nc)
+          xn[i] = __ldg(reinterpret_cast<const float4*>(in_ptr + (row0 + rr) * g.N + p.col0 + c0 + 4 * cc));
+      }
+    };
+    if constexpr (kIn) {
+      if (n_my > 0) issue((int64_t)blockIdx.x * ROWS + q * 32, 0);
+    }
     for (int t = 0; t < n_my; ++t) {
       const int a = t & 1;
-      const uint32_t aph = (t >> 1) & 1;
-      mbar_wait(acc_full + a, aph);
+      const uint32_t acph = (t >> 1) & 1;
+      mbar_wait(acc_full + a, acph);
       tc_fence_after();
-      const int64_t r = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * ROWS + row_in_tile;
-      const bool ok = r < g.M;
-      const float ur = (ok && g.u != nullptr) ? g.u[r] : 1.f;
-      for (int c0 = 0; c0 < p.N_t; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * acc_cols + c0), v);
-        if (!ok) continue;
-        const int64_t o = r * g.N + p.col0 + c0;
-        float out[16];
-        float xin[16];
-        if (g.X != nullptr) {
+      const int64_t row0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * ROWS + q * 32;
+      const int64_t r = row0 + lane;
+      const float ur = (r < g.M && g.u != nullptr) ? g.u[r] : 1.f;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * p.acc_cols);
+      for (int c0 = 0; c0 < p.N_t; c0 += 32) {
+        float v[32], out[32], xin[32];
+        if constexpr (kIn) {
+          // transpose the prefetched chunk into thread-row registers, then prefetch the next one
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 x4 = reinterpret_cast<const float4*>(g.X + o)[j];
-            xin[4 * j] = x4.x, xin[4 * j + 1] = x4.y, xin[4 * j + 2] = x4.z, xin[4 * j + 3] = x4.w;
+          for (int i = 0; i < 8; ++i) *tile_at(buf, (lane >> 3) + 4 * i, lane & 7) = xn[i];
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 w4 = *tile_at(buf, lane, c);
+            xin[4 * c] = w4.x, xin[4 * c + 1] = w4.y, xin[4 * c + 2] = w4.z, xin[4 * c + 3] = w4.w;
           }
+          __syncwarp();
+          if (c0 + 32 < p.N_t) issue(row0, c0 + 32);
+          else if (t + 1 < n_my) issue(row0 + (int64_t)gridDim.x * ROWS, 0);
         }
-        float cold[16];
-        if (g.epi == EPI_ACC) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 c4 = reinterpret_cast<const float4*>(g.C + o)[j];
-            cold[4 * j] = c4.x, cold[4 * j + 1] = c4.y, cold[4 * j + 2] = c4.z, cold[4 * j + 3] = c4.w;
-          }
-        }
-        float aux[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float pv = g.s * v[j];
-          aux[j] = pv;
-          switch (g.epi) {
-            case EPI_STORE: out[j] = pv; break;
-            case EPI_SILU: out[j] = silu(pv); break;
-            case EPI_UMUL_SAVE: out[j] = ur * pv; break;
-            case EPI_RESID: out[j] = g.alpha * xin[j] + g.beta * ur * pv; break;
-            case EPI_URESID: out[j] = g.alpha * xin[j] + g.beta * ur * pv; break;
-            case EPI_USCALE: out[j] = g.beta * ur * pv; break;
-            case EPI_ACC: out[j] = cold[j] + pv; break;
-            case EPI_ADDX: out[j] = pv + xin[j]; break;
-            case EPI_DSILU: out[j] = ur * pv * dsilu(xin[j]); break;
-            default: out[j] = pv; break;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          reinterpret_cast<float4*>(g.C + o)[j] = make_float4(out[4 * j], out[4 * j + 1], out[4 * j + 2], out[4 * j + 3]);
-        if (g.aux != nullptr && (g.epi == EPI_SILU || g.epi == EPI_UMUL_SAVE || g.epi == EPI_RESID)) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            reinterpret_cast<float4*>(g.aux + o)[j] = make_float4(aux[4 * j], aux[4 * j + 1], aux[4 * j + 2], aux[4 * j + 3]);
-        }
+        tmem_ld32(tbase + (uint32_t)c0, v);
+        if (p.diag & 2) continue;
+        const int64_t col = p.col0 + c0;
+        const int nc = (p.N_t - c0) >= 32 ? 8 : (p.N_t - c0) / 4;
+        epi_apply<32, EPI>(g, v, xin, ur, out);
+        scatter_rows(buf, g.C + col, g.N, row0, g.M, lane, out, nc);
+        if (want_aux) scatter_rows(buf, g.aux + col, g.N, row0, g.M, lane, v, nc);
       }
       tc_fence_before();
       __syncwarp();
@@ -321,9 +433,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   }
   __syncthreads();
-  if (warp == 1) {
+  if (warp == 9) {
     tc_fence_after();
-    tmem_dealloc(tmem, tmem_cols);
+    tmem_dealloc(tmem, p.tmem_cols);
   }
 }
 
@@ -342,12 +454,12 @@ void get_encode() {
   });
 }
 
-CUtensorMap make_map(const float* ptr, int64_t rows, int cols, int ld) {
+CUtensorMap make_map(const float* ptr, int64_t rows, int cols, int ld, int box_rows = ROWS) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)(rows > 0 ? rows : 1)};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
-  const cuuint32_t box[2] = {BLK_K, ROWS};
+  const cuuint32_t box[2] = {BLK_K, (cuuint32_t)box_rows};
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, es,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -359,6 +471,8 @@ CUtensorMap make_map(const float* ptr, int64_t rows, int cols, int ld) {
 int g_num_sms = 0;
 
 }  // namespace
+
+TcTuning g_tc_tuning;
 
 float tf32_hi(float x) {
   uint32_t u;
@@ -375,7 +489,7 @@ TcWeight tc_prepare_weight(const std::vector<float>& W, int K, int N, std::vecto
   t.N = N;
   const int nK = (K + BLK_K - 1) / BLK_K;
   // widest N-tile (multiple of 16 dividing N) whose image leaves room for >= 2 stages
-  const size_t budget = SMEM_LIMIT - SMEM_RESERVE - 2 * (size_t)STAGE_BYTES;
+  const size_t budget = SMEM_LIMIT - SMEM_RESERVE - 3 * (size_t)STAGE_BYTES - 4 * (size_t)STAGE_OUT_BYTES;
   int nt = 0;
   for (int c = std::min(N, 256); c >= 16; c -= 16)
     if (N % c == 0 && (size_t)2 * nK * c * 128 <= budget) {
@@ -423,12 +537,17 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const CUtensorMap mA2 = g.A2 ? make_map(g.A2, g.M, g.K - g.K1, g.lda2) : mA;
   const size_t w_bytes = w.tile_bytes;
   const size_t w_round = (w_bytes + 1023) & ~(size_t)1023;
-  int stages = (int)((SMEM_LIMIT - SMEM_RESERVE - w_round) / STAGE_BYTES);
-  stages = std::max(2, std::min(stages, 4));
-  const size_t smem = 1024 + w_round + (size_t)stages * STAGE_BYTES + 256;
+  const size_t out_bytes = 4 * (size_t)STAGE_OUT_BYTES;
+  int stages = (int)((SMEM_LIMIT - SMEM_RESERVE - w_round - out_bytes) / STAGE_BYTES);
+  stages = std::min(stages, g_tc_tuning.max_stages);
+  if (stages < 2) throw CudaError("tc_gemm: shared memory too small for 2 stages");
+  const size_t smem = 1024 + w_round + out_bytes + (size_t)stages * STAGE_BYTES + 256;
   static bool attr_set = false;
   if (!attr_set) {
-    ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
+#define ALG_SET(e) ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<e>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
+    ALG_SET(EPI_STORE) ALG_SET(EPI_SILU) ALG_SET(EPI_UMUL_SAVE) ALG_SET(EPI_RESID) ALG_SET(EPI_URESID)
+    ALG_SET(EPI_USCALE) ALG_SET(EPI_ACC) ALG_SET(EPI_ADDX) ALG_SET(EPI_DSILU)
+#undef ALG_SET
     attr_set = true;
   }
   TcParams p;
@@ -439,6 +558,15 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   p.stages = stages;
   p.w_bytes = (uint32_t)w_bytes;
   p.n_mtiles = (int)((g.M + ROWS - 1) / ROWS);
+  p.acc_cols = (w.N_t + 31) / 32 * 32;
+  // TMEM: two accumulators + the A ring (64 columns per stage), power of two <= 512
+  int a_st = std::min(4, (512 - 2 * p.acc_cols) / A_TMEM_COLS);
+  if (a_st < 2) throw CudaError("tc_gemm: TMEM too small");
+  p.a_stages = a_st;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * p.acc_cols + a_st * A_TMEM_COLS)) cols <<= 1;
+  p.tmem_cols = cols;
+  p.diag = g_tc_tuning.diag;
   const int grid = std::min(p.n_mtiles, g_num_sms);
   const double mn = (double)g.M * g.N;
   const int n_io = 1 + (g.aux != nullptr) + (g.X != nullptr) + (g.epi == EPI_ACC);
@@ -447,7 +575,14 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
     p.wimg = w.dev + tile * (w.tile_bytes / 4);
     ProfScope ps(prof, st, PK_GEMM, 2.0 * mn * g.K / w.n_tiles,
                  4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * n_io) / w.n_tiles);
-    k_tc_gemm<<<grid, TC_THREADS, smem, st>>>(mA, mA2, p);
+    switch (g.epi) {
+#define ALG_EPI(e) \
+  case e: k_tc_gemm<e><<<grid, TC_THREADS, smem, st>>>(mA, mA2, p); break;
+      ALG_EPI(EPI_STORE) ALG_EPI(EPI_SILU) ALG_EPI(EPI_UMUL_SAVE) ALG_EPI(EPI_RESID) ALG_EPI(EPI_URESID)
+      ALG_EPI(EPI_USCALE) ALG_EPI(EPI_ACC) ALG_EPI(EPI_ADDX) ALG_EPI(EPI_DSILU)
+#undef ALG_EPI
+      default: throw CudaError("tc_gemm: unknown epilogue");
+    }
     ALG_LAUNCH_CHECK();
   }
 }

@@ -25,6 +25,14 @@ TcWeight tc_prepare_weight(const std::vector<float>& W, int K, int N, std::vecto
 // C = epi(A W) on the tensor cores.  g.W is ignored; K % 32 == 0 (pad), N % 16 == 0.
 void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* prof);
 
+// Launch tuning / diagnostics (defaults are the production configuration).
+struct TcTuning {
+  int tma_store = 1;   // TMA-store epilogue when N_t % 32 == 0
+  int max_stages = 4;  // A-stage ring depth cap
+  int diag = 0;        // bit0: skip MMAs, bit1: skip the epilogue's global traffic
+};
+extern TcTuning g_tc_tuning;
+
 // Host-side split used for the weights (exposed for tests): hi = fp32 with the low
 // 13 mantissa bits cleared (exactly representable in TF32), lo = fp32(x - hi).
 float tf32_hi(float x);
