@@ -108,7 +108,10 @@ int allegro_compute_energy_forces(allegro_ctx* ctx, int64_t n, int where, const 
                                   double* e_total, double* e_atom, double* forces);
 
 /* MD state lives on the device inside ctx.  set/get take GLOBAL host arrays
- * [n_global] (species, pos [n][3] A, vel [n][3] A/fs); set computes the initial forces. */
+ * [n_global] (species, pos [n][3] A, vel [n][3] A/fs); set computes the initial forces.
+ * With world_size > 1 every rank passes the same global arrays and keeps the atoms of its
+ * domain (atom index = gid); get gathers the global state on rank 0 (other ranks' output
+ * arrays are not written).  Collective. */
 int md_set_state(allegro_ctx* ctx, int64_t n_global, const int32_t* species, const double* pos,
                  const double* vel);
 int md_get_state(allegro_ctx* ctx, int64_t n_global, double* pos, double* vel, double* forces);
@@ -117,7 +120,8 @@ typedef struct {
   int64_t steps_done;
   double e_pot, e_kin, e_total, temperature; /* eV, eV, eV, K after the last step */
   int64_t n_outliers_last;                   /* outliers of the last step vs the step-0 baseline */
-  int64_t n_edges, n_rebuilds;
+  int64_t n_edges, n_rebuilds;                /* edges summed over ranks */
+  int64_t n_local;                           /* atoms this rank owns after the call */
 } md_report;
 
 /* n_steps of velocity Verlet at dt (fs): exactly one
@@ -128,8 +132,10 @@ int md_step(allegro_ctx* ctx, int64_t n_steps, double dt_fs, md_report* out);
 /* End-to-end variant of md_step for HOST-resident state (the e2e measurement of bench.py):
  * copies species [n], pos/vel/forces [n][3] (forces = F at pos, e.g. from the previous call
  * or from md_get_state) host -> device, runs n_steps exactly as md_step, and writes pos, vel
- * and forces back into the caller's arrays (device -> host).  n must equal the md_set_state
- * size.  Pinned host memory makes the copies asynchronous. */
+ * and forces back into the caller's arrays (device -> host).  n must equal the number of
+ * atoms this rank owns (allegro_local_count; all atoms on one GPU).  With world_size > 1
+ * migration may change the local count: the arrays (and species) must have room for it;
+ * out->n_local returns it.  Pinned host memory makes the copies asynchronous. */
 int md_step_host(allegro_ctx* ctx, int64_t n, const int32_t* species, double* pos, double* vel, double* forces,
                  int64_t n_steps, double dt_fs, md_report* out);
 
@@ -149,6 +155,12 @@ int allegro_get_edges(allegro_ctx* ctx, int64_t capacity, int64_t* n_edges, int3
 /* Test hook: per-edge dE/dr_e [E][3] (fp32 widened to double) of the last evaluation,
  * in the edge order of allegro_get_edges. */
 int allegro_get_edge_grad(allegro_ctx* ctx, int64_t capacity, double* g);
+
+/* world_size > 1: rank 0 creates the 128-byte NCCL unique id and broadcasts it (e.g. with
+ * torch.distributed) to every rank's allegro_params.nccl_unique_id. */
+int allegro_nccl_unique_id(void* out128);
+/* atoms owned by this rank (its spatial domain) */
+int64_t allegro_local_count(const allegro_ctx* ctx);
 
 /* Per-kernel-class accounting.  Every launch of the library is counted;
  * with profiling enabled each launch is also bracketed by CUDA events on the stream it is

@@ -59,6 +59,7 @@ class MdReport(C.Structure):
         ("n_outliers_last", C.c_int64),
         ("n_edges", C.c_int64),
         ("n_rebuilds", C.c_int64),
+        ("n_local", C.c_int64),
     ]
 
 
@@ -88,6 +89,9 @@ _lib.allegro_launch_count.argtypes = [_P]
 _lib.allegro_launch_count.restype = C.c_int64
 _lib.allegro_profile_kind_name.argtypes = [C.c_int]
 _lib.allegro_profile_kind_name.restype = C.c_char_p
+_lib.allegro_nccl_unique_id.argtypes = [_P]
+_lib.allegro_local_count.argtypes = [_P]
+_lib.allegro_local_count.restype = C.c_int64
 _lib.allegro_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, _P, _P, _P]
 _lib.allegro_debug_gemm_bench.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                           C.c_int, C.c_int, C.POINTER(C.c_double)]
@@ -98,7 +102,7 @@ EXPORTED = [
     "allegro_get_edges", "allegro_get_edge_grad", "allegro_w3j_table", "allegro_param_count",
     "allegro_layer_paths", "allegro_version", "md_step_host", "allegro_profile", "allegro_profile_read",
     "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name", "allegro_debug_gemm",
-    "allegro_debug_gemm_bench",
+    "allegro_debug_gemm_bench", "allegro_nccl_unique_id", "allegro_local_count",
 ]
 
 
@@ -157,6 +161,15 @@ def debug_gemm_bench(M, N, K, epi=0, precision=PREC_3XTF32, iters=10, tma_store=
     return ms.value
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; broadcast it to every rank)."""
+    buf = (C.c_char * 128)()
+    rc = _lib.allegro_nccl_unique_id(C.addressof(buf))
+    if rc != OK:
+        raise AllegroError(rc, _lib.allegro_last_error(None).decode())
+    return bytes(buf)
+
+
 def version() -> str:
     return _lib.allegro_version().decode()
 
@@ -165,7 +178,8 @@ class Allegro:
     """One ctx of the C ABI (allegro_create ... allegro_destroy)."""
 
     def __init__(self, weights_path: str, box, r_cut: float = 0.0, skin: float = 0.0, device: int = 0,
-                 n_atoms: int = 0, precision: int = PREC_FP32, stream: int | None = None):
+                 n_atoms: int = 0, precision: int = PREC_FP32, stream: int | None = None, rank: int = 0,
+                 world_size: int = 1, nccl_id: bytes | None = None, grid=(0, 0, 0)):
         p = AllegroParams()
         p.weights_path = os.fsencode(weights_path)
         p.r_cut = r_cut
@@ -174,8 +188,11 @@ class Allegro:
             p.box[d] = float(box[d])
         p.n_atoms_global = n_atoms
         p.device = device
-        p.rank, p.world_size = 0, 1
-        p.nccl_unique_id = None
+        p.rank, p.world_size = rank, world_size
+        self._id = None if nccl_id is None else C.create_string_buffer(nccl_id, 128)
+        p.nccl_unique_id = None if self._id is None else C.addressof(self._id)
+        for d in range(3):
+            p.grid[d] = int(grid[d])
         p.precision = precision
         p.cuda_stream = stream
         h = _P()
@@ -235,6 +252,9 @@ class Allegro:
         vel = np.ascontiguousarray(vel, dtype=np.float64)
         self.n = int(pos.shape[0])
         self._check(_lib.md_set_state(self._h, self.n, species.ctypes.data, pos.ctypes.data, vel.ctypes.data))
+
+    def local_count(self) -> int:
+        return int(_lib.allegro_local_count(self._h))
 
     def md_get_state(self):
         pos = np.empty((self.n, 3))

@@ -29,6 +29,12 @@ int guarded(allegro_ctx* c, F&& f) {
     return f();
   } catch (const WeightsError& e) {
     return fail(c, ALLEGRO_E_WEIGHTS, e.what());
+  } catch (const GeometryError& e) {
+    return fail(c, ALLEGRO_E_GEOMETRY, e.what());
+  } catch (const NcclError& e) {
+    return fail(c, ALLEGRO_E_NCCL, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(c, ALLEGRO_E_ARG, e.what());
   } catch (const CudaError& e) {
     const std::string m = e.what();
     return fail(c, m.rfind("OOM", 0) == 0 ? ALLEGRO_E_OOM : ALLEGRO_E_CUDA, m);
@@ -82,8 +88,8 @@ int allegro_create(const allegro_params* p, allegro_ctx** out) {
   *out = nullptr;
   if (!p || !p->weights_path) return fail(nullptr, ALLEGRO_E_ARG, "params or weights_path is NULL");
   if (!box_ok(p->box)) return fail(nullptr, ALLEGRO_E_ARG, "box must be three finite positive lengths");
-  if (p->world_size != 1 || p->rank != 0)
-    return fail(nullptr, ALLEGRO_E_ARG, "this build runs one domain per ctx (world_size == 1)");
+  if (p->world_size < 1 || p->rank < 0 || p->rank >= p->world_size)
+    return fail(nullptr, ALLEGRO_E_ARG, "rank / world_size out of range");
   if (p->precision != ALLEGRO_PREC_FP32 && p->precision != ALLEGRO_PREC_3XTF32)
     return fail(nullptr, ALLEGRO_E_ARG, "built precisions: ALLEGRO_PREC_FP32, ALLEGRO_PREC_3XTF32");
   if (!(p->skin >= 0 && std::isfinite(p->skin))) return fail(nullptr, ALLEGRO_E_ARG, "skin must be >= 0");
@@ -106,6 +112,7 @@ int allegro_create(const allegro_params* p, allegro_ctx** out) {
     for (int d = 0; d < 3; ++d) c->box[d] = p->box[d];
     c->flags.reserve(8);
     c->red.reserve(8);
+    domain_setup(c, p->nccl_unique_id);
     size_t free_b = 0, total_b = 0;
     ALG_CUDA(cudaMemGetInfo(&free_b, &total_b));
     c->ws_budget_bytes = std::min<size_t>(free_b / 2, (size_t)64 << 30);
@@ -125,6 +132,8 @@ void allegro_destroy(allegro_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_model(c->model);
+  domain_teardown(c);
+  c->aspec.release();
   c->pos.release();
   c->vel.release();
   c->frc.release();
@@ -236,9 +245,13 @@ int md_set_state(allegro_ctx* c, int64_t n, const int32_t* species, const double
 int md_get_state(allegro_ctx* c, int64_t n, double* pos, double* vel, double* forces) {
   if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
   if (!c->md_ready) return fail(c, ALLEGRO_E_STATE, "md_set_state has not been called");
-  if (n != c->n) return fail(c, ALLEGRO_E_ARG, "n differs from the state size");
+  if (n != c->n_global) return fail(c, ALLEGRO_E_ARG, "n differs from the state size");
   return guarded(c, [&]() -> int {
     ALG_CUDA(cudaSetDevice(c->device));
+    if (c->dom.multi) {
+      gather_state(c, n, pos, vel, forces);
+      return ALLEGRO_OK;
+    }
     if (pos) ALG_CUDA(cudaMemcpyAsync(pos, c->pos.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
     if (vel) ALG_CUDA(cudaMemcpyAsync(vel, c->vel.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
     if (forces) ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
@@ -253,6 +266,7 @@ static int md_run(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
     int64_t done = 0;
     for (; done < n_steps; ++done) {
       md_half_kick_drift(c, dt);
+      if (c->dom.multi) migrate(c);
       ALG_CUDA(cudaMemsetAsync(c->flags.p, 0, 4 * sizeof(int), c->stream));
       build_neighbors(c);
       compute_forces(c);
@@ -271,9 +285,10 @@ static int md_run(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
       out->e_pot = c->e_pot;
       out->e_kin = md_kinetic(c);
       out->e_total = out->e_pot + out->e_kin;
-      out->temperature = 2.0 * out->e_kin / (3.0 * (double)c->n * 8.617333e-5);
+      out->temperature = 2.0 * out->e_kin / (3.0 * (double)c->n_global * 8.617333e-5);
       out->n_outliers_last = count_outliers(c, c->f_mean0 + 5.0 * c->f_sigma0);
-      out->n_edges = c->n_edges;
+      out->n_edges = allreduce_sum_i64(c, c->n_edges);
+      out->n_local = c->n;
       out->n_rebuilds = c->n_rebuilds;
     }
     c->prof.flush();
@@ -295,7 +310,7 @@ int md_step_host(allegro_ctx* c, int64_t n, const int32_t* species, double* pos,
                  int64_t n_steps, double dt, md_report* out) {
   if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
   if (!c->md_ready) return fail(c, ALLEGRO_E_STATE, "md_set_state has not been called");
-  if (n != c->n || !species || !pos || !vel || !forces) return fail(c, ALLEGRO_E_ARG, "bad arrays or n");
+  if (n != c->n || !species || !pos || !vel || !forces) return fail(c, ALLEGRO_E_ARG, "bad arrays or n (local count)");
   if (n_steps < 0 || !(dt > 0 && std::isfinite(dt))) return fail(c, ALLEGRO_E_ARG, "bad n_steps or dt");
   return guarded(c, [&]() -> int {
     ALG_CUDA(cudaSetDevice(c->device));
@@ -304,13 +319,31 @@ int md_step_host(allegro_ctx* c, int64_t n, const int32_t* species, double* pos,
     ALG_CUDA(cudaMemcpyAsync(c->vel.p, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     ALG_CUDA(cudaMemcpyAsync(c->frc.p, forces, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     const int rc = md_run(c, n_steps, dt, out);
-    ALG_CUDA(cudaMemcpyAsync(pos, c->pos.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
-    ALG_CUDA(cudaMemcpyAsync(vel, c->vel.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
-    ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    // multi-GPU: the local count may change by migration; caller arrays hold >= capacity
+    const int64_t nn = c->n;
+    if (c->dom.multi && species) {
+      ALG_CUDA(cudaMemcpyAsync(const_cast<int32_t*>(species), c->species.p, sizeof(int32_t) * nn,
+                               cudaMemcpyDeviceToHost, c->stream));
+    }
+    ALG_CUDA(cudaMemcpyAsync(pos, c->pos.p, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(vel, c->vel.p, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, c->stream));
     ALG_CUDA(cudaStreamSynchronize(c->stream));
     return rc;
   });
 }
+
+int allegro_nccl_unique_id(void* out128) {
+  if (!out128) return fail(nullptr, ALLEGRO_E_ARG, "out is NULL");
+  return guarded(nullptr, [&]() -> int {
+    ncclUniqueId id;
+    ALG_NCCL(NcclApi::get().GetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return ALLEGRO_OK;
+  });
+}
+
+int64_t allegro_local_count(const allegro_ctx* c) { return c ? c->n : -1; }
 
 int allegro_profile(allegro_ctx* c, int enable) {
   if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");

@@ -11,10 +11,14 @@
 #include "common.cuh"
 #include "prof.cuh"
 #include "tc_gemm.cuh"
+#include "comm.cuh"
 
 namespace allegro {
 
 struct WeightsError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct GeometryError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
@@ -98,6 +102,29 @@ struct Workspace {
   DBuf<float> xbar_a, xbar_b, sbar, vbar_a, vbar_b, wbar, ybar, ubar, zbar, ab2, ab1, ee;
 };
 
+// Spatial domain decomposition (§2.4).
+struct HaloStage {
+  int64_t n_send[2] = {0, 0};   // to the -/+ neighbour
+  int64_t n_recv[2] = {0, 0};   // from the -/+ neighbour
+  int64_t recv_base[2] = {0, 0};  // first atom index of the ghosts received from -/+
+  DBuf<int32_t> send_idx[2];    // local atom indices sent to -/+
+};
+
+struct Domain {
+  bool multi = false;           // world_size > 1
+  int rank = 0, size = 1;
+  int P[3] = {1, 1, 1}, c[3] = {0, 0, 0};
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, w[3] = {0, 0, 0};
+  int nbr[3][2] = {};           // ranks of the -/+ neighbours per axis
+  ncclComm_t comm = nullptr;
+  HaloStage st[3];
+  DBuf<unsigned char> sendbuf[2], recvbuf[2];
+  DBuf<int32_t> flag, pos_idx;
+  DBuf<long long> acc;          // [n + G][3] fixed-point ghost-force accumulators
+  DBuf<long long> cnt;          // scratch counts
+  DBuf<double> red;             // allreduce scratch
+};
+
 }  // namespace allegro
 
 struct allegro_ctx {
@@ -111,12 +138,13 @@ struct allegro_ctx {
   allegro::Model model;
 
   // ---- atoms (owned first, then ghosts) ----
-  int64_t n = 0;        // owned
+  int64_t n = 0;        // owned (this rank)
+  int64_t n_global = 0; // atoms in the whole box (md state)
   int64_t n_ghost = 0;  // ghosts of the last build
   allegro::DBuf<double> pos, vel, frc;       // [n][3] owned state (fp64)
   allegro::DBuf<int32_t> species, gid;       // [n]
   allegro::DBuf<double> apos;                // [n + G][3] canonical image positions
-  allegro::DBuf<int32_t> aowner, ashift, agid;  // [n + G]
+  allegro::DBuf<int32_t> aowner, ashift, agid, aspec;  // [n + G] (aowner = -1 for remote ghosts)
   allegro::DBuf<int32_t> gcount, goff;       // ghost count / offsets per owned atom
   // ---- cells ----
   int ncell[3] = {0, 0, 0};
@@ -143,6 +171,7 @@ struct allegro_ctx {
   double f_mean0 = 0, f_sigma0 = 0;  // step-0 outlier baseline
   bool baseline_set = false;
   allegro::Profiler prof;
+  allegro::Domain dom;
 };
 
 namespace allegro {
@@ -160,6 +189,19 @@ void wrap_positions(allegro_ctx* c);
 
 // model.cu: energies and forces for the current edge list -> c->frc, c->e_atom, c->e_pot
 void compute_forces(allegro_ctx* c);
+
+// domain.cu (world_size > 1)
+void domain_setup(allegro_ctx* c, const void* nccl_id);
+void domain_teardown(allegro_ctx* c);
+void migrate(allegro_ctx* c);
+void halo_exchange(allegro_ctx* c);     // fills apos/agid/aspec/ashift for owned + ghosts
+void ghost_force_return(allegro_ctx* c);  // accumulates ghost forces and returns them to owners
+double allreduce_sum(allegro_ctx* c, double v);
+int64_t allreduce_sum_i64(allegro_ctx* c, int64_t v);
+int allreduce_max_i32(allegro_ctx* c, int v);
+void select_owned(allegro_ctx* c, int64_t n_global, const int32_t* species, const double* pos, const double* vel);
+void gather_state(allegro_ctx* c, int64_t n_global, double* pos, double* vel, double* forces);
+constexpr double kFixScale = 4294967296.0;  // 2^32: fixed-point ghost forces (exact, order independent)
 
 // md.cu
 void md_half_kick_drift(allegro_ctx* c, double dt);

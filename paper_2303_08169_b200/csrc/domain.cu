@@ -1,0 +1,578 @@
+// domain.cu -- spatial domain decomposition over NCCL (world_size > 1).
+//
+// PAPER.md:187-191 (§2.4): "globally scalable spatial decomposition ... non-blocking,
+// lock-free ... minimal internode-data exchange"; SURVEY.md §8(e):
+//   * grid px x py x pz, one rank per domain; an atom on an internal face belongs to the
+//     lower domain: owner = clamp(ceil(x / w) - 1, 0, p - 1);
+//   * domain edge >= r_c + skin, else ALLEGRO_E_GEOMETRY;
+//   * migration (every rebuild) and the ghost halo are three staged exchanges (x, y, z)
+//     with the two face neighbours; atoms received in earlier stages are forwarded, so
+//     edges and corners arrive without diagonal messages.  The periodic shift is applied
+//     once per axis by the sender: fl(x +- L), the canonical image of reading row 12, so
+//     edge sets and d^2 are bit-identical to one GPU;
+//   * ghost forces: every edge whose neighbour is a ghost adds -g_e to that ghost in
+//     int64 fixed point (2^-32 eV/A; exact and order independent => deterministic); the
+//     reverse halo (stages z, y, x) returns them to the owners.
+// A face neighbour that is this rank (p_alpha = 1) is served by a device copy.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ctx.cuh"
+
+namespace allegro {
+
+namespace {
+
+struct HaloAtom {  // 40 B
+  double x, y, z;
+  int32_t gid, spec, shift, pad;
+};
+struct MigAtom {  // 56 B
+  double x, y, z, vx, vy, vz;
+  int32_t gid, spec;
+};
+
+__host__ __device__ __forceinline__ int owner_coord(double x, double w, int P) {
+  int k = (int)ceil(x / w) - 1;
+  return k < 0 ? 0 : (k >= P ? P - 1 : k);
+}
+
+__device__ __forceinline__ int32_t pack_shift3(int nx, int ny, int nz) {
+  return (nx + 128) | ((ny + 128) << 8) | ((nz + 128) << 16);
+}
+
+// ---------------------------------------------------------------- migration
+__global__ void k_mig_class(const double* __restrict__ pos, int64_t n, int axis, double w, int P, int cme,
+                            int32_t* __restrict__ f_stay, int32_t* __restrict__ f_minus, int32_t* __restrict__ f_plus) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const int o = owner_coord(pos[a * 3 + axis], w, P);
+  int cls = 0;
+  if (o != cme) cls = (o == (cme + 1) % P) ? 2 : 1;
+  f_stay[a] = cls == 0;
+  f_minus[a] = cls == 1;
+  f_plus[a] = cls == 2;
+}
+
+__global__ void k_mig_pack(int64_t n, const int32_t* __restrict__ flag, const int32_t* __restrict__ idx,
+                           const double* __restrict__ pos, const double* __restrict__ vel, const int32_t* __restrict__ gid,
+                           const int32_t* __restrict__ spec, MigAtom* __restrict__ out) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n || !flag[a]) return;
+  MigAtom m;
+  m.x = pos[a * 3], m.y = pos[a * 3 + 1], m.z = pos[a * 3 + 2];
+  m.vx = vel[a * 3], m.vy = vel[a * 3 + 1], m.vz = vel[a * 3 + 2];
+  m.gid = gid[a];
+  m.spec = spec[a];
+  out[idx[a]] = m;
+}
+
+__global__ void k_mig_unpack(int64_t cnt, const MigAtom* __restrict__ in, int64_t base, double* __restrict__ pos,
+                             double* __restrict__ vel, int32_t* __restrict__ gid, int32_t* __restrict__ spec) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  const MigAtom m = in[k];
+  const int64_t a = base + k;
+  pos[a * 3] = m.x, pos[a * 3 + 1] = m.y, pos[a * 3 + 2] = m.z;
+  vel[a * 3] = m.vx, vel[a * 3 + 1] = m.vy, vel[a * 3 + 2] = m.vz;
+  gid[a] = m.gid;
+  spec[a] = m.spec;
+}
+
+// ---------------------------------------------------------------- halo
+__global__ void k_halo_flag(const double* __restrict__ apos, int64_t n_cur, int axis, double lo, double hi, double rcp,
+                            int32_t* __restrict__ f_minus, int32_t* __restrict__ f_plus) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n_cur) return;
+  const double x = apos[a * 3 + axis];
+  f_minus[a] = x < lo + rcp;
+  f_plus[a] = x >= hi - rcp;
+}
+
+__global__ void k_halo_pack(int64_t n_cur, const int32_t* __restrict__ flag, const int32_t* __restrict__ idx, int axis,
+                            double shiftL, int dshift, const double* __restrict__ apos, const int32_t* __restrict__ agid,
+                            const int32_t* __restrict__ aspec, const int32_t* __restrict__ ashift,
+                            HaloAtom* __restrict__ out, int32_t* __restrict__ send_idx) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n_cur || !flag[a]) return;
+  HaloAtom h;
+  double p[3] = {apos[a * 3], apos[a * 3 + 1], apos[a * 3 + 2]};
+  if (dshift != 0) p[axis] = __dadd_rn(p[axis], __dmul_rn((double)dshift, shiftL));
+  h.x = p[0], h.y = p[1], h.z = p[2];
+  h.gid = agid[a];
+  h.spec = aspec[a];
+  int s = ashift[a];
+  int n3[3] = {(s & 0xff) - 128, ((s >> 8) & 0xff) - 128, ((s >> 16) & 0xff) - 128};
+  n3[axis] += dshift;
+  h.shift = pack_shift3(n3[0], n3[1], n3[2]);
+  h.pad = 0;
+  const int32_t k = idx[a];
+  out[k] = h;
+  send_idx[k] = (int32_t)a;
+}
+
+__global__ void k_halo_unpack(int64_t cnt, const HaloAtom* __restrict__ in, int64_t base, double* __restrict__ apos,
+                              int32_t* __restrict__ agid, int32_t* __restrict__ aspec, int32_t* __restrict__ ashift,
+                              int32_t* __restrict__ aowner) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  const HaloAtom h = in[k];
+  const int64_t a = base + k;
+  apos[a * 3] = h.x, apos[a * 3 + 1] = h.y, apos[a * 3 + 2] = h.z;
+  agid[a] = h.gid;
+  aspec[a] = h.spec;
+  ashift[a] = h.shift;
+  aowner[a] = -1;
+}
+
+__global__ void k_owned_to_atoms(int64_t n, const double* __restrict__ pos, const int32_t* __restrict__ gid,
+                                 const int32_t* __restrict__ spec, double* __restrict__ apos, int32_t* __restrict__ agid,
+                                 int32_t* __restrict__ aspec, int32_t* __restrict__ ashift, int32_t* __restrict__ aowner) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  apos[a * 3] = pos[a * 3], apos[a * 3 + 1] = pos[a * 3 + 1], apos[a * 3 + 2] = pos[a * 3 + 2];
+  agid[a] = gid[a];
+  aspec[a] = spec[a];
+  ashift[a] = pack_shift3(0, 0, 0);
+  aowner[a] = (int32_t)a;
+}
+
+// ---------------------------------------------------------------- ghost forces
+__global__ void k_ghost_acc(int64_t E, int64_t n, const int32_t* __restrict__ nbr, const float* __restrict__ g,
+                            long long* __restrict__ acc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int32_t a = nbr[e];
+  if (a < n) return;
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    atomicAdd(reinterpret_cast<unsigned long long*>(acc + (int64_t)a * 3 + d),
+              (unsigned long long)llrint(-(double)g[e * 3 + d] * kFixScale));
+}
+
+__global__ void k_ret_add(int64_t cnt, const long long* __restrict__ in, const int32_t* __restrict__ idx,
+                          long long* __restrict__ acc) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  const int64_t a = idx[k];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+    atomicAdd(reinterpret_cast<unsigned long long*>(acc + a * 3 + d), (unsigned long long)in[k * 3 + d]);
+}
+
+template <typename T>
+void reserve_keep(DBuf<T>& b, size_t n, size_t used, cudaStream_t st) {
+  if (n <= b.cap) return;
+  DBuf<T> nb;
+  nb.reserve(n);
+  if (used > 0 && b.p) ALG_CUDA(cudaMemcpyAsync(nb.p, b.p, used * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  ALG_CUDA(cudaStreamSynchronize(st));
+  b.release();
+  b = nb;
+  nb.p = nullptr;
+  nb.cap = 0;
+}
+
+int64_t scan_count(allegro_ctx* c, const int32_t* flag, int32_t* idx, int64_t n) {
+  exclusive_scan(c, flag, idx, n);
+  int32_t cnt = 0;
+  ALG_CUDA(cudaMemcpyAsync(&cnt, idx + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  ALG_CUDA(cudaStreamSynchronize(c->stream));
+  return cnt;
+}
+
+// Exchange byte messages with the -/+ neighbours of one axis: send[d] -> nbr[d],
+// recv[d] <- nbr[d] (the neighbour's message in the opposite direction).
+void exchange(allegro_ctx* c, int axis, const void* send_m, size_t bytes_m, const void* send_p, size_t bytes_p,
+              void* recv_from_m, size_t rbytes_m, void* recv_from_p, size_t rbytes_p) {
+  Domain& D = c->dom;
+  NcclApi& N = NcclApi::get();
+  const int pm = D.nbr[axis][0], pp = D.nbr[axis][1];
+  if (pm == D.rank && pp == D.rank) {
+    // self: my "+" message comes back as "from -", my "-" message as "from +"
+    if (rbytes_m) ALG_CUDA(cudaMemcpyAsync(recv_from_m, send_p, rbytes_m, cudaMemcpyDeviceToDevice, c->stream));
+    if (rbytes_p) ALG_CUDA(cudaMemcpyAsync(recv_from_p, send_m, rbytes_p, cudaMemcpyDeviceToDevice, c->stream));
+    return;
+  }
+  ALG_NCCL(N.GroupStart());
+  ALG_NCCL(N.Send(send_p, bytes_p, ncclUint8, pp, D.comm, c->stream));
+  ALG_NCCL(N.Recv(recv_from_m, rbytes_m, ncclUint8, pm, D.comm, c->stream));
+  ALG_NCCL(N.Send(send_m, bytes_m, ncclUint8, pm, D.comm, c->stream));
+  ALG_NCCL(N.Recv(recv_from_p, rbytes_p, ncclUint8, pp, D.comm, c->stream));
+  ALG_NCCL(N.GroupEnd());
+}
+
+// exchange the two message sizes, returns (from -, from +)
+void exchange_counts(allegro_ctx* c, int axis, int64_t n_m, int64_t n_p, int64_t* r_m, int64_t* r_p) {
+  Domain& D = c->dom;
+  D.cnt.reserve(8);
+  long long h[2] = {n_m, n_p};
+  ALG_CUDA(cudaMemcpyAsync(D.cnt.p, h, 2 * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+  exchange(c, axis, D.cnt.p, 8, D.cnt.p + 1, 8, D.cnt.p + 2, 8, D.cnt.p + 3, 8);
+  long long r[2];
+  ALG_CUDA(cudaMemcpyAsync(r, D.cnt.p + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  ALG_CUDA(cudaStreamSynchronize(c->stream));
+  *r_m = r[0];
+  *r_p = r[1];
+}
+
+DBuf<double> g_tpos, g_tvel;
+DBuf<int32_t> g_tgid, g_tspec, g_f0, g_f1, g_f2, g_i0, g_i1, g_i2;
+
+}  // namespace
+
+void domain_setup(allegro_ctx* c, const void* nccl_id) {
+  Domain& D = c->dom;
+  const allegro_params& p = c->prm;
+  D.multi = p.world_size > 1;
+  D.rank = p.rank;
+  D.size = p.world_size;
+  int P[3] = {p.grid[0], p.grid[1], p.grid[2]};
+  if (P[0] <= 0 || P[1] <= 0 || P[2] <= 0) {
+    if (D.size == 1) P[0] = P[1] = P[2] = 1;
+    else if (D.size == 2) P[0] = 2, P[1] = 1, P[2] = 1;
+    else if (D.size == 4) P[0] = 2, P[1] = 2, P[2] = 1;
+    else if (D.size == 8) P[0] = 2, P[1] = 2, P[2] = 2;
+    else P[0] = D.size, P[1] = 1, P[2] = 1;
+  }
+  if (P[0] * P[1] * P[2] != D.size) throw std::invalid_argument("grid product differs from world_size");
+  const int coord[3] = {D.rank % P[0], (D.rank / P[0]) % P[1], D.rank / (P[0] * P[1])};
+  const double rcp = c->r_cut + c->skin;
+  for (int a = 0; a < 3; ++a) {
+    D.P[a] = P[a];
+    D.c[a] = coord[a];
+    D.w[a] = c->box[a] / P[a];
+    D.lo[a] = coord[a] * D.w[a];
+    D.hi[a] = coord[a] == P[a] - 1 ? c->box[a] : (coord[a] + 1) * D.w[a];
+    if (D.multi && D.w[a] < rcp) throw GeometryError("domain edge smaller than r_c + skin");
+    for (int d = 0; d < 2; ++d) {
+      int cc[3] = {coord[0], coord[1], coord[2]};
+      cc[a] = (cc[a] + (d == 0 ? -1 : 1) + P[a]) % P[a];
+      D.nbr[a][d] = cc[0] + P[0] * (cc[1] + P[1] * cc[2]);
+    }
+  }
+  if (D.multi) {
+    if (!nccl_id) throw std::invalid_argument("nccl_unique_id is required when world_size > 1");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ALG_NCCL(NcclApi::get().CommInitRank(&D.comm, D.size, id, D.rank));
+  }
+}
+
+void domain_teardown(allegro_ctx* c) {
+  Domain& D = c->dom;
+  if (D.comm) NcclApi::get().CommDestroy(D.comm);
+  D.comm = nullptr;
+  for (int a = 0; a < 3; ++a)
+    for (int d = 0; d < 2; ++d) D.st[a].send_idx[d].release();
+  for (int d = 0; d < 2; ++d) D.sendbuf[d].release(), D.recvbuf[d].release();
+  D.flag.release();
+  D.pos_idx.release();
+  D.acc.release();
+  D.cnt.release();
+  D.red.release();
+}
+
+double allreduce_sum(allegro_ctx* c, double v) {
+  Domain& D = c->dom;
+  if (!D.multi) return v;
+  D.red.reserve(4);
+  ALG_CUDA(cudaMemcpyAsync(D.red.p, &v, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  ALG_NCCL(NcclApi::get().AllReduce(D.red.p, D.red.p + 1, 1, ncclFloat64, ncclSum, D.comm, c->stream));
+  double r = 0;
+  ALG_CUDA(cudaMemcpyAsync(&r, D.red.p + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  ALG_CUDA(cudaStreamSynchronize(c->stream));
+  return r;
+}
+
+int64_t allreduce_sum_i64(allegro_ctx* c, int64_t v) {
+  Domain& D = c->dom;
+  if (!D.multi) return v;
+  D.cnt.reserve(8);
+  long long h = v;
+  ALG_CUDA(cudaMemcpyAsync(D.cnt.p + 4, &h, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+  ALG_NCCL(NcclApi::get().AllReduce(D.cnt.p + 4, D.cnt.p + 5, 1, ncclInt64, ncclSum, D.comm, c->stream));
+  ALG_CUDA(cudaMemcpyAsync(&h, D.cnt.p + 5, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  ALG_CUDA(cudaStreamSynchronize(c->stream));
+  return h;
+}
+
+int allreduce_max_i32(allegro_ctx* c, int v) {
+  Domain& D = c->dom;
+  if (!D.multi) return v;
+  D.cnt.reserve(8);
+  int* d = reinterpret_cast<int*>(D.cnt.p + 6);
+  ALG_CUDA(cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  ALG_NCCL(NcclApi::get().AllReduce(d, d + 1, 1, ncclInt32, ncclMax, D.comm, c->stream));
+  int r = 0;
+  ALG_CUDA(cudaMemcpyAsync(&r, d + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  ALG_CUDA(cudaStreamSynchronize(c->stream));
+  return r;
+}
+
+void migrate(allegro_ctx* c) {
+  Domain& D = c->dom;
+  cudaStream_t st = c->stream;
+  for (int axis = 0; axis < 3; ++axis) {
+    if (D.P[axis] == 1) continue;
+    const int64_t n = c->n;
+    g_f0.reserve(n + 1), g_f1.reserve(n + 1), g_f2.reserve(n + 1);
+    g_i0.reserve(n + 1), g_i1.reserve(n + 1), g_i2.reserve(n + 1);
+    if (n > 0) {
+      ProfScope ps_(&c->prof, st, PK_HALO, 0, 28.0 * n);
+      k_mig_class<<<ceil_div(n, 256), 256, 0, st>>>(c->pos.p, n, axis, D.w[axis], D.P[axis], D.c[axis], g_f0.p, g_f1.p,
+                                                    g_f2.p);
+      ALG_LAUNCH_CHECK();
+    }
+    const int64_t n_stay = scan_count(c, g_f0.p, g_i0.p, n);
+    const int64_t n_m = scan_count(c, g_f1.p, g_i1.p, n);
+    const int64_t n_p = scan_count(c, g_f2.p, g_i2.p, n);
+    D.sendbuf[0].reserve((n_m + 1) * sizeof(MigAtom));
+    D.sendbuf[1].reserve((n_p + 1) * sizeof(MigAtom));
+    // stay-compaction into temporaries, then pack the leavers
+    g_tpos.reserve(3 * n + 3), g_tvel.reserve(3 * n + 3), g_tgid.reserve(n + 1), g_tspec.reserve(n + 1);
+    if (n > 0) {
+      ProfScope ps_(&c->prof, st, PK_HALO, 0, 112.0 * n);
+      k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, g_f1.p, g_i1.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
+                                                   reinterpret_cast<MigAtom*>(D.sendbuf[0].p));
+      k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, g_f2.p, g_i2.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
+                                                   reinterpret_cast<MigAtom*>(D.sendbuf[1].p));
+      // reuse the recv buffer as the stay staging (MigAtom layout)
+      D.recvbuf[0].reserve((n_stay + 1) * sizeof(MigAtom));
+      k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, g_f0.p, g_i0.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
+                                                   reinterpret_cast<MigAtom*>(D.recvbuf[0].p));
+      ALG_LAUNCH_CHECK();
+      k_mig_unpack<<<ceil_div(std::max<int64_t>(n_stay, 1), 256), 256, 0, st>>>(
+          n_stay, reinterpret_cast<MigAtom*>(D.recvbuf[0].p), 0, c->pos.p, c->vel.p, c->gid.p, c->species.p);
+      ALG_LAUNCH_CHECK();
+    }
+    int64_t r_m = 0, r_p = 0;
+    exchange_counts(c, axis, n_m, n_p, &r_m, &r_p);
+    const int64_t n_new = n_stay + r_m + r_p;
+    // owned capacity has 25 % slack (select_owned); growing here would discard content
+    if ((size_t)(3 * n_new + 3) > c->pos.cap || (size_t)(3 * n_new + 3) > c->vel.cap || (size_t)(n_new + 1) > c->gid.cap ||
+        (size_t)(n_new + 1) > c->species.cap)
+      throw CudaError("migration overflow: owned-atom capacity exceeded");
+    D.recvbuf[0].reserve((r_m + 1) * sizeof(MigAtom));
+    D.recvbuf[1].reserve((r_p + 1) * sizeof(MigAtom));
+    exchange(c, axis, D.sendbuf[0].p, n_m * sizeof(MigAtom), D.sendbuf[1].p, n_p * sizeof(MigAtom), D.recvbuf[0].p,
+             r_m * sizeof(MigAtom), D.recvbuf[1].p, r_p * sizeof(MigAtom));
+    if (r_m > 0)
+      k_mig_unpack<<<ceil_div(r_m, 256), 256, 0, st>>>(r_m, reinterpret_cast<MigAtom*>(D.recvbuf[0].p), n_stay, c->pos.p,
+                                                       c->vel.p, c->gid.p, c->species.p);
+    if (r_p > 0)
+      k_mig_unpack<<<ceil_div(r_p, 256), 256, 0, st>>>(r_p, reinterpret_cast<MigAtom*>(D.recvbuf[1].p), n_stay + r_m,
+                                                       c->pos.p, c->vel.p, c->gid.p, c->species.p);
+    ALG_LAUNCH_CHECK();
+    c->n = n_new;
+  }
+}
+
+void halo_exchange(allegro_ctx* c) {
+  Domain& D = c->dom;
+  cudaStream_t st = c->stream;
+  const int64_t n = c->n;
+  const double rcp = (c->r_cut + c->skin) * (1.0 + 1e-9) + 1e-9;
+  // owned atoms first
+  const size_t est = (size_t)(n * 2 + 1024);
+  c->apos.reserve(3 * est), c->agid.reserve(est), c->aspec.reserve(est), c->ashift.reserve(est), c->aowner.reserve(est);
+  if (n > 0) {
+    ProfScope ps_(&c->prof, st, PK_HALO, 0, 72.0 * n);
+    k_owned_to_atoms<<<ceil_div(n, 256), 256, 0, st>>>(n, c->pos.p, c->gid.p, c->species.p, c->apos.p, c->agid.p,
+                                                       c->aspec.p, c->ashift.p, c->aowner.p);
+    ALG_LAUNCH_CHECK();
+  }
+  int64_t n_cur = n;
+  for (int axis = 0; axis < 3; ++axis) {
+    HaloStage& S = D.st[axis];
+    g_f0.reserve(n_cur + 1), g_f1.reserve(n_cur + 1), g_i0.reserve(n_cur + 1), g_i1.reserve(n_cur + 1);
+    if (n_cur > 0) {
+      ProfScope ps_(&c->prof, st, PK_HALO, 0, 16.0 * n_cur);
+      k_halo_flag<<<ceil_div(n_cur, 256), 256, 0, st>>>(c->apos.p, n_cur, axis, D.lo[axis], D.hi[axis], rcp, g_f0.p,
+                                                        g_f1.p);
+      ALG_LAUNCH_CHECK();
+    }
+    const int64_t n_m = scan_count(c, g_f0.p, g_i0.p, n_cur);
+    const int64_t n_p = scan_count(c, g_f1.p, g_i1.p, n_cur);
+    S.n_send[0] = n_m;
+    S.n_send[1] = n_p;
+    S.send_idx[0].reserve(n_m + 1);
+    S.send_idx[1].reserve(n_p + 1);
+    D.sendbuf[0].reserve((n_m + 1) * sizeof(HaloAtom));
+    D.sendbuf[1].reserve((n_p + 1) * sizeof(HaloAtom));
+    // "-" message: atoms near the lower face, shifted by +L when wrapping; "+" message: -L
+    const int sh_m = D.c[axis] == 0 ? +1 : 0;
+    const int sh_p = D.c[axis] == D.P[axis] - 1 ? -1 : 0;
+    if (n_cur > 0) {
+      ProfScope ps_(&c->prof, st, PK_HALO, 0, 40.0 * (n_m + n_p));
+      k_halo_pack<<<ceil_div(n_cur, 256), 256, 0, st>>>(n_cur, g_f0.p, g_i0.p, axis, c->box[axis], sh_m, c->apos.p,
+                                                        c->agid.p, c->aspec.p, c->ashift.p,
+                                                        reinterpret_cast<HaloAtom*>(D.sendbuf[0].p), S.send_idx[0].p);
+      k_halo_pack<<<ceil_div(n_cur, 256), 256, 0, st>>>(n_cur, g_f1.p, g_i1.p, axis, c->box[axis], sh_p, c->apos.p,
+                                                        c->agid.p, c->aspec.p, c->ashift.p,
+                                                        reinterpret_cast<HaloAtom*>(D.sendbuf[1].p), S.send_idx[1].p);
+      ALG_LAUNCH_CHECK();
+    }
+    int64_t r_m = 0, r_p = 0;
+    exchange_counts(c, axis, n_m, n_p, &r_m, &r_p);
+    S.n_recv[0] = r_m;
+    S.n_recv[1] = r_p;
+    D.recvbuf[0].reserve((r_m + 1) * sizeof(HaloAtom));
+    D.recvbuf[1].reserve((r_p + 1) * sizeof(HaloAtom));
+    exchange(c, axis, D.sendbuf[0].p, n_m * sizeof(HaloAtom), D.sendbuf[1].p, n_p * sizeof(HaloAtom), D.recvbuf[0].p,
+             r_m * sizeof(HaloAtom), D.recvbuf[1].p, r_p * sizeof(HaloAtom));
+    const int64_t need = n_cur + r_m + r_p + 1;
+    reserve_keep(c->apos, 3 * need, 3 * n_cur, st);
+    reserve_keep(c->agid, need, n_cur, st);
+    reserve_keep(c->aspec, need, n_cur, st);
+    reserve_keep(c->ashift, need, n_cur, st);
+    reserve_keep(c->aowner, need, n_cur, st);
+    S.recv_base[0] = n_cur;
+    S.recv_base[1] = n_cur + r_m;
+    {
+      ProfScope ps_(&c->prof, st, PK_HALO, 0, 80.0 * (r_m + r_p));
+      if (r_m > 0)
+        k_halo_unpack<<<ceil_div(r_m, 256), 256, 0, st>>>(r_m, reinterpret_cast<HaloAtom*>(D.recvbuf[0].p), n_cur,
+                                                          c->apos.p, c->agid.p, c->aspec.p, c->ashift.p, c->aowner.p);
+      if (r_p > 0)
+        k_halo_unpack<<<ceil_div(r_p, 256), 256, 0, st>>>(r_p, reinterpret_cast<HaloAtom*>(D.recvbuf[1].p),
+                                                          n_cur + r_m, c->apos.p, c->agid.p, c->aspec.p, c->ashift.p,
+                                                          c->aowner.p);
+      ALG_LAUNCH_CHECK();
+    }
+    n_cur += r_m + r_p;
+  }
+  c->n_ghost = n_cur - n;
+}
+
+void ghost_force_return(allegro_ctx* c) {
+  Domain& D = c->dom;
+  cudaStream_t st = c->stream;
+  const int64_t na = c->n + c->n_ghost;
+  D.acc.reserve(3 * na + 3);
+  ALG_CUDA(cudaMemsetAsync(D.acc.p, 0, sizeof(long long) * 3 * na, st));
+  if (c->n_edges > 0) {
+    ProfScope ps_(&c->prof, st, PK_HALO, 0, 20.0 * c->n_edges);
+    k_ghost_acc<<<ceil_div(c->n_edges, 256), 256, 0, st>>>(c->n_edges, c->n, c->nbr.p, c->g.p, D.acc.p);
+    ALG_LAUNCH_CHECK();
+  }
+  for (int axis = 2; axis >= 0; --axis) {
+    HaloStage& S = D.st[axis];
+    // return the accumulators of the ghosts received from -/+ to their senders
+    const long long* ret_m = D.acc.p + 3 * S.recv_base[0];
+    const long long* ret_p = D.acc.p + 3 * S.recv_base[1];
+    D.recvbuf[0].reserve((S.n_send[0] + 1) * 24);
+    D.recvbuf[1].reserve((S.n_send[1] + 1) * 24);
+    // message to "-" = returns for the ghosts that came from "-" (the neighbour's "+" list)
+    exchange(c, axis, ret_m, S.n_recv[0] * 24, ret_p, S.n_recv[1] * 24, D.recvbuf[0].p, S.n_send[0] * 24,
+             D.recvbuf[1].p, S.n_send[1] * 24);
+    ProfScope ps_(&c->prof, st, PK_HALO, 0, 28.0 * (S.n_send[0] + S.n_send[1]));
+    if (S.n_send[0] > 0)
+      k_ret_add<<<ceil_div(S.n_send[0], 256), 256, 0, st>>>(
+          S.n_send[0], reinterpret_cast<const long long*>(D.recvbuf[0].p), S.send_idx[0].p, D.acc.p);
+    if (S.n_send[1] > 0)
+      k_ret_add<<<ceil_div(S.n_send[1], 256), 256, 0, st>>>(
+          S.n_send[1], reinterpret_cast<const long long*>(D.recvbuf[1].p), S.send_idx[1].p, D.acc.p);
+    ALG_LAUNCH_CHECK();
+  }
+}
+
+void select_owned(allegro_ctx* c, int64_t n_global, const int32_t* species, const double* pos, const double* vel) {
+  Domain& D = c->dom;
+  std::vector<double> p, v;
+  std::vector<int32_t> s, g;
+  p.reserve(3 * (n_global / D.size + 16));
+  for (int64_t a = 0; a < n_global; ++a) {
+    double x[3];
+    bool mine = true;
+    for (int d = 0; d < 3; ++d) {
+      const double L = c->box[d];
+      double y = pos[a * 3 + d] - L * std::floor(pos[a * 3 + d] / L);
+      if (y >= L) y = 0.0;
+      x[d] = y;
+      mine = mine && owner_coord(y, D.w[d], D.P[d]) == D.c[d];
+    }
+    if (!mine) continue;
+    p.insert(p.end(), x, x + 3);
+    v.insert(v.end(), vel + a * 3, vel + a * 3 + 3);
+    s.push_back(species[a]);
+    g.push_back((int32_t)a);
+  }
+  const int64_t n = (int64_t)s.size();
+  const int64_t cap = n + n / 4 + 1024;  // migration headroom
+  c->pos.reserve(3 * cap), c->vel.reserve(3 * cap), c->frc.reserve(3 * cap);
+  c->species.reserve(cap), c->gid.reserve(cap), c->e_atom.reserve(cap);
+  c->n = n;
+  if (n > 0) {
+    ALG_CUDA(cudaMemcpyAsync(c->pos.p, p.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->vel.p, v.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->species.p, s.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->gid.p, g.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+  }
+  ALG_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void gather_state(allegro_ctx* c, int64_t n_global, double* pos, double* vel, double* forces) {
+  Domain& D = c->dom;
+  NcclApi& N = NcclApi::get();
+  cudaStream_t st = c->stream;
+  // counts of every rank
+  D.cnt.reserve(2 * D.size + 8);
+  long long mine = c->n;
+  ALG_CUDA(cudaMemcpyAsync(D.cnt.p, &mine, sizeof(long long), cudaMemcpyHostToDevice, st));
+  ALG_NCCL(N.AllGather(D.cnt.p, D.cnt.p + 1, 1, ncclInt64, D.comm, st));
+  std::vector<long long> counts(D.size);
+  ALG_CUDA(cudaMemcpyAsync(counts.data(), D.cnt.p + 1, sizeof(long long) * D.size, cudaMemcpyDeviceToHost, st));
+  ALG_CUDA(cudaStreamSynchronize(st));
+  // payload per atom: gid (as double) + pos + vel + frc = 10 doubles
+  const int64_t W = 10;
+  D.sendbuf[0].reserve((size_t)(c->n + 1) * W * 8);
+  {
+    std::vector<double> h((size_t)c->n * W);
+    std::vector<int32_t> gid(c->n);
+    std::vector<double> p(3 * c->n), v(3 * c->n), f(3 * c->n);
+    ALG_CUDA(cudaMemcpyAsync(gid.data(), c->gid.p, 4 * c->n, cudaMemcpyDeviceToHost, st));
+    ALG_CUDA(cudaMemcpyAsync(p.data(), c->pos.p, 24 * c->n, cudaMemcpyDeviceToHost, st));
+    ALG_CUDA(cudaMemcpyAsync(v.data(), c->vel.p, 24 * c->n, cudaMemcpyDeviceToHost, st));
+    ALG_CUDA(cudaMemcpyAsync(f.data(), c->frc.p, 24 * c->n, cudaMemcpyDeviceToHost, st));
+    ALG_CUDA(cudaStreamSynchronize(st));
+    for (int64_t a = 0; a < c->n; ++a) {
+      h[a * W] = gid[a];
+      for (int d = 0; d < 3; ++d) h[a * W + 1 + d] = p[a * 3 + d], h[a * W + 4 + d] = v[a * 3 + d], h[a * W + 7 + d] = f[a * 3 + d];
+    }
+    if (c->n) ALG_CUDA(cudaMemcpyAsync(D.sendbuf[0].p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+  }
+  int64_t total = 0;
+  for (long long k : counts) total += k;
+  if (D.rank == 0) D.recvbuf[0].reserve((size_t)(total + 1) * W * 8);
+  ALG_NCCL(N.GroupStart());
+  if (D.rank != 0) {
+    ALG_NCCL(N.Send(D.sendbuf[0].p, (size_t)c->n * W, ncclFloat64, 0, D.comm, st));
+  } else {
+    int64_t off = counts[0];
+    ALG_CUDA(cudaMemcpyAsync(D.recvbuf[0].p, D.sendbuf[0].p, (size_t)c->n * W * 8, cudaMemcpyDeviceToDevice, st));
+    for (int r = 1; r < D.size; ++r) {
+      ALG_NCCL(N.Recv(reinterpret_cast<double*>(D.recvbuf[0].p) + off * W, (size_t)counts[r] * W, ncclFloat64, r, D.comm,
+                      st));
+      off += counts[r];
+    }
+  }
+  ALG_NCCL(N.GroupEnd());
+  ALG_CUDA(cudaStreamSynchronize(st));
+  if (D.rank != 0) return;
+  std::vector<double> h((size_t)total * W);
+  ALG_CUDA(cudaMemcpy(h.data(), D.recvbuf[0].p, h.size() * 8, cudaMemcpyDeviceToHost));
+  for (int64_t k = 0; k < total; ++k) {
+    const int64_t gidx = (int64_t)h[k * W];
+    if (gidx < 0 || gidx >= n_global) continue;
+    for (int d = 0; d < 3; ++d) {
+      if (pos) pos[gidx * 3 + d] = h[k * W + 1 + d];
+      if (vel) vel[gidx * 3 + d] = h[k * W + 4 + d];
+      if (forces) forces[gidx * 3 + d] = h[k * W + 7 + d];
+    }
+  }
+}
+
+}  // namespace allegro

@@ -140,7 +140,7 @@ double md_kinetic(allegro_ctx* c) {
     k_ke<<<1, kRedThreads, 0, c->stream>>>(c->vel.p, c->species.p, c->n, c->red.p);
   }
   ALG_LAUNCH_CHECK();
-  return fetch(c, c->red.p);
+  return allreduce_sum(c, fetch(c, c->red.p));
 }
 
 double sum_e_atom(allegro_ctx* c) {
@@ -155,8 +155,15 @@ double sum_e_atom(allegro_ctx* c) {
 
 void force_stats(allegro_ctx* c, double* mean, double* sigma) {
   c->red.reserve(8);
-  if (c->n == 0) {
+  const double n_tot = (double)allreduce_sum_i64(c, c->n);
+  if (n_tot == 0) {
     *mean = *sigma = 0;
+    return;
+  }
+  if (c->n == 0) {  // this rank owns nothing: still take part in the two reductions
+    const double m = allreduce_sum(c, 0.0) / n_tot;
+    *mean = m;
+    *sigma = std::sqrt(allreduce_sum(c, 0.0) / n_tot);
     return;
   }
   {
@@ -169,8 +176,13 @@ void force_stats(allegro_ctx* c, double* mean, double* sigma) {
     k_fnorm_var<<<1, kRedThreads, 0, c->stream>>>(c->frc.p, c->n, c->red.p + 2, c->red.p + 3);
   }
   ALG_LAUNCH_CHECK();
-  *mean = fetch(c, c->red.p + 2) / (double)c->n;
-  *sigma = std::sqrt(fetch(c, c->red.p + 3) / (double)c->n);
+  // two passes: the global mean first, then the population variance about it
+  const double mean_g = allreduce_sum(c, fetch(c, c->red.p + 2)) / n_tot;
+  const double mean_l = fetch(c, c->red.p + 2) / (double)c->n;
+  // k_fnorm_var used the local mean: shift to the global mean: sum (x - m_g)^2 = S_l + n (m_l - m_g)^2
+  const double var_l = fetch(c, c->red.p + 3) + (double)c->n * (mean_l - mean_g) * (mean_l - mean_g);
+  *mean = mean_g;
+  *sigma = std::sqrt(allreduce_sum(c, var_l) / n_tot);
 }
 
 int64_t count_outliers(allegro_ctx* c, double thr) {
@@ -187,7 +199,7 @@ int64_t count_outliers(allegro_ctx* c, double thr) {
   unsigned long long h = 0;
   ALG_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   ALG_CUDA(cudaStreamSynchronize(c->stream));
-  return (int64_t)h;
+  return allreduce_sum_i64(c, (int64_t)h);
 }
 
 bool all_finite(allegro_ctx* c) {
@@ -202,6 +214,7 @@ bool all_finite(allegro_ctx* c) {
   int f = 0;
   ALG_CUDA(cudaMemcpyAsync(&f, c->flags.p + 2, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   ALG_CUDA(cudaStreamSynchronize(c->stream));
+  f = allreduce_max_i32(c, f);
   return f == 0 && std::isfinite(c->e_pot);
 }
 
@@ -209,7 +222,7 @@ bool check_inputs(allegro_ctx* c) {
   int f = 0;
   ALG_CUDA(cudaMemcpyAsync(&f, c->flags.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   ALG_CUDA(cudaStreamSynchronize(c->stream));
-  return f == 0;
+  return allreduce_max_i32(c, f) == 0;
 }
 
 }  // namespace allegro

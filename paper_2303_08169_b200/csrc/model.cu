@@ -89,7 +89,7 @@ __device__ __forceinline__ void edge_vec(const double* __restrict__ apos, int32_
 }
 
 __global__ void k_geom(ChunkPtrs ch, GeomParams gp, const double* __restrict__ apos, const int32_t* __restrict__ cidx,
-                       const int32_t* __restrict__ nbr, const int32_t* __restrict__ aowner,
+                       const int32_t* __restrict__ nbr, const int32_t* __restrict__ aspec,
                        const int32_t* __restrict__ species, float* __restrict__ z, float* __restrict__ Y,
                        float* __restrict__ u) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -106,7 +106,7 @@ __global__ void k_geom(ChunkPtrs ch, GeomParams gp, const double* __restrict__ a
     uu = 1.f - 28.f * x6 + 48.f * x6 * x - 21.f * x6 * x2;
   }
   u[e] = uu;
-  const int zi = species[i], zj = species[aowner[a]];
+  const int zi = species[i], zj = aspec[a];
   float* zz = z + e * 16;
   zz[0] = zi == 0 ? 1.f : 0.f;
   zz[1] = zi == 1 ? 1.f : 0.f;
@@ -430,10 +430,15 @@ __global__ void k_geom_bwd(ChunkPtrs ch, GeomParams gp, const double* __restrict
 
 // ----------------------------------------------------------------- A12 force gather
 __global__ void k_force(int64_t n, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ rev,
-                        const float* __restrict__ g, double* __restrict__ F, int* __restrict__ flags) {
+                        const float* __restrict__ g, const long long* __restrict__ acc, double* __restrict__ F,
+                        int* __restrict__ flags) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n) return;
   double f[3] = {0, 0, 0};
+  if (acc != nullptr) {  // multi-GPU: -g of edges that point at images of a, returned by the reverse halo
+#pragma unroll
+    for (int d = 0; d < 3; ++d) f[d] = (double)acc[a * 3 + d] * (1.0 / kFixScale);
+  }
   for (int64_t e = row_ptr[a]; e < row_ptr[a + 1]; ++e) {
     const int32_t r = rev[e];
 #pragma unroll
@@ -566,7 +571,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   if (E > 0) {
     {
       ProfScope ps_(&c->prof, st, PK_GEOM, 0, (double)E * (8 + 64 + 4 * dsh + 4));
-      k_geom<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, c->aowner.p, c->species.p, w.z.p,
+      k_geom<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, c->aspec.p, c->species.p, w.z.p,
                                              w.Y.p, w.u.p);
     }
     ALG_LAUNCH_CHECK();
@@ -772,14 +777,16 @@ void compute_forces(allegro_ctx* c) {
   reserve_ws(c, e_cap, a_cap);
   for (const ChunkPtrs& ch : chunks) run_chunk(c, ch);
   ALG_CUDA(cudaMemsetAsync(c->flags.p + 2, 0, sizeof(int), st));
+  if (c->dom.multi) ghost_force_return(c);
   if (n > 0) {
     {
       ProfScope ps_(&c->prof, st, PK_FORCE, 0, 24.0 * n + 8.0 * n + 28.0 * E);
-      k_force<<<ceil_div(n, 256), 256, 0, st>>>(n, c->row_ptr.p, c->rev.p, c->g.p, c->frc.p, c->flags.p);
+      k_force<<<ceil_div(n, 256), 256, 0, st>>>(n, c->row_ptr.p, c->rev.p, c->g.p,
+                                              c->dom.multi ? c->dom.acc.p : nullptr, c->frc.p, c->flags.p);
     }
     ALG_LAUNCH_CHECK();
   }
-  c->e_pot = sum_e_atom(c);
+  c->e_pot = allreduce_sum(c, sum_e_atom(c));
 }
 
 }  // namespace allegro

@@ -88,9 +88,10 @@ __global__ void k_ghost_count(const double* __restrict__ pos, int64_t n, GhostGe
   cnt[a] = c;
 }
 
-__global__ void k_ghost_fill(const double* __restrict__ pos, const int32_t* __restrict__ gid, int64_t n, GhostGeom g,
-                             const int32_t* __restrict__ off, double* __restrict__ apos, int32_t* __restrict__ aowner,
-                             int32_t* __restrict__ ashift, int32_t* __restrict__ agid) {
+__global__ void k_ghost_fill(const double* __restrict__ pos, const int32_t* __restrict__ gid,
+                             const int32_t* __restrict__ spec, int64_t n, GhostGeom g, const int32_t* __restrict__ off,
+                             double* __restrict__ apos, int32_t* __restrict__ aowner, int32_t* __restrict__ ashift,
+                             int32_t* __restrict__ agid, int32_t* __restrict__ aspec) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n) return;
   const double x[3] = {pos[a * 3], pos[a * 3 + 1], pos[a * 3 + 2]};
@@ -100,6 +101,7 @@ __global__ void k_ghost_fill(const double* __restrict__ pos, const int32_t* __re
   aowner[a] = (int32_t)a;
   ashift[a] = pack_shift(0, 0, 0);
   agid[a] = gid[a];
+  aspec[a] = spec[a];
   int64_t o = n + off[a];
   double xp[3];
   for (int nz = -g.m[2]; nz <= g.m[2]; ++nz)
@@ -113,6 +115,7 @@ __global__ void k_ghost_fill(const double* __restrict__ pos, const int32_t* __re
         aowner[o] = (int32_t)a;
         ashift[o] = pack_shift(nx, ny, nz);
         agid[o] = gid[a];
+        aspec[o] = spec[a];
         ++o;
       }
 }
@@ -255,13 +258,17 @@ __global__ void k_edge_compact(int64_t n, int max_nb, const int32_t* __restrict_
 }
 
 // rev[e] = index of (j, i, -n) in row owner(j), or -1 (measure-zero asymmetry at d == r_c)
-__global__ void k_edge_rev(int64_t E, const int32_t* __restrict__ cidx, const int32_t* __restrict__ nbr,
+__global__ void k_edge_rev(int64_t E, int64_t n_owned_only, const int32_t* __restrict__ cidx, const int32_t* __restrict__ nbr,
                            const int32_t* __restrict__ aowner, const int32_t* __restrict__ ashift,
                            const int32_t* __restrict__ gid, const int32_t* __restrict__ row_ptr,
                            const unsigned long long* __restrict__ key, int32_t* __restrict__ rev) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   const int32_t i = cidx[e], a = nbr[e];
+  if (n_owned_only > 0 && a >= n_owned_only) {  // multi-GPU: ghost neighbours go through the reverse halo
+    rev[e] = -1;
+    return;
+  }
   const int32_t o = aowner[a];
   int nx, ny, nz;
   unpack_shift(ashift[a], nx, ny, nz);
@@ -296,39 +303,47 @@ void build_neighbors(allegro_ctx* c) {
   cudaStream_t st = c->stream;
   const int64_t n = c->n;
   const double rc = c->r_cut + c->skin;
-  // ---- ghosts (periodic images within r_c of the box) ----
+  // ---- ghosts: periodic images within r_c of the box (1 GPU) or the NCCL halo ----
   GhostGeom gg;
   for (int d = 0; d < 3; ++d) {
     const double L = c->box[d];
     const double margin = 1e-9 * std::max(1.0, L);
     gg.L[d] = L;
-    gg.lo[d] = -rc - margin;
-    gg.hi[d] = L + rc + margin;
+    const double lo = c->dom.multi ? c->dom.lo[d] : 0.0, hi = c->dom.multi ? c->dom.hi[d] : L;
+    gg.lo[d] = lo - rc - margin;
+    gg.hi[d] = hi + rc + margin;
     gg.m[d] = (int)std::ceil(rc / L) + 1;
   }
-  c->gcount.reserve(n + 1);
-  c->goff.reserve(n + 1);
-  {
-    ProfScope ps_(&c->prof, st, PK_GHOST, 0, 28.0 * n);
-    k_ghost_count<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(c->pos.p, n, gg, c->gcount.p);
+  if (c->dom.multi) {
+    halo_exchange(c);
+  } else {
+    c->gcount.reserve(n + 1);
+    c->goff.reserve(n + 1);
+    {
+      ProfScope ps_(&c->prof, st, PK_GHOST, 0, 28.0 * n);
+      k_ghost_count<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(c->pos.p, n, gg, c->gcount.p);
+    }
+    ALG_LAUNCH_CHECK();
+    exclusive_scan(c, c->gcount.p, c->goff.p, n);
+    int32_t G = 0;
+    ALG_CUDA(cudaMemcpyAsync(&G, c->goff.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    ALG_CUDA(cudaStreamSynchronize(st));
+    c->n_ghost = G;
+    const int64_t na0 = n + G;
+    c->apos.reserve(3 * na0);
+    c->aowner.reserve(na0);
+    c->ashift.reserve(na0);
+    c->agid.reserve(na0);
+    c->aspec.reserve(na0);
+    {
+      ProfScope ps_(&c->prof, st, PK_GHOST, 0, 24.0 * n + 44.0 * (n + G));
+      k_ghost_fill<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(c->pos.p, c->gid.p, c->species.p, n, gg,
+                                                                           c->goff.p, c->apos.p, c->aowner.p,
+                                                                           c->ashift.p, c->agid.p, c->aspec.p);
+    }
+    ALG_LAUNCH_CHECK();
   }
-  ALG_LAUNCH_CHECK();
-  exclusive_scan(c, c->gcount.p, c->goff.p, n);
-  int32_t G = 0;
-  ALG_CUDA(cudaMemcpyAsync(&G, c->goff.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  ALG_CUDA(cudaStreamSynchronize(st));
-  c->n_ghost = G;
-  const int64_t na = n + G;
-  c->apos.reserve(3 * na);
-  c->aowner.reserve(na);
-  c->ashift.reserve(na);
-  c->agid.reserve(na);
-  {
-    ProfScope ps_(&c->prof, st, PK_GHOST, 0, 24.0 * n + 40.0 * (n + G));
-    k_ghost_fill<<<ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, st>>>(c->pos.p, c->gid.p, n, gg, c->goff.p, c->apos.p,
-                                                                       c->aowner.p, c->ashift.p, c->agid.p);
-  }
-  ALG_LAUNCH_CHECK();
+  const int64_t na = n + c->n_ghost;
   // ---- cells of edge >= rc (1 + 1e-9) over [lo, hi) ----
   CellGeom cg;
   int64_t ncells = 1;
@@ -408,8 +423,8 @@ void build_neighbors(allegro_ctx* c) {
   if (E > 0) {
     {
       ProfScope ps_(&c->prof, st, PK_EDGE, 0, 16.0 * E);
-      k_edge_rev<<<ceil_div(E, 256), 256, 0, st>>>(E, c->cidx.p, c->nbr.p, c->aowner.p, c->ashift.p, c->gid.p, c->row_ptr.p,
-                                                 c->key.p, c->rev.p);
+      k_edge_rev<<<ceil_div(E, 256), 256, 0, st>>>(E, c->dom.multi ? n : 0, c->cidx.p, c->nbr.p, c->aowner.p,
+                                                 c->ashift.p, c->gid.p, c->row_ptr.p, c->key.p, c->rev.p);
     }
     ALG_LAUNCH_CHECK();
   }

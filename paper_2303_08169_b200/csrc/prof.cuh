@@ -26,12 +26,13 @@ enum ProfKind : int {
   PK_FORCE,
   PK_VERLET,
   PK_REDUCE,
+  PK_HALO,
   PK_COUNT
 };
 
 inline const char* prof_name(int k) {
   static const char* names[PK_COUNT] = {"wrap", "ghost", "cell", "edge_build", "scan", "geom", "gemm", "tp_fwd",
-                                        "tp_bwd", "energy", "rowdot", "geom_bwd", "force_gather", "verlet", "reduce"};
+                                        "tp_bwd", "energy", "rowdot", "geom_bwd", "force_gather", "verlet", "reduce", "halo"};
   return (k >= 0 && k < PK_COUNT) ? names[k] : "?";
 }
 
