@@ -147,6 +147,8 @@ def _oracle_rate(cfg, sample, steps, warmup):
     }
 
 
+GRIDS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+
 PREC_TEXT = {
     "3xtf32": "3xTF32 tcgen05 GEMMs (fp32-level accuracy) + fp32 TP (fp64 positions, Verlet, energy sums)",
     "fp32": "fp32 CUDA-core GEMMs + fp32 TP (fp64 positions, Verlet, energy sums)",
@@ -165,7 +167,8 @@ def _config_dict(cfg, n_gpus, edges, precision="3xtf32"):
         "lmax": cfg.lmax,
         "params": irreps.param_count(cfg.n_layers, cfg.lmax),
         "precision": PREC_TEXT[precision],
-        "parallelism": "single domain" if n_gpus == 1 else f"{n_gpus} independent replica domains (no halo exchange yet)",
+        "parallelism": ("single domain" if n_gpus == 1 else
+                        f"spatial decomposition {GRIDS.get(n_gpus, (n_gpus, 1, 1))} domains, NCCL halo + ghost-force return"),
         "l2": "inputs larger than L2 (per-edge activations are GBs per step)",
     }
 
@@ -191,18 +194,25 @@ def main():
     from synth import configs
 
     ws, rank, local = _dist()
+    nccl_id = None
     if ws > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
+        obj = [pb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
     torch.cuda.set_device(local)
     cfg = configs.CONFIGS[args.config]
-    s = configs.system(cfg)
+    grid = GRIDS.get(ws, (ws, 1, 1))
+    # weak scaling: the N-GPU box is the per-GPU box replicated over the domain grid
+    s = configs.system(cfg, reps=grid)
     wf = configs.weight_file(cfg)
     stream = torch.cuda.current_stream()
     prec = pb.PREC_3XTF32 if args.precision == "3xtf32" else pb.PREC_FP32
-    m = pb.Allegro(wf, s.box, device=local, n_atoms=s.n, stream=stream.cuda_stream, precision=prec)
+    m = pb.Allegro(wf, s.box, device=local, n_atoms=s.n, stream=stream.cuda_stream, precision=prec, rank=rank,
+                   world_size=ws, nccl_id=nccl_id, grid=grid)
     m.md_set_state(s.species, s.pos, s.vel)
     m.md_step(args.warmup, DT_FS)
 
@@ -231,30 +241,41 @@ def main():
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = s.n * ws * args.steps / (ms_max / 1e3)
+    value = s.n * args.steps / (ms_max / 1e3)  # s.n = atoms of the whole (replicated) box
 
-    # ---- e2e: the same steps through md_step_host with pinned host state ----
-    pos, vel, frc = m.md_get_state()
-    h_spc = torch.from_numpy(s.species.astype(np.int32)).pin_memory()
+    # ---- e2e: the same steps through md_step_host with this rank's state in pinned host memory ----
+    n_loc = m.local_count()
+    cap = 2 * n_loc + 1024  # migration may change the local count
+    _, spc, _, pos, vel, frc = m.md_get_local_state(cap)
+    h_spc = torch.from_numpy(spc).pin_memory()
     h_pos = torch.from_numpy(pos).pin_memory()
     h_vel = torch.from_numpy(vel).pin_memory()
     h_frc = torch.from_numpy(frc).pin_memory()
-    m.md_step_host(h_spc, h_pos, h_vel, h_frc, 1, DT_FS)
+    r = m.md_step_host(h_spc, h_pos, h_vel, h_frc, 1, DT_FS, n_local=n_loc)
+    n_loc = r.n_local
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    h2d = d2h = 0
     for _ in range(args.steps):
-        m.md_step_host(h_spc, h_pos, h_vel, h_frc, 1, DT_FS)
+        h2d += n_loc * (4 + 3 * 24)
+        r = m.md_step_host(h_spc, h_pos, h_vel, h_frc, 1, DT_FS, n_local=n_loc)
+        n_loc = r.n_local
+        d2h += n_loc * (3 * 24 + (4 if ws > 1 else 0))
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    te = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    te = torch.tensor([e0.elapsed_time(e1), h2d, d2h], device="cuda", dtype=torch.float64)
     if ws > 1:
-        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = s.n * ws * args.steps / (float(te.item()) / 1e3)
-    h2d = s.n * (4 + 3 * 24)
-    d2h = s.n * 3 * 24
+        tm = te[:1].clone()
+        torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
+        tb = te[1:].clone()
+        torch.distributed.all_reduce(tb, op=torch.distributed.ReduceOp.SUM)
+        te = torch.cat([tm, tb])
+    e2e_value = s.n * args.steps / (float(te[0].item()) / 1e3)
+    h2d = int(te[1].item()) // args.steps
+    d2h = int(te[2].item()) // args.steps
 
     # ---- roofline of the dominant kernel class (live CUDA events, algorithmic work) ----
     peaks, peak_src = _peaks()
@@ -304,7 +325,7 @@ def main():
         "roofline": roof,
         "kernels": kernels,
         "gpu_launches": launches,
-        "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": d2h * ws},
+        "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "clocks": clk,
         "md": {"e_pot": rep.e_pot, "e_kin": rep.e_kin, "temperature": rep.temperature,
                "n_outliers_last": rep.n_outliers_last},

@@ -161,6 +161,9 @@ int allegro_get_edge_grad(allegro_ctx* ctx, int64_t capacity, double* g);
 int allegro_nccl_unique_id(void* out128);
 /* atoms owned by this rank (its spatial domain) */
 int64_t allegro_local_count(const allegro_ctx* ctx);
+/* this rank's owned MD state (host arrays with room for `capacity` atoms; any may be NULL) */
+int md_get_local_state(allegro_ctx* ctx, int64_t capacity, int64_t* n_local, int32_t* species, int32_t* gid,
+                       double* pos, double* vel, double* forces);
 
 /* Per-kernel-class accounting.  Every launch of the library is counted;
  * with profiling enabled each launch is also bracketed by CUDA events on the stream it is

@@ -92,6 +92,7 @@ _lib.allegro_profile_kind_name.restype = C.c_char_p
 _lib.allegro_nccl_unique_id.argtypes = [_P]
 _lib.allegro_local_count.argtypes = [_P]
 _lib.allegro_local_count.restype = C.c_int64
+_lib.md_get_local_state.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), _P, _P, _P, _P, _P]
 _lib.allegro_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, _P, _P, _P]
 _lib.allegro_debug_gemm_bench.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                           C.c_int, C.c_int, C.POINTER(C.c_double)]
@@ -103,6 +104,7 @@ EXPORTED = [
     "allegro_layer_paths", "allegro_version", "md_step_host", "allegro_profile", "allegro_profile_read",
     "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name", "allegro_debug_gemm",
     "allegro_debug_gemm_bench", "allegro_nccl_unique_id", "allegro_local_count",
+    "md_get_local_state",
 ]
 
 
@@ -203,9 +205,9 @@ class Allegro:
         self.box = np.asarray(box, dtype=np.float64)
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.allegro_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         self.close()
@@ -256,6 +258,18 @@ class Allegro:
     def local_count(self) -> int:
         return int(_lib.allegro_local_count(self._h))
 
+    def md_get_local_state(self, capacity: int | None = None):
+        """This rank's owned atoms: (species, gid, pos, vel, forces) numpy arrays of length
+        `capacity` (default: the local count); the first n_local rows are valid."""
+        cap = self.local_count() if capacity is None else int(capacity)
+        spc = np.zeros(cap, dtype=np.int32)
+        gid = np.zeros(cap, dtype=np.int32)
+        pos, vel, frc = np.zeros((cap, 3)), np.zeros((cap, 3)), np.zeros((cap, 3))
+        n = C.c_int64(0)
+        self._check(_lib.md_get_local_state(self._h, cap, C.byref(n), spc.ctypes.data, gid.ctypes.data,
+                                            pos.ctypes.data, vel.ctypes.data, frc.ctypes.data))
+        return n.value, spc, gid, pos, vel, frc
+
     def md_get_state(self):
         pos = np.empty((self.n, 3))
         vel = np.empty((self.n, 3))
@@ -278,11 +292,13 @@ class Allegro:
         self._check(_lib.md_force_baseline(self._h, C.byref(m), C.byref(s)))
         return m.value, s.value
 
-    def md_step_host(self, species, pos, vel, forces, n_steps: int = 1, dt_fs: float = 2.0) -> MdReport:
+    def md_step_host(self, species, pos, vel, forces, n_steps: int = 1, dt_fs: float = 2.0,
+                     n_local: int | None = None) -> MdReport:
         """End-to-end step on HOST arrays (updated in place): H2D, n_steps, D2H.
         numpy or (pinned) torch CPU tensors."""
         r = MdReport()
-        self._check(_lib.md_step_host(self._h, int(pos.shape[0]), _ptr(species), _ptr(pos), _ptr(vel), _ptr(forces),
+        n = self.local_count() if n_local is None else int(n_local)
+        self._check(_lib.md_step_host(self._h, n, _ptr(species), _ptr(pos), _ptr(vel), _ptr(forces),
                                       n_steps, dt_fs, C.byref(r)))
         return r
 

@@ -2,6 +2,8 @@
 // host <-> device marshalling and error mapping only; every step of the method runs
 // in the kernels of neighbor.cu, model.cu and md.cu.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -59,12 +61,20 @@ void reserve_atoms(allegro_ctx* c, int64_t n) {
   c->e_atom.reserve(n + 1);
 }
 
+bool debug_on() {
+  static const bool on = std::getenv("ALLEGRO_DEBUG") != nullptr;
+  return on;
+}
+
 int evaluate(allegro_ctx* c) {
   ALG_CUDA(cudaMemsetAsync(c->flags.p, 0, 4 * sizeof(int), c->stream));
   wrap_positions(c);
   if (!check_inputs(c)) return fail(c, ALLEGRO_E_ARG, "non-finite position or species outside {0, 1}");
   build_neighbors(c);
   compute_forces(c);
+  if (debug_on())
+    std::fprintf(stderr, "[allegro rank %d] n=%lld ghosts=%lld edges=%lld e_pot=%.9g max_nb=%d\n", c->dom.rank,
+                 (long long)c->n, (long long)c->n_ghost, (long long)c->n_edges, c->e_pot, c->max_nb);
   if (!all_finite(c)) return fail(c, ALLEGRO_E_NONFINITE, "non-finite energy or force");
   return ALLEGRO_OK;
 }
@@ -182,6 +192,8 @@ int allegro_compute_energy_forces(allegro_ctx* c, int64_t n, int where, const in
   if (n < 0 || !species || !pos || !e_total || !forces) return fail(c, ALLEGRO_E_ARG, "NULL argument or n < 0");
   if (where != ALLEGRO_HOST && where != ALLEGRO_DEVICE) return fail(c, ALLEGRO_E_ARG, "where must be HOST or DEVICE");
   if (box && !box_ok(box)) return fail(c, ALLEGRO_E_ARG, "box must be three finite positive lengths");
+  if (c->dom.multi && !gid) return fail(c, ALLEGRO_E_ARG, "world_size > 1 needs the global ids of the owned atoms");
+  if (c->dom.multi && box) return fail(c, ALLEGRO_E_ARG, "the box is fixed at create when world_size > 1");
   return guarded(c, [&]() -> int {
     ALG_CUDA(cudaSetDevice(c->device));
     if (box)
@@ -221,16 +233,21 @@ int md_set_state(allegro_ctx* c, int64_t n, const int32_t* species, const double
   if (n <= 0 || !species || !pos || !vel) return fail(c, ALLEGRO_E_ARG, "NULL argument or n <= 0");
   return guarded(c, [&]() -> int {
     ALG_CUDA(cudaSetDevice(c->device));
-    c->n = n;
-    reserve_atoms(c, n);
-    ALG_CUDA(cudaMemcpyAsync(c->pos.p, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
-    ALG_CUDA(cudaMemcpyAsync(c->vel.p, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
-    ALG_CUDA(cudaMemcpyAsync(c->species.p, species, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
-    {
-      ProfScope ps_(&c->prof, c->stream, PK_WRAP, 0, 4.0 * n);
-      k_iota<<<ceil_div(n, 256), 256, 0, c->stream>>>(c->gid.p, n);
+    if (c->dom.multi) {
+      select_owned(c, n, species, pos, vel);  // this rank's domain, in gid order
+    } else {
+      c->n = n;
+      reserve_atoms(c, n);
+      ALG_CUDA(cudaMemcpyAsync(c->pos.p, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+      ALG_CUDA(cudaMemcpyAsync(c->vel.p, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+      ALG_CUDA(cudaMemcpyAsync(c->species.p, species, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+      {
+        ProfScope ps_(&c->prof, c->stream, PK_WRAP, 0, 4.0 * n);
+        k_iota<<<ceil_div(n, 256), 256, 0, c->stream>>>(c->gid.p, n);
+      }
+      ALG_LAUNCH_CHECK();
     }
-    ALG_LAUNCH_CHECK();
+    c->n_global = n;
     c->md_ready = false;
     const int rc = evaluate(c);
     if (rc != ALLEGRO_OK) return rc;
@@ -344,6 +361,25 @@ int allegro_nccl_unique_id(void* out128) {
 }
 
 int64_t allegro_local_count(const allegro_ctx* c) { return c ? c->n : -1; }
+
+int md_get_local_state(allegro_ctx* c, int64_t capacity, int64_t* n_local, int32_t* species, int32_t* gid, double* pos,
+                       double* vel, double* forces) {
+  if (!c || !n_local) return fail(c, ALLEGRO_E_ARG, "NULL argument");
+  if (!c->md_ready) return fail(c, ALLEGRO_E_STATE, "md_set_state has not been called");
+  *n_local = c->n;
+  if (capacity < c->n) return fail(c, ALLEGRO_E_ARG, "capacity too small");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    const int64_t n = c->n;
+    if (species) ALG_CUDA(cudaMemcpyAsync(species, c->species.p, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (gid) ALG_CUDA(cudaMemcpyAsync(gid, c->gid.p, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (pos) ALG_CUDA(cudaMemcpyAsync(pos, c->pos.p, 24 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (vel) ALG_CUDA(cudaMemcpyAsync(vel, c->vel.p, 24 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (forces) ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, 24 * n, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaStreamSynchronize(c->stream));
+    return ALLEGRO_OK;
+  });
+}
 
 int allegro_profile(allegro_ctx* c, int enable) {
   if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");

@@ -31,6 +31,15 @@ mine = np.nonzero(np.all(own == coord, axis=1))[0]
 e, ea, F = m.compute_energy_forces(pos[mine], s.species[mine], gid=mine.astype(np.int32))
 allF = [None] * ws
 dist.all_gather_object(allF, (mine, F, ea))
+if rank == 0:
+    ref0 = pb.Allegro(wf, s.box, device=local, precision=prec)
+    e1, ea1, F1 = ref0.compute_energy_forces(pos, s.species)
+    Fm = np.zeros_like(F1); Em = np.zeros_like(ea1)
+    for idx, Fr, er in allF:
+        Fm[idx] = Fr; Em[idx] = er
+    print("FORCE-EVAL", json.dumps({"dE": abs(e - e1), "E": e1, "max_dE_atom": float(np.abs(Em - ea1).max()),
+                                    "max_dF": float(np.abs(Fm - F1).max())}), flush=True)
+    ref0.close()
 # 2) MD: 5 steps
 m.md_set_state(s.species, s.pos, s.vel)
 rep = m.md_step(5, 2.0)

@@ -62,6 +62,7 @@ def weight_file(cfg: Config | str, directory: str | None = None, seed: int = 0, 
     os.makedirs(directory, exist_ok=True)
     tag = "cal" if sigma is None else f"sig{sigma:g}"
     path = os.path.join(directory, f"{weights.model_key(cfg.n_layers, cfg.lmax, cfg.r_cut, seed)}_{tag}.algw")
-    weights.make_weight_file(path + ".tmp", cfg.n_layers, cfg.lmax, cfg.r_cut, seed, sigma)
-    os.replace(path + ".tmp", path)
+    tmp = f"{path}.{os.getpid()}.tmp"  # per process: ranks may write concurrently
+    weights.make_weight_file(tmp, cfg.n_layers, cfg.lmax, cfg.r_cut, seed, sigma)
+    os.replace(tmp, path)
     return path
