@@ -1,0 +1,27 @@
+"""Multi-GPU equivalence (runs when >= 2 GPUs are visible): torchrun scripts/check_multigpu.py
+on 2 ranks; the spatially decomposed evaluation and 5 MD steps must equal one GPU
+(per-atom energies bit for bit, forces <= 1e-6 eV/A, identical edge counts)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def test_two_gpu_decomposition_equals_one_gpu():
+    import torch
+
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "scripts", "check_multigpu.py"), "C2"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-2000:]
+    res = json.loads(lines[-1])
+    assert res["ok"], res
+    assert res["max_dE_atom"] == 0.0
