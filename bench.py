@@ -108,7 +108,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": rec["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": _config_dict(cfg, args.gpus, None),
+        "config": _config_dict(cfg, args.gpus, None, "oracle"),
         "cpu_baseline": {"value": rec["value"], "unit": UNIT, "cores": rec["cores"], "kind": "oracle",
                          "sample": rec["sample"]},
         "e2e": {"value": rec["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -150,6 +150,7 @@ def _oracle_rate(cfg, sample, steps, warmup):
 GRIDS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
 
 PREC_TEXT = {
+    "oracle": "fp64 numpy oracle (oracle/allegro.py) on host cores",
     "3xtf32": "3xTF32 tcgen05 GEMMs (fp32-level accuracy) + fp32 TP (fp64 positions, Verlet, energy sums)",
     "fp32": "fp32 CUDA-core GEMMs + fp32 TP (fp64 positions, Verlet, energy sums)",
 }
