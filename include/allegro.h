@@ -122,7 +122,15 @@ typedef struct {
   int64_t n_outliers_last;                   /* outliers of the last step vs the step-0 baseline */
   int64_t n_edges, n_rebuilds;                /* edges summed over ranks */
   int64_t n_local;                           /* atoms this rank owns after the call */
+  double xi;                                 /* Nose-Hoover friction (1/fs); 0 under NVE */
+  double e_conserved;                        /* NVE: e_total; NVT: e_total + Q xi^2/2 + 3N k_B T eta */
 } md_report;
+
+/* NVT thermalisation (§3.2: 200 K NVT before NVE): one Nose-Hoover
+ * thermostat, Q = 3N k_B T tau^2, symmetric split around the Verlet core
+ * (D23).  tau_fs <= 0 switches back to NVE.  Takes effect for the following
+ * md_step calls; md_set_state resets xi and eta. */
+int md_set_thermostat(allegro_ctx* ctx, double T_target_K, double tau_fs);
 
 /* n_steps of velocity Verlet at dt (fs): exactly one
  * force evaluation per step, forces cached.  Stops at the first non-finite value and

@@ -60,6 +60,8 @@ class MdReport(C.Structure):
         ("n_edges", C.c_int64),
         ("n_rebuilds", C.c_int64),
         ("n_local", C.c_int64),
+        ("xi", C.c_double),
+        ("e_conserved", C.c_double),
     ]
 
 
@@ -92,6 +94,7 @@ _lib.allegro_profile_kind_name.restype = C.c_char_p
 _lib.allegro_nccl_unique_id.argtypes = [_P]
 _lib.allegro_local_count.argtypes = [_P]
 _lib.allegro_local_count.restype = C.c_int64
+_lib.md_set_thermostat.argtypes = [_P, C.c_double, C.c_double]
 _lib.md_get_local_state.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), _P, _P, _P, _P, _P]
 _lib.allegro_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, _P, _P, _P]
 _lib.allegro_debug_gemm_bench.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -104,7 +107,7 @@ EXPORTED = [
     "allegro_layer_paths", "allegro_version", "md_step_host", "allegro_profile", "allegro_profile_read",
     "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name", "allegro_debug_gemm",
     "allegro_debug_gemm_bench", "allegro_nccl_unique_id", "allegro_local_count",
-    "md_get_local_state",
+    "md_get_local_state", "md_set_thermostat",
 ]
 
 
@@ -281,6 +284,10 @@ class Allegro:
         r = MdReport()
         self._check(_lib.md_step(self._h, n_steps, dt_fs, C.byref(r)))
         return r
+
+    def md_set_thermostat(self, T_target: float = 200.0, tau_fs: float = 100.0):
+        """Nose-Hoover NVT at T_target (K) with time constant tau_fs; tau_fs <= 0 -> NVE."""
+        self._check(_lib.md_set_thermostat(self._h, T_target, tau_fs))
 
     def md_count_outliers(self, mean: float, sigma: float, k: float = 5.0) -> int:
         c = C.c_int64(0)

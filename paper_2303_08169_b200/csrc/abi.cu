@@ -253,6 +253,8 @@ int md_set_state(allegro_ctx* c, int64_t n, const int32_t* species, const double
     if (rc != ALLEGRO_OK) return rc;
     force_stats(c, &c->f_mean0, &c->f_sigma0);
     c->baseline_set = true;
+    c->nvt_xi = c->nvt_eta = 0.0;
+    if (c->nvt) c->nvt_Q = 3.0 * (double)c->n_global * 8.617333e-5 * c->nvt_T * c->nvt_tau * c->nvt_tau;
     c->md_ready = true;
     c->md_steps = 0;
     return ALLEGRO_OK;
@@ -277,17 +279,36 @@ int md_get_state(allegro_ctx* c, int64_t n, double* pos, double* vel, double* fo
   });
 }
 
+// Nose-Hoover thermostat over dt/2 (D23; same split as oracle/md.py nvt_half)
+static void nvt_half(allegro_ctx* c, double& K, double dt) {
+  const double g = 3.0 * (double)c->n_global, kT = 8.617333e-5 * c->nvt_T;
+  c->nvt_xi += 0.25 * dt * (2.0 * K - g * kT) / c->nvt_Q;
+  const double s = std::exp(-c->nvt_xi * 0.5 * dt);
+  md_scale_velocities(c, s);
+  K *= s * s;
+  c->nvt_eta += c->nvt_xi * 0.5 * dt;
+  c->nvt_xi += 0.25 * dt * (2.0 * K - g * kT) / c->nvt_Q;
+}
+
 static int md_run(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
   {
     int rc = ALLEGRO_OK;
     int64_t done = 0;
     for (; done < n_steps; ++done) {
+      if (c->nvt) {
+        double K = md_kinetic(c);
+        nvt_half(c, K, dt);
+      }
       md_half_kick_drift(c, dt);
       if (c->dom.multi) migrate(c);
       ALG_CUDA(cudaMemsetAsync(c->flags.p, 0, 4 * sizeof(int), c->stream));
       build_neighbors(c);
       compute_forces(c);
       md_half_kick(c, dt);
+      if (c->nvt) {
+        double K = md_kinetic(c);
+        nvt_half(c, K, dt);
+      }
       if (!all_finite(c)) {
         rc = fail(c, ALLEGRO_E_NONFINITE, "non-finite energy, force or velocity at step " + std::to_string(c->md_steps + 1));
         ++done;
@@ -302,6 +323,11 @@ static int md_run(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
       out->e_pot = c->e_pot;
       out->e_kin = md_kinetic(c);
       out->e_total = out->e_pot + out->e_kin;
+      out->xi = c->nvt ? c->nvt_xi : 0.0;
+      out->e_conserved = out->e_total;
+      if (c->nvt)
+        out->e_conserved += 0.5 * c->nvt_Q * c->nvt_xi * c->nvt_xi +
+                            3.0 * (double)c->n_global * 8.617333e-5 * c->nvt_T * c->nvt_eta;
       out->temperature = 2.0 * out->e_kin / (3.0 * (double)c->n_global * 8.617333e-5);
       out->n_outliers_last = count_outliers(c, c->f_mean0 + 5.0 * c->f_sigma0);
       out->n_edges = allreduce_sum_i64(c, c->n_edges);
@@ -348,6 +374,18 @@ int md_step_host(allegro_ctx* c, int64_t n, const int32_t* species, double* pos,
     ALG_CUDA(cudaStreamSynchronize(c->stream));
     return rc;
   });
+}
+
+int md_set_thermostat(allegro_ctx* c, double T_target, double tau_fs) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (!(std::isfinite(T_target) && std::isfinite(tau_fs)) || (tau_fs > 0 && T_target <= 0))
+    return fail(c, ALLEGRO_E_ARG, "bad thermostat parameters");
+  c->nvt = tau_fs > 0;
+  c->nvt_T = T_target;
+  c->nvt_tau = tau_fs;
+  c->nvt_xi = c->nvt_eta = 0.0;
+  c->nvt_Q = c->nvt ? 3.0 * (double)c->n_global * 8.617333e-5 * T_target * tau_fs * tau_fs : 0.0;
+  return ALLEGRO_OK;
 }
 
 int allegro_nccl_unique_id(void* out128) {

@@ -169,6 +169,9 @@ struct allegro_ctx {
   int64_t md_steps = 0, n_rebuilds = 0;
   double e_pot = 0;
   double f_mean0 = 0, f_sigma0 = 0;  // step-0 outlier baseline
+  // Nose-Hoover NVT (one thermostat; D23): off when tau <= 0
+  bool nvt = false;
+  double nvt_T = 0, nvt_tau = 0, nvt_Q = 0, nvt_xi = 0, nvt_eta = 0;
   bool baseline_set = false;
   allegro::Profiler prof;
   allegro::Domain dom;
@@ -206,6 +209,7 @@ constexpr double kFixScale = 4294967296.0;  // 2^32: fixed-point ghost forces (e
 // md.cu
 void md_half_kick_drift(allegro_ctx* c, double dt);
 void md_half_kick(allegro_ctx* c, double dt);
+void md_scale_velocities(allegro_ctx* c, double s);
 double md_kinetic(allegro_ctx* c);
 void force_stats(allegro_ctx* c, double* mean, double* sigma);
 int64_t count_outliers(allegro_ctx* c, double thr);

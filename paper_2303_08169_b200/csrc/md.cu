@@ -44,6 +44,11 @@ __global__ void k_kick(double* __restrict__ vel, const double* __restrict__ frc,
   for (int d = 0; d < 3; ++d) vel[a * 3 + d] += 0.5 * dt * kKappa * frc[a * 3 + d] / m;
 }
 
+__global__ void k_scale(double* __restrict__ vel, int64_t n3, double s) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a < n3) vel[a] *= s;
+}
+
 // Single-block fixed-order reduction of f(a) over a < n (deterministic).
 template <typename F>
 __device__ void block_reduce_sum(int64_t n, F f, double* out) {
@@ -129,6 +134,15 @@ void md_half_kick(allegro_ctx* c, double dt) {
   {
     ProfScope ps_(&c->prof, c->stream, PK_VERLET, 0, 76.0 * c->n);
     k_kick<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->vel.p, c->frc.p, c->species.p, c->n, dt);
+  }
+  ALG_LAUNCH_CHECK();
+}
+
+void md_scale_velocities(allegro_ctx* c, double s) {
+  if (c->n == 0) return;
+  {
+    ProfScope ps_(&c->prof, c->stream, PK_VERLET, 0, 48.0 * c->n);
+    k_scale<<<ceil_div(3 * c->n, 256), 256, 0, c->stream>>>(c->vel.p, 3 * c->n, s);
   }
   ALG_LAUNCH_CHECK();
 }

@@ -1,0 +1,63 @@
+"""C2 (BASELINE configs[1]): liquid NH3, 1,024 atoms, 2-layer lmax=2 Allegro; the paper's
+protocol: NVT at 200 K, then NVE at dt = 2 fs -- here 1,000 + 1,000 steps
+on one B200.  Logs E_pot, E_kin, T, the 5-sigma outlier count (vs the step-0 baseline) and the
+edge count every 10 steps, and checks snapshot parity against the fp64 oracle at NVE steps
+0, 500, 1000 (per evaluation: trajectories are chaotic, reading D21)."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+import paper_2303_08169_b200 as pb
+from oracle import allegro as oa, weights_io
+from synth import configs
+
+n_nvt = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
+n_nve = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
+tau = float(sys.argv[3]) if len(sys.argv) > 3 else 50.0
+out_dir = sys.argv[4] if len(sys.argv) > 4 else "gpurun_out"
+s = configs.system("C2")
+wf = configs.weight_file("C2")
+model = weights_io.read(wf)
+m = pb.Allegro(wf, s.box, precision=pb.PREC_3XTF32)
+m.md_set_thermostat(200.0, tau)
+m.md_set_state(s.species, s.pos, s.vel)
+mean0, sig0 = m.md_force_baseline()
+log = []
+t0 = time.time()
+for phase, n in (("nvt", n_nvt), ("nve", n_nve)):
+    if phase == "nve":
+        m.md_set_thermostat(200.0, 0.0)
+    snaps = {}
+    for step in range(0, n + 1, 10):
+        if phase == "nve" and step in (0, n // 2, n):
+            snaps[step] = m.md_get_state()
+        if step == n:
+            break
+        r = m.md_step(10, 2.0)
+        log.append(dict(phase=phase, step=step + 10, e_pot=r.e_pot, e_kin=r.e_kin, T=r.temperature,
+                        e_conserved=r.e_conserved, xi=r.xi, n_out=m.md_count_outliers(mean0, sig0, 5.0),
+                        edges=r.n_edges))
+wall = time.time() - t0
+parity = {}
+for step, (p, v, f) in snaps.items():
+    ref = oa.energy_forces(model, p, s.species, s.box)
+    parity[step] = float(np.abs(f - ref["forces"]).max())
+os.makedirs(out_dir, exist_ok=True)
+with open(os.path.join(out_dir, "c2_md_log.json"), "w") as fh:
+    json.dump(log, fh)
+nvt = [x for x in log if x["phase"] == "nvt"]
+nve = [x for x in log if x["phase"] == "nve"]
+summary = dict(
+    steps=dict(nvt=n_nvt, nve=n_nve), tau_fs=tau, wall_s=round(wall, 2),
+    ms_per_step=round(1e3 * wall / max(1, n_nvt + n_nve), 3),
+    T_nvt_last100=float(np.mean([x["T"] for x in nvt[-10:]])) if nvt else None,
+    T_nve_first=nve[0]["T"] if nve else None, T_nve_last=nve[-1]["T"] if nve else None,
+    nve_drift_per_atom_eV=(nve[-1]["e_pot"] + nve[-1]["e_kin"] - nve[0]["e_pot"] - nve[0]["e_kin"]) / s.n if nve else None,
+    nvt_conserved_drift_per_atom_eV=(nvt[-1]["e_conserved"] - nvt[0]["e_conserved"]) / s.n if nvt else None,
+    n_out_max=max(x["n_out"] for x in log), edges_first=log[0]["edges"], edges_last=log[-1]["edges"],
+    snapshot_max_dF=parity, parity_ok=all(v <= 1e-4 for v in parity.values()))
+print(json.dumps(summary), flush=True)

@@ -278,3 +278,26 @@ def test_profiler_counts_launches(pb):
     assert m.launch_count() == sum(v[3] for v in prof.values()) > 20
     assert prof["gemm"][3] > 0 and prof["gemm"][0] > 0 and prof["gemm"][1] > 0
     assert prof["tp_fwd"][3] == prof["tp_bwd"][3] == 2 * 2  # 2 layers x 2 steps
+
+
+def test_nvt_step_matches_oracle(pb):
+    """Nose-Hoover NVT (NEXT-1): 3 GPU steps vs the oracle's nvt_verlet from the
+    same state (bounded by the force tolerance), and the extended energy is conserved."""
+    s = nh3.maxwell_boltzmann(nh3.nh3_box("fcc", (1, 1, 1)), 300.0)
+    wf = configs.weight_file("C1")
+    model = weights_io.read(wf)
+    m = pb.Allegro(wf, s.box, precision=pb.PREC_3XTF32)
+    m.md_set_state(s.species, s.pos, s.vel)
+    m.md_set_thermostat(200.0, 20.0)
+    m.md_set_state(s.species, s.pos, s.vel)  # Q uses the state size
+    reps = [m.md_step(1, 1.0) for _ in range(3)]
+    p, v, f = m.md_get_state()
+    fn = lambda q: (lambda r: (r["energy"], r["forces"]))(oa.energy_forces(model, q, s.species, s.box))
+    po, vo, fo, xi, eta, lg = omd.nvt_verlet(fn, s.pos, s.vel, s.species, s.box, 1.0, 3, 200.0, 20.0)
+    dp = p - po
+    dp -= s.box * np.round(dp / s.box)
+    assert np.abs(dp).max() < 1e-6 and np.abs(v - vo).max() < 1e-5
+    assert abs(reps[-1].xi - xi) < 1e-6 * max(1.0, abs(xi))
+    assert abs(reps[-1].e_conserved - lg[-1][2]) < 1e-3
+    h = [r.e_conserved for r in reps]
+    assert max(h) - min(h) < 1e-2

@@ -92,3 +92,41 @@ def test_model_nve_time_reversal_momentum_and_dt2(c1_model):
         return e.max() - e.min()
     r = fluct(1.0) / fluct(0.5)
     assert 3.0 < r < 5.0
+
+
+def test_nvt_reduces_to_nve_for_infinite_q(c1_model):
+    s = nh3.maxwell_boltzmann(nh3.nh3_box("fcc", (1, 1, 1)), 200.0)
+    fn = lambda p: (lambda r: (r["energy"], r["forces"]))(allegro.energy_forces(c1_model, p, s.species, s.box))
+    p1, v1, _, _ = md.verlet(fn, s.pos, s.vel, s.species, s.box, 1.0, 3)
+    p2, v2, _, xi, eta, _ = md.nvt_verlet(fn, s.pos, s.vel, s.species, s.box, 1.0, 3, 200.0, 1e12)
+    np.testing.assert_allclose(p2, p1, atol=1e-12)
+    np.testing.assert_allclose(v2, v1, atol=1e-12)
+    assert abs(xi) < 1e-20
+
+
+def test_nvt_fixed_point_first_quarter():
+    # K exactly at g k_B T / 2 and xi = 0: the thermostat quarter-kick leaves xi = 0
+    species = np.array([0, 1, 1])
+    v = np.random.default_rng(0).standard_normal((3, 3))
+    K = md.kinetic_energy(v, species)
+    T = 2 * K / (3 * 3 * md.KB)
+    g = 9
+    Q = g * md.KB * T * 50.0**2
+    vel, K2, xi, eta = md.nvt_half(v, species, K, 0.0, 0.0, 1.0, T, Q)
+    assert xi == 0.0 and eta == 0.0 and np.array_equal(vel, v)
+
+
+def test_nvt_conserved_quantity_dt2_and_thermalisation(c1_model):
+    s = nh3.maxwell_boltzmann(nh3.nh3_box("fcc", (1, 1, 1)), 300.0)  # start hot, target 200 K
+    fn = lambda p: (lambda r: (r["energy"], r["forces"]))(allegro.energy_forces(c1_model, p, s.species, s.box))
+
+    def drift(dt):
+        _, _, _, _, _, lg = md.nvt_verlet(fn, s.pos, s.vel, s.species, s.box, dt, int(6 / dt), 200.0, 20.0)
+        h = np.array([c for _, _, c in lg])
+        return h.max() - h.min(), lg
+
+    d1, lg = drift(1.0)
+    d2, _ = drift(0.5)
+    assert 3.0 < d1 / d2 < 5.0  # extended energy conserved to O(dt^2)
+    # the thermostat removes kinetic energy from the 300 K start
+    assert lg[-1][1] < md.kinetic_energy(s.vel, s.species)
