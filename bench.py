@@ -236,6 +236,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     launches = m.launch_count()
     prof = m.profile_read()
+    detail = sorted(m.profile_detail(), key=lambda x: -x[1])
     m.profile(False)
     clk = clocks.stop()
     t = torch.tensor([ms], device="cuda")
@@ -326,6 +327,8 @@ def main():
         "roofline": roof,
         "kernels": kernels,
         "gpu_launches": launches,
+        "shapes": [{"tag": t, "ms_per_step": round(ms_ / args.steps, 3), "gbs": round(by / max(ms_, 1e-9) / 1e6, 1),
+                    "launches_per_step": n_ / args.steps} for t, ms_, by, n_ in detail[:24]],
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "clocks": clk,
         "md": {"e_pot": rep.e_pot, "e_kin": rep.e_kin, "temperature": rep.temperature,

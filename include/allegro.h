@@ -181,6 +181,9 @@ int allegro_profile(allegro_ctx* ctx, int enable);
 int allegro_profile_read(allegro_ctx* ctx, int kind, double* time_ms, double* flops, double* bytes,
                          int64_t* launches);
 int64_t allegro_launch_count(allegro_ctx* ctx); /* launches since the last allegro_profile() */
+/* per-shape detail entry idx (0..): name, time, algorithmic bytes, launches; ALLEGRO_E_ARG past the end */
+int allegro_profile_detail(allegro_ctx* ctx, int idx, char* name, int name_cap, double* time_ms, double* bytes,
+                           int64_t* launches);
 
 /* Test hook: one GEMM C[M][N] = A[M][K] W[K][N] (row-major fp32 HOST arrays) on device
  * `device` with the given ALLEGRO_PREC_* contraction kernel (CUDA-core or tcgen05). */

@@ -94,6 +94,7 @@ _lib.allegro_profile_kind_name.restype = C.c_char_p
 _lib.allegro_nccl_unique_id.argtypes = [_P]
 _lib.allegro_local_count.argtypes = [_P]
 _lib.allegro_local_count.restype = C.c_int64
+_lib.allegro_profile_detail.argtypes = [_P, C.c_int, _P, C.c_int, _P, _P, _P]
 _lib.md_set_thermostat.argtypes = [_P, C.c_double, C.c_double]
 _lib.md_get_local_state.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), _P, _P, _P, _P, _P]
 _lib.allegro_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, _P, _P, _P]
@@ -108,6 +109,7 @@ EXPORTED = [
     "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name", "allegro_debug_gemm",
     "allegro_debug_gemm_bench", "allegro_nccl_unique_id", "allegro_local_count",
     "md_get_local_state", "md_set_thermostat",
+    "allegro_profile_detail",
 ]
 
 
@@ -320,6 +322,19 @@ class Allegro:
             ms, fl, by, n = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
             self._check(_lib.allegro_profile_read(self._h, k, C.byref(ms), C.byref(fl), C.byref(by), C.byref(n)))
             out[_lib.allegro_profile_kind_name(k).decode()] = (ms.value, fl.value, by.value, n.value)
+        return out
+
+    def profile_detail(self):
+        """[(shape tag, time_ms, algorithmic bytes, launches)] of tagged launches."""
+        out = []
+        k = 0
+        while True:
+            name = C.create_string_buffer(128)
+            ms, by, n = C.c_double(), C.c_double(), C.c_int64()
+            if _lib.allegro_profile_detail(self._h, k, name, 128, C.byref(ms), C.byref(by), C.byref(n)) != OK:
+                break
+            out.append((name.value.decode(), ms.value, by.value, n.value))
+            k += 1
         return out
 
     def launch_count(self) -> int:

@@ -442,6 +442,18 @@ int allegro_profile_read(allegro_ctx* c, int kind, double* ms, double* flops, do
 
 int64_t allegro_launch_count(allegro_ctx* c) { return c ? c->prof.launches : -1; }
 
+int allegro_profile_detail(allegro_ctx* c, int idx, char* name, int name_cap, double* time_ms, double* bytes,
+                           int64_t* launches) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  c->prof.flush();
+  if (idx < 0 || idx >= (int)c->prof.tags.size()) return ALLEGRO_E_ARG;
+  if (name && name_cap > 0) std::snprintf(name, name_cap, "%s", c->prof.tags[idx].c_str());
+  if (time_ms) *time_ms = c->prof.tag_ms[idx];
+  if (bytes) *bytes = c->prof.tag_bytes[idx];
+  if (launches) *launches = c->prof.tag_n[idx];
+  return ALLEGRO_OK;
+}
+
 int allegro_profile_kinds(void) { return PK_COUNT; }
 
 const char* allegro_profile_kind_name(int kind) { return prof_name(kind); }

@@ -19,6 +19,7 @@
 //   A12 k_force       F_a = sum_{e in row a} (g_e - g_rev(e)) in row order (fp64)
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 
 #include "ctx.cuh"
 #include "gemm.cuh"
@@ -459,7 +460,9 @@ void launch_tp(bool fwd, const TpArgs& t, cudaStream_t st, Profiler* prof, doubl
   const unsigned blocks = (unsigned)((t.ch.n_c * 32 + 127) / 128);
   if (blocks == 0) return;
   {
-    ProfScope ps_(prof, st, fwd ? PK_TP_FWD : PK_TP_BWD, flops, bytes);
+    char tag[48];
+    std::snprintf(tag, sizeof(tag), "tp_%s layer=%d", fwd ? "fwd" : "bwd", K);
+    ProfScope ps_(prof, st, fwd ? PK_TP_FWD : PK_TP_BWD, flops, bytes, tag);
     if (fwd) k_tp_fwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
     else k_tp_bwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
   }

@@ -6,6 +6,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
+#include <string>
 #include <vector>
 
 namespace allegro {
@@ -45,7 +47,22 @@ struct Profiler {
     int kind;
     cudaEvent_t a, b;
     double flops, bytes;
+    int tag;  // index into tags (-1: none)
   };
+  // optional per-shape detail (e.g. "gemm N=128 K=192 epi=3 M=..."): time, bytes, launches
+  std::vector<std::string> tags;
+  std::map<std::string, int> tag_id;
+  std::vector<double> tag_ms, tag_bytes;
+  std::vector<long long> tag_n;
+  int tag_of(const std::string& t) {
+    auto it = tag_id.find(t);
+    if (it != tag_id.end()) return it->second;
+    const int id = (int)tags.size();
+    tags.push_back(t);
+    tag_id[t] = id;
+    tag_ms.push_back(0), tag_bytes.push_back(0), tag_n.push_back(0);
+    return id;
+  }
   std::vector<Rec> pending;
   std::vector<cudaEvent_t> pool;
 
@@ -63,6 +80,7 @@ struct Profiler {
     flush();
     launches = 0;
     for (int k = 0; k < PK_COUNT; ++k) ms[k] = flops[k] = bytes[k] = 0, count[k] = 0;
+    tags.clear(), tag_id.clear(), tag_ms.clear(), tag_bytes.clear(), tag_n.clear();
   }
   // accumulate completed records (call after a stream synchronisation)
   void flush() {
@@ -74,6 +92,7 @@ struct Profiler {
       flops[r.kind] += r.flops;
       bytes[r.kind] += r.bytes;
       count[r.kind] += 1;
+      if (r.tag >= 0) tag_ms[r.tag] += t, tag_bytes[r.tag] += r.bytes, tag_n[r.tag] += 1;
       pool.push_back(r.a);
       pool.push_back(r.b);
     }
@@ -89,11 +108,12 @@ struct Profiler {
 struct ProfScope {
   Profiler* p;
   cudaStream_t st;
-  ProfScope(Profiler* prof, cudaStream_t s, int kind, double flops = 0, double bytes = 0) : p(prof), st(s) {
+  ProfScope(Profiler* prof, cudaStream_t s, int kind, double flops = 0, double bytes = 0, const char* tag = nullptr)
+      : p(prof), st(s) {
     if (!p) return;
     ++p->launches;
     if (p->on) {
-      Profiler::Rec r{kind, p->ev(), p->ev(), flops, bytes};
+      Profiler::Rec r{kind, p->ev(), p->ev(), flops, bytes, tag ? p->tag_of(tag) : -1};
       cudaEventRecord(r.a, st);
       p->pending.push_back(r);
     }

@@ -13,11 +13,14 @@
 //               into one of two TMEM accumulators [128 lanes x N_t fp32 columns];
 //               tcgen05.commit frees the TMEM A stage / publishes the accumulator.
 //   warps 4-7   epilogue warpgroup: tcgen05.ld 32x32b (thread = row), fused epilogue, and a
-//               per-warp swizzled SMEM transpose so global loads/stores are 4 x 128 B lines.
+//               per-warp swizzled SMEM transpose so global stores are 4 x 128 B lines.
+//   warp 10     epilogue-input producer: the residual / accumulate input (X or old C) is
+//               streamed by TMA in [128 x 32] boxes into a 2-deep SMEM ring ahead of the epilogue.
 // W SMEM descriptors: K-major, SWIZZLE_128B, SBO = 1024 B, version 1 (sm_100).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -26,7 +29,7 @@
 namespace allegro {
 namespace {
 
-constexpr int TC_THREADS = 320;              // 10 warps
+constexpr int TC_THREADS = 352;              // 11 warps
 constexpr int BLK_K = 32;                    // fp32 per 128-byte K-block
 constexpr int ROWS = 128;                    // UMMA M
 constexpr int A_BLOCK_BYTES = ROWS * 128;    // 16 KB raw A K-block (TMA, SWIZZLE_128B)
@@ -35,6 +38,8 @@ constexpr int A_TMEM_COLS = 64;              // one TMEM A stage: hi (32 cols) +
 constexpr size_t SMEM_LIMIT = 227 * 1024;
 constexpr size_t SMEM_RESERVE = 2048;        // barriers + alignment slack
 constexpr int STAGE_OUT_BYTES = 32 * 128;    // per epilogue warp: [32 rows x 32 fp32] transpose tile
+constexpr int X_STAGES = 2;                  // epilogue input ring: [128 rows x 32 fp32] TMA boxes
+constexpr int X_STAGE_BYTES = ROWS * 128;
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -161,6 +166,7 @@ struct TcParams {
   int acc_cols;        // TMEM columns per accumulator (>= N_t, multiple of 32)
   uint32_t tmem_cols;  // allocated TMEM columns
   int diag;            // diagnostics: bit0 skip MMAs, bit1 skip global stores
+  int has_x;           // the epilogue reads an [M][N] input (X, or old C) through the TMA ring
 };
 
 // v <- s v (the saved pre-activation "aux"); out <- epilogue(v, xin) (xin = X, or old C for EPI_ACC)
@@ -231,7 +237,8 @@ __device__ __forceinline__ void scatter_rows(unsigned char* buf, float* dst, int
 
 template <int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    k_tc_gemm(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2, TcParams p) {
+    k_tc_gemm(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
+              const __grid_constant__ CUtensorMap mapX, TcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   // 1024-align inside the __shared__ array (pointer arithmetic keeps the shared address space)
   unsigned char* base = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
@@ -239,7 +246,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   unsigned char* w_lo = base + p.w_bytes / 2;
   unsigned char* stage0 = base + ((p.w_bytes + 1023) & ~1023u);
   unsigned char* out_stage = stage0 + (size_t)p.stages * STAGE_BYTES;  // [4 warps][4 KB]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(out_stage + 4 * STAGE_OUT_BYTES);
+  unsigned char* x_stage = out_stage + 4 * STAGE_OUT_BYTES;            // [X_STAGES][16 KB] (if has_x)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(x_stage + (p.has_x ? X_STAGES * X_STAGE_BYTES : 0));
   uint64_t* raw_full = bars;                          // [stages]  TMA landed
   uint64_t* raw_empty = raw_full + p.stages;          // [stages]  split warps read it
   uint64_t* a_full = raw_empty + p.stages;            // [a_stages] hi/lo in TMEM
@@ -247,7 +255,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* acc_full = a_empty + p.a_stages;          // [2]
   uint64_t* acc_empty = acc_full + 2;                 // [2]
   uint64_t* w_full = acc_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
+  uint64_t* x_full = w_full + 1;                      // [X_STAGES]
+  uint64_t* x_empty = x_full + X_STAGES;              // [X_STAGES]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + X_STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -264,6 +274,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(acc_empty + a, 4);
     }
     mbar_init(w_full, 1);
+    for (int s2 = 0; s2 < X_STAGES; ++s2) {
+      mbar_init(x_full + s2, 1);
+      mbar_init(x_empty + s2, 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 9) tmem_alloc(tmem_slot, p.tmem_cols);
@@ -295,6 +309,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (kb < p.nK1) tma_load_2d(dst, &mapA, kb * BLK_K, m0, raw_full + s);
           else tma_load_2d(dst, &mapA2, (kb - p.nK1) * BLK_K, m0, raw_full + s);
           if (++s == p.stages) s = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 10) {
+    // ---------------- epilogue-input producer: X (or old C) [128 x 32] boxes by TMA ----------------
+    if (lane == 0 && p.has_x) {
+      int s2 = 0;
+      uint32_t ph = 0;
+      for (int t = 0; t < n_my; ++t) {
+        const int m0 = ((int)blockIdx.x + t * (int)gridDim.x) * ROWS;
+        for (int c0 = 0; c0 < p.N_t; c0 += 32) {
+          mbar_wait(x_empty + s2, ph ^ 1);
+          mbar_expect_tx(x_full + s2, X_STAGE_BYTES);
+          tma_load_2d(x_stage + (size_t)s2 * X_STAGE_BYTES, &mapX, p.col0 + c0, m0, x_full + s2);
+          if (++s2 == X_STAGES) s2 = 0, ph ^= 1;
         }
       }
     }
@@ -379,21 +408,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const bool want_aux = kAuxEpi && g.aux != nullptr;
     unsigned char* buf = out_stage + (size_t)q * STAGE_OUT_BYTES;
     constexpr bool kIn = kX || EPI == EPI_ACC;  // epilogue reads a [M][N] input (X or old C)
-    const float* in_ptr = kX ? g.X : g.C;
-    float4 xn[8];  // prefetched input chunk (coalesced layout: rows lane/8 + 4i, chunk lane%8)
-    auto issue = [&](int64_t row0, int c0) {
-      const int nc = (p.N_t - c0) >= 32 ? 8 : (p.N_t - c0) / 4;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int rr = (lane >> 3) + 4 * i, cc = lane & 7;
-        xn[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (row0 + rr < g.M && cc < nc)
-          xn[i] = __ldg(reinterpret_cast<const float4*>(in_ptr + (row0 + rr) * g.N + p.col0 + c0 + 4 * cc));
-      }
-    };
-    if constexpr (kIn) {
-      if (n_my > 0) issue((int64_t)blockIdx.x * ROWS + q * 32, 0);
-    }
+    int xs = 0;
+    uint32_t xph = 0;
     for (int t = 0; t < n_my; ++t) {
       const int a = t & 1;
       const uint32_t acph = (t >> 1) & 1;
@@ -406,18 +422,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int c0 = 0; c0 < p.N_t; c0 += 32) {
         float v[32], out[32], xin[32];
         if constexpr (kIn) {
-          // transpose the prefetched chunk into thread-row registers, then prefetch the next one
-#pragma unroll
-          for (int i = 0; i < 8; ++i) *tile_at(buf, (lane >> 3) + 4 * i, lane & 7) = xn[i];
-          __syncwarp();
+          // this thread's row of the TMA-loaded [128 x 32] input box (SWIZZLE_128B)
+          mbar_wait(x_full + xs, xph);
+          const unsigned char* xb = x_stage + (size_t)xs * X_STAGE_BYTES;
+          const int row = q * 32 + lane;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const float4 w4 = *tile_at(buf, lane, c);
+            const float4 w4 = *reinterpret_cast<const float4*>(xb + row * 128 + ((c ^ (row & 7)) << 4));
             xin[4 * c] = w4.x, xin[4 * c + 1] = w4.y, xin[4 * c + 2] = w4.z, xin[4 * c + 3] = w4.w;
           }
           __syncwarp();
-          if (c0 + 32 < p.N_t) issue(row0, c0 + 32);
-          else if (t + 1 < n_my) issue(row0 + (int64_t)gridDim.x * ROWS, 0);
+          if (lane == 0) mbar_arrive(x_empty + xs);
+          if (++xs == X_STAGES) xs = 0, xph ^= 1;
         }
         tmem_ld32(tbase + (uint32_t)c0, v);
         if (p.diag & 2) continue;
@@ -489,7 +505,8 @@ TcWeight tc_prepare_weight(const std::vector<float>& W, int K, int N, std::vecto
   t.N = N;
   const int nK = (K + BLK_K - 1) / BLK_K;
   // widest N-tile (multiple of 16 dividing N) whose image leaves room for >= 2 stages
-  const size_t budget = SMEM_LIMIT - SMEM_RESERVE - 3 * (size_t)STAGE_BYTES - 4 * (size_t)STAGE_OUT_BYTES;
+  const size_t budget = SMEM_LIMIT - SMEM_RESERVE - 2 * (size_t)STAGE_BYTES - 4 * (size_t)STAGE_OUT_BYTES -
+                        (size_t)X_STAGES * X_STAGE_BYTES;
   int nt = 0;
   for (int c = std::min(N, 256); c >= 16; c -= 16)
     if (N % c == 0 && (size_t)2 * nK * c * 128 <= budget) {
@@ -537,7 +554,9 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const CUtensorMap mA2 = g.A2 ? make_map(g.A2, g.M, g.K - g.K1, g.lda2) : mA;
   const size_t w_bytes = w.tile_bytes;
   const size_t w_round = (w_bytes + 1023) & ~(size_t)1023;
-  const size_t out_bytes = 4 * (size_t)STAGE_OUT_BYTES;
+  const bool has_x = g.epi == EPI_RESID || g.epi == EPI_URESID || g.epi == EPI_ADDX || g.epi == EPI_DSILU ||
+                     g.epi == EPI_ACC;
+  const size_t out_bytes = 4 * (size_t)STAGE_OUT_BYTES + (has_x ? (size_t)X_STAGES * X_STAGE_BYTES : 0);
   int stages = (int)((SMEM_LIMIT - SMEM_RESERVE - w_round - out_bytes) / STAGE_BYTES);
   stages = std::min(stages, g_tc_tuning.max_stages);
   if (stages < 2) throw CudaError("tc_gemm: shared memory too small for 2 stages");
@@ -567,17 +586,22 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   while (cols < (uint32_t)(2 * p.acc_cols + a_st * A_TMEM_COLS)) cols <<= 1;
   p.tmem_cols = cols;
   p.diag = g_tc_tuning.diag;
+  p.has_x = has_x ? 1 : 0;
+  const float* xsrc = g.epi == EPI_ACC ? g.C : g.X;
+  const CUtensorMap mX = has_x ? make_map(xsrc, g.M, g.N, g.N) : mA;
   const int grid = std::min(p.n_mtiles, g_num_sms);
   const double mn = (double)g.M * g.N;
   const int n_io = 1 + (g.aux != nullptr) + (g.X != nullptr) + (g.epi == EPI_ACC);
   for (int tile = 0; tile < w.n_tiles; ++tile) {
     p.col0 = tile * w.N_t;
     p.wimg = w.dev + tile * (w.tile_bytes / 4);
+    char tag[96];
+    std::snprintf(tag, sizeof(tag), "tc N=%d K=%d epi=%d A2=%d Nt=%d", g.N, g.K, g.epi, g.A2 ? 1 : 0, w.N_t);
     ProfScope ps(prof, st, PK_GEMM, 2.0 * mn * g.K / w.n_tiles,
-                 4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * n_io) / w.n_tiles);
+                 4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * n_io) / w.n_tiles, tag);
     switch (g.epi) {
 #define ALG_EPI(e) \
-  case e: k_tc_gemm<e><<<grid, TC_THREADS, smem, st>>>(mA, mA2, p); break;
+  case e: k_tc_gemm<e><<<grid, TC_THREADS, smem, st>>>(mA, mA2, mX, p); break;
       ALG_EPI(EPI_STORE) ALG_EPI(EPI_SILU) ALG_EPI(EPI_UMUL_SAVE) ALG_EPI(EPI_RESID) ALG_EPI(EPI_URESID)
       ALG_EPI(EPI_USCALE) ALG_EPI(EPI_ACC) ALG_EPI(EPI_ADDX) ALG_EPI(EPI_DSILU)
 #undef ALG_EPI
