@@ -281,16 +281,18 @@ __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
         we[l] = t.w[e * AR::NW + l * kC + lane];
         wb[l] = 0.f;
       }
-      float yb_mine = 0.f;
+      float prod[AR::DSH];
 #pragma unroll
       for (int m = 0; m < AR::DSH; ++m) {
         wb[lm_l(m)] = fmaf(vb[m], y[m], wb[lm_l(m)]);
-        const float s = warp_sum(vb[m] * we[lm_l(m)]);
-        if (lane == m) yb_mine = s;
+        prod[m] = vb[m] * we[lm_l(m)];
       }
+      int mm;
+      const float s = warp_sum_multi<AR::DSH>(prod, lane, &mm);
 #pragma unroll
       for (int l = 0; l < AR::NENV; ++l) t.wbar[e * AR::NW + l * kC + lane] = wb[l];
-      if (lane < AR::DSH) t.ybar[e * AR::DSH + lane] += yb_mine;
+      if (mm < AR::DSH && (lane & ((1 << (5 - (AR::DSH <= 1 ? 0 : AR::DSH <= 2 ? 1 : AR::DSH <= 4 ? 2 : AR::DSH <= 8 ? 3 : 4))) - 1)) == 0)
+        t.ybar[e * AR::DSH + mm] += s;
     } else {
       static_for<AR::A.in.n>([&](auto I) {
         constexpr int ii2 = decltype(I)::value;
@@ -313,16 +315,18 @@ __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
       we[l] = t.w[e * AR::NW + AR::ENV_OFF + l * kC + lane];
       wb[l] = 0.f;
     }
-    float yb_mine = 0.f;
+    float prod[AR::DSH];
 #pragma unroll
     for (int m = 0; m < AR::DSH; ++m) {
       wb[lm_l(m)] = fmaf(Gb[m], y[m], wb[lm_l(m)]);
-      const float s = warp_sum(Gb[m] * we[lm_l(m)]);
-      if (lane == m) yb_mine = s;
+      prod[m] = Gb[m] * we[lm_l(m)];
     }
+    int mm;
+    const float s = warp_sum_multi<AR::DSH>(prod, lane, &mm);
 #pragma unroll
     for (int l = 0; l < AR::NENV; ++l) t.wbar[e * AR::NW + AR::ENV_OFF + l * kC + lane] = t.inv_sqrt_nbar * wb[l];
-    if (lane < AR::DSH) t.ybar[e * AR::DSH + lane] += t.inv_sqrt_nbar * yb_mine;
+    if (mm < AR::DSH && (lane & ((1 << (5 - (AR::DSH <= 1 ? 0 : AR::DSH <= 2 ? 1 : AR::DSH <= 4 ? 2 : AR::DSH <= 8 ? 3 : 4))) - 1)) == 0)
+      t.ybar[e * AR::DSH + mm] += t.inv_sqrt_nbar * s;
   }
 }
 
