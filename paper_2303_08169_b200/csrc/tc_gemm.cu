@@ -147,7 +147,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
 }
 
 // sigmoid via exp2 + fast reciprocal (a few ulp; the parity tolerance is ~1e-6 relative)
-__device__ __forceinline__ float sigm(float t) { return __frcp_rn(1.f + exp2f(-1.4426950408889634f * t)); }
+__device__ __forceinline__ float sigm(float t) { return __fdividef(1.f, 1.f + exp2f(-1.4426950408889634f * t)); }
 __device__ __forceinline__ float silu(float t) { return t * sigm(t); }
 __device__ __forceinline__ float dsilu(float t) {
   const float s = sigm(t);
