@@ -108,6 +108,11 @@ __global__ void __launch_bounds__(NT) k_gemm(GemmArgs g) {
         case EPI_ACC: g.C[o] += p; break;
         case EPI_ADDX: g.C[o] = p + g.X[o]; break;
         case EPI_DSILU: g.C[o] = ur * p * dsilu(g.X[o]); break;
+        case EPI_R2: {
+          const int col = col0 + tx + 16 * j;
+          g.C[o] = p + g.rs2[r] * (g.vec1[col] + ur * g.vec2[col]);
+          break;
+        }
         default: break;
       }
     }

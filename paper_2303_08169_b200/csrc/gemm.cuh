@@ -18,6 +18,7 @@ enum GemmEpi : int {
   EPI_ACC = 6,        // C += s acc
   EPI_ADDX = 7,       // C = s acc + X
   EPI_DSILU = 8,      // C = (u ? u[r] : 1) s acc SiLU'(X)
+  EPI_R2 = 9,         // C = s acc + rs2[r] (vec1[col] + u[r] vec2[col])   (rank-2 affine term)
 };
 
 struct GemmArgs {
@@ -33,6 +34,9 @@ struct GemmArgs {
   float* aux = nullptr;      // [M][N]
   const float* X = nullptr;  // [M][N]
   const float* u = nullptr;  // [M]
+  const float* rs2 = nullptr;   // [M]   (EPI_R2)
+  const float* vec1 = nullptr;  // [N]   (EPI_R2)
+  const float* vec2 = nullptr;  // [N]   (EPI_R2)
   float s = 1.f, alpha = 0.f, beta = 0.f;
   int epi = EPI_STORE;
 };

@@ -357,6 +357,60 @@ __global__ void k_energy(ChunkPtrs ch, const int32_t* __restrict__ row_ptr, cons
   if (lane == 0) e_atom[a] = sig * (double)inv_sqrt_nbar * (double)acc + (z == 0 ? mu0 : mu1);
 }
 
+// Last layer folded into the linear read-out: with w_out = W_o1 W_o2 / sqrt(D 32)
+// and q = W_lat(L-1) w_out (all linear),
+//   E_e = a (x.w_out) + (b u / sqrt(fan)) ([x, s].q)            (x = x^{L-1}, s = its scalars)
+// and the reverse mode of the last layer is rank one per edge:
+//   ubar = Ebar (b / sqrt(fan)) [x, s].q,  sbar = Ebar u (b / sqrt(fan)) q_s,
+//   xbar^{L-1} = Ebar (a w_out + u (b / sqrt(fan)) q_x)  (applied in the env^T GEMM epilogue).
+__global__ void k_energy_last(ChunkPtrs ch, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ species,
+                              const float* __restrict__ x, const float* __restrict__ sc, int nsc,
+                              const float* __restrict__ u, const float* __restrict__ wout,
+                              const float* __restrict__ q, double* __restrict__ e_atom, float* __restrict__ ubar,
+                              float* __restrict__ sbar, float* __restrict__ ebar, double s0, double s1, double mu0,
+                              double mu1, float inv_sqrt_nbar, float ra, float sf) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ii = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ii >= ch.n_c) return;
+  const int64_t at = ch.a0 + ii;
+  const int64_t r0 = row_ptr[at] - ch.e0, r1 = row_ptr[at + 1] - ch.e0;
+  const int z = species[at];
+  const double sig = z == 0 ? s0 : s1;
+  const float eb = (float)sig * inv_sqrt_nbar;
+  const float4 w4 = reinterpret_cast<const float4*>(wout)[lane];
+  const float4 q4 = reinterpret_cast<const float4*>(q)[lane];
+  float qs[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) qs[k] = (lane + 32 * k < nsc) ? q[128 + lane + 32 * k] : 0.f;
+  float acc = 0.f;
+  for (int64_t e = r0; e < r1; ++e) {
+    const float4 x4 = reinterpret_cast<const float4*>(x + e * kD)[lane];
+    float d1 = x4.x * w4.x;
+    d1 = fmaf(x4.y, w4.y, d1);
+    d1 = fmaf(x4.z, w4.z, d1);
+    d1 = fmaf(x4.w, w4.w, d1);
+    float d2 = x4.x * q4.x;
+    d2 = fmaf(x4.y, q4.y, d2);
+    d2 = fmaf(x4.z, q4.z, d2);
+    d2 = fmaf(x4.w, q4.w, d2);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (lane + 32 * k < nsc) d2 = fmaf(sc[e * nsc + lane + 32 * k], qs[k], d2);
+    d1 = warp_sum(d1);
+    d2 = warp_sum(d2);
+    const float ue = u[e];
+    acc += ra * d1 + sf * ue * d2;
+    if (lane == 0) {
+      ubar[e] = eb * sf * d2;
+      ebar[e] = eb;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (lane + 32 * k < nsc) sbar[e * nsc + lane + 32 * k] = eb * ue * sf * qs[k];
+  }
+  if (lane == 0) e_atom[at] = sig * (double)inv_sqrt_nbar * (double)acc + (z == 0 ? mu0 : mu1);
+}
+
 // ubar[e] += coef <P[e], Q[e]> over 128 (warp per edge)
 __global__ void k_rowdot(int64_t E, const float* __restrict__ P, const float* __restrict__ Q, float coef,
                          float* __restrict__ ubar) {
@@ -515,7 +569,7 @@ size_t floats_per_edge(const Model& M) {
     nwmax = std::max(nwmax, (size_t)L.nw);
     nsmax = std::max(nsmax, (size_t)L.A.n_s * kC);
   }
-  f += tmax + 2 * 128 + nsmax + 2 * vmax + nwmax + dsh + 1 + 16 + 64 + 32;
+  f += tmax + 2 * 128 + nsmax + 2 * vmax + nwmax + dsh + 1 + 16 + 64 + 32 + 1;
   return f;
 }
 
@@ -557,6 +611,7 @@ void reserve_ws(allegro_ctx* c, size_t e_cap, size_t a_cap) {
   w.zbar.reserve(e_cap * 16);
   w.ab2.reserve(e_cap * 64);
   w.ab1.reserve(e_cap * 32);
+  w.ebar.reserve(e_cap);
   w.e_cap = e_cap;
   w.a_cap = a_cap;
 }
@@ -643,6 +698,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
         run_gemm(M, g, *last_w, st, &c->prof);
       }
     }
+    if (k == M.n_layers - 1) break;  // the last latent update is folded into the read-out (k_energy_last)
     GemmArgs g = G(x, 128, M.w.lat[k], 128, L.fan_lat, xn, 1.f / std::sqrt((float)L.fan_lat), EPI_RESID);
     g.K1 = 128;
     g.A2 = w.T.p;  // T_0e = the scalars s, [E][n_s C] in (q, c) order
@@ -655,26 +711,30 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     run_gemm(M, g, *last_w, st, &c->prof);
     std::swap(x, xn);
   }
-  // ---- energies (E7, E8) and x-bar^L ----
+  // ---- energies (E7, E8) and the rank-one reverse mode of the last layer ----
   float* xb = w.xbar_a.p;
   float* xbn = w.xbar_b.p;
+  const LayerInfo& LL = M.L[M.n_layers - 1];
+  const int nsc_last = LL.A.n_s * kC;
+  const float sf_last = kResB / std::sqrt((float)LL.fan_lat);
   if (warp_blocks) {
     {
-      ProfScope ps_(&c->prof, st, PK_ENERGY, 2.0 * 128 * E, (double)E * 1024);
-      k_energy<<<warp_blocks, 128, 0, st>>>(ch, c->row_ptr.p, c->species.p, x, M.w.wout, xb, c->e_atom.p, M.sigma[0],
-                                          M.sigma[1], M.mu[0], M.mu[1], inv_sqrt_nbar);
+      ProfScope ps_(&c->prof, st, PK_ENERGY, 6.0 * 128 * E, (double)E * (512 + 8.0 * nsc_last + 16));
+      k_energy_last<<<warp_blocks, 128, 0, st>>>(ch, c->row_ptr.p, c->species.p, x, w.T.p, nsc_last, w.u.p, M.w.wout,
+                                                 M.w.q_last, c->e_atom.p, w.ubar.p, w.sbar.p, w.ebar.p, M.sigma[0],
+                                                 M.sigma[1], M.mu[0], M.mu[1], inv_sqrt_nbar, kResA, sf_last);
     }
     ALG_LAUNCH_CHECK();
   }
   // ---- reverse mode (E9) ----
-  ALG_CUDA(cudaMemsetAsync(w.ubar.p, 0, sizeof(float) * E, st));
   ALG_CUDA(cudaMemsetAsync(w.ybar.p, 0, sizeof(float) * E * dsh, st));
   float* vb = w.vbar_a.p;   // V-bar^{k+1} (input to layer k)
   float* vbn = w.vbar_b.p;  // V-bar^k (output of layer k)
   const unsigned edge_warp_blocks = (unsigned)((E * 32 + 255) / 256);
   for (int k = M.n_layers - 1; k >= 0; --k) {
     const LayerInfo& L = M.L[k];
-    if (E > 0) {
+    const bool last = k == M.n_layers - 1;
+    if (E > 0 && !last) {
       {
         ProfScope ps_(&c->prof, st, PK_ROWDOT, 2.0 * 128 * E, (double)E * 1024);
         k_rowdot<<<edge_warp_blocks, 256, 0, st>>>(E, w.h[k].p, xb, kResB, w.ubar.p);
@@ -682,7 +742,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
       ALG_LAUNCH_CHECK();
     }
     const float sl = 1.f / std::sqrt((float)L.fan_lat);
-    {
+    if (!last) {
       GemmArgs g = G(xb, 128, M.w.latT_x[k], 128, 128, xbn, sl, EPI_URESID);
       g.X = xb;
       g.u = w.u.p;
@@ -719,7 +779,13 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     }
     tp_dispatch(M.n_layers, M.lmax, k, false, tp, st, &c->prof, L);
     {
-      GemmArgs g = G(w.wbar.p, L.nw, M.w.envT[k], 128, L.nw, xbn, 1.f / std::sqrt(128.f), EPI_ACC);
+      GemmArgs g = G(w.wbar.p, L.nw, M.w.envT[k], 128, L.nw, xbn, 1.f / std::sqrt(128.f), last ? EPI_R2 : EPI_ACC);
+      if (last) {  // xbar^{L-1} = env^T part + Ebar (a w_out + u (b/sqrt(fan)) q_x)
+        g.rs2 = w.ebar.p;
+        g.u = w.u.p;
+        g.vec1 = M.w.r2_vec1;
+        g.vec2 = M.w.r2_vec2;
+      }
       run_gemm(M, g, *last_w, st, &c->prof);
     }
     std::swap(xb, xbn);

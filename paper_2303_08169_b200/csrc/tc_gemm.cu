@@ -188,6 +188,7 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& g, float* v, const flo
       case EPI_ACC: out[j] = xin[j] + pv; break;
       case EPI_ADDX: out[j] = pv + xin[j]; break;
       case EPI_DSILU: out[j] = ur * pv * dsilu(xin[j]); break;
+      case EPI_R2: out[j] = pv + xin[j]; break;  // xin = rs2 (vec1 + u vec2), prepared by the caller
       default: out[j] = pv; break;
     }
   }
@@ -437,6 +438,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (lane == 0) mbar_arrive(x_empty + xs);
           if (++xs == X_STAGES) xs = 0, xph ^= 1;
         }
+        if constexpr (EPI == EPI_R2) {
+          const float e2 = (r < g.M) ? g.rs2[r] : 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = p.col0 + c0 + j;
+            xin[j] = col < g.N ? e2 * (__ldg(g.vec1 + col) + ur * __ldg(g.vec2 + col)) : 0.f;
+          }
+        }
         tmem_ld32(tbase + (uint32_t)c0, v);
         if (p.diag & 2) continue;
         const int64_t col = p.col0 + c0;
@@ -567,7 +576,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   if (!attr_set) {
 #define ALG_SET(e) ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<e>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
     ALG_SET(EPI_STORE) ALG_SET(EPI_SILU) ALG_SET(EPI_UMUL_SAVE) ALG_SET(EPI_RESID) ALG_SET(EPI_URESID)
-    ALG_SET(EPI_USCALE) ALG_SET(EPI_ACC) ALG_SET(EPI_ADDX) ALG_SET(EPI_DSILU)
+    ALG_SET(EPI_USCALE) ALG_SET(EPI_ACC) ALG_SET(EPI_ADDX) ALG_SET(EPI_DSILU) ALG_SET(EPI_R2)
 #undef ALG_SET
     attr_set = true;
   }
@@ -605,7 +614,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
 #define ALG_EPI(e) \
   case e: k_tc_gemm<e><<<grid, TC_THREADS, smem, st>>>(mA, mA2, mX, p); break;
       ALG_EPI(EPI_STORE) ALG_EPI(EPI_SILU) ALG_EPI(EPI_UMUL_SAVE) ALG_EPI(EPI_RESID) ALG_EPI(EPI_URESID)
-      ALG_EPI(EPI_USCALE) ALG_EPI(EPI_ACC) ALG_EPI(EPI_ADDX) ALG_EPI(EPI_DSILU)
+      ALG_EPI(EPI_USCALE) ALG_EPI(EPI_ACC) ALG_EPI(EPI_ADDX) ALG_EPI(EPI_DSILU) ALG_EPI(EPI_R2)
 #undef ALG_EPI
       default: throw CudaError("tc_gemm: unknown epilogue");
     }

@@ -218,6 +218,33 @@ void load_model(allegro_ctx* c, const char* path) {
       wo[r] = (float)(s / (std::sqrt(128.0) * std::sqrt(32.0)));
     }
     W.wout = upload(W, wo);
+    // q = W_lat(L-1) w_out in the device row order of lat (x rows, then scalar rows (q, c))
+    const LayerInfo& last = M.L[L - 1];
+    const HostTensor& wl = need("lat_" + std::to_string(L - 1), last.fan_lat, D);
+    std::vector<double> wod(D);
+    for (int r = 0; r < D; ++r) {
+      double s = 0;
+      for (int q = 0; q < 32; ++q) s += o1.at(r, q) * o2.at(q, 0);
+      wod[r] = s / (std::sqrt(128.0) * std::sqrt(32.0));
+    }
+    std::vector<float> q(last.fan_lat);
+    auto qrow = [&](int file_row) {
+      double s = 0;
+      for (int v = 0; v < D; ++v) s += wl.at(file_row, v) * wod[v];
+      return s;
+    };
+    for (int r = 0; r < D; ++r) q[r] = (float)qrow(r);
+    for (int cc = 0; cc < C; ++cc)
+      for (int s2 = 0; s2 < last.A.n_s; ++s2) q[D + s2 * C + cc] = (float)qrow(D + cc * last.A.n_s + s2);
+    W.q_last = upload(W, q);
+    const double a = 2.0 / std::sqrt(5.0), b = 1.0 / std::sqrt(5.0), sf = b / std::sqrt((double)last.fan_lat);
+    std::vector<float> v1(D), v2(D);
+    for (int r = 0; r < D; ++r) {
+      v1[r] = (float)(a * wod[r]);
+      v2[r] = (float)(sf * qrow(r));
+    }
+    W.r2_vec1 = upload(W, v1);
+    W.r2_vec2 = upload(W, v2);
   }
 }
 
