@@ -176,11 +176,13 @@ int md_get_local_state(allegro_ctx* ctx, int64_t capacity, int64_t* n_local, int
 /* Per-kernel-class accounting.  Every launch of the library is counted;
  * with profiling enabled each launch is also bracketed by CUDA events on the stream it is
  * launched on and its ALGORITHMIC flops / DRAM bytes are accumulated.
- * allegro_profile(ctx, enable) resets all totals.  Kinds are 0 .. allegro_profile_kinds()-1. */
+ * allegro_profile(ctx, 1) synchronises the stream, resets all totals and the launch counter
+ * and starts recording; allegro_profile(ctx, 0) stops recording (no synchronisation) and
+ * keeps the totals readable.  Kinds are 0 .. allegro_profile_kinds()-1. */
 int allegro_profile(allegro_ctx* ctx, int enable);
 int allegro_profile_read(allegro_ctx* ctx, int kind, double* time_ms, double* flops, double* bytes,
                          int64_t* launches);
-int64_t allegro_launch_count(allegro_ctx* ctx); /* launches since the last allegro_profile() */
+int64_t allegro_launch_count(allegro_ctx* ctx); /* launches since the last allegro_profile(ctx, 1) */
 /* per-shape detail entry idx (0..): name, time, algorithmic bytes, launches; ALLEGRO_E_ARG past the end */
 int allegro_profile_detail(allegro_ctx* ctx, int idx, char* name, int name_cap, double* time_ms, double* bytes,
                            int64_t* launches);

@@ -422,10 +422,14 @@ int md_get_local_state(allegro_ctx* c, int64_t capacity, int64_t* n_local, int32
 int allegro_profile(allegro_ctx* c, int enable) {
   if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
   return guarded(c, [&]() -> int {
+    if (!enable) {  // stop recording; the totals stay readable (no synchronisation)
+      c->prof.on = false;
+      return ALLEGRO_OK;
+    }
     ALG_CUDA(cudaSetDevice(c->device));
     ALG_CUDA(cudaStreamSynchronize(c->stream));
     c->prof.reset();
-    c->prof.on = enable != 0;
+    c->prof.on = true;
     return ALLEGRO_OK;
   });
 }
@@ -589,6 +593,7 @@ int allegro_debug_gemm_bench(int device, int precision, int64_t M, int N, int K,
     if (epi == EPI_RESID || epi == EPI_URESID || epi == EPI_UMUL_SAVE || epi == EPI_USCALE) g.u = du;
     const TcTuning saved = g_tc_tuning;
     g_tc_tuning.tma_store = tma_store;
+    if (tma_store >= 2) g_tc_tuning.max_acc = tma_store;  // test hook: >= 2 sets the accumulator ring cap
     g_tc_tuning.max_stages = max_stages;
     g_tc_tuning.diag = diag;
     TcWeight t;

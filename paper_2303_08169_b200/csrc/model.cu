@@ -142,17 +142,27 @@ struct TpArgs {
   float inv_sqrt_nbar;
 };
 
+// Per-edge operands of the TP kernels.  Every edge loop below is software-pipelined: the
+// loads of edge e+1 are issued before edge e is computed and stored (the stores of edge e
+// may alias the next loads as far as the compiler knows, so without this every edge costs
+// a full DRAM round trip per warp -- ncu: long-scoreboard stalls, 58 % of HBM).
 template <int NL, int LMAX, int K>
-__device__ __forceinline__ void load_v(const TpArgs& t, int64_t e, int lane, float* v) {
+struct VIn {
+  using AR = Arch<NL, LMAX, K>;
+  static constexpr int NY = K == 0 ? AR::DSH : 1;
+  static constexpr int NE = K == 0 ? AR::NENV : 1;
+  static constexpr int NV = K == 0 ? 1 : AR::DIN;
+  float y[NY], we[NE], v[NV];
+};
+
+template <int NL, int LMAX, int K>
+__device__ __forceinline__ void fetch_v(const TpArgs& t, int64_t e, int lane, VIn<NL, LMAX, K>& in) {
   using AR = Arch<NL, LMAX, K>;
   if constexpr (K == 0) {
-    float y[AR::DSH], we[AR::NENV];
 #pragma unroll
-    for (int m = 0; m < AR::DSH; ++m) y[m] = t.Y[e * AR::DSH + m];
+    for (int m = 0; m < AR::DSH; ++m) in.y[m] = t.Y[e * AR::DSH + m];
 #pragma unroll
-    for (int l = 0; l < AR::NENV; ++l) we[l] = t.w[e * AR::NW + l * kC + lane];
-#pragma unroll
-    for (int m = 0; m < AR::DSH; ++m) v[m] = we[lm_l(m)] * y[m];
+    for (int l = 0; l < AR::NENV; ++l) in.we[l] = t.w[e * AR::NW + l * kC + lane];
   } else {
     static_for<AR::A.in.n>([&](auto I) {
       constexpr int ii = decltype(I)::value;
@@ -161,9 +171,44 @@ __device__ __forceinline__ void load_v(const TpArgs& t, int64_t e, int lane, flo
       constexpr int vbase = AR::v_base(ii);
       const float* src = t.V + (int64_t)vbase * t.e_cap + e * dim * kC + lane;
 #pragma unroll
-      for (int m = 0; m < dim; ++m) v[off + m] = src[m * kC];
+      for (int m = 0; m < dim; ++m) in.v[off + m] = src[m * kC];
     });
   }
+}
+
+// V of layer K from the fetched operands (K = 0: V0 = w_edge (x) Y)
+template <int NL, int LMAX, int K>
+__device__ __forceinline__ void expand_v(const VIn<NL, LMAX, K>& in, float* v) {
+  using AR = Arch<NL, LMAX, K>;
+  if constexpr (K == 0) {
+#pragma unroll
+    for (int m = 0; m < AR::DSH; ++m) v[m] = in.we[lm_l(m)] * in.y[m];
+  } else {
+#pragma unroll
+    for (int m = 0; m < AR::DIN; ++m) v[m] = in.v[m];
+  }
+}
+
+// w_env chunk and Y of one edge (the environment sum and its adjoint)
+template <int NL, int LMAX, int K>
+struct EnvIn {
+  float y[Arch<NL, LMAX, K>::DSH], we[Arch<NL, LMAX, K>::NENV];
+};
+
+template <int NL, int LMAX, int K>
+__device__ __forceinline__ void fetch_env(const TpArgs& t, int64_t e, int lane, EnvIn<NL, LMAX, K>& in) {
+  using AR = Arch<NL, LMAX, K>;
+#pragma unroll
+  for (int m = 0; m < AR::DSH; ++m) in.y[m] = t.Y[e * AR::DSH + m];
+#pragma unroll
+  for (int l = 0; l < AR::NENV; ++l) in.we[l] = t.w[e * AR::NW + AR::ENV_OFF + l * kC + lane];
+}
+
+// lanes that own the butterfly total of value mm (warp_sum_multi<DSH>)
+template <int DSH>
+__device__ __forceinline__ bool owns_total(int lane, int mm) {
+  constexpr int LP = DSH <= 1 ? 0 : DSH <= 2 ? 1 : DSH <= 4 ? 2 : DSH <= 8 ? 3 : 4;
+  return mm < DSH && (lane & ((1 << (5 - LP)) - 1)) == 0;
 }
 
 template <int NL, int LMAX, int K>
@@ -177,21 +222,28 @@ __global__ void __launch_bounds__(128) k_tp_fwd(TpArgs t) {
   float G[AR::DSH];
 #pragma unroll
   for (int m = 0; m < AR::DSH; ++m) G[m] = 0.f;
-  for (int64_t e = r0; e < r1; ++e) {
-    float we[AR::NENV];
+  if (r1 > r0) {
+    EnvIn<NL, LMAX, K> nx;
+    fetch_env<NL, LMAX, K>(t, r0, lane, nx);
+    for (int64_t e = r0; e < r1; ++e) {
+      const EnvIn<NL, LMAX, K> cur = nx;
+      fetch_env<NL, LMAX, K>(t, e + 1 < r1 ? e + 1 : e, lane, nx);
 #pragma unroll
-    for (int l = 0; l < AR::NENV; ++l) we[l] = t.w[e * AR::NW + AR::ENV_OFF + l * kC + lane];
-#pragma unroll
-    for (int m = 0; m < AR::DSH; ++m) G[m] = fmaf(we[lm_l(m)], t.Y[e * AR::DSH + m], G[m]);
+      for (int m = 0; m < AR::DSH; ++m) G[m] = fmaf(cur.we[lm_l(m)], cur.y[m], G[m]);
+    }
   }
 #pragma unroll
   for (int m = 0; m < AR::DSH; ++m) {
     G[m] *= t.inv_sqrt_nbar;
     t.G[(ii * AR::DSH + m) * kC + lane] = G[m];
   }
+  if (r1 <= r0) return;
+  VIn<NL, LMAX, K> nx;
+  fetch_v<NL, LMAX, K>(t, r0, lane, nx);
   for (int64_t e = r0; e < r1; ++e) {
     float v[AR::DIN];
-    load_v<NL, LMAX, K>(t, e, lane, v);
+    expand_v<NL, LMAX, K>(nx, v);
+    fetch_v<NL, LMAX, K>(t, e + 1 < r1 ? e + 1 : e, lane, nx);
     float T[AR::DT];
 #pragma unroll
     for (int q = 0; q < AR::DT; ++q) T[q] = 0.f;
@@ -225,6 +277,31 @@ __global__ void __launch_bounds__(128) k_tp_fwd(TpArgs t) {
 
 // ----------------------------------------------------------------- A11 TP backward
 template <int NL, int LMAX, int K>
+struct BwdIn {
+  VIn<NL, LMAX, K> v;
+  float tb[Arch<NL, LMAX, K>::DT];
+  float yb_old;  // K = 0: this lane's Y-bar total slot (read-modify-write)
+};
+
+template <int NL, int LMAX, int K>
+__device__ __forceinline__ void fetch_bwd(const TpArgs& t, int64_t e, int lane, int mm, BwdIn<NL, LMAX, K>& in) {
+  using AR = Arch<NL, LMAX, K>;
+  fetch_v<NL, LMAX, K>(t, e, lane, in.v);
+  static_for<AR::A.n_paths>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    constexpr int o = AR::A.out_idx[q];
+    constexpr int dim = ir_dim(AR::A.out.v[o]);
+    constexpr int nto = AR::A.n_to[o];
+    constexpr int ol = AR::A.out_local[q];
+    constexpr int toff = AR::A.t_off[q];
+    const float* src = t.Tb[o] + (e * dim * nto + ol) * kC + lane;
+#pragma unroll
+    for (int m = 0; m < dim; ++m) in.tb[toff + m] = src[m * nto * kC];
+  });
+  if constexpr (K == 0) in.yb_old = owns_total<AR::DSH>(lane, mm) ? t.ybar[e * AR::DSH + mm] : 0.f;
+}
+
+template <int NL, int LMAX, int K>
 __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
   using AR = Arch<NL, LMAX, K>;
   constexpr LayerArch A = AR::A;
@@ -232,28 +309,24 @@ __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
   const int64_t ii = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (ii >= t.ch.n_c) return;
   const int64_t r0 = t.row_ptr[t.ch.a0 + ii] - t.ch.e0, r1 = t.row_ptr[t.ch.a0 + ii + 1] - t.ch.e0;
+  if (r1 <= r0) return;  // no edges: Gamma-bar = 0, nothing to write
+  constexpr int LP = AR::DSH <= 1 ? 0 : AR::DSH <= 2 ? 1 : AR::DSH <= 4 ? 2 : AR::DSH <= 8 ? 3 : 4;
+  const int mm = lane >> (5 - LP);  // value index of this lane's butterfly total
   float G[AR::DSH], Gb[AR::DSH];
 #pragma unroll
   for (int m = 0; m < AR::DSH; ++m) {
     G[m] = t.G[(ii * AR::DSH + m) * kC + lane];
     Gb[m] = 0.f;
   }
+  BwdIn<NL, LMAX, K> nx;
+  fetch_bwd<NL, LMAX, K>(t, r0, lane, mm, nx);
   for (int64_t e = r0; e < r1; ++e) {
-    float v[AR::DIN], vb[AR::DIN], tb[AR::DT];
-    load_v<NL, LMAX, K>(t, e, lane, v);
+    const BwdIn<NL, LMAX, K> cur = nx;
+    fetch_bwd<NL, LMAX, K>(t, e + 1 < r1 ? e + 1 : e, lane, mm, nx);
+    float v[AR::DIN], vb[AR::DIN];
+    expand_v<NL, LMAX, K>(cur.v, v);
 #pragma unroll
     for (int q = 0; q < AR::DIN; ++q) vb[q] = 0.f;
-    static_for<A.n_paths>([&](auto Q) {
-      constexpr int q = decltype(Q)::value;
-      constexpr int o = AR::A.out_idx[q];
-      constexpr int dim = ir_dim(AR::A.out.v[o]);
-      constexpr int nto = AR::A.n_to[o];
-      constexpr int ol = AR::A.out_local[q];
-      constexpr int toff = AR::A.t_off[q];
-      const float* src = t.Tb[o] + (e * dim * nto + ol) * kC + lane;
-#pragma unroll
-      for (int m = 0; m < dim; ++m) tb[toff + m] = src[m * nto * kC];
-    });
     static_for<A.n_paths>([&](auto Q) {
       constexpr int q = decltype(Q)::value;
       constexpr int L1 = AR::A.path[q].a.l, L2 = AR::A.path[q].b.l, LO = AR::A.path[q].o.l;
@@ -265,7 +338,7 @@ __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
         constexpr float c = (float)(alpha * W3j<L1, L2, LO>::t.v[i]);
         constexpr int it = AR::A.t_off[q] + m3, iv = AR::A.in_off[q] + m1, ig = AR::A.sh_off[q] + m2;
         if constexpr (c != 0.f) {
-          const float ct = c * tb[it];
+          const float ct = c * cur.tb[it];
           vb[iv] = fmaf(ct, G[ig], vb[iv]);
           Gb[ig] = fmaf(ct, v[iv], Gb[ig]);
         }
@@ -273,26 +346,20 @@ __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
     });
     if constexpr (K == 0) {
       // V0 = w_edge (x) Y:  wbar_edge[l] = sum_m vb[m] Y[m];  Ybar[m] += sum_c vb[m] w_edge[l]
-      float y[AR::DSH], we[AR::NENV], wb[AR::NENV];
+      float wb[AR::NENV];
 #pragma unroll
-      for (int m = 0; m < AR::DSH; ++m) y[m] = t.Y[e * AR::DSH + m];
-#pragma unroll
-      for (int l = 0; l < AR::NENV; ++l) {
-        we[l] = t.w[e * AR::NW + l * kC + lane];
-        wb[l] = 0.f;
-      }
+      for (int l = 0; l < AR::NENV; ++l) wb[l] = 0.f;
       float prod[AR::DSH];
 #pragma unroll
       for (int m = 0; m < AR::DSH; ++m) {
-        wb[lm_l(m)] = fmaf(vb[m], y[m], wb[lm_l(m)]);
-        prod[m] = vb[m] * we[lm_l(m)];
+        wb[lm_l(m)] = fmaf(vb[m], cur.v.y[m], wb[lm_l(m)]);
+        prod[m] = vb[m] * cur.v.we[lm_l(m)];
       }
-      int mm;
-      const float s = warp_sum_multi<AR::DSH>(prod, lane, &mm);
+      int mq;
+      const float s = warp_sum_multi<AR::DSH>(prod, lane, &mq);
 #pragma unroll
       for (int l = 0; l < AR::NENV; ++l) t.wbar[e * AR::NW + l * kC + lane] = wb[l];
-      if (mm < AR::DSH && (lane & ((1 << (5 - (AR::DSH <= 1 ? 0 : AR::DSH <= 2 ? 1 : AR::DSH <= 4 ? 2 : AR::DSH <= 8 ? 3 : 4))) - 1)) == 0)
-        t.ybar[e * AR::DSH + mm] += s;
+      if (owns_total<AR::DSH>(lane, mm)) t.ybar[e * AR::DSH + mm] = cur.yb_old + s;
     } else {
       static_for<AR::A.in.n>([&](auto I) {
         constexpr int ii2 = decltype(I)::value;
@@ -306,57 +373,37 @@ __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
     }
   }
   // environment adjoint: w_env-bar and Ybar from Gamma-bar
+  struct EnvB {
+    EnvIn<NL, LMAX, K> env;
+    float yb_old;
+  };
+  auto fetch_envb = [&](int64_t e, EnvB& in) {
+    fetch_env<NL, LMAX, K>(t, e, lane, in.env);
+    in.yb_old = owns_total<AR::DSH>(lane, mm) ? t.ybar[e * AR::DSH + mm] : 0.f;
+  };
+  EnvB en;
+  fetch_envb(r0, en);
   for (int64_t e = r0; e < r1; ++e) {
-    float y[AR::DSH], we[AR::NENV], wb[AR::NENV];
+    const EnvB cur = en;
+    fetch_envb(e + 1 < r1 ? e + 1 : e, en);
+    float wb[AR::NENV];
 #pragma unroll
-    for (int m = 0; m < AR::DSH; ++m) y[m] = t.Y[e * AR::DSH + m];
-#pragma unroll
-    for (int l = 0; l < AR::NENV; ++l) {
-      we[l] = t.w[e * AR::NW + AR::ENV_OFF + l * kC + lane];
-      wb[l] = 0.f;
-    }
+    for (int l = 0; l < AR::NENV; ++l) wb[l] = 0.f;
     float prod[AR::DSH];
 #pragma unroll
     for (int m = 0; m < AR::DSH; ++m) {
-      wb[lm_l(m)] = fmaf(Gb[m], y[m], wb[lm_l(m)]);
-      prod[m] = Gb[m] * we[lm_l(m)];
+      wb[lm_l(m)] = fmaf(Gb[m], cur.env.y[m], wb[lm_l(m)]);
+      prod[m] = Gb[m] * cur.env.we[lm_l(m)];
     }
-    int mm;
-    const float s = warp_sum_multi<AR::DSH>(prod, lane, &mm);
+    int mq;
+    const float s = warp_sum_multi<AR::DSH>(prod, lane, &mq);
 #pragma unroll
     for (int l = 0; l < AR::NENV; ++l) t.wbar[e * AR::NW + AR::ENV_OFF + l * kC + lane] = t.inv_sqrt_nbar * wb[l];
-    if (mm < AR::DSH && (lane & ((1 << (5 - (AR::DSH <= 1 ? 0 : AR::DSH <= 2 ? 1 : AR::DSH <= 4 ? 2 : AR::DSH <= 8 ? 3 : 4))) - 1)) == 0)
-      t.ybar[e * AR::DSH + mm] += t.inv_sqrt_nbar * s;
+    if (owns_total<AR::DSH>(lane, mm)) t.ybar[e * AR::DSH + mm] = cur.yb_old + t.inv_sqrt_nbar * s;
   }
 }
 
 // ----------------------------------------------------------------- A10 energies
-__global__ void k_energy(ChunkPtrs ch, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ species,
-                         const float* __restrict__ x, const float* __restrict__ wout, float* __restrict__ xbar,
-                         double* __restrict__ e_atom, double s0, double s1, double mu0, double mu1, float inv_sqrt_nbar) {
-  const int lane = threadIdx.x & 31;
-  const int64_t ii = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (ii >= ch.n_c) return;
-  const int64_t a = ch.a0 + ii;
-  const int64_t r0 = row_ptr[a] - ch.e0, r1 = row_ptr[a + 1] - ch.e0;
-  const int z = species[a];
-  const double sig = z == 0 ? s0 : s1;
-  const float ebar = (float)sig * inv_sqrt_nbar;
-  const float4 w4 = reinterpret_cast<const float4*>(wout)[lane];
-  const float4 xb4 = make_float4(ebar * w4.x, ebar * w4.y, ebar * w4.z, ebar * w4.w);
-  float acc = 0.f;
-  for (int64_t e = r0; e < r1; ++e) {
-    const float4 x4 = reinterpret_cast<const float4*>(x + e * kD)[lane];
-    float p = x4.x * w4.x;
-    p = fmaf(x4.y, w4.y, p);
-    p = fmaf(x4.z, w4.z, p);
-    p = fmaf(x4.w, w4.w, p);
-    acc += warp_sum(p);
-    reinterpret_cast<float4*>(xbar + e * kD)[lane] = xb4;
-  }
-  if (lane == 0) e_atom[a] = sig * (double)inv_sqrt_nbar * (double)acc + (z == 0 ? mu0 : mu1);
-}
-
 // Last layer folded into the linear read-out: with w_out = W_o1 W_o2 / sqrt(D 32)
 // and q = W_lat(L-1) w_out (all linear),
 //   E_e = a (x.w_out) + (b u / sqrt(fan)) ([x, s].q)            (x = x^{L-1}, s = its scalars)
@@ -383,8 +430,21 @@ __global__ void k_energy_last(ChunkPtrs ch, const int32_t* __restrict__ row_ptr,
 #pragma unroll
   for (int k = 0; k < 3; ++k) qs[k] = (lane + 32 * k < nsc) ? q[128 + lane + 32 * k] : 0.f;
   float acc = 0.f;
+  // pipelined one edge ahead (see the TP kernels)
+  auto fetch = [&](int64_t e, float4& x4, float* sv, float& ue) {
+    x4 = reinterpret_cast<const float4*>(x + e * kD)[lane];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) sv[k] = (lane + 32 * k < nsc) ? sc[e * nsc + lane + 32 * k] : 0.f;
+    ue = u[e];
+  };
+  float4 xn;
+  float sn[3], un = 0.f;
+  if (r1 > r0) fetch(r0, xn, sn, un);
   for (int64_t e = r0; e < r1; ++e) {
-    const float4 x4 = reinterpret_cast<const float4*>(x + e * kD)[lane];
+    const float4 x4 = xn;
+    const float s3[3] = {sn[0], sn[1], sn[2]};
+    const float ue = un;
+    fetch(e + 1 < r1 ? e + 1 : e, xn, sn, un);
     float d1 = x4.x * w4.x;
     d1 = fmaf(x4.y, w4.y, d1);
     d1 = fmaf(x4.z, w4.z, d1);
@@ -394,11 +454,9 @@ __global__ void k_energy_last(ChunkPtrs ch, const int32_t* __restrict__ row_ptr,
     d2 = fmaf(x4.z, q4.z, d2);
     d2 = fmaf(x4.w, q4.w, d2);
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
-      if (lane + 32 * k < nsc) d2 = fmaf(sc[e * nsc + lane + 32 * k], qs[k], d2);
+    for (int k = 0; k < 3; ++k) d2 = fmaf(s3[k], qs[k], d2);  // qs = 0 beyond nsc
     d1 = warp_sum(d1);
     d2 = warp_sum(d2);
-    const float ue = u[e];
     acc += ra * d1 + sf * ue * d2;
     if (lane == 0) {
       ubar[e] = eb * sf * d2;

@@ -166,6 +166,7 @@ struct TcParams {
   uint32_t w_bytes;    // bytes of the W image (hi + lo)
   int n_mtiles;
   int acc_cols;        // TMEM columns per accumulator (>= N_t, multiple of 32)
+  int n_acc;           // accumulator ring depth (2..4)
   uint32_t tmem_cols;  // allocated TMEM columns
   int diag;            // diagnostics: bit0 skip MMAs, bit1 skip global stores
   int has_x;           // the epilogue reads an [M][N] input (X, or old C) through the TMA ring
@@ -255,9 +256,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* raw_empty = raw_full + p.stages;          // [stages]  split warps read it
   uint64_t* a_full = raw_empty + p.stages;            // [a_stages] hi/lo in TMEM
   uint64_t* a_empty = a_full + p.a_stages;            // [a_stages] MMAs done with it
-  uint64_t* acc_full = a_empty + p.a_stages;          // [2]
-  uint64_t* acc_empty = acc_full + 2;                 // [2]
-  uint64_t* w_full = acc_empty + 2;
+  uint64_t* acc_full = a_empty + p.a_stages;          // [n_acc]
+  uint64_t* acc_empty = acc_full + 4;                 // [n_acc]
+  uint64_t* w_full = acc_empty + 4;
   uint64_t* x_full = w_full + 1;                      // [X_STAGES]
   uint64_t* x_empty = x_full + X_STAGES;              // [X_STAGES]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + X_STAGES);
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(a_full + s, 4);
       mbar_init(a_empty + s, 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < p.n_acc; ++a) {
       mbar_init(acc_full + a, 1);
       mbar_init(acc_empty + a, 4);
     }
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_a = tmem + 2u * (uint32_t)p.acc_cols;  // A ring after the two accumulators
+  const uint32_t tmem_a = tmem + (uint32_t)(p.n_acc * p.acc_cols);  // A ring after the accumulators
 
   const int n_my = p.n_mtiles > (int)blockIdx.x ? (p.n_mtiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
@@ -376,8 +377,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int j = 0;
     uint32_t aph = 0;
     for (int t = 0; t < n_my; ++t) {
-      const int a = t & 1;
-      const uint32_t acph = (t >> 1) & 1;
+      const int a = t % p.n_acc;
+      const uint32_t acph = (uint32_t)(t / p.n_acc) & 1u;
       mbar_wait(acc_empty + a, acph ^ 1);
       tc_fence_after();
       const uint32_t d = tmem + (uint32_t)(a * p.acc_cols);
@@ -414,8 +415,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int xs = 0;
     uint32_t xph = 0;
     for (int t = 0; t < n_my; ++t) {
-      const int a = t & 1;
-      const uint32_t acph = (t >> 1) & 1;
+      const int a = t % p.n_acc;
+      const uint32_t acph = (uint32_t)(t / p.n_acc) & 1u;
       mbar_wait(acc_full + a, acph);
       tc_fence_after();
       const int64_t row0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * ROWS + q * 32;
@@ -440,10 +441,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if constexpr (EPI == EPI_R2) {
           const float e2 = (r < g.M) ? g.rs2[r] : 0.f;
+          const int cb = p.col0 + c0;
+          if (cb + 32 <= g.N) {  // warp-uniform float4 loads (broadcast)
+            const float4* v1 = reinterpret_cast<const float4*>(g.vec1 + cb);
+            const float4* v2 = reinterpret_cast<const float4*>(g.vec2 + cb);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = p.col0 + c0 + j;
-            xin[j] = col < g.N ? e2 * (__ldg(g.vec1 + col) + ur * __ldg(g.vec2 + col)) : 0.f;
+            for (int c = 0; c < 8; ++c) {
+              const float4 a4 = __ldg(v1 + c), b4 = __ldg(v2 + c);
+              xin[4 * c] = e2 * fmaf(ur, b4.x, a4.x);
+              xin[4 * c + 1] = e2 * fmaf(ur, b4.y, a4.y);
+              xin[4 * c + 2] = e2 * fmaf(ur, b4.z, a4.z);
+              xin[4 * c + 3] = e2 * fmaf(ur, b4.w, a4.w);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int col = cb + j;
+              xin[j] = col < g.N ? e2 * (__ldg(g.vec1 + col) + ur * __ldg(g.vec2 + col)) : 0.f;
+            }
           }
         }
         tmem_ld32(tbase + (uint32_t)c0, v);
@@ -571,7 +586,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   int stages = (int)((SMEM_LIMIT - SMEM_RESERVE - w_round - out_bytes) / STAGE_BYTES);
   stages = std::min(stages, g_tc_tuning.max_stages);
   if (stages < 2) throw CudaError("tc_gemm: shared memory too small for 2 stages");
-  const size_t smem = 1024 + w_round + out_bytes + (size_t)stages * STAGE_BYTES + 256;
+  const size_t smem = 1024 + w_round + out_bytes + (size_t)stages * STAGE_BYTES + 512;
   static bool attr_set = false;
   if (!attr_set) {
 #define ALG_SET(e) ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<e>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
@@ -590,11 +605,13 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   p.n_mtiles = (int)((g.M + ROWS - 1) / ROWS);
   p.acc_cols = (w.N_t + 31) / 32 * 32;
   // TMEM: two accumulators + the A ring (64 columns per stage), power of two <= 512
-  int a_st = std::min(4, (512 - 2 * p.acc_cols) / A_TMEM_COLS);
+  // a deeper accumulator ring for narrow tiles lets the MMAs run further ahead of the epilogue
+  p.n_acc = std::max(2, std::min(g_tc_tuning.max_acc, (512 - 4 * A_TMEM_COLS) / p.acc_cols));
+  int a_st = std::min(4, (512 - p.n_acc * p.acc_cols) / A_TMEM_COLS);
   if (a_st < 2) throw CudaError("tc_gemm: TMEM too small");
   p.a_stages = a_st;
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * p.acc_cols + a_st * A_TMEM_COLS)) cols <<= 1;
+  while (cols < (uint32_t)(p.n_acc * p.acc_cols + a_st * A_TMEM_COLS)) cols <<= 1;
   p.tmem_cols = cols;
   p.diag = g_tc_tuning.diag;
   p.has_x = has_x ? 1 : 0;

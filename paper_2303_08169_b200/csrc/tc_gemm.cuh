@@ -29,6 +29,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
 struct TcTuning {
   int tma_store = 1;   // TMA-store epilogue when N_t % 32 == 0
   int max_stages = 4;  // A-stage ring depth cap
+  int max_acc = 4;     // TMEM accumulator ring depth cap (>= 2)
   int diag = 0;        // bit0: skip MMAs, bit1: skip the epilogue's global traffic
 };
 extern TcTuning g_tc_tuning;
