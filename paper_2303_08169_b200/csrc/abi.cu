@@ -594,6 +594,7 @@ int allegro_debug_gemm_bench(int device, int precision, int64_t M, int N, int K,
     const TcTuning saved = g_tc_tuning;
     g_tc_tuning.tma_store = tma_store;
     if (tma_store >= 2) g_tc_tuning.max_acc = tma_store;  // test hook: >= 2 sets the accumulator ring cap
+    if (tma_store < 0) g_tc_tuning.stack = 0;             // test hook: < 0 disables the stacked MMAs
     g_tc_tuning.max_stages = max_stages;
     g_tc_tuning.diag = diag;
     TcWeight t;

@@ -10,6 +10,9 @@
 //   warp 9      MMA issuer (one lane): per K-block 4 x K=8 steps of
 //               tcgen05.mma.kind::tf32 (A from TMEM, W from SMEM)
 //                 D += a_hi w_lo;  D += a_lo w_hi;  D += a_hi w_hi
+//               (N_t <= 64: "stacked" -- one MMA a_hi [w_hi | w_lo] of width 2 N_t into
+//               [D | D'] plus a_lo w_hi into D, so a_hi is read from TMEM once per K-step;
+//               the epilogue adds D + D')
 //               into one of two TMEM accumulators [128 lanes x N_t fp32 columns];
 //               tcgen05.commit frees the TMEM A stage / publishes the accumulator.
 //   warps 4-7   epilogue warpgroup: tcgen05.ld 32x32b (thread = row), fused epilogue, and a
@@ -21,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -167,6 +171,7 @@ struct TcParams {
   int n_mtiles;
   int acc_cols;        // TMEM columns per accumulator (>= N_t, multiple of 32)
   int n_acc;           // accumulator ring depth (2..4)
+  int stack;           // 1: stacked hi/lo MMA (N_t in {32, 64})
   uint32_t tmem_cols;  // allocated TMEM columns
   int diag;            // diagnostics: bit0 skip MMAs, bit1 skip global stores
   int has_x;           // the epilogue reads an [M][N] input (X, or old C) through the TMA ring
@@ -246,8 +251,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   // 1024-align inside the __shared__ array (pointer arithmetic keeps the shared address space)
   unsigned char* base = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
-  unsigned char* w_hi = base;
-  unsigned char* w_lo = base + p.w_bytes / 2;
+  unsigned char* w_img = base;  // per K-block: [w_hi rows][w_lo rows]
   unsigned char* stage0 = base + ((p.w_bytes + 1023) & ~1023u);
   unsigned char* out_stage = stage0 + (size_t)p.stages * STAGE_BYTES;  // [4 warps][4 KB]
   unsigned char* x_stage = out_stage + 4 * STAGE_OUT_BYTES;            // [X_STAGES][16 KB] (if has_x)
@@ -372,8 +376,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.N_t >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
     mbar_wait(w_full, 0);
     tc_fence_after();
-    const uint32_t whi = smem_u32(w_hi), wlo = smem_u32(w_lo);
-    const uint32_t wblk = (uint32_t)p.N_t * 128;  // bytes of one W K-block
+    const uint32_t idesc2 = idesc + ((uint32_t)(p.N_t >> 3) << 17);  // width 2 N_t (stacked)
+    const uint32_t wimg = smem_u32(w_img);
+    const uint32_t wblk = (uint32_t)p.N_t * 128;  // bytes of one W half-block (hi or lo)
     int j = 0;
     uint32_t aph = 0;
     for (int t = 0; t < n_my; ++t) {
@@ -391,10 +396,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int k = 0; k < 4; ++k) {
             if (p.diag & 1) break;
             const uint32_t ko = k * 32;  // 8 tf32 = 32 bytes of a W row
-            const uint64_t dwh = sdesc(whi + kb * wblk + ko), dwl = sdesc(wlo + kb * wblk + ko);
-            mma_tf32_ts(d, ahi + 8 * k, dwl, idesc, (kb | k) ? 1u : 0u);
-            mma_tf32_ts(d, alo + 8 * k, dwh, idesc, 1u);
-            mma_tf32_ts(d, ahi + 8 * k, dwh, idesc, 1u);
+            const uint32_t wh = wimg + kb * 2 * wblk + ko;
+            const uint64_t dwh = sdesc(wh), dwl = sdesc(wh + wblk);
+            if (p.stack) {
+              mma_tf32_ts(d, ahi + 8 * k, dwh, idesc2, (kb | k) ? 1u : 0u);  // [D | D'] += a_hi [w_hi | w_lo]
+              mma_tf32_ts(d, alo + 8 * k, dwh, idesc, 1u);
+            } else {
+              mma_tf32_ts(d, ahi + 8 * k, dwl, idesc, (kb | k) ? 1u : 0u);
+              mma_tf32_ts(d, alo + 8 * k, dwh, idesc, 1u);
+              mma_tf32_ts(d, ahi + 8 * k, dwh, idesc, 1u);
+            }
           }
           mma_commit(a_empty + j);
           if (kb == p.nK - 1) mma_commit(acc_full + a);
@@ -462,6 +473,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         tmem_ld32(tbase + (uint32_t)c0, v);
+        if (p.stack) {  // + a_hi w_lo, accumulated beside D
+          float v2[32];
+          tmem_ld32(tbase + (uint32_t)(p.N_t + c0), v2);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += v2[j];
+        }
         if (p.diag & 2) continue;
         const int64_t col = p.col0 + c0;
         const int nc = (p.N_t - c0) >= 32 ? 8 : (p.N_t - c0) / 4;
@@ -514,7 +531,12 @@ int g_num_sms = 0;
 
 }  // namespace
 
-TcTuning g_tc_tuning;
+TcTuning make_tuning() {
+  TcTuning t;
+  if (const char* e = std::getenv("ALLEGRO_TC_STACK")) t.stack = std::atoi(e) != 0;  // A/B switch for measurements
+  return t;
+}
+TcTuning g_tc_tuning = make_tuning();
 
 float tf32_hi(float x) {
   uint32_t u;
@@ -546,14 +568,14 @@ TcWeight tc_prepare_weight(const std::vector<float>& W, int K, int N, std::vecto
   std::vector<float> img(t.tile_bytes / 4 * t.n_tiles, 0.f);
   for (int tile = 0; tile < t.n_tiles; ++tile) {
     float* hi = img.data() + tile * (t.tile_bytes / 4);
-    float* lo = hi + t.tile_bytes / 8;
+    float* lo = hi + (size_t)nt * 128 / 4;  // each K-block holds [hi rows][lo rows]
     for (int n = 0; n < nt; ++n)
       for (int k = 0; k < nK * BLK_K; ++k) {
         const float w = k < K ? W[(size_t)k * N + tile * nt + n] : 0.f;
         const float h = tf32_hi(w);
         const int kb = k / BLK_K, kk = k % BLK_K;
         // byte offset inside the K-block: row n (128 B), 16-byte chunk swizzled by n % 8
-        const size_t off = (size_t)kb * nt * 128 + (size_t)n * 128 + (size_t)(((kk / 4) ^ (n % 8)) * 16) + (kk % 4) * 4;
+        const size_t off = (size_t)kb * 2 * nt * 128 + (size_t)n * 128 + (size_t)(((kk / 4) ^ (n % 8)) * 16) + (kk % 4) * 4;
         hi[off / 4] = h;
         lo[off / 4] = w - h;
       }
@@ -603,7 +625,11 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   p.stages = stages;
   p.w_bytes = (uint32_t)w_bytes;
   p.n_mtiles = (int)((g.M + ROWS - 1) / ROWS);
-  p.acc_cols = (w.N_t + 31) / 32 * 32;
+  // stacked hi/lo MMAs where the tensor pipe paces the kernel (A/B on one B200,
+  // profiles/r01_gemm_stack_ab.jsonl): N_t = 32 always, N_t = 64 from K = 64 (at K = 32 the
+  // doubled accumulator read makes the epilogue the bottleneck)
+  p.stack = (g_tc_tuning.stack && (w.N_t == 32 || (w.N_t == 64 && g.K >= 64))) ? 1 : 0;
+  p.acc_cols = (p.stack ? 2 : 1) * ((w.N_t + 31) / 32 * 32);
   // TMEM: two accumulators + the A ring (64 columns per stage), power of two <= 512
   // a deeper accumulator ring for narrow tiles lets the MMAs run further ahead of the epilogue
   p.n_acc = std::max(2, std::min(g_tc_tuning.max_acc, (512 - 4 * A_TMEM_COLS) / p.acc_cols));

@@ -1,4 +1,4 @@
-"""A-ring / accumulator-ring depth sweep of the C5 contraction shapes (tcgen05 3xTF32 GEMM; diagnostics).
+"""Stacked-vs-three-MMA comparison of the C5 contraction shapes (tcgen05 3xTF32 GEMM; diagnostics).
 
 Prints one JSON line per shape: ms per launch and algorithmic GB/s for each max_stages."""
 import json
@@ -17,8 +17,9 @@ for N, K, epi in SHAPES:
     x = epi in (3, 4, 6, 7, 8)
     byt = 4.0 * M * (K + N * (1 + aux + x))
     out = {"N": N, "K": K, "epi": epi}
-    for st in (4, 8):
-        for acc in (2, 4):  # tma_store >= 2: accumulator ring cap (test hook)
-            ms = pb.debug_gemm_bench(M, N, K, epi, iters=5, max_stages=st, tma_store=acc)
-            out[f"st{st}_acc{acc}_gbs"] = round(byt / 1e6 / ms, 1)
+    # tma_store hook: 1 = production, -1 = stacked hi/lo MMAs disabled, >= 2 = accumulator ring cap
+    for rep in range(2):  # alternate the two variants to cancel drift
+        for name, hook in (("stacked", 1), ("three_mma", -1)):
+            ms = pb.debug_gemm_bench(M, N, K, epi, iters=5, max_stages=4, tma_store=hook)
+            out[f"{name}_gbs_{rep}"] = round(byt / 1e6 / ms, 1)
     print(json.dumps(out), flush=True)

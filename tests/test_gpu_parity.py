@@ -80,7 +80,7 @@ def test_edges_random_boxes_incl_multi_image(pb, tmp_path, seed):
 
 
 @pytest.mark.parametrize("M,N,K", [(1000, 32, 16), (4097, 128, 128), (300, 64, 224), (129, 16, 32), (5000, 192, 128),
-                                   (777, 96, 96)])
+                                   (777, 96, 96), (3001, 32, 96), (2050, 64, 32), (517, 32, 64)])
 def test_gemm_kernels(pb, M, N, K):
     """Both contraction kernels against an fp64 matmul (ragged M, all N/K shapes used)."""
     rng = np.random.default_rng(M + N + K)
