@@ -137,6 +137,46 @@ int md_set_thermostat(allegro_ctx* ctx, double T_target_K, double tau_fs);
  * returns ALLEGRO_E_NONFINITE with steps_done set.  out may be NULL. */
 int md_step(allegro_ctx* ctx, int64_t n_steps, double dt_fs, md_report* out);
 
+/* Time-to-failure harness (NEXT-2 of SURVEY.md §8(f); §3.2 and Eq. 4).
+ * The paper's protocol: NVT at 200 K for 1,000 steps, then NVE "until it fails"; the paper
+ * does not define failure, so the criteria are SPEC.md:459's (D24):
+ *   non_finite           a non-finite energy / force / velocity (every step),
+ *   displacement_blowup  some atom drifts more than disp_max A in one step (every step),
+ *   energy_drift         |E - E0| > drift_tol |E0| with E = E_pot + E_kin, checked every
+ *                        check_interval NVE steps (E0 at the start of NVE).
+ * Outliers (Fig. 1: |F_a| > mean + k sigma of the force norms at NVE start)
+ * are recorded every outlier_interval steps but never trigger a failure. */
+typedef struct {
+  int64_t nvt_steps;        /* NVT steps before NVE (paper 1,000); 0 = start in NVE */
+  double T_K, tau_fs;       /* NVT target (paper 200 K) and time constant (D23) */
+  int64_t max_nve_steps;    /* censoring cap */
+  int64_t check_interval;   /* energy-drift check cadence (SPEC: 100) */
+  double drift_tol;         /* relative energy drift (SPEC: 0.1) */
+  double disp_max;          /* single-step displacement limit, A; <= 0 disables */
+  double outlier_k;         /* outlier threshold in sigmas (paper: 5) */
+  int64_t outlier_interval; /* outlier-count cadence in NVE steps (>= 1) */
+} md_ttf_protocol;
+
+enum { ALLEGRO_TTF_CENSORED = 0, ALLEGRO_TTF_NONFINITE = 1, ALLEGRO_TTF_DISPLACEMENT = 2, ALLEGRO_TTF_ENERGY_DRIFT = 3 };
+
+typedef struct {
+  int64_t steps_survived; /* NVE steps completed before the failing one; max_nve_steps if censored */
+  int64_t fail_step;      /* 1-based NVE step at which failure was detected; 0 if censored */
+  int reason;             /* ALLEGRO_TTF_* */
+  int failed_in_nvt;      /* 1: non-finite during thermalisation (NVE never started) */
+  double e0, e_last;      /* E_pot + E_kin at NVE start and at the last drift check, eV */
+  double f_mean, f_sigma; /* outlier baseline at NVE start, eV/A */
+  int64_t n_series;       /* outlier counts written to the caller's series */
+} md_ttf_result;
+
+/* Runs the protocol from the current MD state (md_set_state first); the state afterwards is
+ * the state at failure.  series (caller-owned, series_cap entries, may be NULL if 0) receives
+ * the global outlier count every outlier_interval NVE steps.  Collective when world_size > 1.
+ * Errors: ALLEGRO_E_ARG (bad protocol), ALLEGRO_E_STATE; a failure of the dynamics is a result
+ * (reason), not an error. */
+int md_run_ttf(allegro_ctx* ctx, double dt_fs, const md_ttf_protocol* protocol, int64_t* series, int64_t series_cap,
+               md_ttf_result* out);
+
 /* End-to-end variant of md_step for HOST-resident state (the e2e measurement of bench.py):
  * copies species [n], pos/vel/forces [n][3] (forces = F at pos, e.g. from the previous call
  * or from md_get_state) host -> device, runs n_steps exactly as md_step, and writes pos, vel

@@ -65,6 +65,36 @@ class MdReport(C.Structure):
     ]
 
 
+class TtfProtocol(C.Structure):
+    _fields_ = [
+        ("nvt_steps", C.c_int64),
+        ("T_K", C.c_double),
+        ("tau_fs", C.c_double),
+        ("max_nve_steps", C.c_int64),
+        ("check_interval", C.c_int64),
+        ("drift_tol", C.c_double),
+        ("disp_max", C.c_double),
+        ("outlier_k", C.c_double),
+        ("outlier_interval", C.c_int64),
+    ]
+
+
+class TtfResult(C.Structure):
+    _fields_ = [
+        ("steps_survived", C.c_int64),
+        ("fail_step", C.c_int64),
+        ("reason", C.c_int),
+        ("failed_in_nvt", C.c_int),
+        ("e0", C.c_double),
+        ("e_last", C.c_double),
+        ("f_mean", C.c_double),
+        ("f_sigma", C.c_double),
+        ("n_series", C.c_int64),
+    ]
+
+
+TTF_REASONS = {0: "censored", 1: "non_finite", 2: "displacement_blowup", 3: "energy_drift"}
+
 _P = C.c_void_p
 _lib.allegro_create.argtypes = [C.POINTER(AllegroParams), C.POINTER(_P)]
 _lib.allegro_destroy.argtypes = [_P]
@@ -96,6 +126,7 @@ _lib.allegro_local_count.argtypes = [_P]
 _lib.allegro_local_count.restype = C.c_int64
 _lib.allegro_profile_detail.argtypes = [_P, C.c_int, _P, C.c_int, _P, _P, _P]
 _lib.md_set_thermostat.argtypes = [_P, C.c_double, C.c_double]
+_lib.md_run_ttf.argtypes = [_P, C.c_double, C.POINTER(TtfProtocol), _P, C.c_int64, C.POINTER(TtfResult)]
 _lib.md_get_local_state.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), _P, _P, _P, _P, _P]
 _lib.allegro_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, _P, _P, _P]
 _lib.allegro_debug_gemm_bench.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -108,7 +139,7 @@ EXPORTED = [
     "allegro_layer_paths", "allegro_version", "md_step_host", "allegro_profile", "allegro_profile_read",
     "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name", "allegro_debug_gemm",
     "allegro_debug_gemm_bench", "allegro_nccl_unique_id", "allegro_local_count",
-    "md_get_local_state", "md_set_thermostat",
+    "md_get_local_state", "md_set_thermostat", "md_run_ttf",
     "allegro_profile_detail",
 ]
 
@@ -290,6 +321,22 @@ class Allegro:
     def md_set_thermostat(self, T_target: float = 200.0, tau_fs: float = 100.0):
         """Nose-Hoover NVT at T_target (K) with time constant tau_fs; tau_fs <= 0 -> NVE."""
         self._check(_lib.md_set_thermostat(self._h, T_target, tau_fs))
+
+    def md_run_ttf(self, dt_fs: float = 2.0, nvt_steps: int = 1000, T_K: float = 200.0, tau_fs: float = 100.0,
+                   max_nve_steps: int = 100000, check_interval: int = 100, drift_tol: float = 0.1,
+                   disp_max: float = 0.5, outlier_k: float = 5.0, outlier_interval: int = 1):
+        """Time-to-failure protocol (include/allegro.h md_run_ttf): NVT thermalisation, then NVE
+        until non-finite / displacement blow-up / energy drift.  Returns (result dict, outlier
+        series as an int64 array)."""
+        pr = TtfProtocol(nvt_steps, T_K, tau_fs, max_nve_steps, check_interval, drift_tol, disp_max, outlier_k,
+                         outlier_interval)
+        cap = max(max_nve_steps, 0) // max(outlier_interval, 1)  # the C side validates the protocol
+        series = np.zeros(max(cap, 1), dtype=np.int64)
+        r = TtfResult()
+        self._check(_lib.md_run_ttf(self._h, dt_fs, C.byref(pr), series.ctypes.data, cap, C.byref(r)))
+        out = {f: getattr(r, f) for f, _ in TtfResult._fields_}
+        out["reason_name"] = TTF_REASONS[r.reason]
+        return out, series[: r.n_series].copy()
 
     def md_count_outliers(self, mean: float, sigma: float, k: float = 5.0) -> int:
         c = C.c_int64(0)

@@ -388,6 +388,72 @@ int md_set_thermostat(allegro_ctx* c, double T_target, double tau_fs) {
   return ALLEGRO_OK;
 }
 
+int md_run_ttf(allegro_ctx* c, double dt, const md_ttf_protocol* pr, int64_t* series, int64_t series_cap,
+               md_ttf_result* out) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (!c->md_ready) return fail(c, ALLEGRO_E_STATE, "md_set_state has not been called");
+  if (!pr || !out || !(dt > 0 && std::isfinite(dt)) || pr->nvt_steps < 0 || pr->max_nve_steps < 0 ||
+      pr->check_interval < 1 || pr->outlier_interval < 1 || series_cap < 0 || (series_cap > 0 && !series) ||
+      !(pr->drift_tol > 0) || (pr->nvt_steps > 0 && !(pr->T_K > 0 && pr->tau_fs > 0)))
+    return fail(c, ALLEGRO_E_ARG, "bad time-to-failure protocol");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    std::memset(out, 0, sizeof(*out));
+    // (1) NVT thermalisation (1,000 steps at 200 K)
+    if (pr->nvt_steps > 0) {
+      const int rc0 = md_set_thermostat(c, pr->T_K, pr->tau_fs);
+      if (rc0 != ALLEGRO_OK) return rc0;
+      const int rc = md_run(c, pr->nvt_steps, dt, nullptr);
+      c->nvt = false;
+      if (rc == ALLEGRO_E_NONFINITE) {  // failed before NVE started
+        out->reason = ALLEGRO_TTF_NONFINITE;
+        out->failed_in_nvt = 1;
+        return ALLEGRO_OK;
+      }
+      if (rc != ALLEGRO_OK) return rc;
+    }
+    c->nvt = false;
+    // (2) NVE until failure ("continue the simulation until it fails")
+    out->e0 = c->e_pot + md_kinetic(c);
+    out->e_last = out->e0;
+    force_stats(c, &out->f_mean, &out->f_sigma);
+    const double thr = out->f_mean + pr->outlier_k * out->f_sigma;
+    c->disp_max2 = pr->disp_max > 0 ? pr->disp_max * pr->disp_max : 0.0;
+    int64_t s = 1;
+    int rc = ALLEGRO_OK;
+    for (; s <= pr->max_nve_steps; ++s) {
+      ALG_CUDA(cudaMemsetAsync(c->flags.p + 4, 0, sizeof(int), c->stream));
+      rc = md_run(c, 1, dt, nullptr);
+      if (rc == ALLEGRO_E_NONFINITE) {
+        out->reason = ALLEGRO_TTF_NONFINITE;
+        rc = ALLEGRO_OK;
+        break;
+      }
+      if (rc != ALLEGRO_OK) break;
+      int blow = 0;
+      ALG_CUDA(cudaMemcpyAsync(&blow, c->flags.p + 4, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      ALG_CUDA(cudaStreamSynchronize(c->stream));
+      if (allreduce_max_i32(c, blow)) {
+        out->reason = ALLEGRO_TTF_DISPLACEMENT;
+        break;
+      }
+      if (s % pr->check_interval == 0) {
+        out->e_last = c->e_pot + md_kinetic(c);
+        if (std::fabs(out->e_last - out->e0) > pr->drift_tol * std::fabs(out->e0)) {
+          out->reason = ALLEGRO_TTF_ENERGY_DRIFT;
+          break;
+        }
+      }
+      if (s % pr->outlier_interval == 0 && out->n_series < series_cap)  // steps that did not fail
+        series[out->n_series++] = count_outliers(c, thr);
+    }
+    c->disp_max2 = 0.0;
+    out->fail_step = out->reason ? s : 0;
+    out->steps_survived = out->reason ? s - 1 : pr->max_nve_steps;
+    return rc;
+  });
+}
+
 int allegro_nccl_unique_id(void* out128) {
   if (!out128) return fail(nullptr, ALLEGRO_E_ARG, "out is NULL");
   return guarded(nullptr, [&]() -> int {

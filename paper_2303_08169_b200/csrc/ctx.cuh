@@ -176,6 +176,7 @@ struct allegro_ctx {
   // Nose-Hoover NVT (one thermostat; D23): off when tau <= 0
   bool nvt = false;
   double nvt_T = 0, nvt_tau = 0, nvt_Q = 0, nvt_xi = 0, nvt_eta = 0;
+  double disp_max2 = 0;  // time-to-failure harness: squared single-step displacement limit (0 = off)
   bool baseline_set = false;
   allegro::Profiler prof;
   allegro::Domain dom;

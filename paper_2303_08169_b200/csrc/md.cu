@@ -18,21 +18,27 @@ constexpr int kRedThreads = 1024;
 
 __device__ __forceinline__ double mass_of(int z) { return z == 1 ? kMassN : kMassH; }
 
+// disp_max2 > 0: flag (blowup) when the drift |dt v| of an atom exceeds sqrt(disp_max2)
+// (time-to-failure harness, "displacement_blowup")
 __global__ void k_kick_drift(double* __restrict__ pos, double* __restrict__ vel, const double* __restrict__ frc,
-                             const int32_t* __restrict__ species, int64_t n, double dt, double Lx, double Ly, double Lz) {
+                             const int32_t* __restrict__ species, int64_t n, double dt, double Lx, double Ly, double Lz,
+                             double disp_max2, int* __restrict__ blowup) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n) return;
   const double m = mass_of(species[a]);
   const double L[3] = {Lx, Ly, Lz};
+  double d2 = 0.0;
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const double v = vel[a * 3 + d] + 0.5 * dt * kKappa * frc[a * 3 + d] / m;
     vel[a * 3 + d] = v;
+    d2 += (dt * v) * (dt * v);
     const double x = pos[a * 3 + d] + dt * v;
     double y = __dsub_rn(x, __dmul_rn(L[d], floor(__ddiv_rn(x, L[d]))));
     if (y >= L[d]) y = 0.0;
     pos[a * 3 + d] = y;
   }
+  if (disp_max2 > 0.0 && !(d2 <= disp_max2)) atomicOr(blowup, 1);
 }
 
 __global__ void k_kick(double* __restrict__ vel, const double* __restrict__ frc, const int32_t* __restrict__ species,
@@ -124,7 +130,8 @@ void md_half_kick_drift(allegro_ctx* c, double dt) {
   {
     ProfScope ps_(&c->prof, c->stream, PK_VERLET, 0, 124.0 * c->n);
     k_kick_drift<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->pos.p, c->vel.p, c->frc.p, c->species.p, c->n, dt,
-                                                           c->box[0], c->box[1], c->box[2]);
+                                                           c->box[0], c->box[1], c->box[2], c->disp_max2,
+                                                           c->flags.p + 4);
   }
   ALG_LAUNCH_CHECK();
 }

@@ -44,10 +44,13 @@ CONFIGS = {
 }
 
 
-def system(cfg: Config | str, temperature: float = 200.0, reps=(1, 1, 1)) -> nh3.System:
+def system(cfg: Config | str, temperature: float = 200.0, reps=(1, 1, 1), seed: int = 0) -> nh3.System:
+    """seed 0 = the recipe's default streams (orientations 1, velocities 2); seed k uses
+    1 + 2k and 2 + 2k (independent instances, e.g. the >= 10 time-to-failure runs per N)."""
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
-    s = nh3.maxwell_boltzmann(nh3.nh3_box(cfg.lattice, cfg.cells), temperature)
+    s = nh3.maxwell_boltzmann(nh3.nh3_box(cfg.lattice, cfg.cells, structure_seed=1 + 2 * seed), temperature,
+                              velocity_seed=2 + 2 * seed)
     if tuple(reps) != (1, 1, 1):
         s = nh3.replicate(s, reps)
     return s
