@@ -177,6 +177,40 @@ typedef struct {
 int md_run_ttf(allegro_ctx* ctx, double dt_fs, const md_ttf_protocol* protocol, int64_t* series, int64_t series_cap,
                md_ttf_result* out);
 
+/* ---- Replica batches and ring-polymer PIMD (NEXT-3; §5; D25) ----
+ * A batch of n_rep independent copies ("replicas", PIMD beads) of one n_per-atom system in
+ * the box given at create, evaluated in ONE pass of the kernels: cells and edges are keyed by
+ * replica, so replica r's energy and forces are exactly those of a single evaluation of it.
+ * world_size must be 1.  pos / forces: [n_rep][n_per][3] A, eV/A (replica-major); species
+ * [n_per] (shared by all replicas); e_rep [n_rep] eV; e_atom [n_rep * n_per] or NULL.
+ * where = ALLEGRO_HOST / ALLEGRO_DEVICE for every array. */
+int allegro_compute_energy_forces_batch(allegro_ctx* ctx, int64_t n_rep, int64_t n_per, int where,
+                                        const int32_t* species, const double* pos, double* e_rep, double* e_atom,
+                                        double* forces);
+
+/* Ring-polymer MD: P = n_beads (1..64) beads per atom at physical temperature T_K, RPMD
+ * Hamiltonian H_P = sum_j [K_j + V(q_j)] + sum_i sum_j m_i w_P^2 |q_ij - q_i,j+1|^2 / 2 with
+ * w_P = P k_B T / hbar; each step: half kick with the bead forces, exact free ring-polymer
+ * evolution in normal modes over dt, one batched force evaluation of all beads, half kick.
+ * No thermostat (microcanonical RPMD).  Host arrays: species [n_per], pos / vel
+ * [n_beads][n_per][3] (A, A/fs; positions are kept unwrapped so the springs see bead
+ * differences, the force evaluation wraps a copy). */
+int pimd_set_state(allegro_ctx* ctx, int64_t n_beads, int64_t n_per, const int32_t* species, const double* pos,
+                   const double* vel, double T_K);
+typedef struct {
+  int64_t steps_done;
+  double e_pot_mean;        /* (1/P) sum_j V(q_j), eV */
+  double e_spring;          /* ring-polymer spring energy, eV */
+  double e_kin;             /* kinetic energy of all beads, eV */
+  double h_conserved;       /* sum_j V(q_j) + e_kin + e_spring (RPMD Hamiltonian), eV */
+  double temperature_beads; /* 2 e_kin / (3 N P k_B), K (equals P T at equilibrium) */
+  double omega_p;           /* P k_B T / hbar, 1/fs */
+  int64_t n_edges;          /* edges of all beads */
+} pimd_report;
+int pimd_step(allegro_ctx* ctx, int64_t n_steps, double dt_fs, pimd_report* out);
+/* host arrays [n_beads][n_per][3] (pos unwrapped) and e_rep [n_beads]; any may be NULL */
+int pimd_get_state(allegro_ctx* ctx, double* pos, double* vel, double* forces, double* e_rep);
+
 /* End-to-end variant of md_step for HOST-resident state (the e2e measurement of bench.py):
  * copies species [n], pos/vel/forces [n][3] (forces = F at pos, e.g. from the previous call
  * or from md_get_state) host -> device, runs n_steps exactly as md_step, and writes pos, vel

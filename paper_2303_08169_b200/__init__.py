@@ -93,6 +93,19 @@ class TtfResult(C.Structure):
     ]
 
 
+class PimdReport(C.Structure):
+    _fields_ = [
+        ("steps_done", C.c_int64),
+        ("e_pot_mean", C.c_double),
+        ("e_spring", C.c_double),
+        ("e_kin", C.c_double),
+        ("h_conserved", C.c_double),
+        ("temperature_beads", C.c_double),
+        ("omega_p", C.c_double),
+        ("n_edges", C.c_int64),
+    ]
+
+
 TTF_REASONS = {0: "censored", 1: "non_finite", 2: "displacement_blowup", 3: "energy_drift"}
 
 _P = C.c_void_p
@@ -126,6 +139,10 @@ _lib.allegro_local_count.argtypes = [_P]
 _lib.allegro_local_count.restype = C.c_int64
 _lib.allegro_profile_detail.argtypes = [_P, C.c_int, _P, C.c_int, _P, _P, _P]
 _lib.md_set_thermostat.argtypes = [_P, C.c_double, C.c_double]
+_lib.allegro_compute_energy_forces_batch.argtypes = [_P, C.c_int64, C.c_int64, C.c_int, _P, _P, _P, _P, _P]
+_lib.pimd_set_state.argtypes = [_P, C.c_int64, C.c_int64, _P, _P, _P, C.c_double]
+_lib.pimd_step.argtypes = [_P, C.c_int64, C.c_double, C.POINTER(PimdReport)]
+_lib.pimd_get_state.argtypes = [_P, _P, _P, _P, _P]
 _lib.md_run_ttf.argtypes = [_P, C.c_double, C.POINTER(TtfProtocol), _P, C.c_int64, C.POINTER(TtfResult)]
 _lib.md_get_local_state.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), _P, _P, _P, _P, _P]
 _lib.allegro_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, _P, _P, _P]
@@ -140,6 +157,7 @@ EXPORTED = [
     "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name", "allegro_debug_gemm",
     "allegro_debug_gemm_bench", "allegro_nccl_unique_id", "allegro_local_count",
     "md_get_local_state", "md_set_thermostat", "md_run_ttf",
+    "allegro_compute_energy_forces_batch", "pimd_set_state", "pimd_step", "pimd_get_state",
     "allegro_profile_detail",
 ]
 
@@ -337,6 +355,41 @@ class Allegro:
         out = {f: getattr(r, f) for f, _ in TtfResult._fields_}
         out["reason_name"] = TTF_REASONS[r.reason]
         return out, series[: r.n_series].copy()
+
+    def compute_energy_forces_batch(self, pos, species):
+        """Replica batch (allegro_compute_energy_forces_batch): pos [n_rep][n_per][3], species
+        [n_per] (host numpy) -> (e_rep [n_rep], e_atom [n_rep][n_per], forces [n_rep][n_per][3])."""
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        species = np.ascontiguousarray(species, dtype=np.int32)
+        n_rep, n_per = pos.shape[0], pos.shape[1]
+        e_rep = np.empty(n_rep)
+        e_atom = np.empty((n_rep, n_per))
+        frc = np.empty((n_rep, n_per, 3))
+        self._check(_lib.allegro_compute_energy_forces_batch(self._h, n_rep, n_per, HOST, species.ctypes.data,
+                                                             pos.ctypes.data, e_rep.ctypes.data, e_atom.ctypes.data,
+                                                             frc.ctypes.data))
+        return e_rep, e_atom, frc
+
+    def pimd_set_state(self, species, pos, vel, T_K: float):
+        """Ring-polymer state: species [n_per], pos / vel [n_beads][n_per][3] (host)."""
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        vel = np.ascontiguousarray(vel, dtype=np.float64)
+        species = np.ascontiguousarray(species, dtype=np.int32)
+        self._pimd_shape = pos.shape
+        self._check(_lib.pimd_set_state(self._h, pos.shape[0], pos.shape[1], species.ctypes.data, pos.ctypes.data,
+                                        vel.ctypes.data, T_K))
+
+    def pimd_step(self, n_steps: int, dt_fs: float = 0.5) -> PimdReport:
+        r = PimdReport()
+        self._check(_lib.pimd_step(self._h, n_steps, dt_fs, C.byref(r)))
+        return r
+
+    def pimd_get_state(self):
+        """-> (pos (unwrapped), vel, forces) [n_beads][n_per][3] and e_rep [n_beads]."""
+        P, N, _ = self._pimd_shape
+        pos, vel, frc, e = np.empty((P, N, 3)), np.empty((P, N, 3)), np.empty((P, N, 3)), np.empty(P)
+        self._check(_lib.pimd_get_state(self._h, pos.ctypes.data, vel.ctypes.data, frc.ctypes.data, e.ctypes.data))
+        return pos, vel, frc, e
 
     def md_count_outliers(self, mean: float, sigma: float, k: float = 5.0) -> int:
         c = C.c_int64(0)

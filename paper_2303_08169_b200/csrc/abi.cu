@@ -144,6 +144,10 @@ void allegro_destroy(allegro_ctx* c) {
   free_model(c->model);
   domain_teardown(c);
   c->aspec.release();
+  c->pq.release();
+  c->pimd_c.release();
+  c->pimd_mode.release();
+  c->e_rep.release();
   c->pos.release();
   c->vel.release();
   c->frc.release();
@@ -199,6 +203,8 @@ int allegro_compute_energy_forces(allegro_ctx* c, int64_t n, int where, const in
     if (box)
       for (int d = 0; d < 3; ++d) c->box[d] = box[d];
     c->n = n;
+    c->n_rep = 1, c->n_per = n;
+    c->pimd_ready = false;
     reserve_atoms(c, n);
     const cudaMemcpyKind kin = where == ALLEGRO_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     const cudaMemcpyKind kout = where == ALLEGRO_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
@@ -233,6 +239,8 @@ int md_set_state(allegro_ctx* c, int64_t n, const int32_t* species, const double
   if (n <= 0 || !species || !pos || !vel) return fail(c, ALLEGRO_E_ARG, "NULL argument or n <= 0");
   return guarded(c, [&]() -> int {
     ALG_CUDA(cudaSetDevice(c->device));
+    c->n_rep = 1, c->n_per = 0;
+    c->pimd_ready = false;
     if (c->dom.multi) {
       select_owned(c, n, species, pos, vel);  // this rank's domain, in gid order
     } else {
@@ -451,6 +459,128 @@ int md_run_ttf(allegro_ctx* c, double dt, const md_ttf_protocol* pr, int64_t* se
     out->fail_step = out->reason ? s : 0;
     out->steps_survived = out->reason ? s - 1 : pr->max_nve_steps;
     return rc;
+  });
+}
+
+int allegro_compute_energy_forces_batch(allegro_ctx* c, int64_t n_rep, int64_t n_per, int where, const int32_t* species,
+                                        const double* pos, double* e_rep, double* e_atom, double* forces) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (n_rep < 1 || n_per < 1 || !species || !pos || !e_rep || !forces)
+    return fail(c, ALLEGRO_E_ARG, "NULL argument or n_rep / n_per < 1");
+  if (where != ALLEGRO_HOST && where != ALLEGRO_DEVICE) return fail(c, ALLEGRO_E_ARG, "where must be HOST or DEVICE");
+  if (c->dom.multi) return fail(c, ALLEGRO_E_ARG, "replica batches need world_size == 1");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    const int64_t n = n_rep * n_per;
+    c->n = n;
+    reserve_atoms(c, n);
+    const cudaMemcpyKind kin = where == ALLEGRO_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const cudaMemcpyKind kout = where == ALLEGRO_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    ALG_CUDA(cudaMemcpyAsync(c->pos.p, pos, sizeof(double) * 3 * n, kin, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->species.p, species, sizeof(int32_t) * n_per, kin, c->stream));
+    set_replicas(c, n_rep, n_per, c->species.p);  // in place: replica 0 is the source
+    c->md_ready = false;
+    c->pimd_ready = false;
+    const int rc = evaluate(c);
+    replica_energies(c);
+    ALG_CUDA(cudaMemcpyAsync(e_rep, c->e_rep.p, sizeof(double) * n_rep, kout, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, sizeof(double) * 3 * n, kout, c->stream));
+    if (e_atom) ALG_CUDA(cudaMemcpyAsync(e_atom, c->e_atom.p, sizeof(double) * n, kout, c->stream));
+    ALG_CUDA(cudaStreamSynchronize(c->stream));
+    c->prof.flush();
+    return rc;
+  });
+}
+
+int pimd_set_state(allegro_ctx* c, int64_t n_beads, int64_t n_per, const int32_t* species, const double* pos,
+                   const double* vel, double T_K) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (n_beads < 1 || n_beads > 64 || n_per < 1 || !species || !pos || !vel || !(T_K > 0 && std::isfinite(T_K)))
+    return fail(c, ALLEGRO_E_ARG, "bad PIMD state (1 <= n_beads <= 64, n_per >= 1, T > 0)");
+  if (c->dom.multi) return fail(c, ALLEGRO_E_ARG, "PIMD needs world_size == 1");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    const int64_t n = n_beads * n_per;
+    c->n = n;
+    c->n_global = n;
+    reserve_atoms(c, n);
+    c->pq.reserve(3 * n);
+    ALG_CUDA(cudaMemcpyAsync(c->pq.p, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->pos.p, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->vel.p, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(c->species.p, species, sizeof(int32_t) * n_per, cudaMemcpyHostToDevice, c->stream));
+    set_replicas(c, n_beads, n_per, c->species.p);
+    c->pimd_T = T_K;
+    pimd_setup_modes(c, (int)n_beads);
+    c->md_ready = false;
+    c->pimd_ready = false;
+    const int rc = evaluate(c);
+    if (rc != ALLEGRO_OK) return rc;
+    c->pimd_ready = true;
+    c->pimd_steps = 0;
+    return ALLEGRO_OK;
+  });
+}
+
+static void pimd_fill_report(allegro_ctx* c, int64_t done, pimd_report* out) {
+  out->steps_done = done;
+  out->e_pot_mean = c->e_pot / (double)c->n_rep;
+  out->e_kin = md_kinetic(c);
+  out->e_spring = pimd_spring_energy(c);
+  out->h_conserved = c->e_pot + out->e_kin + out->e_spring;
+  out->temperature_beads = 2.0 * out->e_kin / (3.0 * (double)c->n * 8.617333e-5);
+  out->omega_p = pimd_omega_p(c);
+  out->n_edges = c->n_edges;
+}
+
+int pimd_step(allegro_ctx* c, int64_t n_steps, double dt, pimd_report* out) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (!c->pimd_ready) return fail(c, ALLEGRO_E_STATE, "pimd_set_state has not been called");
+  if (n_steps < 0 || !(dt > 0 && std::isfinite(dt))) return fail(c, ALLEGRO_E_ARG, "bad n_steps or dt");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    int64_t done = 0;
+    int rc = ALLEGRO_OK;
+    for (; done < n_steps; ++done) {
+      md_half_kick(c, dt);
+      pimd_free_step(c, dt);
+      ALG_CUDA(cudaMemcpyAsync(c->pos.p, c->pq.p, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToDevice, c->stream));
+      rc = evaluate(c);  // wraps the working copy; pq stays unwrapped (the springs need it)
+      if (rc != ALLEGRO_OK) {
+        ++done;
+        break;
+      }
+      md_half_kick(c, dt);
+      if (!all_finite(c)) {
+        rc = fail(c, ALLEGRO_E_NONFINITE, "non-finite velocity at PIMD step " + std::to_string(c->pimd_steps + 1));
+        ++done;
+        ++c->pimd_steps;
+        break;
+      }
+      ++c->pimd_steps;
+      c->prof.flush();
+    }
+    if (out) pimd_fill_report(c, done, out);
+    c->prof.flush();
+    return rc;
+  });
+}
+
+int pimd_get_state(allegro_ctx* c, double* pos, double* vel, double* forces, double* e_rep) {
+  if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
+  if (!c->pimd_ready) return fail(c, ALLEGRO_E_STATE, "pimd_set_state has not been called");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    const int64_t n = c->n;
+    if (pos) ALG_CUDA(cudaMemcpyAsync(pos, c->pq.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (vel) ALG_CUDA(cudaMemcpyAsync(vel, c->vel.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (forces) ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (e_rep) {
+      replica_energies(c);
+      ALG_CUDA(cudaMemcpyAsync(e_rep, c->e_rep.p, sizeof(double) * c->n_rep, cudaMemcpyDeviceToHost, c->stream));
+    }
+    ALG_CUDA(cudaStreamSynchronize(c->stream));
+    return ALLEGRO_OK;
   });
 }
 

@@ -145,6 +145,8 @@ struct allegro_ctx {
   int64_t n = 0;        // owned (this rank)
   int64_t n_global = 0; // atoms in the whole box (md state)
   int64_t n_ghost = 0;  // ghosts of the last build
+  int64_t n_rep = 1;    // replica batch (PIMD beads): n = n_rep * n_per, replica-major
+  int64_t n_per = 0;
   allegro::DBuf<double> pos, vel, frc;       // [n][3] owned state (fp64)
   allegro::DBuf<int32_t> species, gid;       // [n]
   allegro::DBuf<double> apos;                // [n + G][3] canonical image positions
@@ -177,6 +179,11 @@ struct allegro_ctx {
   bool nvt = false;
   double nvt_T = 0, nvt_tau = 0, nvt_Q = 0, nvt_xi = 0, nvt_eta = 0;
   double disp_max2 = 0;  // time-to-failure harness: squared single-step displacement limit (0 = off)
+  // ring-polymer PIMD (NEXT-3; D25): unwrapped bead state, replica-major [P][N][3]
+  bool pimd_ready = false;
+  int64_t pimd_steps = 0;
+  double pimd_T = 0;
+  allegro::DBuf<double> pq, pv, pimd_c, pimd_mode, e_rep;  // C [P][P]; per mode (cos, sin, w); [P]
   bool baseline_set = false;
   allegro::Profiler prof;
   allegro::Domain dom;
@@ -221,5 +228,13 @@ int64_t count_outliers(allegro_ctx* c, double thr);
 bool all_finite(allegro_ctx* c);
 double sum_e_atom(allegro_ctx* c);
 bool check_inputs(allegro_ctx* c);
+
+// pimd.cu (replica batches, ring-polymer MD; world_size == 1)
+void set_replicas(allegro_ctx* c, int64_t n_rep, int64_t n_per, const int32_t* species_dev_per);
+void replica_energies(allegro_ctx* c);  // c->e_rep[r] = sum of e_atom over replica r
+void pimd_setup_modes(allegro_ctx* c, int P);
+void pimd_free_step(allegro_ctx* c, double dt);
+double pimd_spring_energy(allegro_ctx* c);
+double pimd_omega_p(allegro_ctx* c);
 
 }  // namespace allegro

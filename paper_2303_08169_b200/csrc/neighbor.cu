@@ -123,30 +123,40 @@ __global__ void k_ghost_fill(const double* __restrict__ pos, const int32_t* __re
 struct CellGeom {
   double lo[3], inv[3];
   int n[3];
+  // replica batches (PIMD beads, NEXT-3): atom a belongs to replica owner(a) / n_per and the
+  // cells of replica r are [r * ncell_rep, (r + 1) * ncell_rep), so edges never cross
+  // replicas; n_per = 0: one replica
+  int64_t n_per;
+  int ncell_rep;
 };
+
+__device__ __forceinline__ int64_t cell_base(const CellGeom& c, int64_t owner) {
+  return c.n_per > 0 ? (owner / c.n_per) * (int64_t)c.ncell_rep : 0;
+}
 
 __device__ __forceinline__ int cell_coord(double x, const CellGeom& c, int d) {
   int q = (int)floor((x - c.lo[d]) * c.inv[d]);
   return q < 0 ? 0 : (q >= c.n[d] ? c.n[d] - 1 : q);
 }
 
-__global__ void k_cell_count(const double* __restrict__ apos, int64_t na, CellGeom cg, int32_t* __restrict__ ccount,
-                             int32_t* __restrict__ cslot) {
+__global__ void k_cell_count(const double* __restrict__ apos, const int32_t* __restrict__ aowner, int64_t na, CellGeom cg,
+                             int32_t* __restrict__ ccount, int32_t* __restrict__ cslot) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= na) return;
   const int cx = cell_coord(apos[a * 3], cg, 0), cy = cell_coord(apos[a * 3 + 1], cg, 1),
             cz = cell_coord(apos[a * 3 + 2], cg, 2);
-  const int c = (cz * cg.n[1] + cy) * cg.n[0] + cx;
+  const int64_t c = cell_base(cg, aowner[a]) + (cz * cg.n[1] + cy) * cg.n[0] + cx;
   cslot[a] = atomicAdd(ccount + c, 1);
 }
 
-__global__ void k_cell_fill(const double* __restrict__ apos, int64_t na, CellGeom cg, const int32_t* __restrict__ cstart,
-                            const int32_t* __restrict__ cslot, int32_t* __restrict__ sorted) {
+__global__ void k_cell_fill(const double* __restrict__ apos, const int32_t* __restrict__ aowner, int64_t na, CellGeom cg,
+                            const int32_t* __restrict__ cstart, const int32_t* __restrict__ cslot,
+                            int32_t* __restrict__ sorted) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= na) return;
   const int cx = cell_coord(apos[a * 3], cg, 0), cy = cell_coord(apos[a * 3 + 1], cg, 1),
             cz = cell_coord(apos[a * 3 + 2], cg, 2);
-  const int c = (cz * cg.n[1] + cy) * cg.n[0] + cx;
+  const int64_t c = cell_base(cg, aowner[a]) + (cz * cg.n[1] + cy) * cg.n[0] + cx;
   sorted[cstart[c] + cslot[a]] = (int32_t)a;
 }
 
@@ -171,6 +181,7 @@ __global__ void __launch_bounds__(kEdgeWarps * 32) k_edge_build(const double* __
   if (i >= n) return;
   const double xi = apos[i * 3], yi = apos[i * 3 + 1], zi = apos[i * 3 + 2];
   const int cx = cell_coord(xi, cg, 0), cy = cell_coord(yi, cg, 1), cz = cell_coord(zi, cg, 2);
+  const int64_t cb = cell_base(cg, i);
   int cnt = 0;
   for (int dz = -1; dz <= 1; ++dz) {
     const int z = cz + dz;
@@ -181,7 +192,7 @@ __global__ void __launch_bounds__(kEdgeWarps * 32) k_edge_build(const double* __
       for (int dx = -1; dx <= 1; ++dx) {
         const int x = cx + dx;
         if (x < 0 || x >= cg.n[0]) continue;
-        const int c = (z * cg.n[1] + y) * cg.n[0] + x;
+        const int64_t c = cb + (z * cg.n[1] + y) * cg.n[0] + x;
         const int s0 = cstart[c], s1 = cstart[c + 1];
         for (int t0 = s0; t0 < s1; t0 += 32) {
           const int t = t0 + lane;
@@ -357,6 +368,10 @@ void build_neighbors(allegro_ctx* c) {
     c->ncell[d] = nc;
     ncells *= nc;
   }
+  if (c->n_rep > 1 && c->dom.multi) throw std::invalid_argument("replica batches need world_size == 1");
+  cg.n_per = c->n_rep > 1 ? c->n_per : 0;
+  cg.ncell_rep = (int)ncells;
+  ncells *= std::max<int64_t>(c->n_rep, 1);
   c->ccount.reserve(ncells + 1);
   c->cstart.reserve(ncells + 1);
   c->cslot.reserve(na);
@@ -364,13 +379,14 @@ void build_neighbors(allegro_ctx* c) {
   ALG_CUDA(cudaMemsetAsync(c->ccount.p, 0, sizeof(int32_t) * (ncells + 1), st));
   {
     ProfScope ps_(&c->prof, st, PK_CELL, 0, 28.0 * na);
-    k_cell_count<<<ceil_div(na, 256), 256, 0, st>>>(c->apos.p, na, cg, c->ccount.p, c->cslot.p);
+    k_cell_count<<<ceil_div(na, 256), 256, 0, st>>>(c->apos.p, c->aowner.p, na, cg, c->ccount.p, c->cslot.p);
   }
   ALG_LAUNCH_CHECK();
   exclusive_scan(c, c->ccount.p, c->cstart.p, ncells);
   {
     ProfScope ps_(&c->prof, st, PK_CELL, 0, 36.0 * na);
-    k_cell_fill<<<ceil_div(na, 256), 256, 0, st>>>(c->apos.p, na, cg, c->cstart.p, c->cslot.p, c->csorted.p);
+    k_cell_fill<<<ceil_div(na, 256), 256, 0, st>>>(c->apos.p, c->aowner.p, na, cg, c->cstart.p, c->cslot.p,
+                                                 c->csorted.p);
   }
   ALG_LAUNCH_CHECK();
   // ---- edges ----
