@@ -118,6 +118,21 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_
       "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p; }" ::"r"(d),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
+// Warp-wide variants: every lane of the MMA warp executes the loop with warp-uniform operands
+// (kept in uniform registers) and one elected lane issues -- no per-MMA divergent branch and
+// register-to-uniform moves around each UTCHMMA.
+__device__ __forceinline__ void mma_tf32_ts_w(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p, e; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p; }" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
@@ -242,6 +257,57 @@ __device__ __forceinline__ void scatter_rows(unsigned char* buf, float* dst, int
     if (row0 + r < M && c < nc) __stcs(reinterpret_cast<float4*>(dst + (row0 + r) * ld + 4 * c), v[i]);
   }
   __syncwarp();
+}
+
+// MODE 0: 3xTF32 (a_hi w_lo, a_lo w_hi, a_hi w_hi); 1: stacked (a_hi [w_hi | w_lo], a_lo w_hi);
+// diagnostics: 2: the three products into three accumulators, 3: one MMA per K-step, 4: no MMAs.
+template <int MODE>
+__device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uint32_t tmem_a, uint32_t wimg, int n_my,
+                                           uint64_t* a_full, uint64_t* a_empty, uint64_t* acc_full,
+                                           uint64_t* acc_empty) {
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.N_t >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
+  const uint32_t idesc2 = idesc + ((uint32_t)(p.N_t >> 3) << 17);  // width 2 N_t (stacked)
+  const uint32_t wblk = (uint32_t)p.N_t * 128;                      // bytes of one W half-block (hi or lo)
+  const uint64_t desc0 = sdesc(wimg);
+  const uint64_t dlo = (uint64_t)(wblk >> 4);                        // descriptor step hi -> lo
+  int j = 0;
+  uint32_t aph = 0;
+  for (int t = 0; t < n_my; ++t) {
+    const int a = t % p.n_acc;
+    const uint32_t acph = (uint32_t)(t / p.n_acc) & 1u;
+    mbar_wait(acc_empty + a, acph ^ 1);
+    tc_fence_after();
+    const uint32_t d = tmem + (uint32_t)(a * p.acc_cols);
+    for (int kb = 0; kb < p.nK; ++kb) {
+      mbar_wait(a_full + j, aph);
+      tc_fence_after();
+      const uint32_t ahi = tmem_a + (uint32_t)(j * A_TMEM_COLS), alo = ahi + 32;
+      const uint64_t dkb = desc0 + (uint64_t)((kb * 2 * wblk) >> 4);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t dwh = dkb + (uint64_t)(k * 2);  // +32 bytes = 8 tf32 of a W row
+        const uint64_t dwl = dwh + dlo;
+        const uint32_t acc = (kb | k) ? 1u : 0u;
+        if constexpr (MODE == 0) {
+          mma_tf32_ts_w(d, ahi + 8 * k, dwl, idesc, acc);
+          mma_tf32_ts_w(d, alo + 8 * k, dwh, idesc, 1u);
+          mma_tf32_ts_w(d, ahi + 8 * k, dwh, idesc, 1u);
+        } else if constexpr (MODE == 1) {
+          mma_tf32_ts_w(d, ahi + 8 * k, dwh, idesc2, acc);  // [D | D'] += a_hi [w_hi | w_lo]
+          mma_tf32_ts_w(d, alo + 8 * k, dwh, idesc, 1u);
+        } else if constexpr (MODE == 2) {
+          mma_tf32_ts_w(d, ahi + 8 * k, dwl, idesc, acc);
+          mma_tf32_ts_w(d + (uint32_t)p.N_t, alo + 8 * k, dwh, idesc, acc);
+          mma_tf32_ts_w(d + 2u * (uint32_t)p.N_t, ahi + 8 * k, dwh, idesc, acc);
+        } else if constexpr (MODE == 3) {
+          mma_tf32_ts_w(d, ahi + 8 * k, dwh, idesc, acc);
+        }
+      }
+      mma_commit_w(a_empty + j);
+      if (kb == p.nK - 1) mma_commit_w(acc_full + a);
+      if (++j == p.a_stages) j = 0, aph ^= 1;
+    }
+  }
 }
 
 template <int EPI>
@@ -372,47 +438,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp == 9) {
-    // ---------------- MMA issuer ----------------
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.N_t >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
+    // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
     mbar_wait(w_full, 0);
     tc_fence_after();
-    const uint32_t idesc2 = idesc + ((uint32_t)(p.N_t >> 3) << 17);  // width 2 N_t (stacked)
-    const uint32_t wimg = smem_u32(w_img);
-    const uint32_t wblk = (uint32_t)p.N_t * 128;  // bytes of one W half-block (hi or lo)
-    int j = 0;
-    uint32_t aph = 0;
-    for (int t = 0; t < n_my; ++t) {
-      const int a = t % p.n_acc;
-      const uint32_t acph = (uint32_t)(t / p.n_acc) & 1u;
-      mbar_wait(acc_empty + a, acph ^ 1);
-      tc_fence_after();
-      const uint32_t d = tmem + (uint32_t)(a * p.acc_cols);
-      for (int kb = 0; kb < p.nK; ++kb) {
-        mbar_wait(a_full + j, aph);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t ahi = tmem_a + (uint32_t)(j * A_TMEM_COLS), alo = ahi + 32;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (p.diag & 1) break;
-            const uint32_t ko = k * 32;  // 8 tf32 = 32 bytes of a W row
-            const uint32_t wh = wimg + kb * 2 * wblk + ko;
-            const uint64_t dwh = sdesc(wh), dwl = sdesc(wh + wblk);
-            if (p.stack) {
-              mma_tf32_ts(d, ahi + 8 * k, dwh, idesc2, (kb | k) ? 1u : 0u);  // [D | D'] += a_hi [w_hi | w_lo]
-              mma_tf32_ts(d, alo + 8 * k, dwh, idesc, 1u);
-            } else {
-              mma_tf32_ts(d, ahi + 8 * k, dwl, idesc, (kb | k) ? 1u : 0u);
-              mma_tf32_ts(d, alo + 8 * k, dwh, idesc, 1u);
-              mma_tf32_ts(d, ahi + 8 * k, dwh, idesc, 1u);
-            }
-          }
-          mma_commit(a_empty + j);
-          if (kb == p.nK - 1) mma_commit(acc_full + a);
-        }
-        __syncwarp();
-        if (++j == p.a_stages) j = 0, aph ^= 1;
-      }
+    const int mode = (p.diag & 1) ? 4 : (p.diag & 4) ? 3 : (p.diag & 8) ? 2 : p.stack ? 1 : 0;
+    switch (mode) {
+      case 0: mma_issuer<0>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty); break;
+      case 1: mma_issuer<1>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty); break;
+      case 2: mma_issuer<2>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty); break;
+      case 3: mma_issuer<3>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty); break;
+      default: mma_issuer<4>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty); break;
     }
   } else {
     // ---------------- epilogue warpgroup (warps 4..7) ----------------
@@ -629,7 +664,8 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   // profiles/r01_gemm_stack_ab.jsonl): N_t = 32 always, N_t = 64 from K = 64 (at K = 32 the
   // doubled accumulator read makes the epilogue the bottleneck)
   p.stack = (g_tc_tuning.stack && (w.N_t == 32 || (w.N_t == 64 && g.K >= 64))) ? 1 : 0;
-  p.acc_cols = (p.stack ? 2 : 1) * ((w.N_t + 31) / 32 * 32);
+  if (g_tc_tuning.diag & 8) p.stack = 0;
+  p.acc_cols = ((g_tc_tuning.diag & 8) ? 3 : p.stack ? 2 : 1) * ((w.N_t + 31) / 32 * 32);
   // TMEM: two accumulators + the A ring (64 columns per stage), power of two <= 512
   // a deeper accumulator ring for narrow tiles lets the MMAs run further ahead of the epilogue
   p.n_acc = std::max(2, std::min(g_tc_tuning.max_acc, (512 - 4 * A_TMEM_COLS) / p.acc_cols));
