@@ -175,8 +175,9 @@ __device__ __forceinline__ float dsilu(float t) {
 
 struct TcParams {
   GemmArgs g;
-  const float* wimg;   // this launch's N-tile image (hi | lo)
-  int col0;            // first output column of the N-tile
+  const float* wimg;   // N-tile images (hi | lo), tile_floats apart
+  size_t tile_floats;
+  int n_tiles;         // CTAs blockIdx % n_tiles = N-tile of the same M-tiles (siblings share A via L2)
   int N_t;             // tile width (multiple of 16)
   int nK;              // K-blocks of 32
   int nK1;             // K-blocks coming from A (rest from A2)
@@ -361,7 +362,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmem_a = tmem + (uint32_t)(p.n_acc * p.acc_cols);  // A ring after the accumulators
 
-  const int n_my = p.n_mtiles > (int)blockIdx.x ? (p.n_mtiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  // sibling CTAs (one per N-tile) walk the same M-tiles in step, so A is read from HBM once
+  const int tile = (int)blockIdx.x % p.n_tiles, grp = (int)blockIdx.x / p.n_tiles;
+  const int n_grp = (int)gridDim.x / p.n_tiles;
+  const int col0 = tile * p.N_t;
+  const float* wimg_g = p.wimg + (size_t)tile * p.tile_floats;
+  const int n_my = p.n_mtiles > grp ? (p.n_mtiles - 1 - grp) / n_grp + 1 : 0;
 
   if (warp == 8) {
     // ---------------- TMA producer ----------------
@@ -370,12 +376,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t chunk = 32768;
       for (uint32_t off = 0; off < p.w_bytes; off += chunk) {
         const uint32_t b = p.w_bytes - off < chunk ? p.w_bytes - off : chunk;
-        bulk_load(base + off, reinterpret_cast<const unsigned char*>(p.wimg) + off, b, w_full);
+        bulk_load(base + off, reinterpret_cast<const unsigned char*>(wimg_g) + off, b, w_full);
       }
       int s = 0;
       uint32_t ph = 0;
       for (int t = 0; t < n_my; ++t) {
-        const int m0 = ((int)blockIdx.x + t * (int)gridDim.x) * ROWS;
+        const int m0 = (grp + t * n_grp) * ROWS;
         for (int kb = 0; kb < p.nK; ++kb) {
           mbar_wait(raw_empty + s, ph ^ 1);
           unsigned char* dst = stage0 + (size_t)s * STAGE_BYTES;
@@ -392,11 +398,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int s2 = 0;
       uint32_t ph = 0;
       for (int t = 0; t < n_my; ++t) {
-        const int m0 = ((int)blockIdx.x + t * (int)gridDim.x) * ROWS;
+        const int m0 = (grp + t * n_grp) * ROWS;
         for (int c0 = 0; c0 < p.N_t; c0 += 32) {
           mbar_wait(x_empty + s2, ph ^ 1);
           mbar_expect_tx(x_full + s2, X_STAGE_BYTES);
-          tma_load_2d(x_stage + (size_t)s2 * X_STAGE_BYTES, &mapX, p.col0 + c0, m0, x_full + s2);
+          tma_load_2d(x_stage + (size_t)s2 * X_STAGE_BYTES, &mapX, col0 + c0, m0, x_full + s2);
           if (++s2 == X_STAGES) s2 = 0, ph ^= 1;
         }
       }
@@ -465,7 +471,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t acph = (uint32_t)(t / p.n_acc) & 1u;
       mbar_wait(acc_full + a, acph);
       tc_fence_after();
-      const int64_t row0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * ROWS + q * 32;
+      const int64_t row0 = (int64_t)(grp + t * n_grp) * ROWS + q * 32;
       const int64_t r = row0 + lane;
       const float ur = (r < g.M && g.u != nullptr) ? g.u[r] : 1.f;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * p.acc_cols);
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if constexpr (EPI == EPI_R2) {
           const float e2 = (r < g.M) ? g.rs2[r] : 0.f;
-          const int cb = p.col0 + c0;
+          const int cb = col0 + c0;
           if (cb + 32 <= g.N) {  // warp-uniform float4 loads (broadcast)
             const float4* v1 = reinterpret_cast<const float4*>(g.vec1 + cb);
             const float4* v2 = reinterpret_cast<const float4*>(g.vec2 + cb);
@@ -515,7 +521,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int j = 0; j < 32; ++j) v[j] += v2[j];
         }
         if (p.diag & 2) continue;
-        const int64_t col = p.col0 + c0;
+        const int64_t col = col0 + c0;
         const int nc = (p.N_t - c0) >= 32 ? 8 : (p.N_t - c0) / 4;
         epi_apply<32, EPI>(g, v, xin, ur, out);
         scatter_rows(buf, g.C + col, g.N, row0, g.M, lane, out, nc);
@@ -679,16 +685,18 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   p.has_x = has_x ? 1 : 0;
   const float* xsrc = g.epi == EPI_ACC ? g.C : g.X;
   const CUtensorMap mX = has_x ? make_map(xsrc, g.M, g.N, g.N) : mA;
-  const int grid = std::min(p.n_mtiles, g_num_sms);
+  // one launch; CTA b handles N-tile b % n_tiles of M-tile group b / n_tiles
+  const int groups = std::max(1, std::min(p.n_mtiles, g_num_sms / w.n_tiles));
+  const int grid = groups * w.n_tiles;
   const double mn = (double)g.M * g.N;
   const int n_io = 1 + (g.aux != nullptr) + (g.X != nullptr) + (g.epi == EPI_ACC);
-  for (int tile = 0; tile < w.n_tiles; ++tile) {
-    p.col0 = tile * w.N_t;
-    p.wimg = w.dev + tile * (w.tile_bytes / 4);
+  p.n_tiles = w.n_tiles;
+  p.wimg = w.dev;
+  p.tile_floats = w.tile_bytes / 4;
+  {
     char tag[96];
     std::snprintf(tag, sizeof(tag), "tc N=%d K=%d epi=%d A2=%d Nt=%d", g.N, g.K, g.epi, g.A2 ? 1 : 0, w.N_t);
-    ProfScope ps(prof, st, PK_GEMM, 2.0 * mn * g.K / w.n_tiles,
-                 4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * n_io) / w.n_tiles, tag);
+    ProfScope ps(prof, st, PK_GEMM, 2.0 * mn * g.K, 4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * n_io), tag);
     switch (g.epi) {
 #define ALG_EPI(e) \
   case e: k_tc_gemm<e><<<grid, TC_THREADS, smem, st>>>(mA, mA2, mX, p); break;
