@@ -37,6 +37,11 @@ struct GemmArgs {
   const float* rs2 = nullptr;   // [M]   (EPI_R2)
   const float* vec1 = nullptr;  // [N]   (EPI_R2)
   const float* vec2 = nullptr;  // [N]   (EPI_R2)
+  // optional fused row-dot (the u-gradient of a residual update): dot_out[r] += dot_coef <C[r], dotv[r]>
+  // over the N output columns (3xTF32 path: in the epilogue; fp32 path: a separate kernel)
+  const float* dotv = nullptr;  // [M][N]
+  float* dot_out = nullptr;     // [M]
+  float dot_coef = 0.f;
   float s = 1.f, alpha = 0.f, beta = 0.f;
   int epi = EPI_STORE;
 };

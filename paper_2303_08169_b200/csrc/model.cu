@@ -19,6 +19,7 @@
 //   A12 k_force       F_a = sum_{e in row a} (g_e - g_rev(e)) in row order (fp64)
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 
 #include "ctx.cuh"
@@ -610,8 +611,28 @@ void tp_dispatch(int NL, int LMAX, int K, bool fwd, const TpArgs& t, cudaStream_
 
 // CUDA-core fp32 (parity reference mode) or tcgen05 3xTF32 (tensor cores)
 void run_gemm(const Model& M, const GemmArgs& g, const Wt& w, cudaStream_t st, Profiler* prof) {
-  if (M.precision == ALLEGRO_PREC_3XTF32) tc_gemm(g, w.tc, st, prof);
-  else gemm(g, st, prof);
+  static const bool fuse_dot = [] {  // A/B switch for measurements (default: fused)
+    const char* e = std::getenv("ALLEGRO_FUSE_ROWDOT");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (M.precision == ALLEGRO_PREC_3XTF32 && (!g.dotv || (fuse_dot && w.tc.n_tiles == 1))) {
+    tc_gemm(g, w.tc, st, prof);  // the row-dot (if any) is fused into the epilogue
+    return;
+  }
+  GemmArgs g0 = g;
+  g0.dotv = nullptr;
+  if (M.precision == ALLEGRO_PREC_3XTF32) tc_gemm(g0, w.tc, st, prof);
+  else gemm(g0, st, prof);
+  // fp32 reference mode, or an output split over N-tiles (a fused dot would need an
+  // order-dependent cross-CTA sum): a separate row-dot over the finished output
+  if (g.dotv && g.M > 0) {
+    if (g.N != kD) throw CudaError("row-dot over N != 128");
+    {
+      ProfScope ps_(prof, st, PK_ROWDOT, 2.0 * 128 * g.M, (double)g.M * 1024);
+      k_rowdot<<<ceil_div(g.M * 32, 256), 256, 0, st>>>(g.M, g.dotv, g.C, g.dot_coef, g.dot_out);
+    }
+    ALG_LAUNCH_CHECK();
+  }
 }
 
 size_t floats_per_edge(const Model& M) {
@@ -788,17 +809,9 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   ALG_CUDA(cudaMemsetAsync(w.ybar.p, 0, sizeof(float) * E * dsh, st));
   float* vb = w.vbar_a.p;   // V-bar^{k+1} (input to layer k)
   float* vbn = w.vbar_b.p;  // V-bar^k (output of layer k)
-  const unsigned edge_warp_blocks = (unsigned)((E * 32 + 255) / 256);
   for (int k = M.n_layers - 1; k >= 0; --k) {
     const LayerInfo& L = M.L[k];
     const bool last = k == M.n_layers - 1;
-    if (E > 0 && !last) {
-      {
-        ProfScope ps_(&c->prof, st, PK_ROWDOT, 2.0 * 128 * E, (double)E * 1024);
-        k_rowdot<<<edge_warp_blocks, 256, 0, st>>>(E, w.h[k].p, xb, kResB, w.ubar.p);
-      }
-      ALG_LAUNCH_CHECK();
-    }
     const float sl = 1.f / std::sqrt((float)L.fan_lat);
     if (!last) {
       GemmArgs g = G(xb, 128, M.w.latT_x[k], 128, 128, xbn, sl, EPI_URESID);
@@ -844,19 +857,17 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
         g.vec1 = M.w.r2_vec1;
         g.vec2 = M.w.r2_vec2;
       }
+      // xbar^k is complete here: fuse the u-gradient of the update that produced x^k,
+      // ubar += (1/sqrt5) <xbar^k, h^{k-1}> (latent resnet) or <xbar^0, m> (two-body x^0 = u m)
+      g.dotv = k >= 1 ? w.h[k - 1].p : w.m.p;
+      g.dot_coef = k >= 1 ? kResB : 1.f;
+      g.dot_out = w.ubar.p;
       run_gemm(M, g, *last_w, st, &c->prof);
     }
     std::swap(xb, xbn);
     std::swap(vb, vbn);
   }
-  // ---- two-body reverse ----
-  if (E > 0) {
-    {
-      ProfScope ps_(&c->prof, st, PK_ROWDOT, 2.0 * 128 * E, (double)E * 1024);
-      k_rowdot<<<edge_warp_blocks, 256, 0, st>>>(E, w.m.p, xb, 1.f, w.ubar.p);
-    }
-    ALG_LAUNCH_CHECK();
-  }
+  // ---- two-body reverse (its u-gradient row-dot ran in layer 0's env^T epilogue) ----
   {
     GemmArgs g = G(xb, 128, M.w.tb_w2T, 64, 128, w.ab2.p, kCSilu / std::sqrt(64.f), EPI_DSILU);
     g.X = w.a2.p;

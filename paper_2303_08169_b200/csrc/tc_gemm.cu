@@ -260,6 +260,28 @@ __device__ __forceinline__ void scatter_rows(unsigned char* buf, float* dst, int
   __syncwarp();
 }
 
+// scatter_rows + the fused row-dot: while the transposed (coalesced) values v[i] of rows
+// (lane >> 3) + 4 i, columns 4 (lane & 7).. are in registers, accumulate v[i] . dq[i] into acc8[i]
+// (dq = the row-dot operand, loaded in the same coalesced layout).
+__device__ __forceinline__ void scatter_rows_dot(unsigned char* buf, float* dst, int64_t ld, int64_t row0, int64_t M,
+                                                 int lane, const float* src, int nc, const float4* dq, float* acc8) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) *tile_at(buf, lane, c) = make_float4(src[4 * c], src[4 * c + 1], src[4 * c + 2], src[4 * c + 3]);
+  __syncwarp();
+  float4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = *tile_at(buf, (lane >> 3) + 4 * i, lane & 7);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = (lane >> 3) + 4 * i, c = lane & 7;
+    if (row0 + r < M && c < nc) {
+      __stcs(reinterpret_cast<float4*>(dst + (row0 + r) * ld + 4 * c), v[i]);
+      acc8[i] = fmaf(v[i].x, dq[i].x, fmaf(v[i].y, dq[i].y, fmaf(v[i].z, dq[i].z, fmaf(v[i].w, dq[i].w, acc8[i]))));
+    }
+  }
+  __syncwarp();
+}
+
 // MODE 0: 3xTF32 (a_hi w_lo, a_lo w_hi, a_hi w_hi); 1: stacked (a_hi [w_hi | w_lo], a_lo w_hi);
 // diagnostics: 2: the three products into three accumulators, 3: one MMA per K-step, 4: no MMAs.
 template <int MODE>
@@ -475,8 +497,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int64_t r = row0 + lane;
       const float ur = (r < g.M && g.u != nullptr) ? g.u[r] : 1.f;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * p.acc_cols);
+      float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // row-dot partials, rows (lane>>3)+4i
       for (int c0 = 0; c0 < p.N_t; c0 += 32) {
         float v[32], out[32], xin[32];
+        float4 dq[8];
+        if (g.dotv != nullptr) {  // row-dot operand, coalesced like the stores; in flight during the waits
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int64_t rr = row0 + (lane >> 3) + 4 * i;
+            const int cc = 4 * (lane & 7);
+            dq[i] = (rr < g.M && cc < p.N_t - c0) ? __ldg(reinterpret_cast<const float4*>(g.dotv + rr * g.N + col0 + c0 + cc))
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
         if constexpr (kIn) {
           // this thread's row of the TMA-loaded [128 x 32] input box (SWIZZLE_128B)
           mbar_wait(x_full + xs, xph);
@@ -524,8 +557,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int64_t col = col0 + c0;
         const int nc = (p.N_t - c0) >= 32 ? 8 : (p.N_t - c0) / 4;
         epi_apply<32, EPI>(g, v, xin, ur, out);
-        scatter_rows(buf, g.C + col, g.N, row0, g.M, lane, out, nc);
+        if (g.dotv != nullptr) scatter_rows_dot(buf, g.C + col, g.N, row0, g.M, lane, out, nc, dq, acc8);
+        else scatter_rows(buf, g.C + col, g.N, row0, g.M, lane, out, nc);
         if (want_aux) scatter_rows(buf, g.aux + col, g.N, row0, g.M, lane, v, nc);
+      }
+      if (g.dotv != nullptr) {  // reduce the 8 lanes of each row; lane (lane & 7) == i writes row (lane>>3)+4i
+        float mine = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float t8 = acc8[i];
+          t8 += __shfl_xor_sync(0xffffffffu, t8, 1);
+          t8 += __shfl_xor_sync(0xffffffffu, t8, 2);
+          t8 += __shfl_xor_sync(0xffffffffu, t8, 4);
+          if ((lane & 7) == i) mine = t8;
+        }
+        const int64_t rr = row0 + (lane >> 3) + 4 * (lane & 7);
+        if (rr < g.M) g.dot_out[rr] += g.dot_coef * mine;  // host: one N-tile
       }
       tc_fence_before();
       __syncwarp();
@@ -685,6 +732,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   p.has_x = has_x ? 1 : 0;
   const float* xsrc = g.epi == EPI_ACC ? g.C : g.X;
   const CUtensorMap mX = has_x ? make_map(xsrc, g.M, g.N, g.N) : mA;
+  if (g.dotv && w.n_tiles != 1) throw CudaError("tc_gemm: the fused row-dot needs a single N-tile");
   // one launch; CTA b handles N-tile b % n_tiles of M-tile group b / n_tiles
   const int groups = std::max(1, std::min(p.n_mtiles, g_num_sms / w.n_tiles));
   const int grid = groups * w.n_tiles;
@@ -696,7 +744,9 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   {
     char tag[96];
     std::snprintf(tag, sizeof(tag), "tc N=%d K=%d epi=%d A2=%d Nt=%d", g.N, g.K, g.epi, g.A2 ? 1 : 0, w.N_t);
-    ProfScope ps(prof, st, PK_GEMM, 2.0 * mn * g.K, 4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * n_io), tag);
+    ProfScope ps(prof, st, PK_GEMM, 2.0 * mn * g.K + (g.dotv ? 2.0 * mn : 0.0),
+                 4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * (n_io + (g.dotv ? 1 : 0)) + (g.dotv ? 2.0 * g.M : 0.0)),
+                 tag);
     switch (g.epi) {
 #define ALG_EPI(e) \
   case e: k_tc_gemm<e><<<grid, TC_THREADS, smem, st>>>(mA, mA2, mX, p); break;
