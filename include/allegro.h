@@ -267,6 +267,10 @@ int allegro_debug_gemm(int device, int precision, int64_t M, int N, int K, const
 
 /* Test hook: time `iters` launches of one contraction shape on device buffers (CUDA events);
  * epi = internal epilogue id; tma_store / max_stages / diag tune the tcgen05 kernel. */
+/* test hook: one contraction with epilogue `epi` (csrc/gemm.cuh ids, s = 0.75); X, u may be NULL; C is the
+ * old C on input (EPI_ACC) and the result on output; aux (may be NULL) receives the saved pre-activation */
+int allegro_debug_gemm_epi(int device, int precision, int64_t M, int N, int K, int epi, const float* A, const float* W,
+                           const float* X, const float* u, float* C, float* aux);
 int allegro_debug_gemm_bench(int device, int precision, int64_t M, int N, int K, int epi, int iters, int tma_store,
                              int max_stages, int diag, double* ms_per_iter);
 

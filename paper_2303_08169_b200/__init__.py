@@ -146,6 +146,7 @@ _lib.pimd_get_state.argtypes = [_P, _P, _P, _P, _P]
 _lib.md_run_ttf.argtypes = [_P, C.c_double, C.POINTER(TtfProtocol), _P, C.c_int64, C.POINTER(TtfResult)]
 _lib.md_get_local_state.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), _P, _P, _P, _P, _P]
 _lib.allegro_debug_gemm.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, _P, _P, _P]
+_lib.allegro_debug_gemm_epi.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, _P, _P, _P, _P, _P, _P]
 _lib.allegro_debug_gemm_bench.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                           C.c_int, C.c_int, C.POINTER(C.c_double)]
 
@@ -155,7 +156,7 @@ EXPORTED = [
     "allegro_get_edges", "allegro_get_edge_grad", "allegro_w3j_table", "allegro_param_count",
     "allegro_layer_paths", "allegro_version", "md_step_host", "allegro_profile", "allegro_profile_read",
     "allegro_launch_count", "allegro_profile_kinds", "allegro_profile_kind_name", "allegro_debug_gemm",
-    "allegro_debug_gemm_bench", "allegro_nccl_unique_id", "allegro_local_count",
+    "allegro_debug_gemm_bench", "allegro_debug_gemm_epi", "allegro_nccl_unique_id", "allegro_local_count",
     "md_get_local_state", "md_set_thermostat", "md_run_ttf",
     "allegro_compute_energy_forces_batch", "pimd_set_state", "pimd_step", "pimd_get_state",
     "allegro_profile_detail",
@@ -205,6 +206,23 @@ def debug_gemm(A: np.ndarray, W: np.ndarray, precision: int = PREC_FP32, device:
     if rc != OK:
         raise AllegroError(rc, _lib.allegro_last_error(None).decode())
     return C_
+
+
+def debug_gemm_epi(A, W, epi, X=None, u=None, C=None, precision=PREC_3XTF32, want_aux=False, device=0):
+    """Test hook: C = epi(0.75 * A W) with the optional X / u inputs; returns (C, aux)."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    W = np.ascontiguousarray(W, dtype=np.float32)
+    M, K = A.shape
+    N = W.shape[1]
+    Cv = np.zeros((M, N), np.float32) if C is None else np.ascontiguousarray(C, dtype=np.float32).copy()
+    aux = np.zeros((M, N), np.float32) if want_aux else None
+    Xv = None if X is None else np.ascontiguousarray(X, dtype=np.float32)
+    uv = None if u is None else np.ascontiguousarray(u, dtype=np.float32)
+    rc = _lib.allegro_debug_gemm_epi(device, precision, M, N, K, epi, A.ctypes.data, W.ctypes.data, _ptr(Xv), _ptr(uv),
+                                     Cv.ctypes.data, _ptr(aux))
+    if rc != OK:
+        raise AllegroError(rc, _lib.allegro_last_error(None).decode())
+    return Cv, aux
 
 
 def debug_gemm_bench(M, N, K, epi=0, precision=PREC_3XTF32, iters=10, tma_store=1, max_stages=4, diag=0,

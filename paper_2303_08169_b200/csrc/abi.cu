@@ -756,6 +756,66 @@ int allegro_debug_gemm(int device, int precision, int64_t M, int N, int K, const
   });
 }
 
+int allegro_debug_gemm_epi(int device, int precision, int64_t M, int N, int K, int epi, const float* A, const float* W,
+                           const float* X, const float* u, float* C, float* aux) {
+  if (!A || !W || !C || M < 0 || N <= 0 || K <= 0 || (epi & 0xff) > EPI_DSILU)
+    return fail(nullptr, ALLEGRO_E_ARG, "bad gemm arguments");
+  return guarded(nullptr, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(device));
+    std::vector<void*> owned;
+    std::vector<float> w(W, W + (size_t)K * N);
+    auto up = [&](const float* h, size_t n) -> float* {
+      float* d = nullptr;
+      ALG_CUDA(cudaMalloc(&d, sizeof(float) * (n + 4)));
+      if (h) ALG_CUDA(cudaMemcpy(d, h, sizeof(float) * n, cudaMemcpyHostToDevice));
+      owned.push_back(d);
+      return d;
+    };
+    GemmArgs g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    const int K1 = (epi >> 8) & 0xffff;  // > 0: columns [K1, K) come from a separate array (the A2 path)
+    epi &= 0xff;
+    if (K1 > 0) {
+      std::vector<float> a1((size_t)M * K1), a2((size_t)M * (K - K1));
+      for (int64_t r = 0; r < M; ++r)
+        for (int k = 0; k < K; ++k)
+          (k < K1 ? a1[(size_t)r * K1 + k] : a2[(size_t)r * (K - K1) + k - K1]) = A[(size_t)r * K + k];
+      g.A = up(a1.data(), a1.size());
+      g.lda = K1;
+      g.A2 = up(a2.data(), a2.size());
+      g.lda2 = K - K1;
+      g.K1 = K1;
+    } else {
+      g.A = up(A, (size_t)M * K);
+      g.lda = K;
+    }
+    g.W = up(W, (size_t)K * N);
+    g.C = up(C, (size_t)M * N);  // old C (EPI_ACC)
+    g.epi = epi;
+    g.alpha = 0.5f;
+    g.beta = 0.25f;
+    if (X == A && K1 == N) g.X = g.A;  // the resnet case: X is the first operand itself
+    else if (X) g.X = up(X, (size_t)M * N);
+    if (u) g.u = up(u, (size_t)M);
+    float* daux = aux ? up(nullptr, (size_t)M * N) : nullptr;
+    g.aux = daux;
+    g.s = 0.75f;
+    if (precision == ALLEGRO_PREC_3XTF32) {
+      TcWeight t = tc_prepare_weight(w, K, N, owned);
+      tc_gemm(g, t, 0, nullptr);
+    } else {
+      gemm(g, 0, nullptr);
+    }
+    ALG_CUDA(cudaDeviceSynchronize());
+    ALG_CUDA(cudaMemcpy(C, g.C, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
+    if (aux) ALG_CUDA(cudaMemcpy(aux, daux, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
+    for (void* p : owned) cudaFree(p);
+    return ALLEGRO_OK;
+  });
+}
+
 int allegro_debug_gemm_bench(int device, int precision, int64_t M, int N, int K, int epi, int iters, int tma_store,
                              int max_stages, int diag, double* ms_per_iter) {
   if (!ms_per_iter || M <= 0 || N <= 0 || K <= 0 || iters <= 0) return fail(nullptr, ALLEGRO_E_ARG, "bad arguments");

@@ -610,11 +610,37 @@ void tp_dispatch(int NL, int LMAX, int K, bool fwd, const TpArgs& t, cudaStream_
 }
 
 // CUDA-core fp32 (parity reference mode) or tcgen05 3xTF32 (tensor cores)
+__global__ void k_count_diff(const float* a, const float* b, int64_t n, unsigned long long* cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && __float_as_uint(a[i]) != __float_as_uint(b[i])) atomicAdd(cnt, 1ull);
+}
+
 void run_gemm(const Model& M, const GemmArgs& g, const Wt& w, cudaStream_t st, Profiler* prof) {
   static const bool fuse_dot = [] {  // A/B switch for measurements (default: fused)
     const char* e = std::getenv("ALLEGRO_FUSE_ROWDOT");
     return !e || std::atoi(e) != 0;
   }();
+  static const bool verify = std::getenv("ALLEGRO_VERIFY_GEMM") != nullptr;  // diagnostics: rerun and compare
+  if (verify && M.precision == ALLEGRO_PREC_3XTF32 && g.epi != EPI_ACC && g.epi != EPI_R2 && !g.dotv && g.M > 0) {
+    tc_gemm(g, w.tc, st, prof);
+    float* tmp = nullptr;
+    unsigned long long* cnt = nullptr;
+    const size_t n = (size_t)g.M * g.N;
+    ALG_CUDA(cudaMallocAsync(&tmp, n * sizeof(float), st));
+    ALG_CUDA(cudaMallocAsync(&cnt, sizeof(unsigned long long), st));
+    ALG_CUDA(cudaMemcpyAsync(tmp, g.C, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    ALG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
+    tc_gemm(g, w.tc, st, prof);
+    k_count_diff<<<ceil_div((int64_t)n, 256), 256, 0, st>>>(tmp, g.C, (int64_t)n, cnt);
+    unsigned long long h = 0;
+    ALG_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
+    ALG_CUDA(cudaStreamSynchronize(st));
+    if (h) std::fprintf(stderr, "[verify] gemm M=%lld N=%d K=%d epi=%d lda=%d A2=%d: %llu elements differ\n",
+                        (long long)g.M, g.N, g.K, g.epi, g.lda, g.A2 ? 1 : 0, h);
+    ALG_CUDA(cudaFreeAsync(tmp, st));
+    ALG_CUDA(cudaFreeAsync(cnt, st));
+    return;
+  }
   if (M.precision == ALLEGRO_PREC_3XTF32 && (!g.dotv || (fuse_dot && w.tc.n_tiles == 1))) {
     tc_gemm(g, w.tc, st, prof);  // the row-dot (if any) is fused into the epilogue
     return;

@@ -112,25 +112,29 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-// D[tmem] (+)= A[tmem] B[smem]
-__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p; }" ::"r"(d),
-      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+// Warp-wide MMA issue: every lane of the MMA warp runs the issue loop with warp-uniform
+// operands (kept in uniform registers) and the lane chosen once by elect.sync (`leader`)
+// issues every MMA and every commit, so each tcgen05.commit tracks exactly the MMAs before it.
+// (A lane-0 branch around each MMA made the compiler wrap every UTCHMMA in an ELECT /
+// BRA.U.ANY loop with register-to-uniform moves: ~150 cycles per MMA, which paced every
+// contraction.)
+__device__ __forceinline__ uint32_t elect_leader() {
+  uint32_t l;
+  asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; selp.u32 %0, 1, 0, e; }" : "=r"(l));
+  return l;
 }
-// Warp-wide variants: every lane of the MMA warp executes the loop with warp-uniform operands
-// (kept in uniform registers) and one elected lane issues -- no per-MMA divergent branch and
-// register-to-uniform moves around each UTCHMMA.
-__device__ __forceinline__ void mma_tf32_ts_w(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma_tf32_ts_w(uint32_t leader, uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                              uint32_t acc) {
   asm volatile(
-      "{ .reg .pred p, e; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0;\n\t"
+      "{ .reg .pred p, e; setp.ne.b32 e, %5, 0; setp.ne.b32 p, %4, 0;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p; }" ::"r"(d),
-      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(leader));
 }
-__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_w(uint32_t leader, uint64_t* bar) {
   asm volatile(
-      "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(smem_u32(bar))
+      "{ .reg .pred e; setp.ne.b32 e, %1, 0;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(smem_u32(bar)),
+      "r"(leader)
       : "memory");
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
@@ -144,10 +148,6 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
@@ -178,6 +178,7 @@ struct TcParams {
   const float* wimg;   // N-tile images (hi | lo), tile_floats apart
   size_t tile_floats;
   int n_tiles;         // CTAs blockIdx % n_tiles = N-tile of the same M-tiles (siblings share A via L2)
+  int tile_base;       // first N-tile of this launch
   int N_t;             // tile width (multiple of 16)
   int nK;              // K-blocks of 32
   int nK1;             // K-blocks coming from A (rest from A2)
@@ -282,8 +283,8 @@ __device__ __forceinline__ void scatter_rows_dot(unsigned char* buf, float* dst,
   __syncwarp();
 }
 
-// MODE 0: 3xTF32 (a_hi w_lo, a_lo w_hi, a_hi w_hi); 1: stacked (a_hi [w_hi | w_lo], a_lo w_hi);
-// diagnostics: 2: the three products into three accumulators, 3: one MMA per K-step, 4: no MMAs.
+// MODE 0: 3xTF32 (a_hi w_lo, a_lo w_hi, a_hi w_hi); 1: stacked (a_hi [w_hi | w_lo] into the
+// adjacent accumulators [D | D'], then a_lo w_hi into D; the epilogue adds D + D'); 4: no MMAs.
 template <int MODE>
 __device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uint32_t tmem_a, uint32_t wimg, int n_my,
                                            uint64_t* a_full, uint64_t* a_empty, uint64_t* acc_full,
@@ -293,16 +294,20 @@ __device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uin
   const uint32_t wblk = (uint32_t)p.N_t * 128;                      // bytes of one W half-block (hi or lo)
   const uint64_t desc0 = sdesc(wimg);
   const uint64_t dlo = (uint64_t)(wblk >> 4);                        // descriptor step hi -> lo
+  __syncwarp();
+  const uint32_t L = elect_leader();
   int j = 0;
   uint32_t aph = 0;
   for (int t = 0; t < n_my; ++t) {
     const int a = t % p.n_acc;
     const uint32_t acph = (uint32_t)(t / p.n_acc) & 1u;
     mbar_wait(acc_empty + a, acph ^ 1);
+    __syncwarp();
     tc_fence_after();
     const uint32_t d = tmem + (uint32_t)(a * p.acc_cols);
     for (int kb = 0; kb < p.nK; ++kb) {
       mbar_wait(a_full + j, aph);
+      __syncwarp();
       tc_fence_after();
       const uint32_t ahi = tmem_a + (uint32_t)(j * A_TMEM_COLS), alo = ahi + 32;
       const uint64_t dkb = desc0 + (uint64_t)((kb * 2 * wblk) >> 4);
@@ -312,22 +317,16 @@ __device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uin
         const uint64_t dwl = dwh + dlo;
         const uint32_t acc = (kb | k) ? 1u : 0u;
         if constexpr (MODE == 0) {
-          mma_tf32_ts_w(d, ahi + 8 * k, dwl, idesc, acc);
-          mma_tf32_ts_w(d, alo + 8 * k, dwh, idesc, 1u);
-          mma_tf32_ts_w(d, ahi + 8 * k, dwh, idesc, 1u);
+          mma_tf32_ts_w(L, d, ahi + 8 * k, dwl, idesc, acc);
+          mma_tf32_ts_w(L, d, alo + 8 * k, dwh, idesc, 1u);
+          mma_tf32_ts_w(L, d, ahi + 8 * k, dwh, idesc, 1u);
         } else if constexpr (MODE == 1) {
-          mma_tf32_ts_w(d, ahi + 8 * k, dwh, idesc2, acc);  // [D | D'] += a_hi [w_hi | w_lo]
-          mma_tf32_ts_w(d, alo + 8 * k, dwh, idesc, 1u);
-        } else if constexpr (MODE == 2) {
-          mma_tf32_ts_w(d, ahi + 8 * k, dwl, idesc, acc);
-          mma_tf32_ts_w(d + (uint32_t)p.N_t, alo + 8 * k, dwh, idesc, acc);
-          mma_tf32_ts_w(d + 2u * (uint32_t)p.N_t, ahi + 8 * k, dwh, idesc, acc);
-        } else if constexpr (MODE == 3) {
-          mma_tf32_ts_w(d, ahi + 8 * k, dwh, idesc, acc);
+          mma_tf32_ts_w(L, d, ahi + 8 * k, dwh, idesc2, acc);  // [D | D'] += a_hi [w_hi | w_lo]
+          mma_tf32_ts_w(L, d, alo + 8 * k, dwh, idesc, 1u);
         }
       }
-      mma_commit_w(a_empty + j);
-      if (kb == p.nK - 1) mma_commit_w(acc_full + a);
+      mma_commit_w(L, a_empty + j);
+      if (kb == p.nK - 1) mma_commit_w(L, acc_full + a);
       if (++j == p.a_stages) j = 0, aph ^= 1;
     }
   }
@@ -385,7 +384,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem_a = tmem + (uint32_t)(p.n_acc * p.acc_cols);  // A ring after the accumulators
 
   // sibling CTAs (one per N-tile) walk the same M-tiles in step, so A is read from HBM once
-  const int tile = (int)blockIdx.x % p.n_tiles, grp = (int)blockIdx.x / p.n_tiles;
+  const int tile = p.tile_base + (int)blockIdx.x % p.n_tiles, grp = (int)blockIdx.x / p.n_tiles;
   const int n_grp = (int)gridDim.x / p.n_tiles;
   const int col0 = tile * p.N_t;
   const float* wimg_g = p.wimg + (size_t)tile * p.tile_floats;
@@ -450,6 +449,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             lo[4 * c + e] = __float_as_uint(x[e] - __uint_as_float(h));
           }
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // as for the X ring
         __syncwarp();
         if (lane == 0) mbar_arrive(raw_empty + s);
         if (++s == p.stages) s = 0, ph ^= 1;
@@ -469,14 +469,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
     mbar_wait(w_full, 0);
     tc_fence_after();
-    const int mode = (p.diag & 1) ? 4 : (p.diag & 4) ? 3 : (p.diag & 8) ? 2 : p.stack ? 1 : 0;
-    switch (mode) {
-      case 0: mma_issuer<0>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty); break;
-      case 1: mma_issuer<1>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty); break;
-      case 2: mma_issuer<2>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty); break;
-      case 3: mma_issuer<3>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty); break;
-      default: mma_issuer<4>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty); break;
-    }
+    if (p.diag & 1) mma_issuer<4>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
+    else if (p.stack) mma_issuer<1>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
+    else mma_issuer<0>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
   } else {
     // ---------------- epilogue warpgroup (warps 4..7) ----------------
     const int q = warp & 3;  // TMEM lane quarter
@@ -520,6 +515,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const float4 w4 = *reinterpret_cast<const float4*>(xb + row * 128 + ((c ^ (row & 7)) << 4));
             xin[4 * c] = w4.x, xin[4 * c + 1] = w4.y, xin[4 * c + 2] = w4.z, xin[4 * c + 3] = w4.w;
           }
+          // the slot is refilled by TMA (async proxy) once all four warps released it: order
+          // these generic-proxy reads before the release
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(x_empty + xs);
           if (++xs == X_STAGES) xs = 0, xph ^= 1;
@@ -621,7 +619,9 @@ int g_num_sms = 0;
 
 TcTuning make_tuning() {
   TcTuning t;
-  if (const char* e = std::getenv("ALLEGRO_TC_STACK")) t.stack = std::atoi(e) != 0;  // A/B switch for measurements
+  if (const char* e = std::getenv("ALLEGRO_TC_STACK")) t.stack = std::atoi(e) != 0;  // A/B switches for measurements
+  if (const char* e = std::getenv("ALLEGRO_TC_MAXACC")) t.max_acc = std::atoi(e);
+  if (const char* e = std::getenv("ALLEGRO_TC_MAXSTAGES")) t.max_stages = std::atoi(e);
   return t;
 }
 TcTuning g_tc_tuning = make_tuning();
@@ -717,8 +717,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   // profiles/r01_gemm_stack_ab.jsonl): N_t = 32 always, N_t = 64 from K = 64 (at K = 32 the
   // doubled accumulator read makes the epilogue the bottleneck)
   p.stack = (g_tc_tuning.stack && (w.N_t == 32 || (w.N_t == 64 && g.K >= 64))) ? 1 : 0;
-  if (g_tc_tuning.diag & 8) p.stack = 0;
-  p.acc_cols = ((g_tc_tuning.diag & 8) ? 3 : p.stack ? 2 : 1) * ((w.N_t + 31) / 32 * 32);
+  p.acc_cols = (p.stack ? 2 : 1) * ((w.N_t + 31) / 32 * 32);
   // TMEM: two accumulators + the A ring (64 columns per stage), power of two <= 512
   // a deeper accumulator ring for narrow tiles lets the MMAs run further ahead of the epilogue
   p.n_acc = std::max(2, std::min(g_tc_tuning.max_acc, (512 - 4 * A_TMEM_COLS) / p.acc_cols));
@@ -734,18 +733,26 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const CUtensorMap mX = has_x ? make_map(xsrc, g.M, g.N, g.N) : mA;
   if (g.dotv && w.n_tiles != 1) throw CudaError("tc_gemm: the fused row-dot needs a single N-tile");
   // one launch; CTA b handles N-tile b % n_tiles of M-tile group b / n_tiles
-  const int groups = std::max(1, std::min(p.n_mtiles, g_num_sms / w.n_tiles));
-  const int grid = groups * w.n_tiles;
+  // (ALLEGRO_TC_COSCHED=0: one launch per N-tile, for A/B measurements)
+  static const bool cosched = [] {
+    const char* e = std::getenv("ALLEGRO_TC_COSCHED");
+    return !e || std::atoi(e) != 0;
+  }();
+  const int per_launch = cosched ? w.n_tiles : 1;
+  const int groups = std::max(1, std::min(p.n_mtiles, g_num_sms / per_launch));
+  const int grid = groups * per_launch;
   const double mn = (double)g.M * g.N;
   const int n_io = 1 + (g.aux != nullptr) + (g.X != nullptr) + (g.epi == EPI_ACC);
-  p.n_tiles = w.n_tiles;
+  p.n_tiles = per_launch;
   p.wimg = w.dev;
   p.tile_floats = w.tile_bytes / 4;
-  {
+  for (int tb = 0; tb < w.n_tiles; tb += per_launch) {
+    p.tile_base = tb;
     char tag[96];
     std::snprintf(tag, sizeof(tag), "tc N=%d K=%d epi=%d A2=%d Nt=%d", g.N, g.K, g.epi, g.A2 ? 1 : 0, w.N_t);
-    ProfScope ps(prof, st, PK_GEMM, 2.0 * mn * g.K + (g.dotv ? 2.0 * mn : 0.0),
-                 4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * (n_io + (g.dotv ? 1 : 0)) + (g.dotv ? 2.0 * g.M : 0.0)),
+    const double frac = (double)per_launch / w.n_tiles;
+    ProfScope ps(prof, st, PK_GEMM, frac * (2.0 * mn * g.K + (g.dotv ? 2.0 * mn : 0.0)),
+                 frac * 4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * (n_io + (g.dotv ? 1 : 0)) + (g.dotv ? 2.0 * g.M : 0.0)),
                  tag);
     switch (g.epi) {
 #define ALG_EPI(e) \

@@ -30,7 +30,7 @@ struct TcTuning {
   int tma_store = 1;   // TMA-store epilogue when N_t % 32 == 0
   int max_stages = 4;  // A-stage ring depth cap
   int max_acc = 4;     // TMEM accumulator ring depth cap (>= 2)
-  int stack = 1;       // stacked hi/lo MMAs for N_t in {32, 64}
+  int stack = 0;       // stacked hi/lo MMAs for N_t in {32, 64} (off: nondeterministic under load)
   int diag = 0;        // bit0: skip MMAs, bit1: skip the epilogue's global traffic
 };
 extern TcTuning g_tc_tuning;

@@ -301,3 +301,34 @@ def test_nvt_step_matches_oracle(pb):
     assert abs(reps[-1].e_conserved - lg[-1][2]) < 1e-3
     h = [r.e_conserved for r in reps]
     assert max(h) - min(h) < 1e-2
+
+
+def test_repeated_evaluations_bit_identical(pb):
+    """The whole 3xTF32 path is deterministic: 25 evaluations of C2 (many pipelined tiles per
+    CTA through every fused epilogue) give bit-identical energies and forces."""
+    s = configs.system("C2")
+    m = pb.Allegro(configs.weight_file("C2"), s.box, precision=pb.PREC_3XTF32)
+    e0, ea0, f0 = m.compute_energy_forces(s.pos, s.species)
+    for _ in range(25):
+        e, ea, f = m.compute_energy_forces(s.pos, s.species)
+        assert e == e0 and np.array_equal(ea, ea0) and np.array_equal(f, f0)
+    m.close()
+
+
+def test_resnet_contraction_deterministic(pb):
+    """The two-operand resnet contraction (x | s) W with the aux save, X = x, ragged M, two
+    co-scheduled N-tiles: repeated launches are bit-identical and within 3xTF32 accuracy."""
+    rng = np.random.default_rng(2)
+    M, N, K, K1 = 90198, 128, 224, 128
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    W = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    u = rng.uniform(0, 1, M).astype(np.float32)
+    code = 3 | (K1 << 8)  # EPI_RESID with columns [K1, K) from the second operand
+    c0, a0 = pb.debug_gemm_epi(A, W, code, X=A, u=u, want_aux=True)
+    exact = 0.75 * (A.astype(np.float64) @ W.astype(np.float64))
+    assert np.abs(a0 - exact).max() <= 2e-5 * np.abs(exact).max()
+    want_c = 0.5 * A[:, :128].astype(np.float64) + 0.25 * u[:, None] * exact
+    assert np.abs(c0 - want_c).max() <= 2e-5 * np.abs(want_c).max()
+    for _ in range(8):
+        c, a = pb.debug_gemm_epi(A, W, code, X=A, u=u, want_aux=True)
+        assert np.array_equal(c, c0) and np.array_equal(a, a0)
