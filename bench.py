@@ -175,12 +175,13 @@ def _ncu_traffic(cfg_name, cls, alg_bytes_per_launch):
             "traffic_over_algorithmic": round(rec["dram_bytes_per_launch"] / max(alg_bytes_per_launch, 1e-9), 3)}
 
 
-def _config_dict(cfg, n_gpus, edges, precision, params):
+def _config_dict(cfg, n_gpus, edges, precision, params, strong=False):
     return {
         "workload": f"{cfg.name}: {cfg.description}, r_c={cfg.r_cut} A, NVE dt={DT_FS} fs, rebuild every step",
-        "atoms_per_gpu": cfg.n_atoms,
-        "atoms_total": cfg.n_atoms * n_gpus,
-        "edges_per_gpu": edges,
+        "atoms_per_gpu": cfg.n_atoms // n_gpus if strong else cfg.n_atoms,
+        "atoms_total": cfg.n_atoms if strong else cfg.n_atoms * n_gpus,
+        "edges_per_gpu": None if edges is None else edges // n_gpus,
+        "edges_total": edges,
         "layers": cfg.n_layers,
         "lmax": cfg.lmax,
         "params": params,
@@ -202,6 +203,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=512)
     ap.add_argument("--ref-sample", type=int, default=96)
     ap.add_argument("--profile-steps", type=int, default=1)
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: split the config's box over the GPUs (default: replicate it per GPU)")
     ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "fp32"])
     args = ap.parse_args()
     if args.impl == "reference":
@@ -225,8 +228,9 @@ def main():
     torch.cuda.set_device(local)
     cfg = configs.CONFIGS[args.config]
     grid = GRIDS.get(ws, (ws, 1, 1))
-    # weak scaling: the N-GPU box is the per-GPU box replicated over the domain grid
-    s = configs.system(cfg, reps=grid)
+    # weak scaling: the N-GPU box is the per-GPU box replicated over the domain grid;
+    # strong scaling (--strong, e.g. C4): the same box split over the grid
+    s = configs.system(cfg) if args.strong else configs.system(cfg, reps=grid)
     wf = configs.weight_file(cfg)
     stream = torch.cuda.current_stream()
     prec = pb.PREC_3XTF32 if args.precision == "3xtf32" else pb.PREC_FP32
@@ -346,8 +350,9 @@ def main():
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": _config_dict(cfg, ws, int(rep.n_edges), args.precision, pb.param_count(cfg.n_layers, cfg.lmax)),
+        "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config_dict(cfg, ws, int(rep.n_edges), args.precision, pb.param_count(cfg.n_layers, cfg.lmax),
+                               args.strong),
         "roofline": roof,
         "kernels": kernels,
         "gpu_launches": launches,
