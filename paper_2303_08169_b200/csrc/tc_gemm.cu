@@ -1,24 +1,29 @@
 // tc_gemm.cu -- tcgen05 tensor-core GEMM (3xTF32) with TMA-fed operands, TMEM
 // accumulators and the fused epilogues of gemm.cuh.
 //
-// One CTA per SM walks 128-row tiles of A (persistent).  Warp roles (320 threads):
+// One CTA per SM walks 128-row tiles of A (persistent); the N-tiles of a wide contraction are
+// sibling CTAs of the same launch walking the same M-tiles (A comes from HBM once, from L2 for
+// the sibling).  Warp roles (352 threads):
 //   warp 8      TMA producer: A[128 x 32] fp32 K-blocks (SWIZZLE_128B) into a ring of raw
-//               SMEM stages; the W image of this N-tile once (cp.async.bulk).
+//               SMEM stages (from a second tensor map past K1 for two-operand contractions);
+//               the W image of this N-tile once (cp.async.bulk).
 //   warps 0-3   split warpgroup (thread = row = TMEM lane): reads its row of a raw stage,
 //               a_hi = a with the low 13 mantissa bits cleared, a_lo = a - a_hi, and writes
 //               both into a TMEM A stage with tcgen05.st (the raw stage is freed at once).
-//   warp 9      MMA issuer (one lane): per K-block 4 x K=8 steps of
-//               tcgen05.mma.kind::tf32 (A from TMEM, W from SMEM)
+//   warp 9      MMA issuer (whole warp, one elect.sync leader issues): per K-block 4 x K=8
+//               steps of tcgen05.mma.kind::tf32 (A from TMEM, W from SMEM)
 //                 D += a_hi w_lo;  D += a_lo w_hi;  D += a_hi w_hi
-//               (N_t <= 64: "stacked" -- one MMA a_hi [w_hi | w_lo] of width 2 N_t into
-//               [D | D'] plus a_lo w_hi into D, so a_hi is read from TMEM once per K-step;
-//               the epilogue adds D + D')
-//               into one of two TMEM accumulators [128 lanes x N_t fp32 columns];
+//               into a ring of TMEM accumulators [128 lanes x N_t fp32 columns] (2-4 deep);
 //               tcgen05.commit frees the TMEM A stage / publishes the accumulator.
+//               (Optional "stacked" variant for N_t <= 64, off by default: one MMA
+//               a_hi [w_hi | w_lo] of width 2 N_t into [D | D'], the epilogue adds D + D'.)
 //   warps 4-7   epilogue warpgroup: tcgen05.ld 32x32b (thread = row), fused epilogue, and a
-//               per-warp swizzled SMEM transpose so global stores are 4 x 128 B lines.
+//               per-warp swizzled SMEM transpose so global stores are 4 x 128 B lines
+//               (optionally the row-dot of the output with a second [M][N] operand).
 //   warp 10     epilogue-input producer: the residual / accumulate input (X or old C) is
 //               streamed by TMA in [128 x 32] boxes into a 2-deep SMEM ring ahead of the epilogue.
+// Every consumer of a TMA-filled ring slot executes fence.proxy.async.shared::cta before it
+// releases the slot (generic-proxy loads vs the async-proxy refill).
 // W SMEM descriptors: K-major, SWIZZLE_128B, SBO = 1024 B, version 1 (sm_100).
 #include <cuda.h>
 #include <cudaTypedefs.h>
