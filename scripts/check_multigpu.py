@@ -14,6 +14,8 @@ dist.init_process_group("nccl")
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
 prec = pb.PREC_3XTF32
 grids = {2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+if os.environ.get("ALG_GRID"):  # e.g. ALG_GRID=1,1,2 exercises the z-axis halo on 2 GPUs
+    grids[int(os.environ["WORLD_SIZE"])] = tuple(int(v) for v in os.environ["ALG_GRID"].split(","))
 s = configs.system(cfg)
 if cfg == "C2":
     s = nh3.replicate(s, (2, 1, 1)) if ws >= 2 else s
