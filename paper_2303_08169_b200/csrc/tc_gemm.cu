@@ -488,14 +488,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr bool kIn = kX || EPI == EPI_ACC;  // epilogue reads a [M][N] input (X or old C)
     int xs = 0;
     uint32_t xph = 0;
+    // per-row scalars (u, and rs2 for EPI_R2) are loaded one tile ahead: a load issued at the
+    // tile start would stall the epilogue warps for a full DRAM round trip every tile
+    auto row_u = [&](int tt) -> float {
+      const int64_t rr = (int64_t)(grp + tt * n_grp) * ROWS + q * 32 + lane;
+      return (tt < n_my && rr < g.M && g.u != nullptr) ? __ldg(g.u + rr) : 1.f;
+    };
+    auto row_rs2 = [&](int tt) -> float {
+      const int64_t rr = (int64_t)(grp + tt * n_grp) * ROWS + q * 32 + lane;
+      return (EPI == EPI_R2 && tt < n_my && rr < g.M) ? __ldg(g.rs2 + rr) : 0.f;
+    };
+    float u_next = row_u(0), rs2_next = row_rs2(0);
     for (int t = 0; t < n_my; ++t) {
       const int a = t % p.n_acc;
       const uint32_t acph = (uint32_t)(t / p.n_acc) & 1u;
+      const float ur = u_next, e2_row = rs2_next;
+      u_next = row_u(t + 1);
+      rs2_next = row_rs2(t + 1);
       mbar_wait(acc_full + a, acph);
       tc_fence_after();
       const int64_t row0 = (int64_t)(grp + t * n_grp) * ROWS + q * 32;
       const int64_t r = row0 + lane;
-      const float ur = (r < g.M && g.u != nullptr) ? g.u[r] : 1.f;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * p.acc_cols);
       float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // row-dot partials, rows (lane>>3)+4i
       for (int c0 = 0; c0 < p.N_t; c0 += 32) {
@@ -528,7 +541,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (++xs == X_STAGES) xs = 0, xph ^= 1;
         }
         if constexpr (EPI == EPI_R2) {
-          const float e2 = (r < g.M) ? g.rs2[r] : 0.f;
+          const float e2 = e2_row;
           const int cb = col0 + c0;
           if (cb + 32 <= g.N) {  // warp-uniform float4 loads (broadcast)
             const float4* v1 = reinterpret_cast<const float4*>(g.vec1 + cb);
