@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpaper_allegro.so")
+LIB_PATH = os.environ.get("ALLEGRO_LIB") or os.path.join(_HERE, "lib", "libpaper_allegro.so")  # override: A/B builds
 
 OK = 0
 E_ARG, E_GEOMETRY, E_NONFINITE, E_WEIGHTS, E_CUDA, E_NCCL, E_OOM, E_STATE = -1, -2, -3, -4, -5, -6, -7, -8
