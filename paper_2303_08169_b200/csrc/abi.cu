@@ -311,7 +311,7 @@ static int md_run(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
       if (c->dom.multi) migrate(c);
       ALG_CUDA(cudaMemsetAsync(c->flags.p, 0, 4 * sizeof(int), c->stream));
       build_neighbors(c);
-      compute_forces(c);
+      compute_forces(c, /*defer_e=*/true);  // e_pot arrives with the finite check below
       md_half_kick(c, dt);
       if (c->nvt) {
         double K = md_kinetic(c);

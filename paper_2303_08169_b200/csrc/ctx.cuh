@@ -174,6 +174,7 @@ struct allegro_ctx {
   bool md_ready = false;
   int64_t md_steps = 0, n_rebuilds = 0;
   double e_pot = 0;
+  bool e_pot_pending = false;  // e_pot is in red[1] on the device (read by all_finite)
   double f_mean0 = 0, f_sigma0 = 0;  // step-0 outlier baseline
   // Nose-Hoover NVT (one thermostat; D23): off when tau <= 0
   bool nvt = false;
@@ -203,7 +204,7 @@ void build_neighbors(allegro_ctx* c);
 void wrap_positions(allegro_ctx* c);
 
 // model.cu: energies and forces for the current edge list -> c->frc, c->e_atom, c->e_pot
-void compute_forces(allegro_ctx* c);
+void compute_forces(allegro_ctx* c, bool defer_e = false);  // defer_e: e_pot read by all_finite
 
 // domain.cu (world_size > 1)
 void domain_setup(allegro_ctx* c, const void* nccl_id);
@@ -227,6 +228,7 @@ void force_stats(allegro_ctx* c, double* mean, double* sigma);
 int64_t count_outliers(allegro_ctx* c, double thr);
 bool all_finite(allegro_ctx* c);
 double sum_e_atom(allegro_ctx* c);
+void sum_e_atom_async(allegro_ctx* c);  // the sum into red[1] without reading it
 bool check_inputs(allegro_ctx* c);
 
 // pimd.cu (replica batches, ring-polymer MD; world_size == 1)

@@ -164,13 +164,17 @@ double md_kinetic(allegro_ctx* c) {
   return allreduce_sum(c, fetch(c, c->red.p));
 }
 
-double sum_e_atom(allegro_ctx* c) {
+void sum_e_atom_async(allegro_ctx* c) {
   c->red.reserve(8);
   {
     ProfScope ps_(&c->prof, c->stream, PK_REDUCE, 0, 8.0 * c->n);
     k_sum<<<1, kRedThreads, 0, c->stream>>>(c->e_atom.p, c->n, c->red.p + 1);
   }
   ALG_LAUNCH_CHECK();
+}
+
+double sum_e_atom(allegro_ctx* c) {
+  sum_e_atom_async(c);
   return fetch(c, c->red.p + 1);
 }
 
@@ -234,7 +238,9 @@ bool all_finite(allegro_ctx* c) {
   }
   int f = 0;
   ALG_CUDA(cudaMemcpyAsync(&f, c->flags.p + 2, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if (c->e_pot_pending) ALG_CUDA(cudaMemcpyAsync(&c->e_pot, c->red.p + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   ALG_CUDA(cudaStreamSynchronize(c->stream));
+  c->e_pot_pending = false;
   f = allreduce_max_i32(c, f);
   return f == 0 && std::isfinite(c->e_pot);
 }

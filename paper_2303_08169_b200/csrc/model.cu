@@ -917,7 +917,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
 
 }  // namespace
 
-void compute_forces(allegro_ctx* c) {
+void compute_forces(allegro_ctx* c, bool defer_e) {
   cudaStream_t st = c->stream;
   const int64_t n = c->n;
   const int64_t E = c->n_edges;
@@ -927,12 +927,19 @@ void compute_forces(allegro_ctx* c) {
   const size_t fpe = floats_per_edge(c->model);
   size_t e_cap = std::max<size_t>(4096, c->ws_budget_bytes / (fpe * sizeof(float)));
   e_cap = std::min<size_t>(e_cap, (size_t)std::max<int64_t>(E, 4096));
-  c->h_row_ptr.resize(n + 1);
-  ALG_CUDA(cudaMemcpyAsync(c->h_row_ptr.data(), c->row_ptr.p, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, st));
-  ALG_CUDA(cudaStreamSynchronize(st));
   std::vector<ChunkPtrs> chunks;
   int64_t a = 0;
   size_t a_cap = 1;
+  if ((size_t)E <= e_cap) {  // one chunk: no need for the row offsets on the host
+    chunks.push_back(ChunkPtrs{0, n, 0, E});
+    a_cap = std::max<size_t>(1, n);
+    a = n;
+  } else {
+    c->h_row_ptr.resize(n + 1);
+    ALG_CUDA(cudaMemcpyAsync(c->h_row_ptr.data(), c->row_ptr.p, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost,
+                             st));
+    ALG_CUDA(cudaStreamSynchronize(st));
+  }
   while (a < n) {
     int64_t b = a;
     while (b < n && (b == a || (size_t)(c->h_row_ptr[b + 1] - c->h_row_ptr[a]) <= e_cap)) ++b;
@@ -954,7 +961,12 @@ void compute_forces(allegro_ctx* c) {
     }
     ALG_LAUNCH_CHECK();
   }
-  c->e_pot = allreduce_sum(c, sum_e_atom(c));
+  if (defer_e && !c->dom.multi) {  // md_run: fetched together with the finite flag (all_finite)
+    sum_e_atom_async(c);
+    c->e_pot_pending = true;
+  } else {
+    c->e_pot = allreduce_sum(c, sum_e_atom(c));
+  }
 }
 
 }  // namespace allegro

@@ -393,6 +393,7 @@ void build_neighbors(allegro_ctx* c) {
   const double rc2 = rc * rc;
   c->nb_count.reserve(n + 1);
   c->row_ptr.reserve(n + 1);
+  int32_t E = 0;
   for (;;) {
     c->nb_pad.reserve((size_t)n * c->max_nb);
     c->key_pad.reserve((size_t)n * c->max_nb);
@@ -409,8 +410,12 @@ void build_neighbors(allegro_ctx* c) {
       }
       ALG_LAUNCH_CHECK();
     }
+    // the row offsets are scanned before the overflow check so that one host read brings both
+    // (a rebuild after an overflow rescans)
+    exclusive_scan(c, c->nb_count.p, c->row_ptr.p, n);
     int over = 0;
     ALG_CUDA(cudaMemcpyAsync(&over, c->flags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    ALG_CUDA(cudaMemcpyAsync(&E, c->row_ptr.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     ALG_CUDA(cudaStreamSynchronize(st));
     if (over <= c->max_nb) break;
     int nm = c->max_nb;
@@ -418,10 +423,6 @@ void build_neighbors(allegro_ctx* c) {
     if (nm > 4096) throw CudaError("neighbour count exceeds 4096 per atom");
     c->max_nb = nm;
   }
-  exclusive_scan(c, c->nb_count.p, c->row_ptr.p, n);
-  int32_t E = 0;
-  ALG_CUDA(cudaMemcpyAsync(&E, c->row_ptr.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  ALG_CUDA(cudaStreamSynchronize(st));
   c->n_edges = E;
   c->nbr.reserve(E + 1);
   c->key.reserve(E + 1);
