@@ -712,10 +712,11 @@ int allegro_get_edge_grad(allegro_ctx* c, int64_t capacity, double* g) {
   if (capacity < c->n_edges) return fail(c, ALLEGRO_E_ARG, "capacity too small");
   return guarded(c, [&]() -> int {
     ALG_CUDA(cudaSetDevice(c->device));
-    std::vector<float> h(3 * c->n_edges);
+    std::vector<float> h(4 * c->n_edges);  // device layout [E][4]
     ALG_CUDA(cudaMemcpyAsync(h.data(), c->g.p, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream));
     ALG_CUDA(cudaStreamSynchronize(c->stream));
-    for (size_t q = 0; q < h.size(); ++q) g[q] = h[q];
+    for (int64_t e = 0; e < c->n_edges; ++e)
+      for (int d = 0; d < 3; ++d) g[e * 3 + d] = h[e * 4 + d];
     return ALLEGRO_OK;
   });
 }

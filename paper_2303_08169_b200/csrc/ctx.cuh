@@ -161,7 +161,7 @@ struct allegro_ctx {
   int64_t n_edges = 0;
   allegro::DBuf<int32_t> nb_count, nb_pad, row_ptr, nbr, cidx, rev;
   allegro::DBuf<unsigned long long> key_pad, key;
-  allegro::DBuf<float> g;                    // [E][3] dE/dr_e
+  allegro::DBuf<float> g;                    // [E][4] dE/dr_e (x, y, z, pad: 16-B reverse gathers)
   std::vector<int32_t> h_row_ptr;
   // ---- scalars / flags ----
   allegro::DBuf<int> flags;                  // [0] overflow max count, [1] bad input, [2] non-finite

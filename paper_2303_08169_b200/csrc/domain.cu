@@ -149,7 +149,7 @@ __global__ void k_ghost_acc(int64_t E, int64_t n, const int32_t* __restrict__ nb
 #pragma unroll
   for (int d = 0; d < 3; ++d)
     atomicAdd(reinterpret_cast<unsigned long long*>(acc + (int64_t)a * 3 + d),
-              (unsigned long long)llrint(-(double)g[e * 3 + d] * kFixScale));
+              (unsigned long long)llrint(-(double)g[e * 4 + d] * kFixScale));
 }
 
 __global__ void k_ret_add(int64_t cnt, const long long* __restrict__ in, const int32_t* __restrict__ idx,

@@ -16,7 +16,7 @@
 //   A10 k_energy      E_e = x^L . w_out, E_i = sigma nbar^-1/2 sum E_e + mu      E7-E8
 //   A11 reverse mode  the same chain transposed (W^T GEMMs, k_tp_bwd), k_geom_bwd E9
 // then over all atoms:
-//   A12 k_force       F_a = sum_{e in row a} (g_e - g_rev(e)) in row order (fp64)
+//   A12 k_force_warp  F_a = sum_{e in row a} (g_e - g_rev(e)), fixed-order warp sum (fp64)
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -541,34 +541,46 @@ __global__ void k_geom_bwd(ChunkPtrs ch, GeomParams gp, const double* __restrict
       gz += inv * (pz - 2.f * sy * n[2]);
     }
   }
-  g[ge * 3] = gx;
-  g[ge * 3 + 1] = gy;
-  g[ge * 3 + 2] = gz;
+  reinterpret_cast<float4*>(g)[ge] = make_float4(gx, gy, gz, 0.f);  // [E][4]: one 16-B load per reverse gather
 }
 
 // ----------------------------------------------------------------- A12 force gather
-__global__ void k_force(int64_t n, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ rev,
-                        const float* __restrict__ g, const long long* __restrict__ acc, double* __restrict__ F,
-                        int* __restrict__ flags) {
-  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Warp per atom: the lanes stride the atom's CSR row (coalesced g reads, 32 reverse-edge
+// gathers in flight) and the fp64 partial sums are combined by a fixed butterfly, so the
+// result is deterministic (and independent of the chunking).
+// F_a = sum_{e in row a} (g_e - g_rev(e)) (+ the returned ghost forces); rev = -1: no reverse edge.
+__global__ void k_force_warp(int64_t n, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ rev,
+                             const float* __restrict__ g, const long long* __restrict__ acc, double* __restrict__ F,
+                             int* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= n) return;
   double f[3] = {0, 0, 0};
-  if (acc != nullptr) {  // multi-GPU: -g of edges that point at images of a, returned by the reverse halo
-#pragma unroll
-    for (int d = 0; d < 3; ++d) f[d] = (double)acc[a * 3 + d] * (1.0 / kFixScale);
-  }
-  for (int64_t e = row_ptr[a]; e < row_ptr[a + 1]; ++e) {
+  const int64_t r0 = row_ptr[a], r1 = row_ptr[a + 1];
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int64_t e = r0 + lane; e < r1; e += 32) {
     const int32_t r = rev[e];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) f[d] += (double)g[e * 3 + d] - (r >= 0 ? (double)g[(int64_t)r * 3 + d] : 0.0);
+    const float4 a4 = g4[e];
+    const float4 b4 = r >= 0 ? g4[r] : make_float4(0.f, 0.f, 0.f, 0.f);
+    f[0] += (double)a4.x - (double)b4.x;
+    f[1] += (double)a4.y - (double)b4.y;
+    f[2] += (double)a4.z - (double)b4.z;
   }
-  bool bad = false;
 #pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    F[a * 3 + d] = f[d];
-    bad = bad || !isfinite(f[d]);
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) f[d] += __shfl_xor_sync(0xffffffffu, f[d], o);
+  if (lane == 0) {
+    bool bad = false;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      // multi-GPU: -g of edges that point at images of a, returned by the reverse halo
+      const double v = f[d] + (acc != nullptr ? (double)acc[a * 3 + d] * (1.0 / kFixScale) : 0.0);
+      F[a * 3 + d] = v;
+      bad = bad || !isfinite(v);
+    }
+    if (bad) atomicOr(flags + 2, 1);
   }
-  if (bad) atomicOr(flags + 2, 1);
 }
 
 // ----------------------------------------------------------------- dispatch
@@ -955,9 +967,9 @@ void compute_forces(allegro_ctx* c, bool defer_e) {
   if (c->dom.multi) ghost_force_return(c);
   if (n > 0) {
     {
-      ProfScope ps_(&c->prof, st, PK_FORCE, 0, 24.0 * n + 8.0 * n + 28.0 * E);
-      k_force<<<ceil_div(n, 256), 256, 0, st>>>(n, c->row_ptr.p, c->rev.p, c->g.p,
-                                              c->dom.multi ? c->dom.acc.p : nullptr, c->frc.p, c->flags.p);
+      ProfScope ps_(&c->prof, st, PK_FORCE, 0, 24.0 * n + 8.0 * n + 28.0 * E);  // algorithmic: g_e, g_rev (12 B each), rev
+      k_force_warp<<<ceil_div(n * 32, 256), 256, 0, st>>>(n, c->row_ptr.p, c->rev.p, c->g.p,
+                                                        c->dom.multi ? c->dom.acc.p : nullptr, c->frc.p, c->flags.p);
     }
     ALG_LAUNCH_CHECK();
   }

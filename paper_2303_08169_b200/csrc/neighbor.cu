@@ -428,7 +428,7 @@ void build_neighbors(allegro_ctx* c) {
   c->key.reserve(E + 1);
   c->cidx.reserve(E + 1);
   c->rev.reserve(E + 1);
-  c->g.reserve(3 * (size_t)E + 3);
+  c->g.reserve(4 * (size_t)E + 4);  // [E][4] (x, y, z, pad)
   if (n > 0) {
     {
       ProfScope ps_(&c->prof, st, PK_EDGE, 0, 4.0 * n);

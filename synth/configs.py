@@ -7,6 +7,7 @@
 | C3 | 110,592 | bcc 24^3 | 6.0 | (3, 2) = paper's l=2 model | throughput + roofline |
 | C4 | 884,736 | bcc 48^3 | 6.0 | (3, 1) = paper's l=1 model | strong scaling |
 | C5 | 500,000 per GPU | sc 50^3 per GPU, replicated | 6.0 | (3, 1) | weak scaling (bench) |
+| CP | 6,912 per GPU | sc 12^3 per GPU, replicated | 6.0 | (3, 1) | context: the paper's granularity |
 
 r_c = 6.0 A is Table 5's r_max (§4.5); C1's 5 A is BASELINE.json's.
 """
@@ -41,6 +42,8 @@ CONFIGS = {
     "C3": Config("C3", "bcc", (24, 24, 24), 6.0, 3, 2, "liquid NH3 110,592 atoms, 3-layer lmax=2"),
     "C4": Config("C4", "bcc", (48, 48, 48), 6.0, 3, 1, "liquid NH3 884,736 atoms, 3-layer lmax=1"),
     "C5": Config("C5", "sc", (50, 50, 50), 6.0, 3, 1, "liquid NH3 500,000 atoms per GPU, 3-layer lmax=1"),
+    # SURVEY.md §8(d) optional context row: the paper's granularity, 6,912 atoms per GPU
+    "CP": Config("CP", "sc", (12, 12, 12), 6.0, 3, 1, "liquid NH3 6,912 atoms per GPU (the paper's weak-scaling size)"),
 }
 
 
