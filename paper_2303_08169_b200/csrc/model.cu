@@ -653,7 +653,9 @@ void run_gemm(const Model& M, const GemmArgs& g, const Wt& w, cudaStream_t st, P
     ALG_CUDA(cudaFreeAsync(cnt, st));
     return;
   }
-  if (M.precision == ALLEGRO_PREC_3XTF32 && (!g.dotv || (fuse_dot && w.tc.n_tiles == 1))) {
+  // (measured: fused into EPI_ACC it is cost-neutral against the separate pass; with the
+  // EPI_R2 epilogue's own loads it is 2-3 ms slower, so that one keeps the separate pass)
+  if (M.precision == ALLEGRO_PREC_3XTF32 && (!g.dotv || (fuse_dot && w.tc.n_tiles == 1 && g.epi != EPI_R2))) {
     tc_gemm(g, w.tc, st, prof);  // the row-dot (if any) is fused into the epilogue
     return;
   }
