@@ -87,6 +87,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
   asm volatile(
@@ -197,6 +198,7 @@ struct TcParams {
   uint32_t tmem_cols;  // allocated TMEM columns
   int diag;            // diagnostics: bit0 skip MMAs, bit1 skip global stores
   int has_x;           // the epilogue reads an [M][N] input (X, or old C) through the TMA ring
+  int tma_store;       // the output C (and aux) leave by TMA stores of [32 x 32] boxes (no row-dot)
 };
 
 // v <- s v (the saved pre-activation "aux"); out <- epilogue(v, xin) (xin = X, or old C for EPI_ACC)
@@ -340,14 +342,15 @@ __device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uin
 template <int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
-              const __grid_constant__ CUtensorMap mapX, TcParams p) {
+              const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapC,
+              const __grid_constant__ CUtensorMap mapAux, TcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   // 1024-align inside the __shared__ array (pointer arithmetic keeps the shared address space)
   unsigned char* base = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
   unsigned char* w_img = base;  // per K-block: [w_hi rows][w_lo rows]
   unsigned char* stage0 = base + ((p.w_bytes + 1023) & ~1023u);
-  unsigned char* out_stage = stage0 + (size_t)p.stages * STAGE_BYTES;  // [4 warps][4 KB]
-  unsigned char* x_stage = out_stage + 4 * STAGE_OUT_BYTES;            // [X_STAGES][16 KB] (if has_x)
+  unsigned char* out_stage = stage0 + (size_t)p.stages * STAGE_BYTES;  // [4 warps][2][4 KB]
+  unsigned char* x_stage = out_stage + 8 * STAGE_OUT_BYTES;            // [X_STAGES][16 KB] (if has_x)
   uint64_t* bars = reinterpret_cast<uint64_t*>(x_stage + (p.has_x ? X_STAGES * X_STAGE_BYTES : 0));
   uint64_t* raw_full = bars;                          // [stages]  TMA landed
   uint64_t* raw_empty = raw_full + p.stages;          // [stages]  split warps read it
@@ -484,7 +487,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr bool kX = EPI == EPI_RESID || EPI == EPI_URESID || EPI == EPI_ADDX || EPI == EPI_DSILU;
     constexpr bool kAuxEpi = EPI == EPI_SILU || EPI == EPI_UMUL_SAVE || EPI == EPI_RESID;
     const bool want_aux = kAuxEpi && g.aux != nullptr;
-    unsigned char* buf = out_stage + (size_t)q * STAGE_OUT_BYTES;
+    unsigned char* buf = out_stage + (size_t)(2 * q) * STAGE_OUT_BYTES;  // [8][4 KB]: two slots per warp
     constexpr bool kIn = kX || EPI == EPI_ACC;  // epilogue reads a [M][N] input (X or old C)
     int xs = 0;
     uint32_t xph = 0;
@@ -499,6 +502,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       return (EPI == EPI_R2 && tt < n_my && rr < g.M) ? __ldg(g.rs2 + rr) : 0.f;
     };
     float u_next = row_u(0), rs2_next = row_rs2(0);
+    int n_st = 0;  // TMA stores issued by this warp
     for (int t = 0; t < n_my; ++t) {
       const int a = t % p.n_acc;
       const uint32_t acph = (uint32_t)(t / p.n_acc) & 1u;
@@ -573,8 +577,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int64_t col = col0 + c0;
         const int nc = (p.N_t - c0) >= 32 ? 8 : (p.N_t - c0) / 4;
         epi_apply<32, EPI>(g, v, xin, ur, out);
-        if (g.dotv != nullptr) scatter_rows_dot(buf, g.C + col, g.N, row0, g.M, lane, out, nc, dq, acc8);
-        else scatter_rows(buf, g.C + col, g.N, row0, g.M, lane, out, nc);
+        if (g.dotv != nullptr) {
+          scatter_rows_dot(buf, g.C + col, g.N, row0, g.M, lane, out, nc, dq, acc8);
+        } else if (p.tma_store) {  // [32 rows x 32 cols] boxes through this warp's two SMEM slots
+          if (want_aux) {  // C and aux in one group; wait until the previous group has read both slots
+            unsigned char* tc = out_stage + (size_t)(2 * q) * STAGE_OUT_BYTES;
+            unsigned char* ta = tc + STAGE_OUT_BYTES;
+            if (n_st >= 1) {
+              if (lane == 0) bulk_wait_read0();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              *tile_at(tc, lane, c) = make_float4(out[4 * c], out[4 * c + 1], out[4 * c + 2], out[4 * c + 3]);
+              *tile_at(ta, lane, c) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&mapC, (int)col, (int)row0, tc);
+              tma_store_2d(&mapAux, (int)col, (int)row0, ta);
+              bulk_commit();
+            }
+          } else {  // double-buffered: the slot of chunk n_st - 2 must have been read
+            unsigned char* tb = out_stage + (size_t)(2 * q + (n_st & 1)) * STAGE_OUT_BYTES;
+            if (n_st >= 2) {
+              if (lane == 0) bulk_wait_read1();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *tile_at(tb, lane, c) = make_float4(out[4 * c], out[4 * c + 1], out[4 * c + 2], out[4 * c + 3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&mapC, (int)col, (int)row0, tb);
+              bulk_commit();
+            }
+          }
+          ++n_st;
+          continue;  // aux (if any) already stored
+        } else {
+          scatter_rows(buf, g.C + col, g.N, row0, g.M, lane, out, nc);
+        }
         if (want_aux) scatter_rows(buf, g.aux + col, g.N, row0, g.M, lane, v, nc);
       }
       if (g.dotv != nullptr) {  // reduce the 8 lanes of each row; lane (lane & 7) == i writes row (lane>>3)+4i
@@ -594,6 +639,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + a);
     }
+    if (p.tma_store && lane == 0) bulk_wait0();  // the output is complete before the CTA retires
   }
   __syncthreads();
   if (warp == 9) {
@@ -640,6 +686,7 @@ TcTuning make_tuning() {
   if (const char* e = std::getenv("ALLEGRO_TC_STACK")) t.stack = std::atoi(e) != 0;  // A/B switches for measurements
   if (const char* e = std::getenv("ALLEGRO_TC_MAXACC")) t.max_acc = std::atoi(e);
   if (const char* e = std::getenv("ALLEGRO_TC_MAXSTAGES")) t.max_stages = std::atoi(e);
+  if (const char* e = std::getenv("ALLEGRO_TC_TMASTORE")) t.tma_store = std::atoi(e) != 0;
   return t;
 }
 TcTuning g_tc_tuning = make_tuning();
@@ -659,7 +706,7 @@ TcWeight tc_prepare_weight(const std::vector<float>& W, int K, int N, std::vecto
   t.N = N;
   const int nK = (K + BLK_K - 1) / BLK_K;
   // widest N-tile (multiple of 16 dividing N) whose image leaves room for >= 2 stages
-  const size_t budget = SMEM_LIMIT - SMEM_RESERVE - 2 * (size_t)STAGE_BYTES - 4 * (size_t)STAGE_OUT_BYTES -
+  const size_t budget = SMEM_LIMIT - SMEM_RESERVE - 2 * (size_t)STAGE_BYTES - 8 * (size_t)STAGE_OUT_BYTES -
                         (size_t)X_STAGES * X_STAGE_BYTES;
   int nt = 0;
   for (int c = std::min(N, 256); c >= 16; c -= 16)
@@ -710,7 +757,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const size_t w_round = (w_bytes + 1023) & ~(size_t)1023;
   const bool has_x = g.epi == EPI_RESID || g.epi == EPI_URESID || g.epi == EPI_ADDX || g.epi == EPI_DSILU ||
                      g.epi == EPI_ACC;
-  const size_t out_bytes = 4 * (size_t)STAGE_OUT_BYTES + (has_x ? (size_t)X_STAGES * X_STAGE_BYTES : 0);
+  const size_t out_bytes = 8 * (size_t)STAGE_OUT_BYTES + (has_x ? (size_t)X_STAGES * X_STAGE_BYTES : 0);
   int stages = (int)((SMEM_LIMIT - SMEM_RESERVE - w_round - out_bytes) / STAGE_BYTES);
   stages = std::min(stages, g_tc_tuning.max_stages);
   if (stages < 2) throw CudaError("tc_gemm: shared memory too small for 2 stages");
@@ -749,6 +796,10 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   p.has_x = has_x ? 1 : 0;
   const float* xsrc = g.epi == EPI_ACC ? g.C : g.X;
   const CUtensorMap mX = has_x ? make_map(xsrc, g.M, g.N, g.N) : mA;
+  const bool aux_epi = g.aux && (g.epi == EPI_SILU || g.epi == EPI_UMUL_SAVE || g.epi == EPI_RESID);
+  p.tma_store = (g_tc_tuning.tma_store && !g.dotv && w.N_t % 32 == 0 && (p.diag & 2) == 0) ? 1 : 0;
+  const CUtensorMap mC = p.tma_store ? make_map(g.C, g.M, g.N, g.N, 32) : mA;
+  const CUtensorMap mAux = (p.tma_store && aux_epi) ? make_map(g.aux, g.M, g.N, g.N, 32) : mA;
   if (g.dotv && w.n_tiles != 1) throw CudaError("tc_gemm: the fused row-dot needs a single N-tile");
   // one launch; CTA b handles N-tile b % n_tiles of M-tile group b / n_tiles
   // (ALLEGRO_TC_COSCHED=0: one launch per N-tile, for A/B measurements)
@@ -774,7 +825,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
                  tag);
     switch (g.epi) {
 #define ALG_EPI(e) \
-  case e: k_tc_gemm<e><<<grid, TC_THREADS, smem, st>>>(mA, mA2, mX, p); break;
+  case e: k_tc_gemm<e><<<grid, TC_THREADS, smem, st>>>(mA, mA2, mX, mC, mAux, p); break;
       ALG_EPI(EPI_STORE) ALG_EPI(EPI_SILU) ALG_EPI(EPI_UMUL_SAVE) ALG_EPI(EPI_RESID) ALG_EPI(EPI_URESID)
       ALG_EPI(EPI_USCALE) ALG_EPI(EPI_ACC) ALG_EPI(EPI_ADDX) ALG_EPI(EPI_DSILU) ALG_EPI(EPI_R2)
 #undef ALG_EPI
