@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int64_t col = col0 + c0;
         const int nc = (p.N_t - c0) >= 32 ? 8 : (p.N_t - c0) / 4;
         epi_apply<32, EPI>(g, v, xin, ur, out);
-        if (g.dotv != nullptr) {
+        if (g.dotv != nullptr && !p.tma_store) {
           scatter_rows_dot(buf, g.C + col, g.N, row0, g.M, lane, out, nc, dq, acc8);
         } else if (p.tma_store) {  // [32 rows x 32 cols] boxes through this warp's two SMEM slots
           if (want_aux) {  // C and aux in one group; wait until the previous group has read both slots
@@ -613,6 +613,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (lane == 0) {
               tma_store_2d(&mapC, (int)col, (int)row0, tb);
               bulk_commit();
+            }
+            if (g.dotv != nullptr) {  // fused row-dot on the transposed (coalesced) view of the slot
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float4 o4 = *tile_at(tb, (lane >> 3) + 4 * i, lane & 7);
+                acc8[i] = fmaf(o4.x, dq[i].x, fmaf(o4.y, dq[i].y, fmaf(o4.z, dq[i].z, fmaf(o4.w, dq[i].w, acc8[i]))));
+              }
             }
           }
           ++n_st;
@@ -797,7 +804,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const float* xsrc = g.epi == EPI_ACC ? g.C : g.X;
   const CUtensorMap mX = has_x ? make_map(xsrc, g.M, g.N, g.N) : mA;
   const bool aux_epi = g.aux && (g.epi == EPI_SILU || g.epi == EPI_UMUL_SAVE || g.epi == EPI_RESID);
-  p.tma_store = (g_tc_tuning.tma_store && !g.dotv && w.N_t % 32 == 0 && (p.diag & 2) == 0) ? 1 : 0;
+  p.tma_store = (g_tc_tuning.tma_store && w.N_t % 32 == 0 && (p.diag & 2) == 0) ? 1 : 0;
   const CUtensorMap mC = p.tma_store ? make_map(g.C, g.M, g.N, g.N, 32) : mA;
   const CUtensorMap mAux = (p.tma_store && aux_epi) ? make_map(g.aux, g.M, g.N, g.N, 32) : mA;
   if (g.dotv && w.n_tiles != 1) throw CudaError("tc_gemm: the fused row-dot needs a single N-tile");
