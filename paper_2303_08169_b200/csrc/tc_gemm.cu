@@ -84,6 +84,18 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int
                "r"(c1), "r"(smem_u32(src))
                : "memory");
 }
+// same, with an L2 eviction-priority policy (createpolicy) on the written lines
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, int c0, int c1, const void* src, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+                   (uint64_t)map),
+               "r"(c0), "r"(c1), "r"(smem_u32(src)), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -199,6 +211,7 @@ struct TcParams {
   int diag;            // diagnostics: bit0 skip MMAs, bit1 skip global stores
   int has_x;           // the epilogue reads an [M][N] input (X, or old C) through the TMA ring
   int tma_store;       // the output C (and aux) leave by TMA stores of [32 x 32] boxes (no row-dot)
+  int store_hint;      // TMA stores carry an L2 evict_first policy
 };
 
 // v <- s v (the saved pre-activation "aux"); out <- epilogue(v, xin) (xin = X, or old C for EPI_ACC)
@@ -595,8 +608,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&mapC, (int)col, (int)row0, tc);
-              tma_store_2d(&mapAux, (int)col, (int)row0, ta);
+              if (p.store_hint) {
+                const uint64_t pol = policy_evict_first();
+                tma_store_2d_hint(&mapC, (int)col, (int)row0, tc, pol);
+                tma_store_2d_hint(&mapAux, (int)col, (int)row0, ta, pol);
+              } else {
+                tma_store_2d(&mapC, (int)col, (int)row0, tc);
+                tma_store_2d(&mapAux, (int)col, (int)row0, ta);
+              }
               bulk_commit();
             }
           } else {  // double-buffered: the slot of chunk n_st - 2 must have been read
@@ -611,7 +630,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&mapC, (int)col, (int)row0, tb);
+              if (p.store_hint) tma_store_2d_hint(&mapC, (int)col, (int)row0, tb, policy_evict_first());
+              else tma_store_2d(&mapC, (int)col, (int)row0, tb);
               bulk_commit();
             }
             if (g.dotv != nullptr) {  // fused row-dot on the transposed (coalesced) view of the slot
@@ -694,6 +714,7 @@ TcTuning make_tuning() {
   if (const char* e = std::getenv("ALLEGRO_TC_MAXACC")) t.max_acc = std::atoi(e);
   if (const char* e = std::getenv("ALLEGRO_TC_MAXSTAGES")) t.max_stages = std::atoi(e);
   if (const char* e = std::getenv("ALLEGRO_TC_TMASTORE")) t.tma_store = std::atoi(e) != 0;
+  if (const char* e = std::getenv("ALLEGRO_TC_STOREHINT")) t.store_hint = std::atoi(e);
   return t;
 }
 TcTuning g_tc_tuning = make_tuning();
@@ -805,6 +826,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const CUtensorMap mX = has_x ? make_map(xsrc, g.M, g.N, g.N) : mA;
   const bool aux_epi = g.aux && (g.epi == EPI_SILU || g.epi == EPI_UMUL_SAVE || g.epi == EPI_RESID);
   p.tma_store = (g_tc_tuning.tma_store && w.N_t % 32 == 0 && (p.diag & 2) == 0) ? 1 : 0;
+  p.store_hint = g_tc_tuning.store_hint;
   const CUtensorMap mC = p.tma_store ? make_map(g.C, g.M, g.N, g.N, 32) : mA;
   const CUtensorMap mAux = (p.tma_store && aux_epi) ? make_map(g.aux, g.M, g.N, g.N, 32) : mA;
   if (g.dotv && w.n_tiles != 1) throw CudaError("tc_gemm: the fused row-dot needs a single N-tile");

@@ -28,6 +28,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
 // Launch tuning / diagnostics (defaults are the production configuration).
 struct TcTuning {
   int tma_store = 1;   // TMA-store epilogue when N_t % 32 == 0
+  int store_hint = 0;  // L2 evict_first policy on the TMA stores
   int max_stages = 4;  // A-stage ring depth cap
   int max_acc = 4;     // TMEM accumulator ring depth cap (>= 2)
   int stack = 0;       // stacked hi/lo MMAs for N_t in {32, 64} (off: nondeterministic under load)
