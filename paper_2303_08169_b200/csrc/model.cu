@@ -653,9 +653,14 @@ void run_gemm(const Model& M, const GemmArgs& g, const Wt& w, cudaStream_t st, P
     ALG_CUDA(cudaFreeAsync(cnt, st));
     return;
   }
-  // (measured: fused into EPI_ACC it is cost-neutral against the separate pass; with the
-  // EPI_R2 epilogue's own loads it is 2-3 ms slower, so that one keeps the separate pass)
-  if (M.precision == ALLEGRO_PREC_3XTF32 && (!g.dotv || (fuse_dot && w.tc.n_tiles == 1 && g.epi != EPI_R2))) {
+  // (measured: fused into EPI_ACC it is cost-neutral against the separate pass; into EPI_R2 it
+  // was 2-3 ms slower with the STG epilogue and is 2 ms faster with the TMA-store epilogue)
+  static const bool fuse_r2 = [] {  // A/B switch: the row-dot fused into the EPI_R2 epilogue too
+    const char* e = std::getenv("ALLEGRO_FUSE_R2");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (M.precision == ALLEGRO_PREC_3XTF32 &&
+      (!g.dotv || (fuse_dot && w.tc.n_tiles == 1 && (fuse_r2 || g.epi != EPI_R2)))) {
     tc_gemm(g, w.tc, st, prof);  // the row-dot (if any) is fused into the epilogue
     return;
   }
