@@ -109,7 +109,7 @@ __global__ void k_geom(ChunkPtrs ch, GeomParams gp, const double* __restrict__ a
   }
   u[e] = uu;
   const int zi = species[i], zj = aspec[a];
-  float* zz = z + e * 16;
+  float zz[16];
   zz[0] = zi == 0 ? 1.f : 0.f;
   zz[1] = zi == 1 ? 1.f : 0.f;
   zz[2] = zj == 0 ? 1.f : 0.f;
@@ -119,11 +119,19 @@ __global__ void k_geom(ChunkPtrs ch, GeomParams gp, const double* __restrict__ a
   for (int q = 0; q < kNB; ++q) zz[4 + q] = uu * pre * sinf(gp.freq[q] * d * gp.inv_rc);
 #pragma unroll
   for (int q = 12; q < 16; ++q) zz[q] = 0.f;
+  // 16-B vector stores: a warp's row of z is 32 x 64 B, written as four 512-B-wide instructions
+  float4* z4 = reinterpret_cast<float4*>(z + e * 16);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) z4[q] = make_float4(zz[4 * q], zz[4 * q + 1], zz[4 * q + 2], zz[4 * q + 3]);
   const float inv = 1.f / d;
   const float nv[3] = {r[0] * inv, r[1] * inv, r[2] * inv};
   float y[9];
   sh_eval(nv, y, gp.lmax);
-  for (int q = 0; q < gp.dsh; ++q) Y[e * gp.dsh + q] = y[q];
+  if (gp.dsh == 4) {
+    reinterpret_cast<float4*>(Y)[e] = make_float4(y[0], y[1], y[2], y[3]);
+  } else {
+    for (int q = 0; q < gp.dsh; ++q) Y[e * gp.dsh + q] = y[q];
+  }
 }
 
 // ----------------------------------------------------------------- A7+A8 TP forward
