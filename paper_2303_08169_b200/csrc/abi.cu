@@ -163,6 +163,7 @@ void allegro_destroy(allegro_ctx* c) {
   c->cstart.release();
   c->cslot.release();
   c->csorted.release();
+  c->cpos.release();
   c->nb_count.release();
   c->nb_pad.release();
   c->row_ptr.release();

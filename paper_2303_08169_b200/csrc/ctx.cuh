@@ -156,6 +156,7 @@ struct allegro_ctx {
   int ncell[3] = {0, 0, 0};
   double cell_lo[3] = {0, 0, 0}, cell_size[3] = {0, 0, 0};
   allegro::DBuf<int32_t> ccount, cstart, cslot, csorted;
+  allegro::DBuf<double4> cpos;  // positions in cell order (x, y, z, pad)
   // ---- edges (CSR by owned centre, canonical row order) ----
   int max_nb = 256;
   int64_t n_edges = 0;

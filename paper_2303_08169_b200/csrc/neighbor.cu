@@ -151,22 +151,25 @@ __global__ void k_cell_count(const double* __restrict__ apos, const int32_t* __r
 
 __global__ void k_cell_fill(const double* __restrict__ apos, const int32_t* __restrict__ aowner, int64_t na, CellGeom cg,
                             const int32_t* __restrict__ cstart, const int32_t* __restrict__ cslot,
-                            int32_t* __restrict__ sorted) {
+                            int32_t* __restrict__ sorted, double4* __restrict__ spos) {
   const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= na) return;
-  const int cx = cell_coord(apos[a * 3], cg, 0), cy = cell_coord(apos[a * 3 + 1], cg, 1),
-            cz = cell_coord(apos[a * 3 + 2], cg, 2);
+  const double x = apos[a * 3], y = apos[a * 3 + 1], z = apos[a * 3 + 2];
+  const int cx = cell_coord(x, cg, 0), cy = cell_coord(y, cg, 1), cz = cell_coord(z, cg, 2);
   const int64_t c = cell_base(cg, aowner[a]) + (cz * cg.n[1] + cy) * cg.n[0] + cx;
-  sorted[cstart[c] + cslot[a]] = (int32_t)a;
+  const int t = cstart[c] + cslot[a];
+  sorted[t] = (int32_t)a;
+  spos[t] = make_double4(x, y, z, 0.0);  // cell-ordered copy: the edge build reads candidates contiguously
 }
 
 constexpr int kEdgeWarps = 4;
 
 // One warp per owned centre: scan the 27 neighbouring cells, keep candidates with the
-// canonical fp64 test, bitonic-sort the row by key in shared memory.
+// canonical fp64 test, rank-sort the row by key out of shared memory.
 __global__ void __launch_bounds__(kEdgeWarps * 32) k_edge_build(const double* __restrict__ apos, int64_t n, CellGeom cg,
                                                                  const int32_t* __restrict__ cstart,
                                                                  const int32_t* __restrict__ sorted,
+                                                                 const double4* __restrict__ spos,
                                                                  const int32_t* __restrict__ ashift,
                                                                  const int32_t* __restrict__ agid, double rc2, int max_nb,
                                                                  int32_t* __restrict__ nb_count, int32_t* __restrict__ nb_pad,
@@ -182,73 +185,86 @@ __global__ void __launch_bounds__(kEdgeWarps * 32) k_edge_build(const double* __
   const double xi = apos[i * 3], yi = apos[i * 3 + 1], zi = apos[i * 3 + 2];
   const int cx = cell_coord(xi, cg, 0), cy = cell_coord(yi, cg, 1), cz = cell_coord(zi, cg, 2);
   const int64_t cb = cell_base(cg, i);
-  int cnt = 0;
-  for (int dz = -1; dz <= 1; ++dz) {
-    const int z = cz + dz;
-    if (z < 0 || z >= cg.n[2]) continue;
-    for (int dy = -1; dy <= 1; ++dy) {
-      const int y = cy + dy;
-      if (y < 0 || y >= cg.n[1]) continue;
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int x = cx + dx;
-        if (x < 0 || x >= cg.n[0]) continue;
-        const int64_t c = cb + (z * cg.n[1] + y) * cg.n[0] + x;
-        const int s0 = cstart[c], s1 = cstart[c + 1];
-        for (int t0 = s0; t0 < s1; t0 += 32) {
-          const int t = t0 + lane;
-          bool inc = false;
-          int32_t a = -1;
-          if (t < s1) {
-            a = sorted[t];
-            const double dxv = __dsub_rn(apos[(int64_t)a * 3], xi);
-            const double dyv = __dsub_rn(apos[(int64_t)a * 3 + 1], yi);
-            const double dzv = __dsub_rn(apos[(int64_t)a * 3 + 2], zi);
-            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dxv, dxv), __dmul_rn(dyv, dyv)), __dmul_rn(dzv, dzv));
-            inc = (d2 <= rc2) && ((int64_t)a != i);
-          }
-          const unsigned bal = __ballot_sync(0xffffffffu, inc);
-          const int slot = cnt + __popc(bal & ((1u << lane) - 1u));
-          if (inc && slot < max_nb) {
-            sk[slot] = edge_key(agid[a], ashift[a]);
-            si[slot] = a;
-          }
-          cnt += __popc(bal);
-        }
-      }
+  // lane l < 27 owns neighbour cell l (dz, dy, dx in -1..1, x fastest); the warp scans the
+  // cells' candidate counts and then walks the concatenated candidate list 32 at a time, so the
+  // loads of one pass are independent of the previous pass (no cstart -> sorted chain per cell)
+  int s0 = 0, nc = 0;
+  if (lane < 27) {
+    const int x = cx + lane % 3 - 1, y = cy + (lane / 3) % 3 - 1, z = cz + lane / 9 - 1;
+    if (x >= 0 && x < cg.n[0] && y >= 0 && y < cg.n[1] && z >= 0 && z < cg.n[2]) {
+      const int64_t c = cb + (z * cg.n[1] + y) * cg.n[0] + x;
+      s0 = cstart[c];
+      nc = cstart[c + 1] - s0;
     }
+  }
+  int off = nc;  // inclusive scan of the counts
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, off, d);
+    if (lane >= d) off += o;
+  }
+  const int total = __shfl_sync(0xffffffffu, off, 31);
+  off -= nc;  // exclusive
+  int cnt = 0;
+  for (int k0 = 0; k0 < total; k0 += 32) {
+    const int k = k0 + lane;
+    // the cell holding candidate k: the last lane j with off[j] <= k (off is non-decreasing)
+    int j = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int oj = __shfl_sync(0xffffffffu, off, j + step);
+      if (j + step < 27 && oj <= k) j += step;
+    }
+    const int sj = __shfl_sync(0xffffffffu, s0, j), oj = __shfl_sync(0xffffffffu, off, j);
+    bool inc = false;
+    int32_t a = -1;
+    if (k < total) {
+      const int t = sj + (k - oj);
+      a = sorted[t];
+      const double4 pa = spos[t];
+      const double dxv = __dsub_rn(pa.x, xi);
+      const double dyv = __dsub_rn(pa.y, yi);
+      const double dzv = __dsub_rn(pa.z, zi);
+      const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dxv, dxv), __dmul_rn(dyv, dyv)), __dmul_rn(dzv, dzv));
+      inc = (d2 <= rc2) && ((int64_t)a != i);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, inc);
+    const int slot = cnt + __popc(bal & ((1u << lane) - 1u));
+    if (inc && slot < max_nb) {
+      sk[slot] = edge_key(agid[a], ashift[a]);
+      si[slot] = a;
+    }
+    cnt += __popc(bal);
   }
   if (cnt > max_nb) {
     if (lane == 0) atomicMax(flags, cnt);
     cnt = max_nb;
   }
-  int P = 1;
-  while (P < cnt) P <<= 1;
-  for (int t = cnt + lane; t < P; t += 32) {
-    sk[t] = ~0ull;
-    si[t] = -1;
-  }
   __syncwarp();
-  for (int k = 2; k <= P; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = lane; t < P; t += 32) {
-        const int u = t ^ j;
-        if (u > t) {
-          const bool up = (t & k) == 0;
-          const unsigned long long ka = sk[t], kb = sk[u];
-          if ((ka > kb) == up) {
-            sk[t] = kb;
-            sk[u] = ka;
-            const int32_t ia = si[t];
-            si[t] = si[u];
-            si[u] = ia;
-          }
-        }
-      }
-      __syncwarp();
+  // rank sort by key (keys are unique per row; ties would be broken by candidate order): each
+  // lane ranks four of the row's entries against all of them, reading keys as SMEM broadcasts
+  for (int t0 = 0; t0 < cnt; t0 += 128) {
+    unsigned long long kr[4];
+    int rk[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int t = t0 + 32 * r + lane;
+      kr[r] = t < cnt ? sk[t] : ~0ull;
+      rk[r] = 0;
     }
-  for (int t = lane; t < cnt; t += 32) {
-    nb_pad[i * max_nb + t] = si[t];
-    key_pad[i * max_nb + t] = sk[t];
+    for (int m = 0; m < cnt; ++m) {
+      const unsigned long long km = sk[m];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) rk[r] += (km < kr[r]) || (km == kr[r] && m < t0 + 32 * r + lane);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int t = t0 + 32 * r + lane;
+      if (t < cnt) {
+        nb_pad[i * max_nb + rk[r]] = si[t];
+        key_pad[i * max_nb + rk[r]] = kr[r];
+      }
+    }
   }
   if (lane == 0) nb_count[i] = cnt;
 }
@@ -376,6 +392,7 @@ void build_neighbors(allegro_ctx* c) {
   c->cstart.reserve(ncells + 1);
   c->cslot.reserve(na);
   c->csorted.reserve(na);
+  c->cpos.reserve(na);
   ALG_CUDA(cudaMemsetAsync(c->ccount.p, 0, sizeof(int32_t) * (ncells + 1), st));
   {
     ProfScope ps_(&c->prof, st, PK_CELL, 0, 28.0 * na);
@@ -384,9 +401,9 @@ void build_neighbors(allegro_ctx* c) {
   ALG_LAUNCH_CHECK();
   exclusive_scan(c, c->ccount.p, c->cstart.p, ncells);
   {
-    ProfScope ps_(&c->prof, st, PK_CELL, 0, 36.0 * na);
+    ProfScope ps_(&c->prof, st, PK_CELL, 0, 68.0 * na);
     k_cell_fill<<<ceil_div(na, 256), 256, 0, st>>>(c->apos.p, c->aowner.p, na, cg, c->cstart.p, c->cslot.p,
-                                                 c->csorted.p);
+                                                 c->csorted.p, c->cpos.p);
   }
   ALG_LAUNCH_CHECK();
   // ---- edges ----
@@ -405,7 +422,7 @@ void build_neighbors(allegro_ctx* c) {
       {
         ProfScope ps_(&c->prof, st, PK_EDGE, 0, 28.0 * n);
         k_edge_build<<<ceil_div(n, kEdgeWarps), kEdgeWarps * 32, smem, st>>>(
-          c->apos.p, n, cg, c->cstart.p, c->csorted.p, c->ashift.p, c->agid.p, rc2, c->max_nb, c->nb_count.p, c->nb_pad.p,
+          c->apos.p, n, cg, c->cstart.p, c->csorted.p, c->cpos.p, c->ashift.p, c->agid.p, rc2, c->max_nb, c->nb_count.p, c->nb_pad.p,
           c->key_pad.p, c->flags.p);
       }
       ALG_LAUNCH_CHECK();
