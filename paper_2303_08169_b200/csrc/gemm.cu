@@ -40,6 +40,10 @@ __global__ void __launch_bounds__(NT) k_gemm(GemmArgs g) {
     if (a_ok) {
       ra[0] = *reinterpret_cast<const float4*>(src);
       ra[1] = *reinterpret_cast<const float4*>(src + 4);
+      if (g.silu_a) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) ra[q] = make_float4(silu(ra[q].x), silu(ra[q].y), silu(ra[q].z), silu(ra[q].w));
+      }
     } else {
       ra[0] = make_float4(0.f, 0.f, 0.f, 0.f);
       ra[1] = ra[0];

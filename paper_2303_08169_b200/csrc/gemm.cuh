@@ -44,6 +44,7 @@ struct GemmArgs {
   float dot_coef = 0.f;
   float s = 1.f, alpha = 0.f, beta = 0.f;
   int epi = EPI_STORE;
+  int silu_a = 0;  // A holds pre-activations: the contraction multiplies SiLU(A) (applied on load)
 };
 
 void gemm(const GemmArgs& g, cudaStream_t st, Profiler* prof);

@@ -690,7 +690,7 @@ void run_gemm(const Model& M, const GemmArgs& g, const Wt& w, cudaStream_t st, P
 
 size_t floats_per_edge(const Model& M) {
   const int dsh = (M.lmax + 1) * (M.lmax + 1);
-  size_t f = 16 + 32 + 32 + 64 + 64 + 128 + 1 + dsh + 2 * 128;
+  size_t f = 16 + 32 + 64 + 128 + 1 + dsh + 2 * 128;  // z, a1, a2, m, u, Y, x (two buffers)
   size_t tmax = 0, vmax = 0, nwmax = 0, nsmax = 0;
   for (int k = 0; k < M.n_layers; ++k) {
     const LayerInfo& L = M.L[k];
@@ -711,9 +711,7 @@ void reserve_ws(allegro_ctx* c, size_t e_cap, size_t a_cap) {
   const int dsh = (M.lmax + 1) * (M.lmax + 1);
   w.z.reserve(e_cap * 16);
   w.a1.reserve(e_cap * 32);
-  w.h1.reserve(e_cap * 32);
   w.a2.reserve(e_cap * 64);
-  w.h2.reserve(e_cap * 64);
   w.m.reserve(e_cap * 128);
   w.u.reserve(e_cap);
   w.Y.reserve(e_cap * dsh);
@@ -788,13 +786,15 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   };
   // ---- two-body MLP (E4, E5) ----
   {
-    GemmArgs g = G(w.z.p, 16, M.w.tb_w0, 32, 16, w.h1.p, 1.f / std::sqrt(12.f), EPI_SILU);
-    g.aux = w.a1.p;
+    // only the pre-activations a1, a2 are stored (the reverse pass needs them); the next
+    // contraction applies SiLU to its operand on load instead of reading a stored h = SiLU(a)
+    GemmArgs g = G(w.z.p, 16, M.w.tb_w0, 32, 16, w.a1.p, 1.f / std::sqrt(12.f), EPI_STORE);
     run_gemm(M, g, *last_w, st, &c->prof);
-    g = G(w.h1.p, 32, M.w.tb_w1, 64, 32, w.h2.p, kCSilu / std::sqrt(32.f), EPI_SILU);
-    g.aux = w.a2.p;
+    g = G(w.a1.p, 32, M.w.tb_w1, 64, 32, w.a2.p, kCSilu / std::sqrt(32.f), EPI_STORE);
+    g.silu_a = 1;
     run_gemm(M, g, *last_w, st, &c->prof);
-    g = G(w.h2.p, 64, M.w.tb_w2, 128, 64, w.xa.p, kCSilu / std::sqrt(64.f), EPI_UMUL_SAVE);
+    g = G(w.a2.p, 64, M.w.tb_w2, 128, 64, w.xa.p, kCSilu / std::sqrt(64.f), EPI_UMUL_SAVE);
+    g.silu_a = 1;
     g.aux = w.m.p;
     g.u = w.u.p;
     run_gemm(M, g, *last_w, st, &c->prof);

@@ -462,7 +462,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const float4 v = *reinterpret_cast<const float4*>(raw + row * 128 + ((c ^ (row & 7)) << 4));
-          const float x[4] = {v.x, v.y, v.z, v.w};
+          float x[4] = {v.x, v.y, v.z, v.w};
+          if (p.g.silu_a) {  // pre-activation operand (SiLU(0) = 0 keeps the zero-filled tail zero)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] = silu(x[e]);
+          }
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const uint32_t h = __float_as_uint(x[e]) & 0xffffe000u;
