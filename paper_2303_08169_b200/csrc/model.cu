@@ -90,47 +90,73 @@ __device__ __forceinline__ void edge_vec(const double* __restrict__ apos, int32_
   for (int d = 0; d < 3; ++d) r[d] = (float)__dsub_rn(apos[(int64_t)a * 3 + d], apos[(int64_t)i * 3 + d]);
 }
 
-__global__ void k_geom(ChunkPtrs ch, GeomParams gp, const double* __restrict__ apos, const int32_t* __restrict__ cidx,
-                       const int32_t* __restrict__ nbr, const int32_t* __restrict__ aspec,
-                       const int32_t* __restrict__ species, float* __restrict__ z, float* __restrict__ Y,
-                       float* __restrict__ u) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= ch.n_e) return;
-  const int64_t ge = ch.e0 + e;
-  const int32_t i = cidx[ge], a = nbr[ge];
-  float r[3];
-  edge_vec(apos, i, a, r);
-  const float d = sqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-  const float x = d * gp.inv_rc;
-  float uu = 0.f;
-  if (x < 1.f) {
-    const float x2 = x * x, x3 = x2 * x, x6 = x3 * x3;
-    uu = 1.f - 28.f * x6 + 48.f * x6 * x - 21.f * x6 * x2;
+// The first two-body layer is folded in (E4): a1 = (1/sqrt 12) z W0 with z = [onehot(Z_i),
+// onehot(Z_j), u B(d)] never leaves registers -- two selected rows of W0 plus eight Bessel rows.
+__global__ void __launch_bounds__(256) k_geom(ChunkPtrs ch, GeomParams gp, const double* __restrict__ apos,
+                                              const int32_t* __restrict__ cidx, const int32_t* __restrict__ nbr,
+                                              const int32_t* __restrict__ aspec, const int32_t* __restrict__ species,
+                                              const float* __restrict__ w0, float s0, float* __restrict__ a1,
+                                              float* __restrict__ Y, float* __restrict__ u) {
+  __shared__ __align__(16) float sw[12][32];  // W0 rows 0..11 ([K = 12][N = 32]); read as broadcast float4
+  __shared__ float4 stile[256 * 8];           // the block's a1 rows, 16-B chunks XOR-swizzled by row % 8
+  for (int t = threadIdx.x; t < 12 * 32; t += blockDim.x) sw[t / 32][t % 32] = w0[t];
+  __syncthreads();
+  const int64_t e0 = (int64_t)blockIdx.x * blockDim.x;
+  const int row = threadIdx.x;
+  const int64_t e = e0 + row;
+  if (e < ch.n_e) {
+    const int64_t ge = ch.e0 + e;
+    const int32_t i = cidx[ge], a = nbr[ge];
+    float r[3];
+    edge_vec(apos, i, a, r);
+    const float d = sqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+    const float x = d * gp.inv_rc;
+    float uu = 0.f;
+    if (x < 1.f) {
+      const float x2 = x * x, x3 = x2 * x, x6 = x3 * x3;
+      uu = 1.f - 28.f * x6 + 48.f * x6 * x - 21.f * x6 * x2;
+    }
+    u[e] = uu;
+    const int zi = species[i], zj = aspec[a];
+    const float pre = 2.f * gp.inv_rc / d;
+    float zb[kNB];
+#pragma unroll
+    for (int q = 0; q < kNB; ++q) zb[q] = uu * pre * sinf(gp.freq[q] * d * gp.inv_rc);
+    // a1 = s0 (z W0): one-hot rows first, then the Bessel rows in k order; W0 is read as
+    // broadcast float4, the row goes to SMEM and leaves the block as coalesced 16-B stores
+    const float4* s4 = reinterpret_cast<const float4*>(&sw[0][0]);
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (zi < 2) acc = s4[zi * 8 + c4];
+      if (zj < 2) {
+        const float4 b = s4[(2 + zj) * 8 + c4];
+        acc = make_float4(acc.x + b.x, acc.y + b.y, acc.z + b.z, acc.w + b.w);
+      }
+#pragma unroll
+      for (int q = 0; q < kNB; ++q) {
+        const float4 wq = s4[(4 + q) * 8 + c4];
+        acc = make_float4(fmaf(zb[q], wq.x, acc.x), fmaf(zb[q], wq.y, acc.y), fmaf(zb[q], wq.z, acc.z),
+                          fmaf(zb[q], wq.w, acc.w));
+      }
+      stile[row * 8 + (c4 ^ (row & 7))] = make_float4(s0 * acc.x, s0 * acc.y, s0 * acc.z, s0 * acc.w);
+    }
+    const float inv = 1.f / d;
+    const float nv[3] = {r[0] * inv, r[1] * inv, r[2] * inv};
+    float y[9];
+    sh_eval(nv, y, gp.lmax);
+    if (gp.dsh == 4) {
+      reinterpret_cast<float4*>(Y)[e] = make_float4(y[0], y[1], y[2], y[3]);
+    } else {
+      for (int q = 0; q < gp.dsh; ++q) Y[e * gp.dsh + q] = y[q];
+    }
   }
-  u[e] = uu;
-  const int zi = species[i], zj = aspec[a];
-  float zz[16];
-  zz[0] = zi == 0 ? 1.f : 0.f;
-  zz[1] = zi == 1 ? 1.f : 0.f;
-  zz[2] = zj == 0 ? 1.f : 0.f;
-  zz[3] = zj == 1 ? 1.f : 0.f;
-  const float pre = 2.f * gp.inv_rc / d;
-#pragma unroll
-  for (int q = 0; q < kNB; ++q) zz[4 + q] = uu * pre * sinf(gp.freq[q] * d * gp.inv_rc);
-#pragma unroll
-  for (int q = 12; q < 16; ++q) zz[q] = 0.f;
-  // 16-B vector stores: a warp's row of z is 32 x 64 B, written as four 512-B-wide instructions
-  float4* z4 = reinterpret_cast<float4*>(z + e * 16);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) z4[q] = make_float4(zz[4 * q], zz[4 * q + 1], zz[4 * q + 2], zz[4 * q + 3]);
-  const float inv = 1.f / d;
-  const float nv[3] = {r[0] * inv, r[1] * inv, r[2] * inv};
-  float y[9];
-  sh_eval(nv, y, gp.lmax);
-  if (gp.dsh == 4) {
-    reinterpret_cast<float4*>(Y)[e] = make_float4(y[0], y[1], y[2], y[3]);
-  } else {
-    for (int q = 0; q < gp.dsh; ++q) Y[e * gp.dsh + q] = y[q];
+  __syncthreads();
+  const int rows = ch.n_e - e0 < 256 ? (int)(ch.n_e - e0) : 256;
+  float4* dst = reinterpret_cast<float4*>(a1 + e0 * 32);
+  for (int f = threadIdx.x; f < rows * 8; f += 256) {
+    const int rr = f >> 3, c = f & 7;
+    dst[f] = stile[rr * 8 + (c ^ (rr & 7))];
   }
 }
 
@@ -491,11 +517,51 @@ __global__ void k_rowdot(int64_t E, const float* __restrict__ P, const float* __
 }
 
 // ----------------------------------------------------------------- E9 geometry reverse
-__global__ void k_geom_bwd(ChunkPtrs ch, GeomParams gp, const double* __restrict__ apos, const int32_t* __restrict__ cidx,
-                           const int32_t* __restrict__ nbr, const float* __restrict__ ubar,
-                           const float* __restrict__ zbar, const float* __restrict__ ybar, float* __restrict__ g) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// zbar (Bessel part) = s0 ab1 W0[4..11]^T is formed here from ab1 (the first two-body layer's
+// reverse, folded in like its forward in k_geom); the one-hot rows carry no gradient.
+__global__ void __launch_bounds__(256) k_geom_bwd(ChunkPtrs ch, GeomParams gp, const double* __restrict__ apos,
+                                                  const int32_t* __restrict__ cidx, const int32_t* __restrict__ nbr,
+                                                  const float* __restrict__ ubar, const float* __restrict__ w0, float s0,
+                                                  const float* __restrict__ ab1, const float* __restrict__ ybar,
+                                                  float* __restrict__ g) {
+  __shared__ __align__(16) float swt[32][kNB];  // W0 Bessel rows 4..11, transposed: [j][q], broadcast float4 reads
+  __shared__ float4 stile[256 * 8];             // the block's ab1 rows (coalesced load), XOR-swizzled by row % 8
+  for (int t = threadIdx.x; t < kNB * 32; t += blockDim.x) swt[t % 32][t / 32] = w0[4 * 32 + t];
+  const int64_t e0 = (int64_t)blockIdx.x * blockDim.x;
+  {
+    const int rows = ch.n_e - e0 < 256 ? (int)(ch.n_e - e0) : 256;
+    const float4* src = reinterpret_cast<const float4*>(ab1 + e0 * 32);
+    for (int f = threadIdx.x; f < rows * 8; f += 256) {
+      const int rr = f >> 3, c = f & 7;
+      stile[rr * 8 + (c ^ (rr & 7))] = src[f];
+    }
+  }
+  __syncthreads();
+  const int row = threadIdx.x;
+  const int64_t e = e0 + row;
   if (e >= ch.n_e) return;
+  float zbar[kNB];
+#pragma unroll
+  for (int q = 0; q < kNB; ++q) zbar[q] = 0.f;
+  {
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+      const float4 v = stile[row * 8 + (c4 ^ (row & 7))];
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float4* wj = reinterpret_cast<const float4*>(&swt[4 * c4 + t][0]);
+#pragma unroll
+        for (int h = 0; h < kNB / 4; ++h) {
+          const float4 w4 = wj[h];
+          zbar[4 * h] = fmaf(vv[t], w4.x, zbar[4 * h]);
+          zbar[4 * h + 1] = fmaf(vv[t], w4.y, zbar[4 * h + 1]);
+          zbar[4 * h + 2] = fmaf(vv[t], w4.z, zbar[4 * h + 2]);
+          zbar[4 * h + 3] = fmaf(vv[t], w4.w, zbar[4 * h + 3]);
+        }
+      }
+    }
+  }
   const int64_t ge = ch.e0 + e;
   float r[3];
   edge_vec(apos, cidx[ge], nbr[ge], r);
@@ -519,7 +585,7 @@ __global__ void k_geom_bwd(ChunkPtrs ch, GeomParams gp, const double* __restrict
     sincosf(k * d, &sn, &cs);
     const float B = pre * sn * inv;
     const float dB = pre * (k * cs * inv - sn * inv * inv);
-    const float zb = zbar[e * 16 + 4 + q];
+    const float zb = s0 * zbar[q];
     ub = fmaf(zb, B, ub);
     db = fmaf(uu * zb, dB, db);
   }
@@ -690,7 +756,7 @@ void run_gemm(const Model& M, const GemmArgs& g, const Wt& w, cudaStream_t st, P
 
 size_t floats_per_edge(const Model& M) {
   const int dsh = (M.lmax + 1) * (M.lmax + 1);
-  size_t f = 16 + 32 + 64 + 128 + 1 + dsh + 2 * 128;  // z, a1, a2, m, u, Y, x (two buffers)
+  size_t f = 32 + 64 + 128 + 1 + dsh + 2 * 128;  // a1, a2, m, u, Y, x (two buffers)
   size_t tmax = 0, vmax = 0, nwmax = 0, nsmax = 0;
   for (int k = 0; k < M.n_layers; ++k) {
     const LayerInfo& L = M.L[k];
@@ -701,7 +767,7 @@ size_t floats_per_edge(const Model& M) {
     nwmax = std::max(nwmax, (size_t)L.nw);
     nsmax = std::max(nsmax, (size_t)L.A.n_s * kC);
   }
-  f += tmax + 2 * 128 + nsmax + 2 * vmax + nwmax + dsh + 1 + 16 + 64 + 32 + 1;
+  f += tmax + 2 * 128 + nsmax + 2 * vmax + nwmax + dsh + 1 + 64 + 32 + 1;
   return f;
 }
 
@@ -709,7 +775,6 @@ void reserve_ws(allegro_ctx* c, size_t e_cap, size_t a_cap) {
   Workspace& w = c->ws;
   const Model& M = c->model;
   const int dsh = (M.lmax + 1) * (M.lmax + 1);
-  w.z.reserve(e_cap * 16);
   w.a1.reserve(e_cap * 32);
   w.a2.reserve(e_cap * 64);
   w.m.reserve(e_cap * 128);
@@ -738,7 +803,6 @@ void reserve_ws(allegro_ctx* c, size_t e_cap, size_t a_cap) {
   w.wbar.reserve(e_cap * nwmax);
   w.ybar.reserve(e_cap * dsh);
   w.ubar.reserve(e_cap);
-  w.zbar.reserve(e_cap * 16);
   w.ab2.reserve(e_cap * 64);
   w.ab1.reserve(e_cap * 32);
   w.ebar.reserve(e_cap);
@@ -762,9 +826,9 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   gp.dsh = dsh;
   if (E > 0) {
     {
-      ProfScope ps_(&c->prof, st, PK_GEOM, 0, (double)E * (8 + 64 + 4 * dsh + 4));
-      k_geom<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, c->aspec.p, c->species.p, w.z.p,
-                                             w.Y.p, w.u.p);
+      ProfScope ps_(&c->prof, st, PK_GEOM, 0, (double)E * (8 + 128 + 4 * dsh + 4));
+      k_geom<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, c->aspec.p, c->species.p,
+                                             M.w.tb_w0.f, 1.f / std::sqrt(12.f), w.a1.p, w.Y.p, w.u.p);
     }
     ALG_LAUNCH_CHECK();
   }
@@ -788,9 +852,8 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   {
     // only the pre-activations a1, a2 are stored (the reverse pass needs them); the next
     // contraction applies SiLU to its operand on load instead of reading a stored h = SiLU(a)
-    GemmArgs g = G(w.z.p, 16, M.w.tb_w0, 32, 16, w.a1.p, 1.f / std::sqrt(12.f), EPI_STORE);
-    run_gemm(M, g, *last_w, st, &c->prof);
-    g = G(w.a1.p, 32, M.w.tb_w1, 64, 32, w.a2.p, kCSilu / std::sqrt(32.f), EPI_STORE);
+    // (a1 = z W0 / sqrt 12 was formed by k_geom)
+    GemmArgs g = G(w.a1.p, 32, M.w.tb_w1, 64, 32, w.a2.p, kCSilu / std::sqrt(32.f), EPI_STORE);
     g.silu_a = 1;
     run_gemm(M, g, *last_w, st, &c->prof);
     g = G(w.a2.p, 64, M.w.tb_w2, 128, 64, w.xa.p, kCSilu / std::sqrt(64.f), EPI_UMUL_SAVE);
@@ -929,14 +992,13 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     g = G(w.ab2.p, 64, M.w.tb_w1T, 32, 64, w.ab1.p, kCSilu / std::sqrt(32.f), EPI_DSILU);
     g.X = w.a1.p;
     run_gemm(M, g, *last_w, st, &c->prof);
-    g = G(w.ab1.p, 32, M.w.tb_w0T, 16, 32, w.zbar.p, 1.f / std::sqrt(12.f), EPI_STORE);
-    run_gemm(M, g, *last_w, st, &c->prof);
+    // (ab1 W0^T is formed inside k_geom_bwd)
   }
   if (E > 0) {
     {
-      ProfScope ps_(&c->prof, st, PK_GEOM_BWD, 0, (double)E * (8 + 4 + 64 + 4 * dsh + 12));
-      k_geom_bwd<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, w.ubar.p, w.zbar.p, w.ybar.p,
-                                                 c->g.p);
+      ProfScope ps_(&c->prof, st, PK_GEOM_BWD, 0, (double)E * (8 + 4 + 128 + 4 * dsh + 16));
+      k_geom_bwd<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, w.ubar.p, M.w.tb_w0.f,
+                                                 1.f / std::sqrt(12.f), w.ab1.p, w.ybar.p, c->g.p);
     }
     ALG_LAUNCH_CHECK();
   }
