@@ -7,7 +7,8 @@
 //   warp 8      TMA producer: A[128 x 32] fp32 K-blocks (SWIZZLE_128B) into a ring of raw
 //               SMEM stages (from a second tensor map past K1 for two-operand contractions);
 //               the W image of this N-tile once (cp.async.bulk).
-//   warps 0-3   split warpgroup (thread = row = TMEM lane): reads its row of a raw stage,
+//   warps 0-3   split warpgroup (thread = row = TMEM lane): reads its row of a raw stage
+//               (applying SiLU first when the operand is a stored pre-activation, silu_a),
 //               a_hi = a with the low 13 mantissa bits cleared, a_lo = a - a_hi, and writes
 //               both into a TMEM A stage with tcgen05.st (the raw stage is freed at once).
 //   warp 9      MMA issuer (whole warp, one elect.sync leader issues): per K-block 4 x K=8
@@ -17,9 +18,13 @@
 //               tcgen05.commit frees the TMEM A stage / publishes the accumulator.
 //               (Optional "stacked" variant for N_t <= 64, off by default: one MMA
 //               a_hi [w_hi | w_lo] of width 2 N_t into [D | D'], the epilogue adds D + D'.)
-//   warps 4-7   epilogue warpgroup: tcgen05.ld 32x32b (thread = row), fused epilogue, and a
-//               per-warp swizzled SMEM transpose so global stores are 4 x 128 B lines
-//               (optionally the row-dot of the output with a second [M][N] operand).
+//   warps 4-7   epilogue warpgroup: tcgen05.ld 32x32b (thread = row), fused epilogue; each
+//               [32 rows x 32 cols] output box is staged in one of the warp's two swizzled
+//               SMEM slots and written by one TMA store (cp.async.bulk.tensor, bulk groups
+//               recycle the slots; the saved pre-activation "aux" leaves the same way); the
+//               optional row-dot with a second [M][N] operand reads the staged box back in
+//               the transposed, coalesced view.  (Fallback without TMA stores: the same
+//               slot as a transpose tile, global stores as 4 x 128 B lines.)
 //   warp 10     epilogue-input producer: the residual / accumulate input (X or old C) is
 //               streamed by TMA in [128 x 32] boxes into a 2-deep SMEM ring ahead of the epilogue.
 // Every consumer of a TMA-filled ring slot executes fence.proxy.async.shared::cta before it
