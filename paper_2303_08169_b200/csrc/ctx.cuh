@@ -214,6 +214,7 @@ void migrate(allegro_ctx* c);
 void halo_exchange(allegro_ctx* c);     // fills apos/agid/aspec/ashift for owned + ghosts
 void ghost_force_return(allegro_ctx* c);  // accumulates ghost forces and returns them to owners
 double allreduce_sum(allegro_ctx* c, double v);
+void allreduce_e_flag(allegro_ctx* c, const double* d_e, const int* d_flag, double* e, int* flag);
 int64_t allreduce_sum_i64(allegro_ctx* c, int64_t v);
 int allreduce_max_i32(allegro_ctx* c, int v);
 void select_owned(allegro_ctx* c, int64_t n_global, const int32_t* species, const double* pos, const double* vel);

@@ -275,6 +275,26 @@ void domain_teardown(allegro_ctx* c) {
   D.red.release();
 }
 
+__global__ void k_pack_e_flag(const double* __restrict__ e, const int* __restrict__ flag, double* __restrict__ out) {
+  out[0] = *e;
+  out[1] = (double)*flag;
+}
+
+// One allreduce for the two per-step scalars of md_run: sum of the ranks' potential energies
+// (device-resident partial sums) and of their non-finite flags (non-negative ints, exact in fp64).
+void allreduce_e_flag(allegro_ctx* c, const double* d_e, const int* d_flag, double* e, int* flag) {
+  Domain& D = c->dom;
+  D.red.reserve(4);
+  k_pack_e_flag<<<1, 1, 0, c->stream>>>(d_e, d_flag, D.red.p);
+  ALG_LAUNCH_CHECK();
+  ALG_NCCL(NcclApi::get().AllReduce(D.red.p, D.red.p + 2, 2, ncclFloat64, ncclSum, D.comm, c->stream));
+  double h[2] = {0.0, 0.0};
+  ALG_CUDA(cudaMemcpyAsync(h, D.red.p + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  ALG_CUDA(cudaStreamSynchronize(c->stream));
+  *e = h[0];
+  *flag = h[1] != 0.0 ? 1 : 0;
+}
+
 double allreduce_sum(allegro_ctx* c, double v) {
   Domain& D = c->dom;
   if (!D.multi) return v;

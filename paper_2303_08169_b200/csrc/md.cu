@@ -237,6 +237,11 @@ bool all_finite(allegro_ctx* c) {
     ALG_LAUNCH_CHECK();
   }
   int f = 0;
+  if (c->dom.multi && c->e_pot_pending) {  // one packed allreduce + one host read per step
+    allreduce_e_flag(c, c->red.p + 1, c->flags.p + 2, &c->e_pot, &f);
+    c->e_pot_pending = false;
+    return f == 0 && std::isfinite(c->e_pot);
+  }
   ALG_CUDA(cudaMemcpyAsync(&f, c->flags.p + 2, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   if (c->e_pot_pending) ALG_CUDA(cudaMemcpyAsync(&c->e_pot, c->red.p + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   ALG_CUDA(cudaStreamSynchronize(c->stream));

@@ -1050,7 +1050,7 @@ void compute_forces(allegro_ctx* c, bool defer_e) {
     }
     ALG_LAUNCH_CHECK();
   }
-  if (defer_e && !c->dom.multi) {  // md_run: fetched together with the finite flag (all_finite)
+  if (defer_e) {  // md_run: fetched (multi-GPU: allreduced) together with the finite flag (all_finite)
     sum_e_atom_async(c);
     c->e_pot_pending = true;
   } else {
