@@ -548,6 +548,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             dq[i] = (rr < g.M && cc < p.N_t - c0) ? __ldg(reinterpret_cast<const float4*>(g.dotv + rr * g.N + col0 + c0 + cc))
                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
           }
+          // warm L2 with the next chunk's [32 x 32] block (one 128-B line per lane, no registers held)
+          const int tn = c0 + 32 < p.N_t ? t : t + 1, cn = c0 + 32 < p.N_t ? c0 + 32 : 0;
+          const int64_t rn = (int64_t)(grp + tn * n_grp) * ROWS + q * 32 + lane;
+          if (tn < n_my && rn < g.M)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(g.dotv + rn * g.N + col0 + cn));
         }
         if constexpr (kIn) {
           // this thread's row of the TMA-loaded [128 x 32] input box (SWIZZLE_128B)
