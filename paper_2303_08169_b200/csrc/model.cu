@@ -239,6 +239,42 @@ __device__ __forceinline__ void fetch_env(const TpArgs& t, int64_t e, int lane, 
   for (int l = 0; l < AR::NENV; ++l) in.we[l] = t.w[e * AR::NW + AR::ENV_OFF + l * kC + lane];
 }
 
+// L2 prefetch of edge e's per-edge blocks (each lane one 128-B line of a [dim][32] block): issued
+// a fixed number of edges ahead of the register pipeline, holds no registers.  Measured on C5
+// (profiles/r01_tp_prefetch_ab.jsonl): k_tp_fwd 46.9 -> 44.6 ms per step at distance 2; in
+// k_tp_bwd it raises the register count (72 -> 96) and nets nothing, so it is off there.
+#ifndef ALG_TP_PFD_FWD
+#define ALG_TP_PFD_FWD 2
+#endif
+#ifndef ALG_TP_PFD_BWD
+#define ALG_TP_PFD_BWD 0
+#endif
+__device__ __forceinline__ void pf_lines(const float* base, int nlines, int lane) {
+  if (lane < nlines) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + lane * kC));
+}
+
+template <int NL, int LMAX, int K, bool TB>
+__device__ __forceinline__ void prefetch_edge(const TpArgs& t, int64_t e, int lane) {
+  using AR = Arch<NL, LMAX, K>;
+  if constexpr (K == 0) {
+    pf_lines(t.w + e * AR::NW, AR::NENV, lane);
+  } else {
+    static_for<AR::A.in.n>([&](auto I) {
+      constexpr int ii = decltype(I)::value;
+      constexpr int dim = ir_dim(AR::A.in.v[ii]);
+      pf_lines(t.V + (int64_t)AR::v_base(ii) * t.e_cap + e * dim * kC, dim, lane);
+    });
+  }
+  if constexpr (TB) {
+    static_for<AR::A.out.n>([&](auto O) {
+      constexpr int o = decltype(O)::value;
+      constexpr int dim = ir_dim(AR::A.out.v[o]);
+      constexpr int nto = AR::A.n_to[o];
+      pf_lines(t.Tb[o] + e * dim * nto * kC, dim * nto, lane);
+    });
+  }
+}
+
 // lanes that own the butterfly total of value mm (warp_sum_multi<DSH>)
 template <int DSH>
 __device__ __forceinline__ bool owns_total(int lane, int mm) {
@@ -279,6 +315,8 @@ __global__ void __launch_bounds__(128) k_tp_fwd(TpArgs t) {
     float v[AR::DIN];
     expand_v<NL, LMAX, K>(nx, v);
     fetch_v<NL, LMAX, K>(t, e + 1 < r1 ? e + 1 : e, lane, nx);
+    if constexpr (ALG_TP_PFD_FWD > 0)
+      if (e + ALG_TP_PFD_FWD < r1) prefetch_edge<NL, LMAX, K, false>(t, e + ALG_TP_PFD_FWD, lane);
     float T[AR::DT];
 #pragma unroll
     for (int q = 0; q < AR::DT; ++q) T[q] = 0.f;
@@ -358,6 +396,8 @@ __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
   for (int64_t e = r0; e < r1; ++e) {
     const BwdIn<NL, LMAX, K> cur = nx;
     fetch_bwd<NL, LMAX, K>(t, e + 1 < r1 ? e + 1 : e, lane, mm, nx);
+    if constexpr (ALG_TP_PFD_BWD > 0)
+      if (e + ALG_TP_PFD_BWD < r1) prefetch_edge<NL, LMAX, K, true>(t, e + ALG_TP_PFD_BWD, lane);
     float v[AR::DIN], vb[AR::DIN];
     expand_v<NL, LMAX, K>(cur.v, v);
 #pragma unroll
