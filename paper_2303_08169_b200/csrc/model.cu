@@ -275,6 +275,40 @@ __device__ __forceinline__ void prefetch_edge(const TpArgs& t, int64_t e, int la
   }
 }
 
+// one prefetch per lane per edge: lane i owns line i of the edge's V (or w) blocks followed by its
+// T-bar blocks; a base pointer and a per-edge stride are all it holds across the edge loop
+struct PfPlan {
+  const float* base = nullptr;
+  int64_t stride = 0;
+};
+
+template <int NL, int LMAX, int K>
+__device__ __forceinline__ PfPlan pf_plan_bwd(const TpArgs& t, int lane) {
+  using AR = Arch<NL, LMAX, K>;
+  PfPlan pl;
+  int first = 0;
+  auto take = [&](const float* blk, int nlines, int64_t stride) {
+    if (lane >= first && lane < first + nlines) pl.base = blk + (lane - first) * kC, pl.stride = stride;
+    first += nlines;
+  };
+  if constexpr (K == 0) {
+    take(t.w, AR::NENV, AR::NW);
+  } else {
+    static_for<AR::A.in.n>([&](auto I) {
+      constexpr int ii = decltype(I)::value;
+      constexpr int dim = ir_dim(AR::A.in.v[ii]);
+      take(t.V + (int64_t)AR::v_base(ii) * t.e_cap, dim, dim * kC);
+    });
+  }
+  static_for<AR::A.out.n>([&](auto O) {
+    constexpr int o = decltype(O)::value;
+    constexpr int dim = ir_dim(AR::A.out.v[o]);
+    constexpr int nto = AR::A.n_to[o];
+    take(t.Tb[o], dim * nto, dim * nto * kC);
+  });
+  return pl;
+}
+
 // lanes that own the butterfly total of value mm (warp_sum_multi<DSH>)
 template <int DSH>
 __device__ __forceinline__ bool owns_total(int lane, int mm) {
@@ -393,11 +427,13 @@ __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
   }
   BwdIn<NL, LMAX, K> nx;
   fetch_bwd<NL, LMAX, K>(t, r0, lane, mm, nx);
+  [[maybe_unused]] const PfPlan pf = ALG_TP_PFD_BWD > 0 ? pf_plan_bwd<NL, LMAX, K>(t, lane) : PfPlan{};
   for (int64_t e = r0; e < r1; ++e) {
     const BwdIn<NL, LMAX, K> cur = nx;
     fetch_bwd<NL, LMAX, K>(t, e + 1 < r1 ? e + 1 : e, lane, mm, nx);
     if constexpr (ALG_TP_PFD_BWD > 0)
-      if (e + ALG_TP_PFD_BWD < r1) prefetch_edge<NL, LMAX, K, true>(t, e + ALG_TP_PFD_BWD, lane);
+      if (pf.base != nullptr && e + ALG_TP_PFD_BWD < r1)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pf.base + (e + ALG_TP_PFD_BWD) * pf.stride));
     float v[AR::DIN], vb[AR::DIN];
     expand_v<NL, LMAX, K>(cur.v, v);
 #pragma unroll
