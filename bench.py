@@ -154,6 +154,7 @@ PREC_TEXT = {
     "oracle": "fp64 numpy oracle (oracle/allegro.py) on host cores",
     "3xtf32": "3xTF32 tcgen05 GEMMs (fp32-level accuracy) + fp32 TP (fp64 positions, Verlet, energy sums)",
     "fp32": "fp32 CUDA-core GEMMs + fp32 TP (fp64 positions, Verlet, energy sums)",
+    "tf32": "single-pass TF32 tcgen05 GEMMs (outside the force bound; reported, not gated) + fp32 TP",
 }
 
 
@@ -192,6 +193,42 @@ def _config_dict(cfg, n_gpus, edges, precision, params, strong=False):
     }
 
 
+def _spawn(args_list, n):
+    """`bench.py --gpus N` outside torchrun: re-launch itself with one process per GPU."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + args_list
+    return subprocess.call(cmd)
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _cpu_baseline(cfg, sample_all, sample_1t):
+    """The oracle as it stands on this host: all BLAS threads, and one thread."""
+    from threadpoolctl import threadpool_limits
+
+    rec = _oracle_rate(cfg, sample_all, 1, 0)
+    out = {"value": round(rec["value"], 2), "unit": UNIT, "cores": rec["cores"], "kind": "oracle",
+           "sample": rec["sample"], "cpu_model": _cpu_model(), "logical_cpus": os.cpu_count()}
+    if sample_1t > 0:
+        with threadpool_limits(limits=1):
+            r1 = _oracle_rate(cfg, sample_1t, 1, 0)
+        out["one_thread"] = {"value": round(r1["value"], 2), "unit": UNIT, "cores": 1, "sample": r1["sample"]}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -201,14 +238,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=512)
+    ap.add_argument("--cpu-sample-1t", type=int, default=96)
     ap.add_argument("--ref-sample", type=int, default=96)
     ap.add_argument("--profile-steps", type=int, default=1)
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: split the config's box over the GPUs (default: replicate it per GPU)")
-    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "fp32"])
+    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "fp32", "tf32"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _spawn(sys.argv[1:], args.gpus)
 
     import torch
 
@@ -216,6 +256,8 @@ def main():
     from synth import configs
 
     ws, rank, local = _dist()
+    if ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
     nccl_id = None
     if ws > 1:
         import torch.distributed as dist
@@ -233,11 +275,21 @@ def main():
     s = configs.system(cfg) if args.strong else configs.system(cfg, reps=grid)
     wf = configs.weight_file(cfg)
     stream = torch.cuda.current_stream()
-    prec = pb.PREC_3XTF32 if args.precision == "3xtf32" else pb.PREC_FP32
+    prec = {"3xtf32": pb.PREC_3XTF32, "fp32": pb.PREC_FP32, "tf32": pb.PREC_TF32}[args.precision]
     m = pb.Allegro(wf, s.box, device=local, n_atoms=s.n, stream=stream.cuda_stream, precision=prec, rank=rank,
                    world_size=ws, nccl_id=nccl_id, grid=grid)
     m.md_set_state(s.species, s.pos, s.vel)
-    m.md_step(args.warmup, DT_FS)
+    r_w = m.md_step(args.warmup, DT_FS)
+    edges_first = int(r_w.n_edges)
+
+    # the start state of the timed window, kept so that the e2e leg runs the SAME MD steps
+    pos_w, vel_w, _ = m.md_get_state()  # world_size > 1: gathered on rank 0
+    if ws > 1:
+        tp = torch.from_numpy(pos_w).cuda()
+        tv = torch.from_numpy(vel_w).cuda()
+        torch.distributed.broadcast(tp, 0)
+        torch.distributed.broadcast(tv, 0)
+        pos_w, vel_w = tp.cpu().numpy(), tv.cpu().numpy()
 
     def barrier():
         if ws > 1:
@@ -255,6 +307,7 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     rep = m.md_step(n_prof, DT_FS)
+    edges_prof = int(rep.n_edges)
     m.profile(False)
     if args.steps > n_prof:
         rep = m.md_step(args.steps - n_prof, DT_FS)
@@ -266,13 +319,16 @@ def main():
     prof = m.profile_read()
     detail = sorted(m.profile_detail(), key=lambda x: -x[1])
     clk = clocks.stop()
+    edges_last = int(rep.n_edges)
+    e_pot_dev = rep.e_pot
     t = torch.tensor([ms], device="cuda")
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(t.item())
     value = s.n * args.steps / (ms_max / 1e3)  # s.n = atoms of the whole (replicated) box
 
-    # ---- e2e: the same steps through md_step_host with this rank's state in pinned host memory ----
+    # ---- e2e: the SAME K steps (same start state) through md_step_host, state in pinned host memory ----
+    m.md_set_state(s.species, pos_w, vel_w)
     n_loc = m.local_count()
     cap = 2 * n_loc + 1024  # migration may change the local count
     _, spc, _, pos, vel, frc = m.md_get_local_state(cap)
@@ -280,8 +336,6 @@ def main():
     h_pos = torch.from_numpy(pos).pin_memory()
     h_vel = torch.from_numpy(vel).pin_memory()
     h_frc = torch.from_numpy(frc).pin_memory()
-    r = m.md_step_host(h_spc, h_pos, h_vel, h_frc, 1, DT_FS, n_local=n_loc)
-    n_loc = r.n_local
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -305,8 +359,9 @@ def main():
     e2e_value = s.n * args.steps / (float(te[0].item()) / 1e3)
     h2d = int(te[1].item()) // args.steps
     d2h = int(te[2].item()) // args.steps
+    e2e_same = bool(r.e_pot == e_pot_dev and int(r.n_edges) == edges_last)
 
-    # ---- roofline of the dominant kernel class (live CUDA events, algorithmic work) ----
+    # ---- roofline: dominant kernel class + the step bound ----
     peaks, peak_src = _peaks()
     total_ms = sum(v[0] for v in prof.values())
     dom = max(prof, key=lambda k: prof[k][0])
@@ -319,32 +374,50 @@ def main():
                       "launches_per_step": kn / n_prof,
                       "gflops": round(kfl / max(kms, 1e-9) / 1e6, 1), "gbs": round(kby / max(kms, 1e-9) / 1e6, 1)}
     alu_peak = _fp32_alu_peak_tflops(peaks.get("sm_max_mhz", 1965.0))
-    # tensor peak in ALGORITHMIC flops: measured bf16 x 0.5 (TF32 : BF16 nominal) / 3 (3xTF32 passes)
-    # the contractions run inside a long, power-capped step: the sustained bf16 figure applies
-    # (B200_PROFILING.md); the fallback is the guide's ~1.4 PFLOP/s sustained
+    # tensor peak for the contraction dtype: measured bf16 x 0.5 (TF32 : BF16 nominal) / passes
+    # (3 for 3xTF32); the contractions run inside a long, power-capped step, so the sustained
+    # bf16 figure applies (B200_PROFILING.md)
     tc_key = "bf16_tflops_sustained" if "bf16_tflops_sustained" in peaks else "bf16_tflops"
-    tc_peak = peaks.get(tc_key, 1400.0) * 0.5 / 3.0
+    passes = {"3xtf32": 3.0, "tf32": 1.0, "fp32": None}[args.precision]
+    tc_peak = peaks.get(tc_key, 1400.0) * 0.5 / passes if passes else None
     gbs = d_by / (d_ms / 1e3) / 1e9
     tfs = d_fl / (d_ms / 1e3) / 1e12
     hbm_frac = gbs / peaks["hbm_gbs"]
-    if dom == "gemm" and args.precision == "3xtf32":
-        cmp_peak, cmp_bound, cmp_src = tc_peak, "tensor", (f"{peak_src} {tc_key} x 0.5 (TF32/BF16 nominal) / 3 "
-                                                           "(3xTF32 passes), algorithmic flops")
+    if d_fl > 0 and dom in ("gemm", "tp_lin_fwd", "tp_lin_bwd") and tc_peak:
+        roof = {"kernel": dom, "bound": "tensor", "achieved": round(tfs, 2), "peak": round(tc_peak, 1),
+                "unit": "TFLOP/s", "frac": round(tfs / tc_peak, 4), "traffic": None,
+                "peak_source": (f"{peak_src} {tc_key} {peaks.get(tc_key)} x 0.5 (TF32/BF16 nominal) / {passes:g} "
+                                f"({args.precision} passes)"),
+                "per_launch": f"{d_fl / d_n:.4g} algorithmic flop / {d_ms / d_n:.4g} ms",
+                "hbm_secondary": {"achieved_gbs": round(gbs, 1), "frac": round(hbm_frac, 4),
+                                  "note": "bytes this design materialises per contraction, not the method's minimum"}}
+    elif d_fl > 0 and hbm_frac < tfs / alu_peak:
+        roof = {"kernel": dom, "bound": "alu", "achieved": round(tfs, 2), "peak": round(alu_peak, 1),
+                "unit": "TFLOP/s", "frac": round(tfs / alu_peak, 4), "traffic": None,
+                "peak_source": "derived: 148 SMs x 128 fp32 lanes x 2 x sm_max_mhz",
+                "per_launch": f"{d_fl / d_n:.4g} flop / {d_ms / d_n:.4g} ms"}
     else:
-        cmp_peak, cmp_bound, cmp_src = alu_peak, "alu", "derived: 148 SMs x 128 fp32 lanes x 2 x sm_max_mhz"
-    cmp_frac = tfs / cmp_peak
-    if d_fl == 0 or hbm_frac >= cmp_frac:
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(hbm_frac, 4), "traffic": None, "peak_source": f"{peak_src} hbm_gbs",
-                "per_launch": f"{d_by / d_n:.4g} B / {d_ms / d_n:.4g} ms",
-                "compute": {"bound": cmp_bound, "achieved_tflops": round(tfs, 2), "peak": round(cmp_peak, 1),
-                            "frac": round(cmp_frac, 4), "peak_source": cmp_src}}
-    else:
-        roof = {"kernel": dom, "bound": cmp_bound, "achieved": round(tfs, 3), "peak": round(cmp_peak, 2),
-                "unit": "TFLOP/s", "frac": round(cmp_frac, 4), "traffic": None, "peak_source": cmp_src,
-                "per_launch": f"{d_fl / d_n:.4g} flop / {d_ms / d_n:.4g} ms",
-                "hbm": {"achieved_gbs": round(gbs, 1), "frac": round(hbm_frac, 4)}}
+                "per_launch": f"{d_by / d_n:.4g} B / {d_ms / d_n:.4g} ms"}
     roof.update(_ncu_traffic(cfg.name, dom, d_by / d_n))
+    # step-level bound: T_roof = max(bytes_alg / BW, GEMM_flop_alg / P_tensor, TP_flop_alg / P_fp32)
+    mac_e, tpf_e = pb.work_per_edge(cfg.n_layers, cfg.lmax)
+    e_step = edges_prof / ws  # edges per GPU of the profiled step
+    a_step = s.n / ws
+    gemm_flop = 4.0 * mac_e * e_step      # forward + input-gradient reverse (no dW), 2 flop per MAC
+    tp_flop = 6.0 * tpf_e * e_step        # forward + 2x in the reverse, 2 flop per FMA
+    bytes_alg = 190.0 * a_step + 32.0 * e_step  # §8(d): state + cells ~190 B/atom; CSR + g ~32 B/edge
+    t_gemm = gemm_flop / ((tc_peak or alu_peak) * 1e12) * 1e3
+    t_tp = tp_flop / (alu_peak * 1e12) * 1e3
+    t_hbm = bytes_alg / (peaks["hbm_gbs"] * 1e9) * 1e3
+    t_roof = max(t_gemm, t_tp, t_hbm)
+    t_meas = ms_max / args.steps
+    roof["step"] = {"t_roof_ms": round(t_roof, 3), "t_meas_ms": round(t_meas, 3), "frac": round(t_roof / t_meas, 4),
+                    "t_gemm_ms": round(t_gemm, 3), "t_tp_ms": round(t_tp, 3), "t_hbm_ms": round(t_hbm, 3),
+                    "gemm_mflop_per_atom_step": round(gemm_flop / a_step / 1e6, 2),
+                    "tp_mflop_per_atom_step": round(tp_flop / a_step / 1e6, 3),
+                    "note": "SURVEY.md §8(d): T_roof = max(bytes_alg/BW, GEMM_FLOP/P_tensor(mode), TP_FLOP/P_fp32)"}
     # HBM roofline of the streaming edge kernel (north_star: >= 60% on the edge kernels)
     fg = prof.get("force_gather")
     if fg and fg[3]:
@@ -362,15 +435,16 @@ def main():
         "shapes": [{"tag": t, "ms_per_step": round(ms_ / n_prof, 3), "gbs": round(by / max(ms_, 1e-9) / 1e6, 1),
                     "launches_per_step": n_ / n_prof} for t, ms_, by, n_ in detail[:24]],
         "profiled_steps": n_prof,
-        "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "edges": {"first": edges_first, "profiled": edges_prof, "last": edges_last,
+                  "edges_per_s": round(0.5 * (edges_first + edges_last) * args.steps / (ms_max / 1e3), 1)},
+        "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "same_steps_as_value": e2e_same},
         "clocks": clk,
         "md": {"e_pot": rep.e_pot, "e_kin": rep.e_kin, "temperature": rep.temperature,
                "n_outliers_last": rep.n_outliers_last},
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rec = _oracle_rate(cfg, args.cpu_sample, 1, 0)
-        line["cpu_baseline"] = {"value": round(rec["value"], 2), "unit": UNIT, "cores": rec["cores"], "kind": "oracle",
-                                "sample": rec["sample"]}
+        line["cpu_baseline"] = _cpu_baseline(cfg, args.cpu_sample, args.cpu_sample_1t)
     if rank == 0:
         print(json.dumps(line), flush=True)
     m.close()
@@ -379,4 +453,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

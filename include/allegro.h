@@ -59,8 +59,14 @@ enum {
 
 enum { ALLEGRO_HOST = 0, ALLEGRO_DEVICE = 1 };
 
-/* Arithmetic of the per-edge MLP contractions (the only dense GEMMs).
- * FP32: CUDA-core fp32 FMA (the parity mode of this build). */
+/* Arithmetic of the per-edge MLP contractions (the only dense GEMMs; SURVEY.md App. C).
+ *   3XTF32  tcgen05 kind::tf32 in split precision (a_hi w_hi + a_hi w_lo + a_lo w_hi):
+ *           fp32-level accuracy; the production and parity mode (the binding's default).
+ *   FP32    CUDA-core fp32 FMA: the second parity gate (reference arithmetic).
+ *   TF32    tcgen05, one pass (a_hi w_hi): fast, outside the force bound by ~30x (App. C);
+ *           reported, not gated.
+ *   BF16X3, BF16: reserved; allegro_create returns ALLEGRO_E_ARG (not built: the unfused
+ *           contractions are HBM-bound, so halving their operand precision buys nothing). */
 enum {
   ALLEGRO_PREC_FP32 = 0,
   ALLEGRO_PREC_3XTF32 = 1,
@@ -80,8 +86,12 @@ typedef struct {
   int rank, world_size;     /* 1 GPU: 0, 1 */
   const void* nccl_unique_id; /* 128-byte ncclUniqueId broadcast by the caller; NULL if world_size == 1 */
   int grid[3];              /* domain grid px,py,pz (product == world_size); {0,0,0} = auto */
-  int precision;            /* ALLEGRO_PREC_* */
-  void* cuda_stream;        /* cudaStream_t to run on (e.g. torch's current stream); NULL = ctx-owned stream */
+  int precision;            /* ALLEGRO_PREC_* (0 = FP32 for a zeroed struct; ALLEGRO_PREC_3XTF32 is production) */
+  void* cuda_stream;        /* cudaStream_t to run on (e.g. torch's current stream); NULL = ctx-owned stream.
+                               Device pointers passed to the calls are read / written on this stream: the
+                               caller orders their producers / consumers with it (e.g. pass torch's current
+                               stream, or synchronise before the call); every call that returns results to
+                               the host synchronises the stream before it returns. */
 } allegro_params;
 
 /* Create a ctx: reads and validates the weight file (tensor shapes and the parameter
@@ -214,12 +224,14 @@ int pimd_get_state(allegro_ctx* ctx, double* pos, double* vel, double* forces, d
 /* End-to-end variant of md_step for HOST-resident state (the e2e measurement of bench.py):
  * copies species [n], pos/vel/forces [n][3] (forces = F at pos, e.g. from the previous call
  * or from md_get_state) host -> device, runs n_steps exactly as md_step, and writes pos, vel
- * and forces back into the caller's arrays (device -> host).  n must equal the number of
- * atoms this rank owns (allegro_local_count; all atoms on one GPU).  With world_size > 1
- * migration may change the local count: the arrays (and species) must have room for it;
- * out->n_local returns it.  Pinned host memory makes the copies asynchronous. */
-int md_step_host(allegro_ctx* ctx, int64_t n, const int32_t* species, double* pos, double* vel, double* forces,
-                 int64_t n_steps, double dt_fs, md_report* out);
+ * and forces (and, with world_size > 1, species) back into the caller's arrays (device ->
+ * host).  n must equal the number of atoms this rank owns (allegro_local_count; all atoms on
+ * one GPU).  capacity (>= n) is the number of rows the caller's arrays hold: with
+ * world_size > 1 migration may change the local count (out->n_local returns it); if it
+ * exceeds capacity nothing is copied back and ALLEGRO_E_ARG is returned (the state stays on
+ * the device: md_get_local_state).  Pinned host memory makes the copies asynchronous. */
+int md_step_host(allegro_ctx* ctx, int64_t n, int64_t capacity, int32_t* species, double* pos, double* vel,
+                 double* forces, int64_t n_steps, double dt_fs, md_report* out);
 
 /* Count atoms with |F_a| > mean + k*sigma (strict) for the current
  * forces.  Collective. */
@@ -237,6 +249,16 @@ int allegro_get_edges(allegro_ctx* ctx, int64_t capacity, int64_t* n_edges, int3
 /* Test hook: per-edge dE/dr_e [E][3] (fp32 widened to double) of the last evaluation,
  * in the edge order of allegro_get_edges. */
 int allegro_get_edge_grad(allegro_ctx* ctx, int64_t capacity, double* g);
+
+/* Test hook: the edges of selected rows (owned local atom indices `rows`, in that order; each
+ * row in canonical order) as (i_gid, j_gid, shift) and their dE/dr_e [.][3] (g may be NULL).
+ * *n_out receives the edge count; all outputs NULL = query.  ALLEGRO_E_ARG if capacity is too
+ * small or a row is out of range. */
+int allegro_get_row_edges(allegro_ctx* ctx, int64_t n_rows, const int64_t* rows, int64_t capacity, int64_t* n_out,
+                          int32_t* i_gid, int32_t* j_gid, int8_t* shift, double* g);
+/* Test hook: the first centre atom of each chunk of complete CSR rows the model ran in at the
+ * last evaluation (chunks bound the per-edge workspace; results do not depend on them). */
+int allegro_chunk_starts(allegro_ctx* ctx, int64_t capacity, int64_t* n_chunks, int64_t* first_atom);
 
 /* world_size > 1: rank 0 creates the 128-byte NCCL unique id and broadcasts it (e.g. with
  * torch.distributed) to every rank's allegro_params.nccl_unique_id. */
@@ -283,6 +305,11 @@ int allegro_w3j_table(int l1, int l2, int l3, double* out);
 int64_t allegro_param_count(int n_layers, int lmax);
 /* per-layer (#paths, #scalar paths) of (n_layers, lmax): out[2*k], out[2*k+1] */
 int allegro_layer_paths(int n_layers, int lmax, int* out);
+/* algorithmic forward work per edge of the (n_layers, lmax) model: out[0] =
+ * dense-contraction MACs (two-body, env-embed, TP-linear of all but the last layer, latent,
+ * edge-energy), out[1] = tensor-product FMAs (non-zero W3j entries x channels).  The step does
+ * the forward plus the input-gradient reverse: 2x the MACs and 3x the TP FMAs. */
+int allegro_work_per_edge(int n_layers, int lmax, double* out);
 const char* allegro_version(void);
 
 #ifdef __cplusplus

@@ -122,12 +122,15 @@ _lib.md_count_outliers.argtypes = [_P, C.c_double, C.c_double, C.c_double, C.POI
 _lib.md_force_baseline.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
 _lib.allegro_get_edges.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), _P, _P, _P]
 _lib.allegro_get_edge_grad.argtypes = [_P, C.c_int64, _P]
+_lib.allegro_get_row_edges.argtypes = [_P, C.c_int64, _P, C.c_int64, C.POINTER(C.c_int64), _P, _P, _P, _P]
+_lib.allegro_chunk_starts.argtypes = [_P, C.c_int64, C.POINTER(C.c_int64), _P]
 _lib.allegro_w3j_table.argtypes = [C.c_int, C.c_int, C.c_int, _P]
 _lib.allegro_param_count.argtypes = [C.c_int, C.c_int]
 _lib.allegro_param_count.restype = C.c_int64
 _lib.allegro_layer_paths.argtypes = [C.c_int, C.c_int, _P]
 _lib.allegro_version.restype = C.c_char_p
-_lib.md_step_host.argtypes = [_P, C.c_int64, _P, _P, _P, _P, C.c_int64, C.c_double, C.POINTER(MdReport)]
+_lib.allegro_work_per_edge.argtypes = [C.c_int, C.c_int, _P]
+_lib.md_step_host.argtypes = [_P, C.c_int64, C.c_int64, _P, _P, _P, _P, C.c_int64, C.c_double, C.POINTER(MdReport)]
 _lib.allegro_profile.argtypes = [_P, C.c_int]
 _lib.allegro_profile_read.argtypes = [_P, C.c_int, _P, _P, _P, _P]
 _lib.allegro_launch_count.argtypes = [_P]
@@ -159,7 +162,7 @@ EXPORTED = [
     "allegro_debug_gemm_bench", "allegro_debug_gemm_epi", "allegro_nccl_unique_id", "allegro_local_count",
     "md_get_local_state", "md_set_thermostat", "md_run_ttf",
     "allegro_compute_energy_forces_batch", "pimd_set_state", "pimd_step", "pimd_get_state",
-    "allegro_profile_detail",
+    "allegro_profile_detail", "allegro_work_per_edge", "allegro_get_row_edges", "allegro_chunk_starts",
 ]
 
 
@@ -194,6 +197,15 @@ def layer_paths(n_layers: int, lmax: int):
     out = np.zeros(2 * n_layers, dtype=np.int32)
     _lib.allegro_layer_paths(n_layers, lmax, out.ctypes.data)
     return [(int(out[2 * k]), int(out[2 * k + 1])) for k in range(n_layers)]
+
+
+def work_per_edge(n_layers: int, lmax: int):
+    """(forward GEMM MACs, forward TP FMAs) per edge of the (n_layers, lmax) model."""
+    out = np.zeros(2)
+    rc = _lib.allegro_work_per_edge(n_layers, lmax, out.ctypes.data)
+    if rc != OK:
+        raise AllegroError(rc, "bad (n_layers, lmax)")
+    return float(out[0]), float(out[1])
 
 
 def debug_gemm(A: np.ndarray, W: np.ndarray, precision: int = PREC_FP32, device: int = 0) -> np.ndarray:
@@ -252,7 +264,7 @@ class Allegro:
     """One ctx of the C ABI (allegro_create ... allegro_destroy)."""
 
     def __init__(self, weights_path: str, box, r_cut: float = 0.0, skin: float = 0.0, device: int = 0,
-                 n_atoms: int = 0, precision: int = PREC_FP32, stream: int | None = None, rank: int = 0,
+                 n_atoms: int = 0, precision: int = PREC_3XTF32, stream: int | None = None, rank: int = 0,
                  world_size: int = 1, nccl_id: bytes | None = None, grid=(0, 0, 0)):
         p = AllegroParams()
         p.weights_path = os.fsencode(weights_path)
@@ -291,7 +303,12 @@ class Allegro:
     # ---- allegro_compute_energy_forces -------------------------------------------------
     def compute_energy_forces(self, pos, species, gid=None, box=None, e_atom=None, forces=None):
         """pos [n,3] f64, species [n] i32 (numpy => host pointers; torch cuda => device
-        pointers, zero copy).  Returns (e_total, e_atom, forces) in the same kind."""
+        pointers, zero copy).  Returns (e_total, e_atom, forces) in the same kind.
+
+        Device tensors are read and written on the ctx's stream (include/allegro.h): the
+        caller's current torch stream is synchronised first, so the inputs are complete and
+        the output blocks are no longer in use there; the call synchronises its own stream
+        before it returns, so the outputs are complete afterwards."""
         n = int(pos.shape[0])
         on_dev = not isinstance(pos, np.ndarray)
         if on_dev:
@@ -303,6 +320,7 @@ class Allegro:
                 e_atom = torch.empty(n, dtype=torch.float64, device=pos.device)
             if forces is None:
                 forces = torch.empty((n, 3), dtype=torch.float64, device=pos.device)
+            torch.cuda.current_stream(pos.device).synchronize()
         else:
             pos = np.ascontiguousarray(pos, dtype=np.float64)
             species = np.ascontiguousarray(species, dtype=np.int32)
@@ -422,10 +440,11 @@ class Allegro:
     def md_step_host(self, species, pos, vel, forces, n_steps: int = 1, dt_fs: float = 2.0,
                      n_local: int | None = None) -> MdReport:
         """End-to-end step on HOST arrays (updated in place): H2D, n_steps, D2H.
-        numpy or (pinned) torch CPU tensors."""
+        numpy or (pinned) torch CPU tensors; their row count is the capacity passed to the C ABI."""
         r = MdReport()
         n = self.local_count() if n_local is None else int(n_local)
-        self._check(_lib.md_step_host(self._h, n, _ptr(species), _ptr(pos), _ptr(vel), _ptr(forces),
+        cap = min(int(species.shape[0]), int(pos.shape[0]), int(vel.shape[0]), int(forces.shape[0]))
+        self._check(_lib.md_step_host(self._h, n, cap, _ptr(species), _ptr(pos), _ptr(vel), _ptr(forces),
                                       n_steps, dt_fs, C.byref(r)))
         return r
 
@@ -468,6 +487,28 @@ class Allegro:
         s = np.empty((E, 3), dtype=np.int8)
         self._check(_lib.allegro_get_edges(self._h, E, C.byref(n), i.ctypes.data, j.ctypes.data, s.ctypes.data))
         return i, j, s
+
+    def get_row_edges(self, rows):
+        """Edges of the listed owned rows: (i_gid, j_gid, shift [E][3], g [E][3])."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        n = C.c_int64(0)
+        self._check(_lib.allegro_get_row_edges(self._h, rows.size, rows.ctypes.data, 0, C.byref(n), None, None, None,
+                                               None))
+        E = n.value
+        i = np.empty(E, dtype=np.int32)
+        j = np.empty(E, dtype=np.int32)
+        s = np.empty((E, 3), dtype=np.int8)
+        g = np.empty((E, 3))
+        self._check(_lib.allegro_get_row_edges(self._h, rows.size, rows.ctypes.data, E, C.byref(n), i.ctypes.data,
+                                               j.ctypes.data, s.ctypes.data, g.ctypes.data))
+        return i, j, s, g
+
+    def chunk_starts(self):
+        n = C.c_int64(0)
+        self._check(_lib.allegro_chunk_starts(self._h, 0, C.byref(n), None))
+        out = np.empty(max(n.value, 1), dtype=np.int64)
+        self._check(_lib.allegro_chunk_starts(self._h, out.size, C.byref(n), out.ctypes.data))
+        return out[: n.value]
 
     def get_edge_grad(self):
         n = C.c_int64(0)

@@ -66,10 +66,12 @@ bool debug_on() {
   return on;
 }
 
-int evaluate(allegro_ctx* c) {
+int evaluate(allegro_ctx* c, bool check_domain = false) {
   ALG_CUDA(cudaMemsetAsync(c->flags.p, 0, 4 * sizeof(int), c->stream));
   wrap_positions(c);
   if (!check_inputs(c)) return fail(c, ALLEGRO_E_ARG, "non-finite position or species outside {0, 1}");
+  if (check_domain && c->dom.multi && !all_owned(c))
+    return fail(c, ALLEGRO_E_ARG, "an atom passed to this rank lies outside its spatial domain");
   build_neighbors(c);
   compute_forces(c);
   if (debug_on())
@@ -100,8 +102,10 @@ int allegro_create(const allegro_params* p, allegro_ctx** out) {
   if (!box_ok(p->box)) return fail(nullptr, ALLEGRO_E_ARG, "box must be three finite positive lengths");
   if (p->world_size < 1 || p->rank < 0 || p->rank >= p->world_size)
     return fail(nullptr, ALLEGRO_E_ARG, "rank / world_size out of range");
-  if (p->precision != ALLEGRO_PREC_FP32 && p->precision != ALLEGRO_PREC_3XTF32)
-    return fail(nullptr, ALLEGRO_E_ARG, "built precisions: ALLEGRO_PREC_FP32, ALLEGRO_PREC_3XTF32");
+  if (p->precision != ALLEGRO_PREC_FP32 && p->precision != ALLEGRO_PREC_3XTF32 && p->precision != ALLEGRO_PREC_TF32)
+    return fail(nullptr, ALLEGRO_E_ARG,
+                "built precisions: ALLEGRO_PREC_3XTF32 (default), ALLEGRO_PREC_FP32, ALLEGRO_PREC_TF32; "
+                "the bf16 modes are reserved");
   if (!(p->skin >= 0 && std::isfinite(p->skin))) return fail(nullptr, ALLEGRO_E_ARG, "skin must be >= 0");
   allegro_ctx* c = new allegro_ctx();
   c->prm = *p;
@@ -176,6 +180,8 @@ void allegro_destroy(allegro_ctx* c) {
   c->flags.release();
   c->red.release();
   c->e_atom.release();
+  c->scan_tmp.release();
+  for (auto& b : c->scan_lv) b.release();
   Workspace& w = c->ws;
   for (DBuf<float>* b : {&w.z, &w.a1, &w.h1, &w.a2, &w.h2, &w.m, &w.u, &w.Y, &w.xa, &w.xb, &w.T, &w.xbar_a, &w.xbar_b,
                          &w.sbar, &w.vbar_a, &w.vbar_b, &w.wbar, &w.ybar, &w.ubar, &w.zbar, &w.ab2, &w.ab1, &w.ee, &w.ebar})
@@ -223,7 +229,7 @@ int allegro_compute_energy_forces(allegro_ctx* c, int64_t n, int where, const in
       }
     }
     c->md_ready = false;
-    const int rc = evaluate(c);
+    const int rc = evaluate(c, /*check_domain=*/true);
     *e_total = c->e_pot;
     if (n > 0) {
       ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, sizeof(double) * 3 * n, kout, c->stream));
@@ -358,11 +364,12 @@ int md_step(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
   });
 }
 
-int md_step_host(allegro_ctx* c, int64_t n, const int32_t* species, double* pos, double* vel, double* forces,
-                 int64_t n_steps, double dt, md_report* out) {
+int md_step_host(allegro_ctx* c, int64_t n, int64_t capacity, int32_t* species, double* pos, double* vel,
+                 double* forces, int64_t n_steps, double dt, md_report* out) {
   if (!c) return fail(nullptr, ALLEGRO_E_ARG, "ctx is NULL");
   if (!c->md_ready) return fail(c, ALLEGRO_E_STATE, "md_set_state has not been called");
   if (n != c->n || !species || !pos || !vel || !forces) return fail(c, ALLEGRO_E_ARG, "bad arrays or n (local count)");
+  if (capacity < n) return fail(c, ALLEGRO_E_ARG, "capacity < n");
   if (n_steps < 0 || !(dt > 0 && std::isfinite(dt))) return fail(c, ALLEGRO_E_ARG, "bad n_steps or dt");
   return guarded(c, [&]() -> int {
     ALG_CUDA(cudaSetDevice(c->device));
@@ -371,11 +378,16 @@ int md_step_host(allegro_ctx* c, int64_t n, const int32_t* species, double* pos,
     ALG_CUDA(cudaMemcpyAsync(c->vel.p, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     ALG_CUDA(cudaMemcpyAsync(c->frc.p, forces, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     const int rc = md_run(c, n_steps, dt, out);
-    // multi-GPU: the local count may change by migration; caller arrays hold >= capacity
+    // multi-GPU: the local count may change by migration; the caller's arrays hold `capacity` rows
     const int64_t nn = c->n;
-    if (c->dom.multi && species) {
-      ALG_CUDA(cudaMemcpyAsync(const_cast<int32_t*>(species), c->species.p, sizeof(int32_t) * nn,
-                               cudaMemcpyDeviceToHost, c->stream));
+    if (nn > capacity) {
+      ALG_CUDA(cudaStreamSynchronize(c->stream));
+      return fail(c, ALLEGRO_E_ARG,
+                  "local count after migration (" + std::to_string(nn) + ") exceeds capacity; the state stays on "
+                  "the device (md_get_local_state)");
+    }
+    if (c->dom.multi) {
+      ALG_CUDA(cudaMemcpyAsync(species, c->species.p, sizeof(int32_t) * nn, cudaMemcpyDeviceToHost, c->stream));
     }
     ALG_CUDA(cudaMemcpyAsync(pos, c->pos.p, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, c->stream));
     ALG_CUDA(cudaMemcpyAsync(vel, c->vel.p, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost, c->stream));
@@ -708,6 +720,61 @@ int allegro_get_edges(allegro_ctx* c, int64_t capacity, int64_t* n_edges, int32_
   });
 }
 
+int allegro_get_row_edges(allegro_ctx* c, int64_t n_rows, const int64_t* rows, int64_t capacity, int64_t* n_out,
+                          int32_t* i_gid, int32_t* j_gid, int8_t* shift, double* g) {
+  if (!c || !n_out || (n_rows > 0 && !rows) || n_rows < 0) return fail(c, ALLEGRO_E_ARG, "NULL argument");
+  return guarded(c, [&]() -> int {
+    ALG_CUDA(cudaSetDevice(c->device));
+    const int64_t n = c->n, na = c->n + c->n_ghost;
+    for (int64_t r = 0; r < n_rows; ++r)
+      if (rows[r] < 0 || rows[r] >= n) return fail(c, ALLEGRO_E_ARG, "row outside the owned atoms");
+    std::vector<int32_t> rp(n + 1), gid(n), agid(na), ash(na);
+    ALG_CUDA(cudaMemcpyAsync(rp.data(), c->row_ptr.p, 4 * (n + 1), cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(gid.data(), c->gid.p, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(agid.data(), c->agid.p, 4 * na, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaMemcpyAsync(ash.data(), c->ashift.p, 4 * na, cudaMemcpyDeviceToHost, c->stream));
+    ALG_CUDA(cudaStreamSynchronize(c->stream));
+    int64_t tot = 0;
+    for (int64_t r = 0; r < n_rows; ++r) tot += rp[rows[r] + 1] - rp[rows[r]];
+    *n_out = tot;
+    if (!i_gid && !j_gid && !shift && !g) return ALLEGRO_OK;
+    if (capacity < tot) return fail(c, ALLEGRO_E_ARG, "capacity too small");
+    int64_t o = 0;
+    for (int64_t r = 0; r < n_rows; ++r) {
+      const int64_t e0 = rp[rows[r]], ne = rp[rows[r] + 1] - e0;
+      std::vector<int32_t> nb(ne);
+      std::vector<float> gg(4 * ne);
+      if (ne > 0) {
+        ALG_CUDA(cudaMemcpyAsync(nb.data(), c->nbr.p + e0, 4 * ne, cudaMemcpyDeviceToHost, c->stream));
+        ALG_CUDA(cudaMemcpyAsync(gg.data(), c->g.p + 4 * e0, 16 * ne, cudaMemcpyDeviceToHost, c->stream));
+        ALG_CUDA(cudaStreamSynchronize(c->stream));
+      }
+      for (int64_t e = 0; e < ne; ++e, ++o) {
+        if (i_gid) i_gid[o] = gid[rows[r]];
+        if (j_gid) j_gid[o] = agid[nb[e]];
+        if (shift) {
+          const int32_t sh = ash[nb[e]];
+          shift[3 * o] = (int8_t)((sh & 0xff) - 128);
+          shift[3 * o + 1] = (int8_t)(((sh >> 8) & 0xff) - 128);
+          shift[3 * o + 2] = (int8_t)(((sh >> 16) & 0xff) - 128);
+        }
+        if (g)
+          for (int d = 0; d < 3; ++d) g[3 * o + d] = gg[4 * e + d];
+      }
+    }
+    return ALLEGRO_OK;
+  });
+}
+
+int allegro_chunk_starts(allegro_ctx* c, int64_t capacity, int64_t* n_chunks, int64_t* first_atom) {
+  if (!c || !n_chunks) return fail(c, ALLEGRO_E_ARG, "NULL argument");
+  *n_chunks = (int64_t)c->chunk_a0.size();
+  if (!first_atom) return ALLEGRO_OK;
+  if (capacity < *n_chunks) return fail(c, ALLEGRO_E_ARG, "capacity too small");
+  for (size_t k = 0; k < c->chunk_a0.size(); ++k) first_atom[k] = c->chunk_a0[k];
+  return ALLEGRO_OK;
+}
+
 int allegro_get_edge_grad(allegro_ctx* c, int64_t capacity, double* g) {
   if (!c || !g) return fail(c, ALLEGRO_E_ARG, "NULL argument");
   if (capacity < c->n_edges) return fail(c, ALLEGRO_E_ARG, "capacity too small");
@@ -742,7 +809,8 @@ int allegro_debug_gemm(int device, int precision, int64_t M, int N, int K, const
     g.lda = K;
     g.W = dW;
     g.C = dC;
-    if (precision == ALLEGRO_PREC_3XTF32) {
+    if (tc_mode(precision)) {
+      g.single_pass = precision == ALLEGRO_PREC_TF32 ? 1 : 0;
       TcWeight t = tc_prepare_weight(w, K, N, owned);
       tc_gemm(g, t, 0, nullptr);
     } else {
@@ -904,6 +972,30 @@ int allegro_layer_paths(int n_layers, int lmax, int* out) {
     out[2 * k] = A.n_paths;
     out[2 * k + 1] = A.n_s;
   }
+  return ALLEGRO_OK;
+}
+
+int allegro_work_per_edge(int n_layers, int lmax, double* out) {
+  if (!out || n_layers < 1 || n_layers > kMaxLayers || lmax < 0 || lmax > 2) return ALLEGRO_E_ARG;
+  const int n_env = lmax + 1;
+  double mac = 12 * 32 + 32 * 64 + 64 * 128;  // two-body MLP
+  double tp = 0;
+  for (int k = 0; k < n_layers; ++k) {
+    const LayerArch A = layer_arch(n_layers, lmax, k);
+    mac += (double)kD * kC * n_env * (k == 0 ? 2 : 1);  // env embed
+    if (k < n_layers - 1)                              // TP-linear (the last layer's output is unused)
+      for (int o = 0; o < A.out.n; ++o) mac += (double)ir_dim(A.out.v[o]) * A.n_to[o] * kC * kC;
+    mac += (double)(kD + kC * A.n_s) * kD;              // latent update
+    for (int q = 0; q < A.n_paths; ++q) {               // TP: non-zero W3j entries x channels
+      const int l1 = A.path[q].a.l, l2 = A.path[q].b.l, l3 = A.path[q].o.l;
+      for (int m1 = 0; m1 < 2 * l1 + 1; ++m1)
+        for (int m2 = 0; m2 < 2 * l2 + 1; ++m2)
+          for (int m3 = 0; m3 < 2 * l3 + 1; ++m3) tp += w3j_value(l1, l2, l3, m1, m2, m3) != 0.0 ? kC : 0;
+    }
+  }
+  mac += kD * 32 + 32;  // edge-energy MLP
+  out[0] = mac;
+  out[1] = tp;
   return ALLEGRO_OK;
 }
 

@@ -127,6 +127,9 @@ struct Domain {
   DBuf<long long> acc;          // [n + G][3] fixed-point ghost-force accumulators
   DBuf<long long> cnt;          // scratch counts
   DBuf<double> red;             // allreduce scratch
+  // migration / halo scratch (per ctx, so ctxs on different devices or threads never share it)
+  DBuf<double> tpos, tvel;
+  DBuf<int32_t> tgid, tspec, f0, f1, f2, i0, i1, i2;
 };
 
 }  // namespace allegro
@@ -164,11 +167,13 @@ struct allegro_ctx {
   allegro::DBuf<unsigned long long> key_pad, key;
   allegro::DBuf<float> g;                    // [E][4] dE/dr_e (x, y, z, pad: 16-B reverse gathers)
   std::vector<int32_t> h_row_ptr;
+  std::vector<int64_t> chunk_a0;             // first centre atom of each model chunk (last evaluation)
   // ---- scalars / flags ----
   allegro::DBuf<int> flags;                  // [0] overflow max count, [1] bad input, [2] non-finite
   allegro::DBuf<double> red;                 // reduction scratch
   allegro::DBuf<double> e_atom;              // [n]
   allegro::DBuf<int32_t> scan_tmp;
+  allegro::DBuf<int32_t> scan_lv[8];          // exclusive_scan block sums per recursion level
   allegro::Workspace ws;
   size_t ws_budget_bytes = 0;
   // ---- MD ----
@@ -211,6 +216,7 @@ void compute_forces(allegro_ctx* c, bool defer_e = false);  // defer_e: e_pot re
 void domain_setup(allegro_ctx* c, const void* nccl_id);
 void domain_teardown(allegro_ctx* c);
 void migrate(allegro_ctx* c);
+bool all_owned(allegro_ctx* c);          // every owned atom lies in this rank's domain (collective)
 void halo_exchange(allegro_ctx* c);     // fills apos/agid/aspec/ashift for owned + ghosts
 void ghost_force_return(allegro_ctx* c);  // accumulates ghost forces and returns them to owners
 double allreduce_sum(allegro_ctx* c, double v);

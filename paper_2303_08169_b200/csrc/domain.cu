@@ -218,8 +218,6 @@ void exchange_counts(allegro_ctx* c, int axis, int64_t n_m, int64_t n_p, int64_t
   *r_p = r[1];
 }
 
-DBuf<double> g_tpos, g_tvel;
-DBuf<int32_t> g_tgid, g_tspec, g_f0, g_f1, g_f2, g_i0, g_i1, g_i2;
 
 }  // namespace
 
@@ -273,6 +271,8 @@ void domain_teardown(allegro_ctx* c) {
   D.acc.release();
   D.cnt.release();
   D.red.release();
+  for (DBuf<double>* b : {&D.tpos, &D.tvel}) b->release();
+  for (DBuf<int32_t>* b : {&D.tgid, &D.tspec, &D.f0, &D.f1, &D.f2, &D.i0, &D.i1, &D.i2}) b->release();
 }
 
 __global__ void k_pack_e_flag(const double* __restrict__ e, const int* __restrict__ flag, double* __restrict__ out) {
@@ -332,36 +332,65 @@ int allreduce_max_i32(allegro_ctx* c, int v) {
   return r;
 }
 
+// allegro_compute_energy_forces with world_size > 1 takes the caller's atoms as owned: each
+// must lie in this rank's domain (after wrapping), else its neighbours / ghosts would be
+// incomplete and the result silently wrong
+__global__ void k_check_owned(const double* __restrict__ pos, int64_t n, double wx, double wy, double wz, int px,
+                              int py, int pz, int cx, int cy, int cz, int* __restrict__ bad) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  if (owner_coord(pos[a * 3], wx, px) != cx || owner_coord(pos[a * 3 + 1], wy, py) != cy ||
+      owner_coord(pos[a * 3 + 2], wz, pz) != cz)
+    atomicOr(bad, 1);
+}
+
+bool all_owned(allegro_ctx* c) {
+  Domain& D = c->dom;
+  D.cnt.reserve(2);
+  int* bad = reinterpret_cast<int*>(D.cnt.p);
+  ALG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+  if (c->n > 0) {
+    ProfScope ps_(&c->prof, c->stream, PK_WRAP, 0, 24.0 * c->n);
+    k_check_owned<<<ceil_div(c->n, 256), 256, 0, c->stream>>>(c->pos.p, c->n, D.w[0], D.w[1], D.w[2], D.P[0], D.P[1],
+                                                            D.P[2], D.c[0], D.c[1], D.c[2], bad);
+    ALG_LAUNCH_CHECK();
+  }
+  int h = 0;
+  ALG_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  ALG_CUDA(cudaStreamSynchronize(c->stream));
+  return allreduce_max_i32(c, h) == 0;
+}
+
 void migrate(allegro_ctx* c) {
   Domain& D = c->dom;
   cudaStream_t st = c->stream;
   for (int axis = 0; axis < 3; ++axis) {
     if (D.P[axis] == 1) continue;
     const int64_t n = c->n;
-    g_f0.reserve(n + 1), g_f1.reserve(n + 1), g_f2.reserve(n + 1);
-    g_i0.reserve(n + 1), g_i1.reserve(n + 1), g_i2.reserve(n + 1);
+    D.f0.reserve(n + 1), D.f1.reserve(n + 1), D.f2.reserve(n + 1);
+    D.i0.reserve(n + 1), D.i1.reserve(n + 1), D.i2.reserve(n + 1);
     if (n > 0) {
       ProfScope ps_(&c->prof, st, PK_HALO, 0, 28.0 * n);
-      k_mig_class<<<ceil_div(n, 256), 256, 0, st>>>(c->pos.p, n, axis, D.w[axis], D.P[axis], D.c[axis], g_f0.p, g_f1.p,
-                                                    g_f2.p);
+      k_mig_class<<<ceil_div(n, 256), 256, 0, st>>>(c->pos.p, n, axis, D.w[axis], D.P[axis], D.c[axis], D.f0.p, D.f1.p,
+                                                    D.f2.p);
       ALG_LAUNCH_CHECK();
     }
-    const int64_t n_stay = scan_count(c, g_f0.p, g_i0.p, n);
-    const int64_t n_m = scan_count(c, g_f1.p, g_i1.p, n);
-    const int64_t n_p = scan_count(c, g_f2.p, g_i2.p, n);
+    const int64_t n_stay = scan_count(c, D.f0.p, D.i0.p, n);
+    const int64_t n_m = scan_count(c, D.f1.p, D.i1.p, n);
+    const int64_t n_p = scan_count(c, D.f2.p, D.i2.p, n);
     D.sendbuf[0].reserve((n_m + 1) * sizeof(MigAtom));
     D.sendbuf[1].reserve((n_p + 1) * sizeof(MigAtom));
     // stay-compaction into temporaries, then pack the leavers
-    g_tpos.reserve(3 * n + 3), g_tvel.reserve(3 * n + 3), g_tgid.reserve(n + 1), g_tspec.reserve(n + 1);
+    D.tpos.reserve(3 * n + 3), D.tvel.reserve(3 * n + 3), D.tgid.reserve(n + 1), D.tspec.reserve(n + 1);
     if (n > 0) {
       ProfScope ps_(&c->prof, st, PK_HALO, 0, 112.0 * n);
-      k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, g_f1.p, g_i1.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
+      k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, D.f1.p, D.i1.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
                                                    reinterpret_cast<MigAtom*>(D.sendbuf[0].p));
-      k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, g_f2.p, g_i2.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
+      k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, D.f2.p, D.i2.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
                                                    reinterpret_cast<MigAtom*>(D.sendbuf[1].p));
       // reuse the recv buffer as the stay staging (MigAtom layout)
       D.recvbuf[0].reserve((n_stay + 1) * sizeof(MigAtom));
-      k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, g_f0.p, g_i0.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
+      k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, D.f0.p, D.i0.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
                                                    reinterpret_cast<MigAtom*>(D.recvbuf[0].p));
       ALG_LAUNCH_CHECK();
       k_mig_unpack<<<ceil_div(std::max<int64_t>(n_stay, 1), 256), 256, 0, st>>>(
@@ -407,15 +436,15 @@ void halo_exchange(allegro_ctx* c) {
   int64_t n_cur = n;
   for (int axis = 0; axis < 3; ++axis) {
     HaloStage& S = D.st[axis];
-    g_f0.reserve(n_cur + 1), g_f1.reserve(n_cur + 1), g_i0.reserve(n_cur + 1), g_i1.reserve(n_cur + 1);
+    D.f0.reserve(n_cur + 1), D.f1.reserve(n_cur + 1), D.i0.reserve(n_cur + 1), D.i1.reserve(n_cur + 1);
     if (n_cur > 0) {
       ProfScope ps_(&c->prof, st, PK_HALO, 0, 16.0 * n_cur);
-      k_halo_flag<<<ceil_div(n_cur, 256), 256, 0, st>>>(c->apos.p, n_cur, axis, D.lo[axis], D.hi[axis], rcp, g_f0.p,
-                                                        g_f1.p);
+      k_halo_flag<<<ceil_div(n_cur, 256), 256, 0, st>>>(c->apos.p, n_cur, axis, D.lo[axis], D.hi[axis], rcp, D.f0.p,
+                                                        D.f1.p);
       ALG_LAUNCH_CHECK();
     }
-    const int64_t n_m = scan_count(c, g_f0.p, g_i0.p, n_cur);
-    const int64_t n_p = scan_count(c, g_f1.p, g_i1.p, n_cur);
+    const int64_t n_m = scan_count(c, D.f0.p, D.i0.p, n_cur);
+    const int64_t n_p = scan_count(c, D.f1.p, D.i1.p, n_cur);
     S.n_send[0] = n_m;
     S.n_send[1] = n_p;
     S.send_idx[0].reserve(n_m + 1);
@@ -427,10 +456,10 @@ void halo_exchange(allegro_ctx* c) {
     const int sh_p = D.c[axis] == D.P[axis] - 1 ? -1 : 0;
     if (n_cur > 0) {
       ProfScope ps_(&c->prof, st, PK_HALO, 0, 40.0 * (n_m + n_p));
-      k_halo_pack<<<ceil_div(n_cur, 256), 256, 0, st>>>(n_cur, g_f0.p, g_i0.p, axis, c->box[axis], sh_m, c->apos.p,
+      k_halo_pack<<<ceil_div(n_cur, 256), 256, 0, st>>>(n_cur, D.f0.p, D.i0.p, axis, c->box[axis], sh_m, c->apos.p,
                                                         c->agid.p, c->aspec.p, c->ashift.p,
                                                         reinterpret_cast<HaloAtom*>(D.sendbuf[0].p), S.send_idx[0].p);
-      k_halo_pack<<<ceil_div(n_cur, 256), 256, 0, st>>>(n_cur, g_f1.p, g_i1.p, axis, c->box[axis], sh_p, c->apos.p,
+      k_halo_pack<<<ceil_div(n_cur, 256), 256, 0, st>>>(n_cur, D.f1.p, D.i1.p, axis, c->box[axis], sh_p, c->apos.p,
                                                         c->agid.p, c->aspec.p, c->ashift.p,
                                                         reinterpret_cast<HaloAtom*>(D.sendbuf[1].p), S.send_idx[1].p);
       ALG_LAUNCH_CHECK();

@@ -45,6 +45,7 @@ struct GemmArgs {
   float s = 1.f, alpha = 0.f, beta = 0.f;
   int epi = EPI_STORE;
   int silu_a = 0;  // A holds pre-activations: the contraction multiplies SiLU(A) (applied on load)
+  int single_pass = 0;  // tcgen05 path: one TF32 MMA (a_hi w_hi) instead of 3xTF32 (ALLEGRO_PREC_TF32)
 };
 
 void gemm(const GemmArgs& g, cudaStream_t st, Profiler* prof);

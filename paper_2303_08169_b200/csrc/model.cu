@@ -777,13 +777,15 @@ __global__ void k_count_diff(const float* a, const float* b, int64_t n, unsigned
   if (i < n && __float_as_uint(a[i]) != __float_as_uint(b[i])) atomicAdd(cnt, 1ull);
 }
 
-void run_gemm(const Model& M, const GemmArgs& g, const Wt& w, cudaStream_t st, Profiler* prof) {
+void run_gemm(const Model& M, const GemmArgs& g_in, const Wt& w, cudaStream_t st, Profiler* prof) {
+  GemmArgs g = g_in;
+  g.single_pass = M.precision == ALLEGRO_PREC_TF32 ? 1 : 0;
   static const bool fuse_dot = [] {  // A/B switch for measurements (default: fused)
     const char* e = std::getenv("ALLEGRO_FUSE_ROWDOT");
     return !e || std::atoi(e) != 0;
   }();
   static const bool verify = std::getenv("ALLEGRO_VERIFY_GEMM") != nullptr;  // diagnostics: rerun and compare
-  if (verify && M.precision == ALLEGRO_PREC_3XTF32 && g.epi != EPI_ACC && g.epi != EPI_R2 && !g.dotv && g.M > 0) {
+  if (verify && tc_mode(M.precision) && g.epi != EPI_ACC && g.epi != EPI_R2 && !g.dotv && g.M > 0) {
     tc_gemm(g, w.tc, st, prof);
     float* tmp = nullptr;
     unsigned long long* cnt = nullptr;
@@ -809,14 +811,14 @@ void run_gemm(const Model& M, const GemmArgs& g, const Wt& w, cudaStream_t st, P
     const char* e = std::getenv("ALLEGRO_FUSE_R2");
     return !e || std::atoi(e) != 0;
   }();
-  if (M.precision == ALLEGRO_PREC_3XTF32 &&
+  if (tc_mode(M.precision) &&
       (!g.dotv || (fuse_dot && w.tc.n_tiles == 1 && (fuse_r2 || g.epi != EPI_R2)))) {
     tc_gemm(g, w.tc, st, prof);  // the row-dot (if any) is fused into the epilogue
     return;
   }
   GemmArgs g0 = g;
   g0.dotv = nullptr;
-  if (M.precision == ALLEGRO_PREC_3XTF32) tc_gemm(g0, w.tc, st, prof);
+  if (tc_mode(M.precision)) tc_gemm(g0, w.tc, st, prof);
   else gemm(g0, st, prof);
   // fp32 reference mode, or an output split over N-tiles (a fused dot would need an
   // order-dependent cross-CTA sum): a separate row-dot over the finished output
@@ -987,6 +989,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   float* xbn = w.xbar_b.p;
   const LayerInfo& LL = M.L[M.n_layers - 1];
   const int nsc_last = LL.A.n_s * kC;
+  if (nsc_last > 3 * 32) throw CudaError("k_energy_last holds at most 96 last-layer scalar channels (lmax <= 2)");
   const float sf_last = kResB / std::sqrt((float)LL.fan_lat);
   if (warp_blocks) {
     {
@@ -1115,6 +1118,8 @@ void compute_forces(allegro_ctx* c, bool defer_e) {
     a = b;
   }
   reserve_ws(c, e_cap, a_cap);
+  c->chunk_a0.clear();
+  for (const ChunkPtrs& ch : chunks) c->chunk_a0.push_back(ch.a0);
   for (const ChunkPtrs& ch : chunks) run_chunk(c, ch);
   ALG_CUDA(cudaMemsetAsync(c->flags.p + 2, 0, sizeof(int), st));
   if (c->dom.multi) ghost_force_return(c);

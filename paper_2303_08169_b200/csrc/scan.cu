@@ -94,12 +94,10 @@ void scan_rec(cudaStream_t st, const int32_t* in, int32_t* out, int64_t n, DBuf<
   ALG_LAUNCH_CHECK();
 }
 
-DBuf<int32_t> g_scan_tmp[8];
-
 }  // namespace
 
 void exclusive_scan(allegro_ctx* c, const int32_t* in, int32_t* out, int64_t n) {
-  scan_rec(c->stream, in, out, n, g_scan_tmp, 0, &c->prof);
+  scan_rec(c->stream, in, out, n, c->scan_lv, 0, &c->prof);  // per-ctx scratch (one device each)
   ProfScope ps_(&c->prof, c->stream, PK_SCAN, 0, 0);
   scan_total<<<1, 1, 0, c->stream>>>(in, out, n);
   ALG_LAUNCH_CHECK();

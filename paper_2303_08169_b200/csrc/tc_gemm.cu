@@ -309,7 +309,8 @@ __device__ __forceinline__ void scatter_rows_dot(unsigned char* buf, float* dst,
 }
 
 // MODE 0: 3xTF32 (a_hi w_lo, a_lo w_hi, a_hi w_hi); 1: stacked (a_hi [w_hi | w_lo] into the
-// adjacent accumulators [D | D'], then a_lo w_hi into D; the epilogue adds D + D'); 4: no MMAs.
+// adjacent accumulators [D | D'], then a_lo w_hi into D; the epilogue adds D + D'); 2: single-pass
+// TF32 (a_hi w_hi; ALLEGRO_PREC_TF32, reported, not gated: SURVEY.md App. C); 4: no MMAs.
 template <int MODE>
 __device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uint32_t tmem_a, uint32_t wimg, int n_my,
                                            uint64_t* a_full, uint64_t* a_empty, uint64_t* acc_full,
@@ -348,6 +349,8 @@ __device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uin
         } else if constexpr (MODE == 1) {
           mma_tf32_ts_w(L, d, ahi + 8 * k, dwh, idesc2, acc);  // [D | D'] += a_hi [w_hi | w_lo]
           mma_tf32_ts_w(L, d, alo + 8 * k, dwh, idesc, 1u);
+        } else if constexpr (MODE == 2) {
+          mma_tf32_ts_w(L, d, ahi + 8 * k, dwh, idesc, acc);  // single-pass TF32: a_hi w_hi only
         }
       }
       mma_commit_w(L, a_empty + j);
@@ -500,6 +503,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     mbar_wait(w_full, 0);
     tc_fence_after();
     if (p.diag & 1) mma_issuer<4>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
+    else if (p.g.single_pass) mma_issuer<2>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
     else if (p.stack) mma_issuer<1>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
     else mma_issuer<0>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
   } else {
@@ -718,7 +722,11 @@ CUtensorMap make_map(const float* ptr, int64_t rows, int cols, int ld, int box_r
   return m;
 }
 
-int g_num_sms = 0;
+// per-device launch state (a process may drive ctxs on several devices)
+constexpr int kMaxDev = 64;
+int g_num_sms[kMaxDev] = {};
+bool g_attr_set[kMaxDev] = {};
+std::mutex g_dev_mu;
 
 }  // namespace
 
@@ -786,11 +794,9 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   if (g.N != w.N || g.K != w.K || (g.A2 && g.K1 % BLK_K != 0))
     throw CudaError("tc_gemm: shape mismatch N=" + std::to_string(g.N) + " K=" + std::to_string(g.K));
   get_encode();
-  if (g_num_sms == 0) {
-    int dev;
-    ALG_CUDA(cudaGetDevice(&dev));
-    ALG_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int dev = 0;
+  ALG_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDev) throw CudaError("tc_gemm: device ordinal out of range");
   const int nK = (g.K + BLK_K - 1) / BLK_K;
   const int K1 = g.A2 ? g.K1 : g.K;
   const CUtensorMap mA = make_map(g.A, g.M, K1, g.lda);
@@ -804,13 +810,16 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   stages = std::min(stages, g_tc_tuning.max_stages);
   if (stages < 2) throw CudaError("tc_gemm: shared memory too small for 2 stages");
   const size_t smem = 1024 + w_round + out_bytes + (size_t)stages * STAGE_BYTES + 512;
-  static bool attr_set = false;
-  if (!attr_set) {
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!g_attr_set[dev]) {  // the function attribute is per device
 #define ALG_SET(e) ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<e>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
-    ALG_SET(EPI_STORE) ALG_SET(EPI_SILU) ALG_SET(EPI_UMUL_SAVE) ALG_SET(EPI_RESID) ALG_SET(EPI_URESID)
-    ALG_SET(EPI_USCALE) ALG_SET(EPI_ACC) ALG_SET(EPI_ADDX) ALG_SET(EPI_DSILU) ALG_SET(EPI_R2)
+      ALG_SET(EPI_STORE) ALG_SET(EPI_SILU) ALG_SET(EPI_UMUL_SAVE) ALG_SET(EPI_RESID) ALG_SET(EPI_URESID)
+      ALG_SET(EPI_USCALE) ALG_SET(EPI_ACC) ALG_SET(EPI_ADDX) ALG_SET(EPI_DSILU) ALG_SET(EPI_R2)
 #undef ALG_SET
-    attr_set = true;
+      ALG_CUDA(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev));
+      g_attr_set[dev] = true;
+    }
   }
   TcParams p;
   p.g = g;
@@ -851,7 +860,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
     return !e || std::atoi(e) != 0;
   }();
   const int per_launch = cosched ? w.n_tiles : 1;
-  const int groups = std::max(1, std::min(p.n_mtiles, g_num_sms / per_launch));
+  const int groups = std::max(1, std::min(p.n_mtiles, g_num_sms[dev] / per_launch));
   const int grid = groups * per_launch;
   const double mn = (double)g.M * g.N;
   const int n_io = 1 + (g.aux != nullptr) + (g.X != nullptr) + (g.epi == EPI_ACC);

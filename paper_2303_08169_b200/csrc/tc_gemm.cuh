@@ -36,6 +36,9 @@ struct TcTuning {
 };
 extern TcTuning g_tc_tuning;
 
+// tcgen05 contraction modes: 3xTF32 (parity / production) and single-pass TF32 (reported only)
+inline bool tc_mode(int precision) { return precision == 1 /*ALLEGRO_PREC_3XTF32*/ || precision == 3 /*ALLEGRO_PREC_TF32*/; }
+
 // Host-side split used for the weights (exposed for tests): hi = fp32 with the low
 // 13 mantissa bits cleared (exactly representable in TF32), lo = fp32(x - hi).
 float tf32_hi(float x);

@@ -126,7 +126,7 @@ void load_model(allegro_ctx* c, const char* path) {
   M.mu[1] = dh[5];
   const int n_env = lmax + 1;
   DevWeights& W = M.w;
-  const bool tc = M.precision == ALLEGRO_PREC_3XTF32;
+  const bool tc = tc_mode(M.precision);
 
   const HostTensor& bf = need("bessel_freq", 1, kNB);
   for (int i = 0; i < kNB; ++i) W.bessel[i] = (float)bf.v[i];

@@ -128,25 +128,38 @@ def test_every_architecture_on_c1_geometry(pb, tmp_path, L, lmax, prec):
     _check_energy_forces(ref, e, ea, F * 1.0)
 
 
-@pytest.mark.parametrize("cfg,prec", [("C3", "fp32"), ("C3", "3xtf32"), ("C5", "3xtf32")])
+@pytest.mark.parametrize("cfg,prec", [("C3", "fp32"), ("C3", "3xtf32"), ("C4", "3xtf32"), ("C5", "3xtf32")])
 def test_full_size_sampled(pb, cfg, prec):
-    """C3 (110,592 atoms, paper's l=2 model) and C5 (500,000 atoms, the bench workload, in
-    the bench's launch configuration) at full size; the oracle computes sampled atoms one
-    by one (rows of the atoms and of all their neighbours)."""
+    """C3 (110,592 atoms, the paper's l=2 model), C4 (884,736 atoms, many chunks) and C5
+    (500,000 atoms, the bench workload) at full size in the bench's launch configuration.  The
+    oracle evaluates >= 64 sampled rows -- the first and last row of every model chunk plus
+    random rows -- and the GPU's rows are compared edge by edge: the edge set (bit-exact),
+    each edge's dE/dr_e, and E_i; exact forces on 3 atoms need the rows of all their
+    neighbours (oracle.sampled_forces)."""
     s = configs.system(cfg)
     wf = configs.weight_file(cfg)
+    model = weights_io.read(wf)
     m = pb.Allegro(wf, s.box, precision=_prec(pb, prec), n_atoms=s.n)
     e, ea, F = m.compute_energy_forces(s.pos, s.species)
-    atoms = np.array([0, s.n // 2 + 1, s.n - 1])
-    Fo, Eo, _ = oa.sampled_forces(weights_io.read(wf), s.pos, s.species, s.box, atoms)
+    starts = m.chunk_starts()
+    ends = np.append(starts[1:], s.n) - 1
+    rng = np.random.default_rng(11)
+    rows = np.unique(np.concatenate([starts, ends, rng.choice(s.n, 64, replace=False)]))
+    assert rows.size >= 64 and (cfg != "C4" or starts.size > 1)
+    gi, gj, gs, gg = m.get_row_edges(rows)
+    ref = oa.energy_forces(model, s.pos, s.species, s.box, centers=rows)
+    ri, rj, rn = ref["edges"]
+    assert _edge_set(gi, gj, gs) == _edge_set(ri, rj, rn)
+    og = np.lexsort((gs[:, 2], gs[:, 1], gs[:, 0], gj, gi))
+    orf = np.lexsort((rn[:, 2], rn[:, 1], rn[:, 0], rj, ri))
+    assert np.abs(gg[og] - ref["g"][orf]).max() <= F_TOL
+    assert np.abs(ea[rows] - ref["e_atom"][rows]).max() <= E_TOL * np.abs(ea).max()
+    atoms = np.array([rows[0], rows[rows.size // 2], rows[-1]])
+    Fo, Eo, _ = oa.sampled_forces(model, s.pos, s.species, s.box, atoms)
     assert np.abs(F[atoms] - Fo).max() <= F_TOL
-    assert np.abs(ea[atoms] - Eo).max() <= E_TOL * np.abs(ea).max()
-    # properties at any size: zero net force, per-row edge-set rows of the sample
+    # properties at any size: zero net force
     assert np.abs(F.sum(0)).max() < 1e-6 * s.n
-    gi, gj, gs = m.get_edges()
-    ri, rj, rn = onb.cell_list(onb.wrap(s.pos, s.box), s.box, configs.CONFIGS[cfg].r_cut, atoms)
-    mask = np.isin(gi, atoms)
-    assert _edge_set(gi[mask], gj[mask], gs[mask]) == _edge_set(ri, rj, rn)
+    print(f"{cfg} {prec}: {starts.size} chunks, {rows.size} rows / {gi.size} edges checked")
 
 
 def test_deterministic_and_device_pointers(pb):
@@ -263,9 +276,14 @@ def test_md_step_host_matches_device(pb):
     pd, vd, fd = m.md_get_state()
     m.md_set_state(s.species, s.pos, s.vel)
     p, v, f = p0.copy(), v0.copy(), f0.copy()
+    spc = s.species.astype(np.int32)
     for _ in range(3):
-        m.md_step_host(s.species.astype(np.int32), p, v, f, 1, 2.0)
+        m.md_step_host(spc, p, v, f, 1, 2.0)
     assert np.array_equal(p, pd) and np.array_equal(v, vd) and np.array_equal(f, fd)
+    # the caller's arrays must hold the local count (capacity, include/allegro.h)
+    with pytest.raises(pb.AllegroError) as ex:
+        m.md_step_host(spc, p[:-1].copy(), v, f, 1, 2.0)
+    assert ex.value.code == pb.E_ARG
 
 
 def test_profiler_counts_launches(pb):
