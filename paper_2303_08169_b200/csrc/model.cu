@@ -24,6 +24,8 @@
 
 #include "ctx.cuh"
 #include "gemm.cuh"
+#include "layer.cuh"
+#include "tp_fused.cuh"
 
 namespace allegro {
 namespace {
@@ -31,34 +33,6 @@ namespace {
 constexpr float kCSilu = 1.6765324703f;  // E[SiLU(z)^2]^-1/2 (reading row 5)
 constexpr float kResA = 0.89442719099991588f;  // 2/sqrt5
 constexpr float kResB = 0.44721359549995794f;  // 1/sqrt5
-
-template <int NL, int LMAX, int K>
-struct Arch {
-  static constexpr LayerArch A = layer_arch(NL, LMAX, K);
-  static constexpr int DSH = (LMAX + 1) * (LMAX + 1);
-  static constexpr int NENV = LMAX + 1;
-  static constexpr int NW = kC * NENV * (K == 0 ? 2 : 1);
-  static constexpr int ENV_OFF = K == 0 ? kC * NENV : 0;  // column offset of the env chunk in w
-  static constexpr int DIN = A.dim_in;
-  static constexpr int DT = A.dim_T;
-  static constexpr int t_base(int o) {
-    int b = 0;
-    for (int q = 0; q < o; ++q) b += ir_dim(A.out.v[q]) * A.n_to[q] * kC;
-    return b;
-  }
-  static constexpr int v_base(int i) {
-    int b = 0;
-    for (int q = 0; q < i; ++q) b += ir_dim(A.in.v[q]) * kC;
-    return b;
-  }
-};
-
-constexpr int lm_l(int m) { return m == 0 ? 0 : (m < 4 ? 1 : 2); }
-
-struct ChunkPtrs {
-  int64_t a0, n_c;  // first centre atom, number of centres
-  int64_t e0, n_e;  // first edge, number of edges
-};
 
 // ----------------------------------------------------------------- K3 geometry
 __device__ __forceinline__ void sh_eval(const float n[3], float* Y, int lmax) {
@@ -316,7 +290,9 @@ __device__ __forceinline__ bool owns_total(int lane, int mm) {
   return mm < DSH && (lane & ((1 << (5 - LP)) - 1)) == 0;
 }
 
-template <int NL, int LMAX, int K>
+// GAMMA_ONLY: only the environment sums Gamma_i (k_gamma; the fused TP + TP-linear kernel of
+// tp_fused.cu does the rest)
+template <int NL, int LMAX, int K, bool GAMMA_ONLY = false>
 __global__ void __launch_bounds__(128) k_tp_fwd(TpArgs t) {
   using AR = Arch<NL, LMAX, K>;
   constexpr LayerArch A = AR::A;
@@ -342,7 +318,7 @@ __global__ void __launch_bounds__(128) k_tp_fwd(TpArgs t) {
     G[m] *= t.inv_sqrt_nbar;
     t.G[(ii * AR::DSH + m) * kC + lane] = G[m];
   }
-  if (r1 <= r0) return;
+  if (GAMMA_ONLY || r1 <= r0) return;
   VIn<NL, LMAX, K> nx;
   fetch_v<NL, LMAX, K>(t, r0, lane, nx);
   for (int64_t e = r0; e < r1; ++e) {
@@ -735,15 +711,16 @@ __global__ void k_force_warp(int64_t n, const int32_t* __restrict__ row_ptr, con
 
 // ----------------------------------------------------------------- dispatch
 template <int NL, int LMAX, int K>
-void launch_tp(bool fwd, const TpArgs& t, cudaStream_t st, Profiler* prof, double flops, double bytes) {
+void launch_tp(int mode, const TpArgs& t, cudaStream_t st, Profiler* prof, double flops, double bytes) {
   const unsigned blocks = (unsigned)((t.ch.n_c * 32 + 127) / 128);
   if (blocks == 0) return;
   {
     char tag[48];
-    std::snprintf(tag, sizeof(tag), "tp_%s layer=%d", fwd ? "fwd" : "bwd", K);
-    ProfScope ps_(prof, st, fwd ? PK_TP_FWD : PK_TP_BWD, flops, bytes, tag);
-    if (fwd) k_tp_fwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
-    else k_tp_bwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
+    std::snprintf(tag, sizeof(tag), "%s layer=%d", mode == 0 ? "tp_fwd" : mode == 1 ? "tp_bwd" : "gamma", K);
+    ProfScope ps_(prof, st, mode == 0 ? PK_TP_FWD : mode == 1 ? PK_TP_BWD : PK_GAMMA, flops, bytes, tag);
+    if (mode == 0) k_tp_fwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
+    else if (mode == 1) k_tp_bwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
+    else k_tp_fwd<NL, LMAX, K, true><<<blocks, 128, 0, st>>>(t);
   }
   ALG_LAUNCH_CHECK();
 }
@@ -752,16 +729,21 @@ void launch_tp(bool fwd, const TpArgs& t, cudaStream_t st, Profiler* prof, doubl
 // (DSH FMA) + TP (nnz FMA) per channel; backward = 2 nnz FMA + env adjoint.  Bytes:
 // the per-edge operands the method reads/writes once (w, Y, V in; T out / T-bar, V,
 // w, Y in; w-bar, Y-bar, V-bar out), fp32.
-void tp_dispatch(int NL, int LMAX, int K, bool fwd, const TpArgs& t, cudaStream_t st, Profiler* prof,
+// mode 0: TP forward (Gamma + T), 1: TP backward, 2: Gamma only (the fused path)
+void tp_dispatch(int NL, int LMAX, int K, int mode, const TpArgs& t, cudaStream_t st, Profiler* prof,
                  const LayerInfo& L) {
   const double E = (double)t.ch.n_e;
   const int dsh = (LMAX + 1) * (LMAX + 1);
   const double vin = K == 0 ? 0.0 : (double)L.A.dim_in * kC;
-  const double flops = fwd ? E * kC * 2.0 * (L.tp_nnz + dsh) : E * kC * 2.0 * (2.0 * L.tp_nnz + 2 * dsh);
-  const double bytes = fwd ? 4.0 * E * (L.nw + dsh + vin + (double)L.A.dim_T * kC)
-                           : 4.0 * E * ((double)L.A.dim_T * kC + 2.0 * vin + 2.0 * L.nw + 2.0 * dsh);
+  const double nenv = LMAX + 1;
+  const double flops = mode == 0   ? E * kC * 2.0 * (L.tp_nnz + dsh)
+                       : mode == 1 ? E * kC * 2.0 * (2.0 * L.tp_nnz + 2 * dsh)
+                                   : E * kC * 2.0 * dsh;
+  const double bytes = mode == 0   ? 4.0 * E * (L.nw + dsh + vin + (double)L.A.dim_T * kC)
+                       : mode == 1 ? 4.0 * E * ((double)L.A.dim_T * kC + 2.0 * vin + 2.0 * L.nw + 2.0 * dsh)
+                                   : 4.0 * E * (nenv * kC + dsh) + 4.0 * t.ch.n_c * dsh * kC;
 #define ALG_TP(nl, lm, k) \
-  if (NL == nl && LMAX == lm && K == k) return launch_tp<nl, lm, k>(fwd, t, st, prof, flops, bytes);
+  if (NL == nl && LMAX == lm && K == k) return launch_tp<nl, lm, k>(mode, t, st, prof, flops, bytes);
   ALG_TP(2, 1, 0) ALG_TP(2, 1, 1)
   ALG_TP(2, 2, 0) ALG_TP(2, 2, 1)
   ALG_TP(3, 0, 0) ALG_TP(3, 0, 1) ALG_TP(3, 0, 2)
@@ -960,8 +942,30 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     tp.w = w.w[k].p;
     tp.V = k >= 1 ? w.V[k].p : nullptr;
     tp.G = w.G[k].p;
-    tp_dispatch(M.n_layers, M.lmax, k, true, tp, st, &c->prof, L);
-    if (k < M.n_layers - 1) {
+    const char* fz_env = std::getenv("ALLEGRO_FUSED_TP");  // A/B switch (default: fused where built)
+    const bool fused_tp = !fz_env || std::atoi(fz_env) != 0;
+    const bool fused = fused_tp && M.precision == ALLEGRO_PREC_3XTF32 && tpl_fwd_supported(M.n_layers, M.lmax, k);
+    if (fused) {
+      tp_dispatch(M.n_layers, M.lmax, k, 2, tp, st, &c->prof, L);  // Gamma_i
+      TplIO io;
+      io.ch = ch;
+      io.cidx = c->cidx.p;
+      io.G = w.G[k].p;
+      io.Y = w.Y.p;
+      io.w = w.w[k].p;
+      for (int i = 0; i < L.A.in.n; ++i) io.vin[i] = k >= 1 ? w.V[k].p + (int64_t)L.v_base[i] * ecap : nullptr;
+      for (int o = 0; o < L.A.out.n; ++o) {
+        io.vout[o] = w.V[k + 1].p + (int64_t)M.L[k + 1].v_base[o] * ecap;
+        io.wimg[o] = M.w.lin[k][o].tc.dev;
+        io.wbytes[o] = M.w.lin[k][o].tc.tile_bytes;
+      }
+      io.s = w.T.p;  // T_0e = s, [E][n_s C] (the latent update's second operand)
+      io.tp_fma_per_edge = (double)L.tp_nnz * kC;
+      tpl_fwd(M.n_layers, M.lmax, k, io, st, &c->prof);
+    } else {
+      tp_dispatch(M.n_layers, M.lmax, k, 0, tp, st, &c->prof, L);
+    }
+    if (k < M.n_layers - 1 && !fused) {
       for (int o = 0; o < L.A.out.n; ++o) {
         const int dim = ir_dim(L.A.out.v[o]);
         GemmArgs g = G(w.T.p + (int64_t)L.t_base[o] * ecap, L.A.n_to[o] * kC, M.w.lin[k][o], kC, L.A.n_to[o] * kC,
@@ -1043,7 +1047,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
         tp.Tb[o] = dst;
       }
     }
-    tp_dispatch(M.n_layers, M.lmax, k, false, tp, st, &c->prof, L);
+    tp_dispatch(M.n_layers, M.lmax, k, 1, tp, st, &c->prof, L);
     {
       GemmArgs g = G(w.wbar.p, L.nw, M.w.envT[k], 128, L.nw, xbn, 1.f / std::sqrt(128.f), last ? EPI_R2 : EPI_ACC);
       if (last) {  // xbar^{L-1} = env^T part + Ebar (a w_out + u (b/sqrt(fan)) q_x)

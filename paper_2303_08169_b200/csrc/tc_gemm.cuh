@@ -5,6 +5,8 @@
 // (a = a_hi + a_lo, w = w_hi + w_lo, a w ~ a_hi w_lo + a_lo w_hi + a_hi w_hi) keeps the
 // error at the fp32 level.  W is pre-split and pre-swizzled on the host once per weight.
 #pragma once
+#include <cuda.h>
+
 #include <vector>
 
 #include "gemm.cuh"
@@ -24,6 +26,11 @@ TcWeight tc_prepare_weight(const std::vector<float>& W, int K, int N, std::vecto
 
 // C = epi(A W) on the tensor cores.  g.W is ignored; K % 32 == 0 (pad), N % 16 == 0.
 void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* prof);
+
+// fp32 tensor map (rank 2 or 3; dims / box innermost first; strides in bytes of dims 1..rank-1),
+// SWIZZLE_128B (the innermost box extent must be 32 fp32), zero fill out of bounds.
+CUtensorMap tc_map_f32(const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                       const uint32_t* box);
 
 // Launch tuning / diagnostics (defaults are the production configuration).
 struct TcTuning {

@@ -1,0 +1,505 @@
+// tp_fused.cu -- the tensor product (A8) and the TP-linear channel mix (A9) of one layer in ONE
+// kernel: the "uuu" product is computed straight into tensor memory, one MMA row per thread, and
+// multiplied by the TP-linear weights on the tcgen05 tensor cores (3xTF32), so T never reaches HBM
+// (only its scalar paths s, which the latent update reads).
+//
+//   T_e[c, p, m3] = sqrt(2 l_o + 1) sum_{m1, m2} W3j[m1, m2, m3] V_e[c, ir1, m1] Gamma_i[c, ir2, m2]
+//   V^{k+1}_e[v, o, m] = sum_{p -> o} sum_c T_e[c, p, m] W^k_p[c, v] / sqrt(C n_{->o})
+// (§2.1, "tensor products using their irreducible representations"; concrete
+// reading SURVEY.md §8(c) E6, D1/D7).  Gamma_i (the environment sum, a segmented
+// reduction over the CSR row of i) is formed beforehand by k_gamma (model.cu).
+//
+// Layout of one 32-edge tile (edges e0 .. e0+31 of the chunk) for out irrep o of dim d:
+//   MMA rows r = 32 m3 + e (m-major), so TMEM lane quarter q holds one m3 for all 32 edges;
+//   A[r][(p, c)] = T_e[c, p, m3] (K = n_{->o} 32), B = W_o (K x 32, the GEMM path's pre-split
+//   image), D[r][v] in TMEM -> V^{k+1}_o[e0 + e][m3][v] by a 3-D TMA store of [32 e x 32 v].
+// Warp roles (320 threads, one CTA per SM, persistent over tiles):
+//   warps 0-3  TP warpgroup: thread = MMA row (lane quarter w): per (o, p) K-block the warp(s)
+//              assigned to o compute T for their m3 from the tile's inputs in SMEM, split it into
+//              TF32 hi / lo and tcgen05.st both into a TMEM A stage (the scalar irrep's T also
+//              leaves as s by TMA store).  Irreps are spread over the four quarters (base warp).
+//   warps 4-7  epilogue: tcgen05.ld of D (thread = row), scale, SMEM box, TMA store.
+//   warp 8     producer: the tile's centre indices (coalesced loads), then TMA loads of its V^k
+//              rows (or w_edge for layer 0) and bulk copies of Y and of the Gamma rows of its
+//              centre atoms into a ring of input stages.
+//   warp 9     TMEM allocator and MMA issuer (one elected lane): D += a_hi w_lo + a_lo w_hi +
+//              a_hi w_hi per K-step of 8, A from TMEM, W from SMEM.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "ctx.cuh"
+#include "layer.cuh"
+#include "tc_gemm.cuh"
+#include "tc_ptx.cuh"
+#include "tp_fused.cuh"
+
+namespace allegro {
+namespace {
+
+constexpr int kTile = 32;           // edges per tile
+constexpr int kThreads = 320;       // 10 warps
+constexpr int kATm = 64;            // TMEM columns of one A stage (hi 32 | lo 32)
+constexpr int kAStages = 4;         // TMEM A ring depth
+constexpr int kBoxBytes = 32 * 128; // one [32 x 32 fp32] TMA box
+constexpr size_t kSmemLimit = 227 * 1024;
+
+template <int NL, int LMAX, int K>
+struct Fz {
+  using AR = Arch<NL, LMAX, K>;
+  static constexpr LayerArch A = AR::A;
+  static constexpr int NO = A.out.n;
+  static constexpr int NI = A.in.n;
+  static constexpr int DSH = AR::DSH;
+  static constexpr int dim(int o) { return ir_dim(A.out.v[o]); }
+  static constexpr int nto(int o) { return A.n_to[o]; }
+  static constexpr bool scalar(int o) { return A.out.v[o].l == 0 && A.out.v[o].p == 1; }
+  static constexpr int path_of(int o, int p) {
+    for (int q = 0; q < A.n_paths; ++q)
+      if (A.out_idx[q] == o && A.out_local[q] == p) return q;
+    return -1;
+  }
+  // K-block (A stage) index of (o, p) within a tile
+  static constexpr int kb_of(int o, int p) {
+    int b = 0;
+    for (int q = 0; q < o; ++q) b += nto(q);
+    return b + p;
+  }
+  static constexpr int n_kb() { return kb_of(NO, 0); }
+  // lane quarter of m3 = 0 of irrep o: a greedy spread of the K-block work over the four warps
+  static constexpr int base(int o) {
+    int load[4] = {0, 0, 0, 0};
+    int b_of[kMaxIr] = {};
+    bool done[kMaxIr] = {};
+    for (int it = 0; it < NO; ++it) {
+      int pick = -1;  // heaviest unassigned irrep first
+      for (int q = 0; q < NO; ++q)
+        if (!done[q] && (pick < 0 || dim(q) * nto(q) > dim(pick) * nto(pick))) pick = q;
+      int best = 0, best_cost = 1 << 30;
+      for (int b = 0; b < 4; ++b) {
+        int cost = 0;
+        for (int m = 0; m < dim(pick); ++m) cost = cost > load[(b + m) % 4] + nto(pick) ? cost : load[(b + m) % 4] + nto(pick);
+        if (cost < best_cost) best_cost = cost, best = b;
+      }
+      for (int m = 0; m < dim(pick); ++m) load[(best + m) % 4] += nto(pick);
+      b_of[pick] = best;
+      done[pick] = true;
+    }
+    return b_of[o];
+  }
+  // warp holding m3 = 0 of the scalar irrep (its T values are s)
+  static constexpr int s_warp() {
+    for (int o = 0; o < NO; ++o)
+      if (scalar(o)) return base(o);
+    return -1;
+  }
+  // input stage layout (bytes): V^k per in irrep (K >= 1) or w_edge per l (K = 0), Y, Gamma, header
+  static constexpr int in_rows(int i) { return kTile * ir_dim(A.in.v[i]); }
+  static constexpr int v_off(int i) {
+    int b = 0;
+    for (int q = 0; q < i; ++q) b += in_rows(q) * 128;
+    return b;
+  }
+  static constexpr int wv_bytes() { return K == 0 ? AR::NENV * kBoxBytes : v_off(NI); }
+  static constexpr int y_off() { return wv_bytes(); }
+  static constexpr int g_off() { return y_off() + (K == 0 ? kTile * DSH * 4 : 0); }
+  static constexpr int g_bytes() { return kTile * DSH * 128; }  // at most one centre per edge
+  static constexpr int h_off() { return g_off() + g_bytes(); }
+  static constexpr int stage_bytes() { return (h_off() + 256 + 1023) / 1024 * 1024; }
+  static constexpr int acc_cols() { return NO * 32; }
+};
+
+struct TplParams {
+  int64_t n_e;          // edges of the chunk
+  int64_t e0g, a0;      // first global edge / centre atom of the chunk
+  const int32_t* cidx;  // [global edges] centre atom (local atom index)
+  const float* G;       // [n_c][DSH][C]
+  const float* Y;       // [E][DSH]
+  const float* wimg[kMaxIr];
+  uint32_t wbytes[kMaxIr];
+  float scale[kMaxIr];
+  int n_tiles;
+  int stages;           // input ring depth
+};
+
+struct TplMaps {
+  CUtensorMap in[kMaxIr];   // V^k per in irrep [E*dim][32] (K >= 1) or w [E][NW] (K = 0, in[0])
+  CUtensorMap out[kMaxIr];  // V^{k+1} per out irrep, 3-D [E][dim][32]
+  CUtensorMap s;            // scalar paths of T, [E][n_s 32]
+};
+
+template <int NL, int LMAX, int K>
+__global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__ TplMaps maps, const TplParams p) {
+  using F = Fz<NL, LMAX, K>;
+  using AR = typename F::AR;
+  constexpr LayerArch A = F::A;
+  constexpr int NO = F::NO, DSH = F::DSH, NKB = F::n_kb();
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  unsigned char* base = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
+  uint32_t woff[kMaxIr + 1];
+  woff[0] = 0;
+#pragma unroll
+  for (int o = 0; o < kMaxIr; ++o) woff[o + 1] = woff[o] + (o < NO ? p.wbytes[o] : 0u);
+  unsigned char* w_img = base;
+  unsigned char* stage0 = base + ((woff[NO] + 1023u) & ~1023u);
+  unsigned char* epi = stage0 + (size_t)p.stages * F::stage_bytes();  // [4 warps][2][4 KB]
+  unsigned char* sbuf = epi + 8 * kBoxBytes;                           // [2][4 KB] s boxes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sbuf + 2 * kBoxBytes);
+  uint64_t* in_full = bars;
+  uint64_t* in_empty = in_full + 4;
+  uint64_t* a_full = in_empty + 4;
+  uint64_t* a_empty = a_full + kAStages;
+  uint64_t* acc_full = a_empty + kAStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* w_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) mbar_init(in_full + s, 1), mbar_init(in_empty + s, 4);
+    for (int s = 0; s < kAStages; ++s) mbar_init(a_full + s, 4), mbar_init(a_empty + s, 1);
+    for (int b = 0; b < 2; ++b) mbar_init(acc_full + b, 1), mbar_init(acc_empty + b, 4);
+    mbar_init(w_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_a = tmem + 2u * F::acc_cols();  // A ring after the two accumulator sets
+  const int n_my = p.n_tiles > (int)blockIdx.x ? (p.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  if (warp == 8) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      mbar_expect_tx(w_full, woff[NO]);
+      for (int o = 0; o < NO; ++o) bulk_load(w_img + woff[o], p.wimg[o], p.wbytes[o], w_full);
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = 0; t < n_my; ++t) {
+      const int64_t e0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kTile;
+      const int nv = (int)(p.n_e - e0 < kTile ? p.n_e - e0 : kTile);
+      mbar_wait(in_empty + s, ph ^ 1);
+      unsigned char* st = stage0 + (size_t)s * F::stage_bytes();
+      int* hdr = reinterpret_cast<int*>(st + F::h_off());
+      const int ci = lane < nv ? p.cidx[p.e0g + e0 + lane] - (int)p.a0 : 0;
+      const int a_lo = __shfl_sync(0xffffffffu, ci, 0);
+      const int a_hi = __shfl_sync(0xffffffffu, ci, nv - 1);
+      hdr[lane] = lane < nv ? ci - a_lo : 0;  // Gamma row block of this edge's centre
+      if (lane == 0) hdr[32] = nv;
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t gbytes = (uint32_t)(a_hi - a_lo + 1) * DSH * 128;
+        uint32_t bytes = gbytes;
+        if constexpr (K == 0) bytes += AR::NENV * kBoxBytes + (uint32_t)nv * DSH * 4;
+        else bytes += (uint32_t)F::v_off(F::NI);
+        mbar_expect_tx(in_full + s, bytes);
+        if constexpr (K == 0) {
+#pragma unroll
+          for (int l = 0; l < AR::NENV; ++l) tma_load_2d(st + l * kBoxBytes, &maps.in[0], 32 * l, (int)e0, in_full + s);
+          bulk_load(st + F::y_off(), p.Y + e0 * DSH, (uint32_t)nv * DSH * 4, in_full + s);
+        } else {
+#pragma unroll
+          for (int i = 0; i < F::NI; ++i)
+            tma_load_2d(st + F::v_off(i), &maps.in[i], 0, (int)(e0 * ir_dim(A.in.v[i])), in_full + s);
+        }
+        bulk_load(st + F::g_off(), p.G + (int64_t)a_lo * DSH * 32, gbytes, in_full + s);
+      }
+      if (++s == p.stages) s = 0, ph ^= 1;
+    }
+  } else if (warp < 4) {
+    // ---------------- TP warpgroup: thread = MMA row (m3, e) ----------------
+    int s = 0, j = 0, sb = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int t = 0; t < n_my; ++t) {
+      const int64_t e0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kTile;
+      mbar_wait(in_full + s, ph);
+      const unsigned char* st = stage0 + (size_t)s * F::stage_bytes();
+      const int* hdr = reinterpret_cast<const int*>(st + F::h_off());
+      const int e = lane;
+      const int ga = hdr[e];  // Gamma row block (valid edges; 0 for the padding rows)
+      const unsigned char* gb = st + F::g_off() + (size_t)ga * DSH * 128;
+      static_for<NO>([&](auto O) {
+        constexpr int o = decltype(O)::value;
+        constexpr int D3 = F::dim(o);
+        constexpr int B0 = F::base(o);
+        const int m3 = (warp - B0 + 4) & 3;
+        static_for<F::nto(o)>([&](auto P) {
+          constexpr int pl = decltype(P)::value;
+          constexpr int q = F::path_of(o, pl);
+          constexpr int L1 = A.path[q].a.l, L2 = A.path[q].b.l, LO = A.path[q].o.l;
+          constexpr int D1 = 2 * L1 + 1, D2 = 2 * L2 + 1;
+          mbar_wait(a_empty + j, aph ^ 1);
+          if (m3 < D3) {
+            float acc[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+            static_for<D3>([&](auto M3) {
+              constexpr int mm3 = decltype(M3)::value;
+              if (m3 == mm3) {
+                static_for<D1 * D2>([&](auto I) {
+                  constexpr int m1 = decltype(I)::value / D2, m2 = decltype(I)::value % D2;
+                  constexpr float cf = (float)(csqrt(2.0 * LO + 1.0) * W3j<L1, L2, LO>::t.v[(m1 * D2 + m2) * (2 * LO + 1) + mm3]);
+                  if constexpr (cf != 0.f) {
+                    const unsigned char* grow = gb + (A.sh_off[q] + m2) * 128;
+                    if constexpr (K == 0) {
+                      constexpr int mv = A.in_off[q] + m1;  // V0[m] = w_edge[l(m)] Y[m]
+                      const float yv = reinterpret_cast<const float*>(st + F::y_off())[e * DSH + mv];
+                      const unsigned char* vrow = st + lm_l(mv) * kBoxBytes + e * 128;
+#pragma unroll
+                      for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 v = *reinterpret_cast<const float4*>(vrow + ((c4 ^ (e & 7)) << 4));
+                        const float4 g = *reinterpret_cast<const float4*>(grow + (c4 << 4));
+                        acc[4 * c4 + 0] = fmaf(cf * (v.x * yv), g.x, acc[4 * c4 + 0]);
+                        acc[4 * c4 + 1] = fmaf(cf * (v.y * yv), g.y, acc[4 * c4 + 1]);
+                        acc[4 * c4 + 2] = fmaf(cf * (v.z * yv), g.z, acc[4 * c4 + 2]);
+                        acc[4 * c4 + 3] = fmaf(cf * (v.w * yv), g.w, acc[4 * c4 + 3]);
+                      }
+                    } else {
+                      constexpr int ii = A.in.index(A.path[q].a);
+                      const int r = e * D1 + m1;
+                      const unsigned char* vrow = st + F::v_off(ii) + r * 128;
+#pragma unroll
+                      for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 v = *reinterpret_cast<const float4*>(vrow + ((c4 ^ (r & 7)) << 4));
+                        const float4 g = *reinterpret_cast<const float4*>(grow + (c4 << 4));
+                        acc[4 * c4 + 0] = fmaf(cf * v.x, g.x, acc[4 * c4 + 0]);
+                        acc[4 * c4 + 1] = fmaf(cf * v.y, g.y, acc[4 * c4 + 1]);
+                        acc[4 * c4 + 2] = fmaf(cf * v.z, g.z, acc[4 * c4 + 2]);
+                        acc[4 * c4 + 3] = fmaf(cf * v.w, g.w, acc[4 * c4 + 3]);
+                      }
+                    }
+                  }
+                });
+              }
+            });
+            if constexpr (F::scalar(o)) {
+              if (m3 == 0) {  // s = the scalar paths of T, [E][n_s 32]: one [32 e x 32 c] box per path
+                unsigned char* box = sbuf + sb * kBoxBytes;
+                if (lane == 0) bulk_wait_read1();  // the box used two stores ago has been read
+                __syncwarp();
+#pragma unroll
+                for (int c4 = 0; c4 < 8; ++c4)
+                  *reinterpret_cast<float4*>(box + e * 128 + ((c4 ^ (e & 7)) << 4)) =
+                      make_float4(acc[4 * c4], acc[4 * c4 + 1], acc[4 * c4 + 2], acc[4 * c4 + 3]);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                  tma_store_2d(&maps.s, 32 * pl, (int)e0, box);
+                  bulk_commit();
+                }
+                sb ^= 1;
+              }
+            }
+            uint32_t hi[32], lo[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const uint32_t h = __float_as_uint(acc[c]) & 0xffffe000u;
+              hi[c] = h;
+              lo[c] = __float_as_uint(acc[c] - __uint_as_float(h));
+            }
+            tc_fence_after();
+            const uint32_t ta = tmem_a + (uint32_t)(j * kATm) + ((uint32_t)(warp * 32) << 16);
+            tmem_st32(ta, hi);
+            tmem_st32(ta + 32, lo);
+            tmem_st_wait();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(a_full + j);
+          if (++j == kAStages) j = 0, aph ^= 1;
+        });
+      });
+      // the stage is refilled by TMA (async proxy): order these generic reads first
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(in_empty + s);
+      if (++s == p.stages) s = 0, ph ^= 1;
+    }
+    if (lane == 0) bulk_wait0();
+  } else if (warp == 9) {
+    // ---------------- MMA issuer ----------------
+    mbar_wait(w_full, 0);
+    tc_fence_after();
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t wblk = 32 * 128;  // one W half-block (hi or lo) of a K-block
+    __syncwarp();
+    const uint32_t L = elect_leader();
+    int j = 0;
+    uint32_t aph = 0;
+    for (int t = 0; t < n_my; ++t) {
+      const int buf = t & 1;
+      mbar_wait(acc_empty + buf, ((uint32_t)(t >> 1) & 1u) ^ 1u);
+      __syncwarp();
+      tc_fence_after();
+      static_for<NO>([&](auto O) {
+        constexpr int o = decltype(O)::value;
+        const uint32_t d = tmem + (uint32_t)(buf * F::acc_cols() + 32 * o);
+        const uint64_t desc_o = sdesc(smem_u32(w_img + woff[o]));
+        static_for<F::nto(o)>([&](auto P) {
+          constexpr int pl = decltype(P)::value;
+          mbar_wait(a_full + j, aph);
+          __syncwarp();
+          tc_fence_after();
+          const uint32_t ahi = tmem_a + (uint32_t)(j * kATm), alo = ahi + 32;
+          const uint64_t dkb = desc_o + (uint64_t)((pl * 2 * wblk) >> 4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t dwh = dkb + (uint64_t)(k * 2);
+            const uint64_t dwl = dwh + (uint64_t)(wblk >> 4);
+            mma_tf32_ts_w(L, d, ahi + 8 * k, dwl, idesc, (pl | k) ? 1u : 0u);
+            mma_tf32_ts_w(L, d, alo + 8 * k, dwh, idesc, 1u);
+            mma_tf32_ts_w(L, d, ahi + 8 * k, dwh, idesc, 1u);
+          }
+          mma_commit_w(L, a_empty + j);
+          if (++j == kAStages) j = 0, aph ^= 1;
+        });
+      });
+      mma_commit_w(L, acc_full + buf);
+    }
+  } else {
+    // ---------------- epilogue (warps 4-7): D -> V^{k+1} ----------------
+    const int qd = warp & 3;  // TMEM lane quarter
+    int n_st = 0;
+    for (int t = 0; t < n_my; ++t) {
+      const int64_t e0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kTile;
+      const int buf = t & 1;
+      mbar_wait(acc_full + buf, (uint32_t)(t >> 1) & 1u);
+      tc_fence_after();
+      static_for<NO>([&](auto O) {
+        constexpr int o = decltype(O)::value;
+        constexpr int B0 = F::base(o);
+        const int m3 = (qd - B0 + 4) & 3;
+        if (m3 < F::dim(o)) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(buf * F::acc_cols() + 32 * o), v);
+          unsigned char* box = epi + (size_t)(2 * qd + (n_st & 1)) * kBoxBytes;
+          if (n_st >= 2) {
+            if (lane == 0) bulk_wait_read1();
+            __syncwarp();
+          }
+          const float sc = p.scale[o];
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4)
+            *reinterpret_cast<float4*>(box + lane * 128 + ((c4 ^ (lane & 7)) << 4)) =
+                make_float4(sc * v[4 * c4], sc * v[4 * c4 + 1], sc * v[4 * c4 + 2], sc * v[4 * c4 + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&maps.out[o], 0, m3, (int)e0, box);
+            bulk_commit();
+          }
+          ++n_st;
+        }
+      });
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + buf);
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int NL, int LMAX, int K>
+void launch(const TplIO& io, cudaStream_t st, Profiler* prof) {
+  using F = Fz<NL, LMAX, K>;
+  constexpr LayerArch A = F::A;
+  const int64_t E = io.ch.n_e;
+  if (E <= 0) return;
+  TplMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  TplParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.n_e = E;
+  p.e0g = io.ch.e0;
+  p.a0 = io.ch.a0;
+  p.cidx = io.cidx;
+  p.G = io.G;
+  p.Y = io.Y;
+  p.n_tiles = (int)((E + kTile - 1) / kTile);
+  uint32_t wsum = 0;
+  for (int o = 0; o < F::NO; ++o) {
+    p.wimg[o] = io.wimg[o];
+    p.wbytes[o] = (uint32_t)io.wbytes[o];
+    if (io.wbytes[o] != (size_t)F::nto(o) * 2 * 32 * 128) throw CudaError("tpl_fwd: unexpected TP-linear weight image");
+    p.scale[o] = 1.f / std::sqrt((float)(kC * F::nto(o)));
+    wsum += p.wbytes[o];
+    const uint64_t dims[3] = {32, (uint64_t)F::dim(o), (uint64_t)E};
+    const uint64_t strides[2] = {128, (uint64_t)F::dim(o) * 128};
+    const uint32_t box[3] = {32, 1, 32};
+    maps.out[o] = tc_map_f32(io.vout[o], 3, dims, strides, box);
+  }
+  if constexpr (K == 0) {
+    const uint64_t dims[2] = {(uint64_t)Arch<NL, LMAX, K>::NW, (uint64_t)E};
+    const uint64_t strides[1] = {(uint64_t)Arch<NL, LMAX, K>::NW * 4};
+    const uint32_t box[2] = {32, 32};
+    maps.in[0] = tc_map_f32(io.w, 2, dims, strides, box);
+  } else {
+    for (int i = 0; i < F::NI; ++i) {
+      const uint64_t dims[2] = {32, (uint64_t)E * ir_dim(A.in.v[i])};
+      const uint64_t strides[1] = {128};
+      const uint32_t box[2] = {32, (uint32_t)F::in_rows(i)};
+      maps.in[i] = tc_map_f32(io.vin[i], 2, dims, strides, box);
+    }
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)A.n_s * 32, (uint64_t)E};
+    const uint64_t strides[1] = {(uint64_t)A.n_s * 128};
+    const uint32_t box[2] = {32, 32};
+    maps.s = tc_map_f32(io.s, 2, dims, strides, box);
+  }
+  const size_t fixed = 1024 + ((wsum + 1023) / 1024) * 1024 + 8 * kBoxBytes + 2 * kBoxBytes + 512;
+  int stages = (int)std::min<size_t>(4, (kSmemLimit - fixed) / F::stage_bytes());
+  if (stages < 2) throw CudaError("tpl_fwd: shared memory too small for two input stages");
+  p.stages = stages;
+  const size_t smem = fixed + (size_t)stages * F::stage_bytes();
+  int dev = 0;
+  ALG_CUDA(cudaGetDevice(&dev));
+  static bool attr[64] = {};
+  static int nsm[64] = {};
+  if (!attr[dev]) {
+    ALG_CUDA(cudaFuncSetAttribute(k_tpl_fwd<NL, LMAX, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
+    ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
+    attr[dev] = true;
+  }
+  const int grid = std::max(1, std::min(p.n_tiles, nsm[dev]));
+  {
+    char tag[48];
+    std::snprintf(tag, sizeof(tag), "tpl_fwd layer=%d", K);
+    // algorithmic work: the TP FMAs (CUDA cores) + the TP-linear MACs (tensor cores), per edge
+    double mac = 0;
+    for (int o = 0; o < F::NO; ++o) mac += (double)F::dim(o) * F::nto(o) * kC * kC;
+    const double flops = (double)E * (2.0 * io.tp_fma_per_edge + 2.0 * mac);
+    double bytes = 0;
+    for (int i = 0; i < F::NI; ++i) bytes += K == 0 ? 0.0 : (double)ir_dim(A.in.v[i]) * 128;
+    if (K == 0) bytes += Arch<NL, LMAX, K>::NENV * 128 + F::DSH * 4;
+    for (int o = 0; o < F::NO; ++o) bytes += (double)F::dim(o) * 128;
+    bytes += (double)A.n_s * 128 + 4;  // s, cidx
+    ProfScope ps_(prof, st, PK_TPL_FWD, flops, bytes * E, tag);
+    k_tpl_fwd<NL, LMAX, K><<<grid, kThreads, smem, st>>>(maps, p);
+  }
+  ALG_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+bool tpl_fwd_supported(int NL, int LMAX, int K) { return LMAX == 1 && K < NL - 1 && (NL == 2 || NL == 3); }
+
+void tpl_fwd(int NL, int LMAX, int K, const TplIO& io, cudaStream_t st, Profiler* prof) {
+#define ALG_TPL(nl, lm, k) \
+  if (NL == nl && LMAX == lm && K == k) return launch<nl, lm, k>(io, st, prof);
+  ALG_TPL(2, 1, 0)
+  ALG_TPL(3, 1, 0) ALG_TPL(3, 1, 1)
+#undef ALG_TPL
+  throw CudaError("tpl_fwd: no fused kernel for this layer");
+}
+
+}  // namespace allegro

@@ -295,7 +295,9 @@ def test_profiler_counts_launches(pb):
     prof = m.profile_read()
     assert m.launch_count() == sum(v[3] for v in prof.values()) > 20
     assert prof["gemm"][3] > 0 and prof["gemm"][0] > 0 and prof["gemm"][1] > 0
-    assert prof["tp_fwd"][3] == prof["tp_bwd"][3] == 2 * 2  # 2 layers x 2 steps
+    # 2 layers x 2 steps: layer 0 runs the fused TP + TP-linear kernel (3xTF32 default), layer 1 the TP kernel
+    assert prof["tp_fwd"][3] + prof["tp_lin_fwd"][3] == prof["tp_bwd"][3] == 2 * 2
+    assert prof["tp_lin_fwd"][3] == prof["gamma"][3]
 
 
 def test_nvt_step_matches_oracle(pb):
@@ -350,3 +352,24 @@ def test_resnet_contraction_deterministic(pb):
     for _ in range(8):
         c, a = pb.debug_gemm_epi(A, W, code, X=A, u=u, want_aux=True)
         assert np.array_equal(c, c0) and np.array_equal(a, a0)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C5"])
+def test_fused_tp_linear_matches_unfused(pb, cfg, monkeypatch):
+    """The fused TP + TP-linear kernel (tp_fused.cu) computes the same T (same FMA order) and the
+    same 3xTF32 contraction as the unfused TP kernel + GEMM: energies and forces agree to
+    rounding (in practice bit for bit), C1 (2, 1) and the bench's C5 (3, 1) at full size."""
+    s = configs.system(cfg)
+    wf = configs.weight_file(cfg)
+    m = pb.Allegro(wf, s.box, precision=pb.PREC_3XTF32, n_atoms=s.n)
+    monkeypatch.setenv("ALLEGRO_FUSED_TP", "0")
+    e0, ea0, f0 = m.compute_energy_forces(s.pos, s.species)
+    monkeypatch.setenv("ALLEGRO_FUSED_TP", "1")
+    m.profile(True)
+    e1, ea1, f1 = m.compute_energy_forces(s.pos, s.species)
+    assert m.profile_read()["tp_lin_fwd"][3] > 0
+    m.profile(False)
+    print(f"{cfg}: fused vs unfused bitwise: E {e1 == e0}, F {np.array_equal(f1, f0)}, "
+          f"max|dF| = {np.abs(f1 - f0).max():.3g}")
+    assert abs(e1 - e0) <= 1e-9 * np.abs(ea0).sum()
+    assert np.abs(f1 - f0).max() <= 1e-6
