@@ -723,6 +723,7 @@ void launch_tp(int mode, const TpArgs& t, cudaStream_t st, Profiler* prof, doubl
     else k_tp_fwd<NL, LMAX, K, true><<<blocks, 128, 0, st>>>(t);
   }
   ALG_LAUNCH_CHECK();
+  if (mode == 2 && std::getenv("ALLEGRO_SYNC_CHECK")) ALG_CUDA(cudaStreamSynchronize(st));
 }
 
 // Algorithmic work of the TP kernels per edge: forward = Gamma sum
@@ -943,8 +944,9 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     tp.V = k >= 1 ? w.V[k].p : nullptr;
     tp.G = w.G[k].p;
     const char* fz_env = std::getenv("ALLEGRO_FUSED_TP");  // A/B switch (default: fused where built)
-    const bool fused_tp = !fz_env || std::atoi(fz_env) != 0;
-    const bool fused = fused_tp && M.precision == ALLEGRO_PREC_3XTF32 && tpl_fwd_supported(M.n_layers, M.lmax, k);
+    const int fz_mask = fz_env ? std::atoi(fz_env) : -1;  // bit k: fuse layer k (0: none)
+    const bool fused = ((fz_mask >> k) & 1) && M.precision == ALLEGRO_PREC_3XTF32 &&
+                       tpl_fwd_supported(M.n_layers, M.lmax, k);
     if (fused) {
       tp_dispatch(M.n_layers, M.lmax, k, 2, tp, st, &c->prof, L);  // Gamma_i
       TplIO io;

@@ -13,21 +13,25 @@
 //   MMA rows r = 32 m3 + e (m-major), so TMEM lane quarter q holds one m3 for all 32 edges;
 //   A[r][(p, c)] = T_e[c, p, m3] (K = n_{->o} 32), B = W_o (K x 32, the GEMM path's pre-split
 //   image), D[r][v] in TMEM -> V^{k+1}_o[e0 + e][m3][v] by a 3-D TMA store of [32 e x 32 v].
-// Warp roles (320 threads, one CTA per SM, persistent over tiles):
-//   warps 0-3  TP warpgroup: thread = MMA row (lane quarter w): per (o, p) K-block the warp(s)
-//              assigned to o compute T for their m3 from the tile's inputs in SMEM, split it into
-//              TF32 hi / lo and tcgen05.st both into a TMEM A stage (the scalar irrep's T also
-//              leaves as s by TMA store).  Irreps are spread over the four quarters (base warp).
-//   warps 4-7  epilogue: tcgen05.ld of D (thread = row), scale, SMEM box, TMA store.
-//   warp 8     producer: the tile's centre indices (coalesced loads), then TMA loads of its V^k
+// Warp roles (704 threads, one CTA per SM, persistent over tiles):
+//   warps 0-15 TP warps: thread = MMA row (lane quarter w & 3), 8 channels per warp (w >> 2): per
+//              (o, p) K-block the warps assigned to o compute T for their m3 from the tile's inputs
+//              in SMEM, split it into TF32 hi / lo and tcgen05.st both into a TMEM A stage (the
+//              scalar irrep's T also leaves as s).  Irreps are spread over the four quarters (base).
+//              (Four warps with 32 channels each were latency-bound: one warp per SMSP, 4.5 us per
+//              tile; sixteen warps with 8 channels each: 17 + 16 ms per C5 step for layers 0, 1.)
+//   warps 16-19 epilogue: tcgen05.ld of D (thread = row), scale, SMEM box, TMA store.
+//   warp 20    producer: the tile's centre indices (coalesced loads), then TMA loads of its V^k
 //              rows (or w_edge for layer 0) and bulk copies of Y and of the Gamma rows of its
 //              centre atoms into a ring of input stages.
-//   warp 9     TMEM allocator and MMA issuer (one elected lane): D += a_hi w_lo + a_lo w_hi +
+//   warp 21    TMEM allocator and MMA issuer (one elected lane): D += a_hi w_lo + a_lo w_hi +
 //              a_hi w_hi per K-step of 8, A from TMEM, W from SMEM.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "ctx.cuh"
 #include "layer.cuh"
@@ -39,7 +43,10 @@ namespace allegro {
 namespace {
 
 constexpr int kTile = 32;           // edges per tile
-constexpr int kThreads = 320;       // 10 warps
+constexpr int kTpWarps = 16;        // TP warps: 4 lane quarters x 4 channel groups
+constexpr int kProdWarp = kTpWarps + 4;
+constexpr int kMmaWarp = kTpWarps + 5;
+constexpr int kThreads = 32 * (kTpWarps + 6);  // 22 warps
 constexpr int kATm = 64;            // TMEM columns of one A stage (hi 32 | lo 32)
 constexpr int kAStages = 4;         // TMEM A ring depth
 constexpr int kBoxBytes = 32 * 128; // one [32 x 32 fp32] TMA box
@@ -116,17 +123,19 @@ struct TplParams {
   const int32_t* cidx;  // [global edges] centre atom (local atom index)
   const float* G;       // [n_c][DSH][C]
   const float* Y;       // [E][DSH]
+  float* s;             // [E][n_s C] scalar paths of T
   const float* wimg[kMaxIr];
   uint32_t wbytes[kMaxIr];
   float scale[kMaxIr];
   int n_tiles;
   int stages;           // input ring depth
+  int diag;             // diagnostics (ALLEGRO_TPL_DIAG): bit0 no Gamma copy, bit1 no V/w loads, bit2 no TP
+                        // reads, bit3 no output stores, bit4 no s stores, bit5 no MMAs
 };
 
 struct TplMaps {
   CUtensorMap in[kMaxIr];   // V^k per in irrep [E*dim][32] (K >= 1) or w [E][NW] (K = 0, in[0])
   CUtensorMap out[kMaxIr];  // V^{k+1} per out irrep, 3-D [E][dim][32]
-  CUtensorMap s;            // scalar paths of T, [E][n_s 32]
 };
 
 template <int NL, int LMAX, int K>
@@ -144,8 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
   unsigned char* w_img = base;
   unsigned char* stage0 = base + ((woff[NO] + 1023u) & ~1023u);
   unsigned char* epi = stage0 + (size_t)p.stages * F::stage_bytes();  // [4 warps][2][4 KB]
-  unsigned char* sbuf = epi + 8 * kBoxBytes;                           // [2][4 KB] s boxes
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sbuf + 2 * kBoxBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi + 8 * kBoxBytes);
   uint64_t* in_full = bars;
   uint64_t* in_empty = in_full + 4;
   uint64_t* a_full = in_empty + 4;
@@ -157,13 +165,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s) mbar_init(in_full + s, 1), mbar_init(in_empty + s, 4);
-    for (int s = 0; s < kAStages; ++s) mbar_init(a_full + s, 4), mbar_init(a_empty + s, 1);
+    for (int s = 0; s < p.stages; ++s) mbar_init(in_full + s, 1), mbar_init(in_empty + s, kTpWarps);
+    for (int s = 0; s < kAStages; ++s) mbar_init(a_full + s, kTpWarps), mbar_init(a_empty + s, 1);
     for (int b = 0; b < 2; ++b) mbar_init(acc_full + b, 1), mbar_init(acc_empty + b, 4);
     mbar_init(w_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
   const uint32_t tmem_a = tmem + 2u * F::acc_cols();  // A ring after the two accumulator sets
   const int n_my = p.n_tiles > (int)blockIdx.x ? (p.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
-  if (warp == 8) {
+  if (warp == kProdWarp) {
     // ---------------- producer ----------------
     if (lane == 0) {
       mbar_expect_tx(w_full, woff[NO]);
@@ -179,13 +187,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
     }
     int s = 0;
     uint32_t ph = 0;
+    // centre indices of tile t (the load for tile t + 1 is issued before tile t waits for its stage)
+    auto load_ci = [&](int t) -> int {
+      const int64_t e0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kTile;
+      return (t < n_my && e0 + lane < p.n_e) ? __ldg(p.cidx + p.e0g + e0 + lane) - (int)p.a0 : 0;
+    };
+    int ci_next = load_ci(0);
     for (int t = 0; t < n_my; ++t) {
       const int64_t e0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kTile;
       const int nv = (int)(p.n_e - e0 < kTile ? p.n_e - e0 : kTile);
+      const int ci = ci_next;
+      ci_next = load_ci(t + 1);
       mbar_wait(in_empty + s, ph ^ 1);
       unsigned char* st = stage0 + (size_t)s * F::stage_bytes();
       int* hdr = reinterpret_cast<int*>(st + F::h_off());
-      const int ci = lane < nv ? p.cidx[p.e0g + e0 + lane] - (int)p.a0 : 0;
       const int a_lo = __shfl_sync(0xffffffffu, ci, 0);
       const int a_hi = __shfl_sync(0xffffffffu, ci, nv - 1);
       hdr[lane] = lane < nv ? ci - a_lo : 0;  // Gamma row block of this edge's centre
@@ -193,26 +208,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
       __syncwarp();
       if (lane == 0) {
         const uint32_t gbytes = (uint32_t)(a_hi - a_lo + 1) * DSH * 128;
-        uint32_t bytes = gbytes;
-        if constexpr (K == 0) bytes += AR::NENV * kBoxBytes + (uint32_t)nv * DSH * 4;
-        else bytes += (uint32_t)F::v_off(F::NI);
+        uint32_t bytes = (p.diag & 1) ? 0u : gbytes;
+        if (!(p.diag & 2)) {
+          if constexpr (K == 0) bytes += AR::NENV * kBoxBytes + (uint32_t)nv * DSH * 4;
+          else bytes += (uint32_t)F::v_off(F::NI);
+        }
         mbar_expect_tx(in_full + s, bytes);
-        if constexpr (K == 0) {
+        if (p.diag & 2) {
+        } else if constexpr (K == 0) {
 #pragma unroll
           for (int l = 0; l < AR::NENV; ++l) tma_load_2d(st + l * kBoxBytes, &maps.in[0], 32 * l, (int)e0, in_full + s);
           bulk_load(st + F::y_off(), p.Y + e0 * DSH, (uint32_t)nv * DSH * 4, in_full + s);
         } else {
-#pragma unroll
-          for (int i = 0; i < F::NI; ++i)
-            tma_load_2d(st + F::v_off(i), &maps.in[i], 0, (int)(e0 * ir_dim(A.in.v[i])), in_full + s);
+          // compile-time loop: a runtime index into the constexpr arch would read host-only data
+          static_for<F::NI>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int dim = ir_dim(A.in.v[i]);
+            tma_load_2d(st + F::v_off(i), &maps.in[i], 0, (int)(e0 * dim), in_full + s);
+          });
         }
-        bulk_load(st + F::g_off(), p.G + (int64_t)a_lo * DSH * 32, gbytes, in_full + s);
+        if (!(p.diag & 1)) bulk_load(st + F::g_off(), p.G + (int64_t)a_lo * DSH * 32, gbytes, in_full + s);
       }
       if (++s == p.stages) s = 0, ph ^= 1;
     }
-  } else if (warp < 4) {
-    // ---------------- TP warpgroup: thread = MMA row (m3, e) ----------------
-    int s = 0, j = 0, sb = 0;
+  } else if (warp < kTpWarps) {
+    // ---------------- TP warps: thread = MMA row (m3, e), 8 channels per warp ----------------
+    const int qw = warp & 3;                 // TMEM lane quarter
+    const int cg = warp >> 2;                // channel group: channels 8 cg .. 8 cg + 7
+    int s = 0, j = 0;
     uint32_t ph = 0, aph = 0;
     for (int t = 0; t < n_my; ++t) {
       const int64_t e0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kTile;
@@ -220,13 +243,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
       const unsigned char* st = stage0 + (size_t)s * F::stage_bytes();
       const int* hdr = reinterpret_cast<const int*>(st + F::h_off());
       const int e = lane;
+      const int nv = hdr[32];
       const int ga = hdr[e];  // Gamma row block (valid edges; 0 for the padding rows)
       const unsigned char* gb = st + F::g_off() + (size_t)ga * DSH * 128;
       static_for<NO>([&](auto O) {
         constexpr int o = decltype(O)::value;
         constexpr int D3 = F::dim(o);
         constexpr int B0 = F::base(o);
-        const int m3 = (warp - B0 + 4) & 3;
+        const int m3 = (qw - B0 + 4) & 3;
         static_for<F::nto(o)>([&](auto P) {
           constexpr int pl = decltype(P)::value;
           constexpr int q = F::path_of(o, pl);
@@ -234,12 +258,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
           constexpr int D1 = 2 * L1 + 1, D2 = 2 * L2 + 1;
           mbar_wait(a_empty + j, aph ^ 1);
           if (m3 < D3) {
-            float acc[32];
+            float acc[8];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+            for (int c = 0; c < 8; ++c) acc[c] = 0.f;
             static_for<D3>([&](auto M3) {
               constexpr int mm3 = decltype(M3)::value;
-              if (m3 == mm3) {
+              if (m3 == mm3 && !(p.diag & 4)) {
                 static_for<D1 * D2>([&](auto I) {
                   constexpr int m1 = decltype(I)::value / D2, m2 = decltype(I)::value % D2;
                   constexpr float cf = (float)(csqrt(2.0 * LO + 1.0) * W3j<L1, L2, LO>::t.v[(m1 * D2 + m2) * (2 * LO + 1) + mm3]);
@@ -250,26 +274,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
                       const float yv = reinterpret_cast<const float*>(st + F::y_off())[e * DSH + mv];
                       const unsigned char* vrow = st + lm_l(mv) * kBoxBytes + e * 128;
 #pragma unroll
-                      for (int c4 = 0; c4 < 8; ++c4) {
+                      for (int h = 0; h < 2; ++h) {
+                        const int c4 = 2 * cg + h;
                         const float4 v = *reinterpret_cast<const float4*>(vrow + ((c4 ^ (e & 7)) << 4));
                         const float4 g = *reinterpret_cast<const float4*>(grow + (c4 << 4));
-                        acc[4 * c4 + 0] = fmaf(cf * (v.x * yv), g.x, acc[4 * c4 + 0]);
-                        acc[4 * c4 + 1] = fmaf(cf * (v.y * yv), g.y, acc[4 * c4 + 1]);
-                        acc[4 * c4 + 2] = fmaf(cf * (v.z * yv), g.z, acc[4 * c4 + 2]);
-                        acc[4 * c4 + 3] = fmaf(cf * (v.w * yv), g.w, acc[4 * c4 + 3]);
+                        acc[4 * h + 0] = fmaf(cf * (v.x * yv), g.x, acc[4 * h + 0]);
+                        acc[4 * h + 1] = fmaf(cf * (v.y * yv), g.y, acc[4 * h + 1]);
+                        acc[4 * h + 2] = fmaf(cf * (v.z * yv), g.z, acc[4 * h + 2]);
+                        acc[4 * h + 3] = fmaf(cf * (v.w * yv), g.w, acc[4 * h + 3]);
                       }
                     } else {
                       constexpr int ii = A.in.index(A.path[q].a);
                       const int r = e * D1 + m1;
                       const unsigned char* vrow = st + F::v_off(ii) + r * 128;
 #pragma unroll
-                      for (int c4 = 0; c4 < 8; ++c4) {
+                      for (int h = 0; h < 2; ++h) {
+                        const int c4 = 2 * cg + h;
                         const float4 v = *reinterpret_cast<const float4*>(vrow + ((c4 ^ (r & 7)) << 4));
                         const float4 g = *reinterpret_cast<const float4*>(grow + (c4 << 4));
-                        acc[4 * c4 + 0] = fmaf(cf * v.x, g.x, acc[4 * c4 + 0]);
-                        acc[4 * c4 + 1] = fmaf(cf * v.y, g.y, acc[4 * c4 + 1]);
-                        acc[4 * c4 + 2] = fmaf(cf * v.z, g.z, acc[4 * c4 + 2]);
-                        acc[4 * c4 + 3] = fmaf(cf * v.w, g.w, acc[4 * c4 + 3]);
+                        acc[4 * h + 0] = fmaf(cf * v.x, g.x, acc[4 * h + 0]);
+                        acc[4 * h + 1] = fmaf(cf * v.y, g.y, acc[4 * h + 1]);
+                        acc[4 * h + 2] = fmaf(cf * v.z, g.z, acc[4 * h + 2]);
+                        acc[4 * h + 3] = fmaf(cf * v.w, g.w, acc[4 * h + 3]);
                       }
                     }
                   }
@@ -277,34 +303,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
               }
             });
             if constexpr (F::scalar(o)) {
-              if (m3 == 0) {  // s = the scalar paths of T, [E][n_s 32]: one [32 e x 32 c] box per path
-                unsigned char* box = sbuf + sb * kBoxBytes;
-                if (lane == 0) bulk_wait_read1();  // the box used two stores ago has been read
-                __syncwarp();
-#pragma unroll
-                for (int c4 = 0; c4 < 8; ++c4)
-                  *reinterpret_cast<float4*>(box + e * 128 + ((c4 ^ (e & 7)) << 4)) =
-                      make_float4(acc[4 * c4], acc[4 * c4 + 1], acc[4 * c4 + 2], acc[4 * c4 + 3]);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) {
-                  tma_store_2d(&maps.s, 32 * pl, (int)e0, box);
-                  bulk_commit();
-                }
-                sb ^= 1;
+              // s = the scalar paths of T, [E][n_s 32]: this thread's 8 channels (32 B) of row e0 + e
+              if (m3 == 0 && e < nv && !(p.diag & 16)) {
+                float4* dst = reinterpret_cast<float4*>(p.s + (e0 + e) * (A.n_s * 32) + pl * 32 + 8 * cg);
+                __stcs(dst, make_float4(acc[0], acc[1], acc[2], acc[3]));
+                __stcs(dst + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
               }
             }
-            uint32_t hi[32], lo[32];
+            uint32_t hi[8], lo[8];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
+            for (int c = 0; c < 8; ++c) {
               const uint32_t h = __float_as_uint(acc[c]) & 0xffffe000u;
               hi[c] = h;
               lo[c] = __float_as_uint(acc[c] - __uint_as_float(h));
             }
             tc_fence_after();
-            const uint32_t ta = tmem_a + (uint32_t)(j * kATm) + ((uint32_t)(warp * 32) << 16);
-            tmem_st32(ta, hi);
-            tmem_st32(ta + 32, lo);
+            const uint32_t ta = tmem_a + (uint32_t)(j * kATm + 8 * cg) + ((uint32_t)(qw * 32) << 16);
+            tmem_st8(ta, hi);
+            tmem_st8(ta + 32, lo);
             tmem_st_wait();
           }
           tc_fence_before();
@@ -319,8 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
       if (lane == 0) mbar_arrive(in_empty + s);
       if (++s == p.stages) s = 0, ph ^= 1;
     }
-    if (lane == 0) bulk_wait0();
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer ----------------
     mbar_wait(w_full, 0);
     tc_fence_after();
@@ -347,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
           const uint32_t ahi = tmem_a + (uint32_t)(j * kATm), alo = ahi + 32;
           const uint64_t dkb = desc_o + (uint64_t)((pl * 2 * wblk) >> 4);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < 4 && !(p.diag & 32); ++k) {
             const uint64_t dwh = dkb + (uint64_t)(k * 2);
             const uint64_t dwl = dwh + (uint64_t)(wblk >> 4);
             mma_tf32_ts_w(L, d, ahi + 8 * k, dwl, idesc, (pl | k) ? 1u : 0u);
@@ -362,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
     }
   } else {
     // ---------------- epilogue (warps 4-7): D -> V^{k+1} ----------------
-    const int qd = warp & 3;  // TMEM lane quarter
+    const int qd = warp & 3;  // TMEM lane quarter (warps 16-19)
     int n_st = 0;
     for (int t = 0; t < n_my; ++t) {
       const int64_t e0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kTile;
@@ -388,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
                 make_float4(sc * v[4 * c4], sc * v[4 * c4 + 1], sc * v[4 * c4 + 2], sc * v[4 * c4 + 3]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && !(p.diag & 8)) {
             tma_store_3d(&maps.out[o], 0, m3, (int)e0, box);
             bulk_commit();
           }
@@ -402,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
     if (lane == 0) bulk_wait0();
   }
   __syncthreads();
-  if (warp == 9) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -424,7 +439,9 @@ void launch(const TplIO& io, cudaStream_t st, Profiler* prof) {
   p.cidx = io.cidx;
   p.G = io.G;
   p.Y = io.Y;
+  p.s = io.s;
   p.n_tiles = (int)((E + kTile - 1) / kTile);
+  if (const char* d = std::getenv("ALLEGRO_TPL_DIAG")) p.diag = std::atoi(d);
   uint32_t wsum = 0;
   for (int o = 0; o < F::NO; ++o) {
     p.wimg[o] = io.wimg[o];
@@ -450,13 +467,15 @@ void launch(const TplIO& io, cudaStream_t st, Profiler* prof) {
       maps.in[i] = tc_map_f32(io.vin[i], 2, dims, strides, box);
     }
   }
-  {
-    const uint64_t dims[2] = {(uint64_t)A.n_s * 32, (uint64_t)E};
-    const uint64_t strides[1] = {(uint64_t)A.n_s * 128};
-    const uint32_t box[2] = {32, 32};
-    maps.s = tc_map_f32(io.s, 2, dims, strides, box);
+  if (std::getenv("ALLEGRO_SYNC_CHECK")) {
+    std::fprintf(stderr, "[tpl_fwd K=%d] E=%lld e0g=%lld a0=%lld n_c=%lld G=%p Y=%p w=%p s=%p\n", K, (long long)E,
+                 (long long)io.ch.e0, (long long)io.ch.a0, (long long)io.ch.n_c, (const void*)io.G, (const void*)io.Y,
+                 (const void*)io.w, (void*)io.s);
+    for (int i = 0; i < F::NI; ++i) std::fprintf(stderr, "  vin[%d]=%p rows=%d\n", i, (const void*)io.vin[i], F::in_rows(i));
+    for (int o = 0; o < F::NO; ++o)
+      std::fprintf(stderr, "  vout[%d]=%p wimg=%p wbytes=%zu\n", o, (void*)io.vout[o], (const void*)io.wimg[o], io.wbytes[o]);
   }
-  const size_t fixed = 1024 + ((wsum + 1023) / 1024) * 1024 + 8 * kBoxBytes + 2 * kBoxBytes + 512;
+  const size_t fixed = 1024 + ((wsum + 1023) / 1024) * 1024 + 8 * kBoxBytes + 512;
   int stages = (int)std::min<size_t>(4, (kSmemLimit - fixed) / F::stage_bytes());
   if (stages < 2) throw CudaError("tpl_fwd: shared memory too small for two input stages");
   p.stages = stages;
@@ -487,6 +506,11 @@ void launch(const TplIO& io, cudaStream_t st, Profiler* prof) {
     k_tpl_fwd<NL, LMAX, K><<<grid, kThreads, smem, st>>>(maps, p);
   }
   ALG_LAUNCH_CHECK();
+  if (std::getenv("ALLEGRO_SYNC_CHECK")) {  // diagnostics: attribute a fault to this launch
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess)
+      throw CudaError(std::string("k_tpl_fwd layer ") + std::to_string(K) + ": " + cudaGetErrorString(e));
+  }
 }
 
 }  // namespace
