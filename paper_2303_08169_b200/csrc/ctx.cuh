@@ -103,7 +103,7 @@ struct Workspace {
   DBuf<float> xa, xb;
   DBuf<float> w[kMaxLayers], h[kMaxLayers], V[kMaxLayers], G[kMaxLayers];
   DBuf<float> T;
-  DBuf<float> xbar_a, xbar_b, sbar, vbar_a, vbar_b, wbar, ybar, ubar, zbar, ab2, ab1, ee, ebar;
+  DBuf<float> xbar_a, xbar_b, sbar, vbar_a, vbar_b, wbar, ybar, ubar, zbar, ab2, ab1, ee, ebar, gp;
 };
 
 // Spatial domain decomposition (§2.4).

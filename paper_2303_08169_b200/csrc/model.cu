@@ -147,6 +147,7 @@ struct TpArgs {
   float* Vb;           // backward: V-bar store of layer K (K >= 1)
   float* wbar;         // backward: [E][NW]
   float* ybar;         // backward: [E][DSH] accumulated
+  const float* gp;     // fused backward: [E][DSH][C] per-edge Gamma-bar terms
   int64_t e_cap;
   float inv_sqrt_nbar;
 };
@@ -384,6 +385,41 @@ __device__ __forceinline__ void fetch_bwd(const TpArgs& t, int64_t e, int lane, 
   if constexpr (K == 0) in.yb_old = owns_total<AR::DSH>(lane, mm) ? t.ybar[e * AR::DSH + mm] : 0.f;
 }
 
+// environment adjoint of one CSR row: w_env-bar and Y-bar from the complete Gamma-bar_i
+template <int NL, int LMAX, int K>
+__device__ __forceinline__ void env_adjoint(const TpArgs& t, int64_t r0, int64_t r1, int lane, int mm,
+                                            const float (&Gb)[Arch<NL, LMAX, K>::DSH]) {
+  using AR = Arch<NL, LMAX, K>;
+  struct EnvB {
+    EnvIn<NL, LMAX, K> env;
+    float yb_old;
+  };
+  auto fetch_envb = [&](int64_t e, EnvB& in) {
+    fetch_env<NL, LMAX, K>(t, e, lane, in.env);
+    in.yb_old = owns_total<AR::DSH>(lane, mm) ? t.ybar[e * AR::DSH + mm] : 0.f;
+  };
+  EnvB en;
+  fetch_envb(r0, en);
+  for (int64_t e = r0; e < r1; ++e) {
+    const EnvB cur = en;
+    fetch_envb(e + 1 < r1 ? e + 1 : e, en);
+    float wb[AR::NENV];
+#pragma unroll
+    for (int l = 0; l < AR::NENV; ++l) wb[l] = 0.f;
+    float prod[AR::DSH];
+#pragma unroll
+    for (int m = 0; m < AR::DSH; ++m) {
+      wb[lm_l(m)] = fmaf(Gb[m], cur.env.y[m], wb[lm_l(m)]);
+      prod[m] = Gb[m] * cur.env.we[lm_l(m)];
+    }
+    int mq;
+    const float s = warp_sum_multi<AR::DSH>(prod, lane, &mq);
+#pragma unroll
+    for (int l = 0; l < AR::NENV; ++l) t.wbar[e * AR::NW + AR::ENV_OFF + l * kC + lane] = t.inv_sqrt_nbar * wb[l];
+    if (owns_total<AR::DSH>(lane, mm)) t.ybar[e * AR::DSH + mm] = cur.yb_old + t.inv_sqrt_nbar * s;
+  }
+}
+
 template <int NL, int LMAX, int K>
 __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
   using AR = Arch<NL, LMAX, K>;
@@ -459,35 +495,35 @@ __global__ void __launch_bounds__(128) k_tp_bwd(TpArgs t) {
       });
     }
   }
-  // environment adjoint: w_env-bar and Ybar from Gamma-bar
-  struct EnvB {
-    EnvIn<NL, LMAX, K> env;
-    float yb_old;
-  };
-  auto fetch_envb = [&](int64_t e, EnvB& in) {
-    fetch_env<NL, LMAX, K>(t, e, lane, in.env);
-    in.yb_old = owns_total<AR::DSH>(lane, mm) ? t.ybar[e * AR::DSH + mm] : 0.f;
-  };
-  EnvB en;
-  fetch_envb(r0, en);
-  for (int64_t e = r0; e < r1; ++e) {
-    const EnvB cur = en;
-    fetch_envb(e + 1 < r1 ? e + 1 : e, en);
-    float wb[AR::NENV];
+  env_adjoint<NL, LMAX, K>(t, r0, r1, lane, mm, Gb);
+}
+
+// Fused backward path (tp_fused.cu): Gamma-bar_i = sum over the row, in edge order, of the
+// per-edge terms gp that k_tpl_bwd wrote, then the environment adjoint of the row.
+template <int NL, int LMAX, int K>
+__global__ void __launch_bounds__(128) k_env_adj(TpArgs t) {
+  using AR = Arch<NL, LMAX, K>;
+  const int lane = threadIdx.x & 31;
+  const int64_t ii = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ii >= t.ch.n_c) return;
+  const int64_t r0 = t.row_ptr[t.ch.a0 + ii] - t.ch.e0, r1 = t.row_ptr[t.ch.a0 + ii + 1] - t.ch.e0;
+  if (r1 <= r0) return;
+  constexpr int LP = AR::DSH <= 1 ? 0 : AR::DSH <= 2 ? 1 : AR::DSH <= 4 ? 2 : AR::DSH <= 8 ? 3 : 4;
+  const int mm = lane >> (5 - LP);
+  float Gb[AR::DSH], nx[AR::DSH];
 #pragma unroll
-    for (int l = 0; l < AR::NENV; ++l) wb[l] = 0.f;
-    float prod[AR::DSH];
+  for (int m = 0; m < AR::DSH; ++m) Gb[m] = 0.f, nx[m] = t.gp[(r0 * AR::DSH + m) * kC + lane];
+  for (int64_t e = r0; e < r1; ++e) {  // pipelined one edge ahead
+    float cur[AR::DSH];
 #pragma unroll
-    for (int m = 0; m < AR::DSH; ++m) {
-      wb[lm_l(m)] = fmaf(Gb[m], cur.env.y[m], wb[lm_l(m)]);
-      prod[m] = Gb[m] * cur.env.we[lm_l(m)];
-    }
-    int mq;
-    const float s = warp_sum_multi<AR::DSH>(prod, lane, &mq);
+    for (int m = 0; m < AR::DSH; ++m) cur[m] = nx[m];
+    const int64_t en = e + 1 < r1 ? e + 1 : e;
 #pragma unroll
-    for (int l = 0; l < AR::NENV; ++l) t.wbar[e * AR::NW + AR::ENV_OFF + l * kC + lane] = t.inv_sqrt_nbar * wb[l];
-    if (owns_total<AR::DSH>(lane, mm)) t.ybar[e * AR::DSH + mm] = cur.yb_old + t.inv_sqrt_nbar * s;
+    for (int m = 0; m < AR::DSH; ++m) nx[m] = t.gp[(en * AR::DSH + m) * kC + lane];
+#pragma unroll
+    for (int m = 0; m < AR::DSH; ++m) Gb[m] += cur[m];
   }
+  env_adjoint<NL, LMAX, K>(t, r0, r1, lane, mm, Gb);
 }
 
 // ----------------------------------------------------------------- A10 energies
@@ -684,13 +720,27 @@ __global__ void k_force_warp(int64_t n, const int32_t* __restrict__ row_ptr, con
   double f[3] = {0, 0, 0};
   const int64_t r0 = row_ptr[a], r1 = row_ptr[a + 1];
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  for (int64_t e = r0 + lane; e < r1; e += 32) {
-    const int32_t r = rev[e];
-    const float4 a4 = g4[e];
-    const float4 b4 = r >= 0 ? g4[r] : make_float4(0.f, 0.f, 0.f, 0.f);
-    f[0] += (double)a4.x - (double)b4.x;
-    f[1] += (double)a4.y - (double)b4.y;
-    f[2] += (double)a4.z - (double)b4.z;
+  // Four edges per lane per round: all reverse indices, then all 16-B gathers in flight before the
+  // first use (each lane still adds its edges in the order r0 + lane, + 32, + 64, ...).
+  for (int64_t base = r0; base < r1; base += 128) {
+    int32_t rr[4];
+    float4 a4[4], b4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = base + lane + 32 * k;
+      rr[k] = e < r1 ? __ldg(rev + e) : -1;
+      a4[k] = e < r1 ? __ldg(g4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) b4[k] = rr[k] >= 0 ? __ldg(g4 + rr[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (base + lane + 32 * k < r1) {
+        f[0] += (double)a4[k].x - (double)b4[k].x;
+        f[1] += (double)a4[k].y - (double)b4[k].y;
+        f[2] += (double)a4[k].z - (double)b4[k].z;
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
@@ -716,21 +766,25 @@ void launch_tp(int mode, const TpArgs& t, cudaStream_t st, Profiler* prof, doubl
   if (blocks == 0) return;
   {
     char tag[48];
-    std::snprintf(tag, sizeof(tag), "%s layer=%d", mode == 0 ? "tp_fwd" : mode == 1 ? "tp_bwd" : "gamma", K);
-    ProfScope ps_(prof, st, mode == 0 ? PK_TP_FWD : mode == 1 ? PK_TP_BWD : PK_GAMMA, flops, bytes, tag);
+    static const char* names[4] = {"tp_fwd", "tp_bwd", "gamma", "env_adj"};
+    static const int kinds[4] = {PK_TP_FWD, PK_TP_BWD, PK_GAMMA, PK_ENV_ADJ};
+    std::snprintf(tag, sizeof(tag), "%s layer=%d", names[mode], K);
+    ProfScope ps_(prof, st, kinds[mode], flops, bytes, tag);
     if (mode == 0) k_tp_fwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
     else if (mode == 1) k_tp_bwd<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
-    else k_tp_fwd<NL, LMAX, K, true><<<blocks, 128, 0, st>>>(t);
+    else if (mode == 2) k_tp_fwd<NL, LMAX, K, true><<<blocks, 128, 0, st>>>(t);
+    else k_env_adj<NL, LMAX, K><<<blocks, 128, 0, st>>>(t);
   }
   ALG_LAUNCH_CHECK();
-  if (mode == 2 && std::getenv("ALLEGRO_SYNC_CHECK")) ALG_CUDA(cudaStreamSynchronize(st));
+  if (mode >= 2 && std::getenv("ALLEGRO_SYNC_CHECK")) ALG_CUDA(cudaStreamSynchronize(st));
 }
 
 // Algorithmic work of the TP kernels per edge: forward = Gamma sum
 // (DSH FMA) + TP (nnz FMA) per channel; backward = 2 nnz FMA + env adjoint.  Bytes:
 // the per-edge operands the method reads/writes once (w, Y, V in; T out / T-bar, V,
 // w, Y in; w-bar, Y-bar, V-bar out), fp32.
-// mode 0: TP forward (Gamma + T), 1: TP backward, 2: Gamma only (the fused path)
+// mode 0: TP forward (Gamma + T), 1: TP backward, 2: Gamma only, 3: Gamma-bar row sums + environment
+// adjoint (2 and 3: the fused path of tp_fused.cu)
 void tp_dispatch(int NL, int LMAX, int K, int mode, const TpArgs& t, cudaStream_t st, Profiler* prof,
                  const LayerInfo& L) {
   const double E = (double)t.ch.n_e;
@@ -739,10 +793,12 @@ void tp_dispatch(int NL, int LMAX, int K, int mode, const TpArgs& t, cudaStream_
   const double nenv = LMAX + 1;
   const double flops = mode == 0   ? E * kC * 2.0 * (L.tp_nnz + dsh)
                        : mode == 1 ? E * kC * 2.0 * (2.0 * L.tp_nnz + 2 * dsh)
-                                   : E * kC * 2.0 * dsh;
+                       : mode == 2 ? E * kC * 2.0 * dsh
+                                   : E * kC * (dsh + 4.0 * dsh);
   const double bytes = mode == 0   ? 4.0 * E * (L.nw + dsh + vin + (double)L.A.dim_T * kC)
                        : mode == 1 ? 4.0 * E * ((double)L.A.dim_T * kC + 2.0 * vin + 2.0 * L.nw + 2.0 * dsh)
-                                   : 4.0 * E * (nenv * kC + dsh) + 4.0 * t.ch.n_c * dsh * kC;
+                       : mode == 2 ? 4.0 * E * (nenv * kC + dsh) + 4.0 * t.ch.n_c * dsh * kC
+                                   : 4.0 * E * (dsh * kC + 2.0 * nenv * kC + 3.0 * dsh);
 #define ALG_TP(nl, lm, k) \
   if (NL == nl && LMAX == lm && K == k) return launch_tp<nl, lm, k>(mode, t, st, prof, flops, bytes);
   ALG_TP(2, 1, 0) ALG_TP(2, 1, 1)
@@ -829,6 +885,7 @@ size_t floats_per_edge(const Model& M) {
     nsmax = std::max(nsmax, (size_t)L.A.n_s * kC);
   }
   f += tmax + 2 * 128 + nsmax + 2 * vmax + nwmax + dsh + 1 + 64 + 32 + 1;
+  f += dsh * kC;  // gp (fused backward)
   return f;
 }
 
@@ -867,6 +924,7 @@ void reserve_ws(allegro_ctx* c, size_t e_cap, size_t a_cap) {
   w.ab2.reserve(e_cap * 64);
   w.ab1.reserve(e_cap * 32);
   w.ebar.reserve(e_cap);
+  w.gp.reserve(e_cap * dsh * kC);
   w.e_cap = e_cap;
   w.a_cap = a_cap;
 }
@@ -1032,7 +1090,35 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     tp.wbar = w.wbar.p;
     tp.ybar = w.ybar.p;
     tp.Vb = vbn;
-    if (k == M.n_layers - 1) {
+    const char* fb_env = std::getenv("ALLEGRO_FUSED_TP_BWD");  // A/B switch (bit k: fuse layer k)
+    const int fb_mask = fb_env ? std::atoi(fb_env) : -1;
+    const bool fused_bwd = ((fb_mask >> k) & 1) && M.precision == ALLEGRO_PREC_3XTF32 &&
+                           tpl_fwd_supported(M.n_layers, M.lmax, k);
+    if (fused_bwd) {
+      TpbIO io;
+      io.ch = ch;
+      io.cidx = c->cidx.p;
+      io.G = w.G[k].p;
+      io.Y = w.Y.p;
+      io.w = w.w[k].p;
+      for (int i = 0; i < L.A.in.n; ++i) {
+        io.vin[i] = k >= 1 ? w.V[k].p + (int64_t)L.v_base[i] * ecap : nullptr;
+        io.vbar_out[i] = k >= 1 ? vbn + (int64_t)L.v_base[i] * ecap : nullptr;
+      }
+      for (int o = 0; o < L.A.out.n; ++o) {
+        io.vbar_in[o] = vb + (int64_t)M.L[k + 1].v_base[o] * ecap;
+        io.wimg[o] = M.w.linT[k][o].tc.dev;
+        io.wbytes[o] = M.w.linT[k][o].tc.tile_bytes;
+      }
+      io.sbar = w.sbar.p;
+      io.wbar = w.wbar.p;
+      io.ybar = w.ybar.p;
+      io.gp = w.gp.p;
+      io.tp_fma_per_edge = (double)L.tp_nnz * kC;
+      tpl_bwd(M.n_layers, M.lmax, k, io, st, &c->prof);
+      tp.gp = w.gp.p;
+      tp_dispatch(M.n_layers, M.lmax, k, 3, tp, st, &c->prof, L);  // Gamma-bar + environment adjoint
+    } else if (k == M.n_layers - 1) {
       tp.Tb[0] = w.sbar.p;  // last layer: out = {0e}, T-bar = s-bar
     } else {
       for (int o = 0; o < L.A.out.n; ++o) {
@@ -1049,7 +1135,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
         tp.Tb[o] = dst;
       }
     }
-    tp_dispatch(M.n_layers, M.lmax, k, 1, tp, st, &c->prof, L);
+    if (!fused_bwd) tp_dispatch(M.n_layers, M.lmax, k, 1, tp, st, &c->prof, L);
     {
       GemmArgs g = G(w.wbar.p, L.nw, M.w.envT[k], 128, L.nw, xbn, 1.f / std::sqrt(128.f), last ? EPI_R2 : EPI_ACC);
       if (last) {  // xbar^{L-1} = env^T part + Ebar (a w_out + u (b/sqrt(fan)) q_x)

@@ -31,12 +31,14 @@ enum ProfKind : int {
   PK_HALO,
   PK_GAMMA,     // environment sums Gamma_i (fused path)
   PK_TPL_FWD,   // fused TP + TP-linear (tcgen05), forward
+  PK_TPL_BWD,   // fused TP-linear^T + TP adjoint (tcgen05), backward
+  PK_ENV_ADJ,   // Gamma-bar row sums + environment adjoint (fused path)
   PK_COUNT
 };
 
 inline const char* prof_name(int k) {
   static const char* names[PK_COUNT] = {"wrap", "ghost", "cell", "edge_build", "scan", "geom", "gemm", "tp_fwd",
-                                        "tp_bwd", "energy", "rowdot", "geom_bwd", "force_gather", "verlet", "reduce", "halo", "gamma", "tp_lin_fwd"};
+                                        "tp_bwd", "energy", "rowdot", "geom_bwd", "force_gather", "verlet", "reduce", "halo", "gamma", "tp_lin_fwd", "tp_lin_bwd", "env_adj"};
   return (k >= 0 && k < PK_COUNT) ? names[k] : "?";
 }
 

@@ -111,7 +111,8 @@ struct Fz {
   static constexpr int wv_bytes() { return K == 0 ? AR::NENV * kBoxBytes : v_off(NI); }
   static constexpr int y_off() { return wv_bytes(); }
   static constexpr int g_off() { return y_off() + (K == 0 ? kTile * DSH * 4 : 0); }
-  static constexpr int g_bytes() { return kTile * DSH * 128; }  // at most one centre per edge
+  static constexpr int GA = 32;  // Gamma rows staged per tile (atoms); a wider span reads the rest from L2
+  static constexpr int g_bytes() { return GA * DSH * 128; }
   static constexpr int h_off() { return g_off() + g_bytes(); }
   static constexpr int stage_bytes() { return (h_off() + 256 + 1023) / 1024 * 1024; }
   static constexpr int acc_cols() { return NO * 32; }
@@ -204,10 +205,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
       const int a_lo = __shfl_sync(0xffffffffu, ci, 0);
       const int a_hi = __shfl_sync(0xffffffffu, ci, nv - 1);
       hdr[lane] = lane < nv ? ci - a_lo : 0;  // Gamma row block of this edge's centre
-      if (lane == 0) hdr[32] = nv;
+      if (lane == 0) hdr[32] = nv, hdr[33] = a_lo;
       __syncwarp();
       if (lane == 0) {
-        const uint32_t gbytes = (uint32_t)(a_hi - a_lo + 1) * DSH * 128;
+        const int span = a_hi - a_lo + 1;
+        const uint32_t gbytes = (uint32_t)(span < F::GA ? span : F::GA) * DSH * 128;
         uint32_t bytes = (p.diag & 1) ? 0u : gbytes;
         if (!(p.diag & 2)) {
           if constexpr (K == 0) bytes += AR::NENV * kBoxBytes + (uint32_t)nv * DSH * 4;
@@ -245,7 +247,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
       const int e = lane;
       const int nv = hdr[32];
       const int ga = hdr[e];  // Gamma row block (valid edges; 0 for the padding rows)
-      const unsigned char* gb = st + F::g_off() + (size_t)ga * DSH * 128;
+      // staged rows, or (a tile spanning more than GA atoms: atoms without edges in between) L2
+      const unsigned char* gb = ga < F::GA ? st + F::g_off() + (size_t)ga * DSH * 128
+                                           : reinterpret_cast<const unsigned char*>(p.G + (int64_t)(hdr[33] + ga) * DSH * 32);
       static_for<NO>([&](auto O) {
         constexpr int o = decltype(O)::value;
         constexpr int D3 = F::dim(o);
@@ -513,9 +517,517 @@ void launch(const TplIO& io, cudaStream_t st, Profiler* prof) {
   }
 }
 
+// ====================================================================== backward
+// One layer k < L-1, per 32-edge tile:
+//   T-bar_o = V-bar^{k+1}_o W_o^T / sqrt(C n_{->o})  (+ s-bar on the scalar paths)    tcgen05 (3xTF32)
+//   then per edge (warp per edge, lane = channel) the TP adjoint of k_tp_bwd (model.cu):
+//   V-bar^k (k >= 1) or w-bar_edge and Y-bar (k = 0), and the edge's term of Gamma-bar_i (to HBM;
+//   k_env_adj sums it over the row in edge order and applies the environment adjoint).
+// T-bar never reaches HBM.  Warp roles (704 threads):
+//   warps 0-11  TP adjoint (lane = channel) from the T-bar tile in SMEM and the tile's inputs
+//   warps 12-15 split: V-bar rows (TMA boxes, one per (o, m3)) -> TF32 hi / lo -> TMEM A stage
+//   warps 16-19 T-bar copy: tcgen05.ld of D (thread = row), scale, + s-bar, -> SMEM tile
+//   warp 20     producer (TMA / bulk loads), warp 21 TMEM allocator + MMA issuer
+constexpr int kBTp = 12;
+constexpr int kBSplit0 = kBTp;
+constexpr int kBCopy0 = kBTp + 4;
+constexpr int kBProd = kBTp + 8;
+constexpr int kBMma = kBTp + 9;
+constexpr int kBThreads = 32 * (kBTp + 10);
+constexpr int kBAStages = 3;
+constexpr int kBGA = 8;  // Gamma rows staged per tile (atoms); wider spans read from L2
+
+template <int NL, int LMAX, int K>
+struct Bz {
+  using F = Fz<NL, LMAX, K>;
+  using AR = Arch<NL, LMAX, K>;
+  static constexpr LayerArch A = AR::A;
+  static constexpr int NO = A.out.n, NI = A.in.n, DSH = AR::DSH, DT = A.dim_T, DIN = A.dim_in;
+  static constexpr int col_off(int o) {
+    int b = 0;
+    for (int q = 0; q < o; ++q) b += A.n_to[q] * 32;
+    return b;
+  }
+  static constexpr int acc_cols() { return col_off(NO); }
+  static constexpr int vb_off(int o) {
+    int b = 0;
+    for (int q = 0; q < o; ++q) b += ir_dim(A.out.v[q]) * kBoxBytes;
+    return b;
+  }
+  static constexpr int sb_off() { return vb_off(NO); }
+  static constexpr int in_off() { return sb_off() + A.n_s * kBoxBytes; }
+  static constexpr int v_off(int i) { return in_off() + F::v_off(i); }
+  static constexpr int y_off() { return in_off() + AR::NENV * kBoxBytes; }
+  static constexpr int g_off() { return K == 0 ? y_off() + kTile * DSH * 4 : in_off() + F::v_off(NI); }
+  static constexpr int h_off() { return g_off() + kBGA * DSH * 128; }
+  static constexpr int stage_bytes() { return (h_off() + 256 + 1023) / 1024 * 1024; }
+  static constexpr int tb_bytes() { return kTile * DT * 128; }
+  static constexpr int tma_bytes() { return in_off() + (K == 0 ? AR::NENV * kBoxBytes : F::v_off(NI)); }
+};
+
+template <int NL, int LMAX, int K>
+constexpr double DSH_bytes() { return 2.0 * Arch<NL, LMAX, K>::DSH * 4; }
+
+struct TpbParams {
+  int64_t n_e, e0g, a0;
+  const int32_t* cidx;
+  const float* G;
+  const float* Y;
+  float* vbo[kMaxIr];  // V-bar^k per in irrep (k >= 1)
+  float* wbar;         // [E][NW] (k = 0: the w_edge columns)
+  float* ybar;         // [E][DSH] (k = 0)
+  float* gp;           // [E][DSH][C]
+  const float* wimg[kMaxIr];
+  uint32_t wbytes[kMaxIr];
+  float scale[kMaxIr];
+  int n_tiles, stages;
+};
+
+struct TpbMaps {
+  CUtensorMap vb[kMaxIr];  // V-bar^{k+1} per out irrep, 3-D [E][dim][32], box [32 e][1][32 c]
+  CUtensorMap sb;          // s-bar [E][n_s 32], box [32 e][32 c]
+  CUtensorMap in[kMaxIr];  // V^k per in irrep (k >= 1) or w [E][NW] (k = 0, in[0])
+};
+
+template <int NL, int LMAX, int K>
+__global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant__ TpbMaps maps, const TpbParams p) {
+  using B = Bz<NL, LMAX, K>;
+  using F = Fz<NL, LMAX, K>;
+  using AR = Arch<NL, LMAX, K>;
+  constexpr LayerArch A = B::A;
+  constexpr int NO = B::NO, DSH = B::DSH, DT = B::DT, DIN = B::DIN;
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  unsigned char* base = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
+  uint32_t woff[kMaxIr + 1];
+  woff[0] = 0;
+#pragma unroll
+  for (int o = 0; o < kMaxIr; ++o) woff[o + 1] = woff[o] + (o < NO ? p.wbytes[o] : 0u);
+  unsigned char* w_img = base;
+  unsigned char* stage0 = base + ((woff[NO] + 1023u) & ~1023u);
+  unsigned char* tbt = stage0 + (size_t)p.stages * B::stage_bytes();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tbt + B::tb_bytes());
+  uint64_t* in_full = bars;
+  uint64_t* in_empty = in_full + 4;
+  uint64_t* a_full = in_empty + 4;
+  uint64_t* a_empty = a_full + kBAStages;
+  uint64_t* acc_full = a_empty + kBAStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* tb_full = acc_empty + 2;
+  uint64_t* tb_empty = tb_full + 1;
+  uint64_t* w_full = tb_empty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) mbar_init(in_full + s, 1), mbar_init(in_empty + s, kBTp + 8);
+    for (int s = 0; s < kBAStages; ++s) mbar_init(a_full + s, 4), mbar_init(a_empty + s, 1);
+    for (int b = 0; b < 2; ++b) mbar_init(acc_full + b, 1), mbar_init(acc_empty + b, 4);
+    mbar_init(tb_full, 4);
+    mbar_init(tb_empty, kBTp);
+    mbar_init(w_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kBMma) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_a = tmem + 2u * B::acc_cols();
+  const int n_my = p.n_tiles > (int)blockIdx.x ? (p.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto tile_e0 = [&](int t) -> int64_t { return (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kTile; };
+
+  if (warp == kBProd) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      mbar_expect_tx(w_full, woff[NO]);
+      for (int o = 0; o < NO; ++o) bulk_load(w_img + woff[o], p.wimg[o], p.wbytes[o], w_full);
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    auto load_ci = [&](int t) -> int {
+      const int64_t e0 = tile_e0(t);
+      return (t < n_my && e0 + lane < p.n_e) ? __ldg(p.cidx + p.e0g + e0 + lane) - (int)p.a0 : 0;
+    };
+    int ci_next = load_ci(0);
+    for (int t = 0; t < n_my; ++t) {
+      const int64_t e0 = tile_e0(t);
+      const int nv = (int)(p.n_e - e0 < kTile ? p.n_e - e0 : kTile);
+      const int ci = ci_next;
+      ci_next = load_ci(t + 1);
+      mbar_wait(in_empty + s, ph ^ 1);
+      unsigned char* st = stage0 + (size_t)s * B::stage_bytes();
+      int* hdr = reinterpret_cast<int*>(st + B::h_off());
+      const int a_lo = __shfl_sync(0xffffffffu, ci, 0);
+      const int a_hi = __shfl_sync(0xffffffffu, ci, nv - 1);
+      hdr[lane] = lane < nv ? ci - a_lo : 0;
+      if (lane == 0) hdr[32] = nv, hdr[33] = a_lo;
+      __syncwarp();
+      if (lane == 0) {
+        const int span = a_hi - a_lo + 1;
+        const uint32_t gbytes = (uint32_t)(span < kBGA ? span : kBGA) * DSH * 128;
+        uint32_t bytes = (uint32_t)B::tma_bytes() + gbytes + (K == 0 ? (uint32_t)nv * DSH * 4 : 0u);
+        mbar_expect_tx(in_full + s, bytes);
+        static_for<NO>([&](auto O) {
+          constexpr int o = decltype(O)::value;
+          static_for<ir_dim(A.out.v[o])>([&](auto M) {
+            constexpr int m = decltype(M)::value;
+            tma_load_3d(st + B::vb_off(o) + m * kBoxBytes, &maps.vb[o], 0, m, (int)e0, in_full + s);
+          });
+        });
+        for (int q = 0; q < A.n_s; ++q) tma_load_2d(st + B::sb_off() + q * kBoxBytes, &maps.sb, 32 * q, (int)e0, in_full + s);
+        if constexpr (K == 0) {
+#pragma unroll
+          for (int l = 0; l < AR::NENV; ++l) tma_load_2d(st + B::in_off() + l * kBoxBytes, &maps.in[0], 32 * l, (int)e0, in_full + s);
+          bulk_load(st + B::y_off(), p.Y + e0 * DSH, (uint32_t)nv * DSH * 4, in_full + s);
+        } else {
+          static_for<B::NI>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int dim = ir_dim(A.in.v[i]);
+            tma_load_2d(st + B::v_off(i), &maps.in[i], 0, (int)(e0 * dim), in_full + s);
+          });
+        }
+        bulk_load(st + B::g_off(), p.G + (int64_t)a_lo * DSH * 32, gbytes, in_full + s);
+      }
+      if (++s == p.stages) s = 0, ph ^= 1;
+    }
+  } else if (warp >= kBSplit0 && warp < kBSplit0 + 4) {
+    // ---------------- split: V-bar rows -> TF32 hi / lo in TMEM ----------------
+    const int qw = warp & 3;
+    int s = 0, j = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int t = 0; t < n_my; ++t) {
+      mbar_wait(in_full + s, ph);
+      const unsigned char* st = stage0 + (size_t)s * B::stage_bytes();
+      static_for<NO>([&](auto O) {
+        constexpr int o = decltype(O)::value;
+        constexpr int B0 = F::base(o);
+        const int m3 = (qw - B0 + 4) & 3;
+        mbar_wait(a_empty + j, aph ^ 1);
+        if (m3 < F::dim(o)) {
+          const unsigned char* row = st + B::vb_off(o) + m3 * kBoxBytes + lane * 128;
+          uint32_t hi[32], lo[32];
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 v = *reinterpret_cast<const float4*>(row + ((c4 ^ (lane & 7)) << 4));
+            const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t h = __float_as_uint(x[q]) & 0xffffe000u;
+              hi[4 * c4 + q] = h;
+              lo[4 * c4 + q] = __float_as_uint(x[q] - __uint_as_float(h));
+            }
+          }
+          tc_fence_after();
+          const uint32_t ta = tmem_a + (uint32_t)(j * kATm) + ((uint32_t)(qw * 32) << 16);
+          tmem_st32(ta, hi);
+          tmem_st32(ta + 32, lo);
+          tmem_st_wait();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full + j);
+        if (++j == kBAStages) j = 0, aph ^= 1;
+      });
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(in_empty + s);
+      if (++s == p.stages) s = 0, ph ^= 1;
+    }
+  } else if (warp == kBMma) {
+    // ---------------- MMA issuer: D_o = A_o W_o^T ----------------
+    mbar_wait(w_full, 0);
+    tc_fence_after();
+    __syncwarp();
+    const uint32_t L = elect_leader();
+    int j = 0;
+    uint32_t aph = 0;
+    for (int t = 0; t < n_my; ++t) {
+      const int buf = t & 1;
+      mbar_wait(acc_empty + buf, ((uint32_t)(t >> 1) & 1u) ^ 1u);
+      __syncwarp();
+      tc_fence_after();
+      static_for<NO>([&](auto O) {
+        constexpr int o = decltype(O)::value;
+        constexpr uint32_t N = (uint32_t)A.n_to[o] * 32;
+        constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        const uint32_t d = tmem + (uint32_t)(buf * B::acc_cols() + B::col_off(o));
+        const uint64_t desc_o = sdesc(smem_u32(w_img + woff[o]));
+        mbar_wait(a_full + j, aph);
+        __syncwarp();
+        tc_fence_after();
+        const uint32_t ahi = tmem_a + (uint32_t)(j * kATm), alo = ahi + 32;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t dwh = desc_o + (uint64_t)(k * 2);
+          const uint64_t dwl = dwh + (uint64_t)((N * 128) >> 4);
+          mma_tf32_ts_w(L, d, ahi + 8 * k, dwl, idesc, k ? 1u : 0u);
+          mma_tf32_ts_w(L, d, alo + 8 * k, dwh, idesc, 1u);
+          mma_tf32_ts_w(L, d, ahi + 8 * k, dwh, idesc, 1u);
+        }
+        mma_commit_w(L, a_empty + j);
+        if (++j == kBAStages) j = 0, aph ^= 1;
+      });
+      mma_commit_w(L, acc_full + buf);
+    }
+  } else if (warp >= kBCopy0 && warp < kBCopy0 + 4) {
+    // ---------------- T-bar copy: TMEM rows -> SMEM tile [e][t][c] (+ s-bar) ----------------
+    const int qw = warp & 3;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = 0; t < n_my; ++t) {
+      const int buf = t & 1;
+      mbar_wait(acc_full + buf, (uint32_t)(t >> 1) & 1u);
+      tc_fence_after();
+      mbar_wait(in_full + s, ph);                      // (complete: its s-bar boxes are read here)
+      mbar_wait(tb_empty, ((uint32_t)t & 1u) ^ 1u);    // the TP warps are done with the previous tile
+      const unsigned char* st = stage0 + (size_t)s * B::stage_bytes();
+      const int e = lane;
+      static_for<NO>([&](auto O) {
+        constexpr int o = decltype(O)::value;
+        constexpr int B0 = F::base(o);
+        const int m3 = (qw - B0 + 4) & 3;
+        if (m3 < F::dim(o)) {
+          static_for<A.n_to[o]>([&](auto P) {
+            constexpr int pl = decltype(P)::value;
+            constexpr int q = F::path_of(o, pl);
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(buf * B::acc_cols() + B::col_off(o) + 32 * pl), v);
+            const float sc = p.scale[o];
+            const int row = e * DT + A.t_off[q] + m3;
+            unsigned char* dst = tbt + (size_t)row * 128;
+            const unsigned char* sbr = st + B::sb_off() + pl * kBoxBytes + e * 128;
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+              float4 w4 = make_float4(sc * v[4 * c4], sc * v[4 * c4 + 1], sc * v[4 * c4 + 2], sc * v[4 * c4 + 3]);
+              if constexpr (F::scalar(o)) {  // T-bar of the scalar paths += s-bar (same order as EPI_ADDX)
+                const float4 a4 = *reinterpret_cast<const float4*>(sbr + ((c4 ^ (e & 7)) << 4));
+                w4 = make_float4(w4.x + a4.x, w4.y + a4.y, w4.z + a4.z, w4.w + a4.w);
+              }
+              *reinterpret_cast<float4*>(dst + ((c4 ^ (row & 7)) << 4)) = w4;
+            }
+          });
+        }
+      });
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + buf);
+      if (lane == 0) mbar_arrive(tb_full);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(in_empty + s);
+      if (++s == p.stages) s = 0, ph ^= 1;
+    }
+  } else if (warp < kBTp) {
+    // ---------------- TP adjoint: warp per edge, lane = channel ----------------
+    const int c = lane;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = 0; t < n_my; ++t) {
+      const int64_t e0 = tile_e0(t);
+      mbar_wait(in_full + s, ph);
+      mbar_wait(tb_full, (uint32_t)t & 1u);
+      const unsigned char* st = stage0 + (size_t)s * B::stage_bytes();
+      const int* hdr = reinterpret_cast<const int*>(st + B::h_off());
+      const int nv = hdr[32], a_lo = hdr[33];
+      for (int e = warp; e < nv; e += kBTp) {
+        const int ga = hdr[e];
+        const float* gsrc = ga < kBGA ? reinterpret_cast<const float*>(st + B::g_off() + (size_t)ga * DSH * 128)
+                                      : p.G + (int64_t)(a_lo + ga) * DSH * 32;
+        float G[DSH], tb[DT], v[DIN], vb[DIN], gp[DSH];
+#pragma unroll
+        for (int m = 0; m < DSH; ++m) G[m] = gsrc[m * 32 + c], gp[m] = 0.f;
+#pragma unroll
+        for (int q = 0; q < DT; ++q) {
+          const int row = e * DT + q;
+          tb[q] = *reinterpret_cast<const float*>(tbt + row * 128 + ((((c >> 2) ^ (row & 7))) << 4) + (c & 3) * 4);
+        }
+        [[maybe_unused]] float we[AR::NENV], yv[DSH];
+        if constexpr (K == 0) {
+#pragma unroll
+          for (int l = 0; l < AR::NENV; ++l)
+            we[l] = *reinterpret_cast<const float*>(st + B::in_off() + l * kBoxBytes + e * 128 + (((c >> 2) ^ (e & 7)) << 4) + (c & 3) * 4);
+#pragma unroll
+          for (int m = 0; m < DSH; ++m) yv[m] = reinterpret_cast<const float*>(st + B::y_off())[e * DSH + m];
+#pragma unroll
+          for (int m = 0; m < DSH; ++m) v[m] = we[lm_l(m)] * yv[m];
+        } else {
+          static_for<B::NI>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int dim = ir_dim(A.in.v[i]);
+            constexpr int off = A.in.off(i);
+#pragma unroll
+            for (int m = 0; m < dim; ++m) {
+              const int row = e * dim + m;
+              v[off + m] = *reinterpret_cast<const float*>(st + B::v_off(i) + row * 128 + ((((c >> 2) ^ (row & 7))) << 4) + (c & 3) * 4);
+            }
+          });
+        }
+#pragma unroll
+        for (int q = 0; q < DIN; ++q) vb[q] = 0.f;
+        static_for<A.n_paths>([&](auto Q) {
+          constexpr int q = decltype(Q)::value;
+          constexpr int L1 = A.path[q].a.l, L2 = A.path[q].b.l, LO = A.path[q].o.l;
+          constexpr int D2 = 2 * L2 + 1, D3 = 2 * LO + 1;
+          constexpr double alpha = csqrt(2.0 * LO + 1.0);
+          static_for<(2 * L1 + 1) * D2 * D3>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int m1 = i / (D2 * D3), m2 = (i / D3) % D2, m3 = i % D3;
+            constexpr float cf = (float)(alpha * W3j<L1, L2, LO>::t.v[i]);
+            constexpr int it = A.t_off[q] + m3, iv = A.in_off[q] + m1, ig = A.sh_off[q] + m2;
+            if constexpr (cf != 0.f) {
+              const float ct = cf * tb[it];
+              vb[iv] = fmaf(ct, G[ig], vb[iv]);
+              gp[ig] = fmaf(ct, v[iv], gp[ig]);
+            }
+          });
+        });
+        const int64_t ge = e0 + e;
+        if constexpr (K == 0) {
+          // V0 = w_edge (x) Y:  w-bar_edge[l] = sum_m vb[m] Y[m];  Y-bar[m] += sum_c vb[m] w_edge[l(m)]
+          float wb[AR::NENV], prod[DSH];
+#pragma unroll
+          for (int l = 0; l < AR::NENV; ++l) wb[l] = 0.f;
+#pragma unroll
+          for (int m = 0; m < DSH; ++m) {
+            wb[lm_l(m)] = fmaf(vb[m], yv[m], wb[lm_l(m)]);
+            prod[m] = vb[m] * we[lm_l(m)];
+          }
+          int mq;
+          const float sm = warp_sum_multi<DSH>(prod, lane, &mq);
+#pragma unroll
+          for (int l = 0; l < AR::NENV; ++l) p.wbar[ge * AR::NW + l * 32 + c] = wb[l];
+          constexpr int LP = DSH <= 1 ? 0 : DSH <= 2 ? 1 : DSH <= 4 ? 2 : DSH <= 8 ? 3 : 4;
+          if (mq < DSH && (lane & ((1 << (5 - LP)) - 1)) == 0) p.ybar[ge * DSH + mq] += sm;
+        } else {
+          static_for<B::NI>([&](auto I) {
+            constexpr int i = decltype(I)::value;
+            constexpr int dim = ir_dim(A.in.v[i]);
+            constexpr int off = A.in.off(i);
+#pragma unroll
+            for (int m = 0; m < dim; ++m) p.vbo[i][(ge * dim + m) * 32 + c] = vb[off + m];
+          });
+        }
+#pragma unroll
+        for (int m = 0; m < DSH; ++m) p.gp[(ge * DSH + m) * 32 + c] = gp[m];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tb_empty);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(in_empty + s);
+      if (++s == p.stages) s = 0, ph ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == kBMma) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int NL, int LMAX, int K>
+void launch_bwd(const TpbIO& io, cudaStream_t st, Profiler* prof) {
+  using B = Bz<NL, LMAX, K>;
+  using F = Fz<NL, LMAX, K>;
+  constexpr LayerArch A = B::A;
+  const int64_t E = io.ch.n_e;
+  if (E <= 0) return;
+  TpbMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  TpbParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.n_e = E;
+  p.e0g = io.ch.e0;
+  p.a0 = io.ch.a0;
+  p.cidx = io.cidx;
+  p.G = io.G;
+  p.Y = io.Y;
+  for (int i = 0; i < B::NI; ++i) p.vbo[i] = io.vbar_out[i];
+  p.wbar = io.wbar;
+  p.ybar = io.ybar;
+  p.gp = io.gp;
+  p.n_tiles = (int)((E + kTile - 1) / kTile);
+  uint32_t wsum = 0;
+  for (int o = 0; o < B::NO; ++o) {
+    p.wimg[o] = io.wimg[o];
+    p.wbytes[o] = (uint32_t)io.wbytes[o];
+    if (io.wbytes[o] != (size_t)F::nto(o) * 32 * 2 * 128) throw CudaError("tpl_bwd: unexpected TP-linear^T weight image");
+    p.scale[o] = 1.f / std::sqrt((float)(kC * F::nto(o)));
+    wsum += p.wbytes[o];
+    const uint64_t dims[3] = {32, (uint64_t)F::dim(o), (uint64_t)E};
+    const uint64_t strides[2] = {128, (uint64_t)F::dim(o) * 128};
+    const uint32_t box[3] = {32, 1, 32};
+    maps.vb[o] = tc_map_f32(io.vbar_in[o], 3, dims, strides, box);
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)A.n_s * 32, (uint64_t)E};
+    const uint64_t strides[1] = {(uint64_t)A.n_s * 128};
+    const uint32_t box[2] = {32, 32};
+    maps.sb = tc_map_f32(io.sbar, 2, dims, strides, box);
+  }
+  if constexpr (K == 0) {
+    const uint64_t dims[2] = {(uint64_t)Arch<NL, LMAX, K>::NW, (uint64_t)E};
+    const uint64_t strides[1] = {(uint64_t)Arch<NL, LMAX, K>::NW * 4};
+    const uint32_t box[2] = {32, 32};
+    maps.in[0] = tc_map_f32(io.w, 2, dims, strides, box);
+  } else {
+    for (int i = 0; i < B::NI; ++i) {
+      const uint64_t dims[2] = {32, (uint64_t)E * ir_dim(A.in.v[i])};
+      const uint64_t strides[1] = {128};
+      const uint32_t box[2] = {32, (uint32_t)F::in_rows(i)};
+      maps.in[i] = tc_map_f32(io.vin[i], 2, dims, strides, box);
+    }
+  }
+  const size_t fixed = 1024 + ((wsum + 1023) / 1024) * 1024 + B::tb_bytes() + 512;
+  int stages = (int)std::min<size_t>(4, (kSmemLimit - fixed) / B::stage_bytes());
+  if (stages < 2) throw CudaError("tpl_bwd: shared memory too small for two input stages");
+  p.stages = stages;
+  const size_t smem = fixed + (size_t)stages * B::stage_bytes();
+  int dev = 0;
+  ALG_CUDA(cudaGetDevice(&dev));
+  static bool attr[64] = {};
+  static int nsm[64] = {};
+  if (!attr[dev]) {
+    ALG_CUDA(cudaFuncSetAttribute(k_tpl_bwd<NL, LMAX, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
+    ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
+    attr[dev] = true;
+  }
+  const int grid = std::max(1, std::min(p.n_tiles, nsm[dev]));
+  {
+    char tag[48];
+    std::snprintf(tag, sizeof(tag), "tpl_bwd layer=%d", K);
+    double mac = 0;
+    for (int o = 0; o < B::NO; ++o) mac += (double)F::dim(o) * F::nto(o) * kC * kC;
+    const double flops = (double)E * (2.0 * 2.0 * io.tp_fma_per_edge + 2.0 * mac);
+    double bytes = 0;
+    for (int o = 0; o < B::NO; ++o) bytes += (double)F::dim(o) * 128;       // V-bar^{k+1}
+    bytes += (double)A.n_s * 128 + 4;                                        // s-bar, cidx
+    if (K == 0) bytes += Arch<NL, LMAX, K>::NENV * 128 * 2 + DSH_bytes<NL, LMAX, K>();  // w_edge in, w-bar out, Y, Y-bar
+    else bytes += 2.0 * A.dim_in * 128;                                      // V^k in, V-bar^k out
+    bytes += (double)B::DSH * 128;                                           // Gamma-bar terms out
+    ProfScope ps_(prof, st, PK_TPL_BWD, flops, bytes * E, tag);
+    k_tpl_bwd<NL, LMAX, K><<<grid, kBThreads, smem, st>>>(maps, p);
+  }
+  ALG_LAUNCH_CHECK();
+  if (std::getenv("ALLEGRO_SYNC_CHECK")) {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess)
+      throw CudaError(std::string("k_tpl_bwd layer ") + std::to_string(K) + ": " + cudaGetErrorString(e));
+  }
+}
+
 }  // namespace
 
 bool tpl_fwd_supported(int NL, int LMAX, int K) { return LMAX == 1 && K < NL - 1 && (NL == 2 || NL == 3); }
+
+void tpl_bwd(int NL, int LMAX, int K, const TpbIO& io, cudaStream_t st, Profiler* prof) {
+#define ALG_TPB(nl, lm, k) \
+  if (NL == nl && LMAX == lm && K == k) return launch_bwd<nl, lm, k>(io, st, prof);
+  ALG_TPB(2, 1, 0)
+  ALG_TPB(3, 1, 0) ALG_TPB(3, 1, 1)
+#undef ALG_TPB
+  throw CudaError("tpl_bwd: no fused kernel for this layer");
+}
 
 void tpl_fwd(int NL, int LMAX, int K, const TplIO& io, cudaStream_t st, Profiler* prof) {
 #define ALG_TPL(nl, lm, k) \

@@ -1,5 +1,5 @@
-"""Fused TP + TP-linear forward vs the unfused path on small multi-tile cases (debugging aid):
-C1 replicated 4x4x4 (1,024 atoms) with the (2, 1) and (3, 1) models."""
+"""Fused TP + TP-linear forward / backward vs the unfused path (debugging aid): C1 replicated
+rep^3 times with the given models; prints whether E and F agree bit for bit and max|dF|."""
 import os
 import sys
 
@@ -17,8 +17,11 @@ for L, lmax in arch:
     sw.write(wf, L, lmax, 5.0, sw.generate(L, lmax, 0), sw.nbar_for(5.0), (1.0, 1.0), (0.0, 0.0))
     m = pb.Allegro(wf, s.box, precision=pb.PREC_3XTF32, n_atoms=s.n)
     os.environ["ALLEGRO_FUSED_TP"] = "0"
+    os.environ["ALLEGRO_FUSED_TP_BWD"] = "0"
     e0, ea0, f0 = m.compute_energy_forces(s.pos, s.species)
-    os.environ["ALLEGRO_FUSED_TP"] = "1"
-    e1, ea1, f1 = m.compute_energy_forces(s.pos, s.species)
-    print(f"({L},{lmax}) n={s.n}: bitwise E {e1 == e0} F {np.array_equal(f1, f0)} max|dF| {np.abs(f1 - f0).max():.3g}",
-          flush=True)
+    for fwd, bwd in (("-1", "0"), ("-1", "-1")):
+        os.environ["ALLEGRO_FUSED_TP"] = fwd
+        os.environ["ALLEGRO_FUSED_TP_BWD"] = bwd
+        e1, ea1, f1 = m.compute_energy_forces(s.pos, s.species)
+        print(f"({L},{lmax}) n={s.n} fused fwd {fwd} bwd {bwd}: bitwise E {e1 == e0} F {np.array_equal(f1, f0)} "
+              f"max|dF| {np.abs(f1 - f0).max():.3g} max|F| {np.abs(f0).max():.3g}", flush=True)
