@@ -558,10 +558,11 @@ struct Bz {
   static constexpr int in_off() { return sb_off() + A.n_s * kBoxBytes; }
   static constexpr int v_off(int i) { return in_off() + F::v_off(i); }
   static constexpr int y_off() { return in_off() + AR::NENV * kBoxBytes; }
-  static constexpr int g_off() { return K == 0 ? y_off() + kTile * DSH * 4 : in_off() + F::v_off(NI); }
+  static constexpr int yb_off() { return y_off() + kTile * DSH * 4; }  // K == 0: Y-bar rows (read-modify-write)
+  static constexpr int g_off() { return K == 0 ? yb_off() + kTile * DSH * 4 : in_off() + F::v_off(NI); }
   static constexpr int h_off() { return g_off() + kBGA * DSH * 128; }
   static constexpr int stage_bytes() { return (h_off() + 256 + 1023) / 1024 * 1024; }
-  static constexpr int tb_bytes() { return kTile * DT * 128; }
+  static constexpr int tb_bytes() { return kTile * DT * 128; }  // two 16-edge halves, double-buffered in turn
   static constexpr int tma_bytes() { return in_off() + (K == 0 ? AR::NENV * kBoxBytes : F::v_off(NI)); }
 };
 
@@ -606,24 +607,25 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
   unsigned char* stage0 = base + ((woff[NO] + 1023u) & ~1023u);
   unsigned char* tbt = stage0 + (size_t)p.stages * B::stage_bytes();
   uint64_t* bars = reinterpret_cast<uint64_t*>(tbt + B::tb_bytes());
-  uint64_t* in_full = bars;
+  uint64_t* in_full = bars;           // [4] the tile's V-bar and s-bar boxes (split / MMA / copy chain)
   uint64_t* in_empty = in_full + 4;
   uint64_t* a_full = in_empty + 4;
   uint64_t* a_empty = a_full + kBAStages;
   uint64_t* acc_full = a_empty + kBAStages;
   uint64_t* acc_empty = acc_full + 2;
-  uint64_t* tb_full = acc_empty + 2;
-  uint64_t* tb_empty = tb_full + 1;
-  uint64_t* w_full = tb_empty + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
+  uint64_t* tb_full = acc_empty + 2;  // [2] T-bar halves (edges 0-15, 16-31)
+  uint64_t* tb_empty = tb_full + 2;   // [2]
+  uint64_t* w_full = tb_empty + 2;
+  uint64_t* in_full_b = w_full + 1;   // [4] the TP inputs (V^k or w_edge, Y, Y-bar, Gamma)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(in_full_b + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s) mbar_init(in_full + s, 1), mbar_init(in_empty + s, kBTp + 8);
+    for (int s = 0; s < p.stages; ++s)
+      mbar_init(in_full + s, 1), mbar_init(in_full_b + s, 1), mbar_init(in_empty + s, kBTp + 8);
     for (int s = 0; s < kBAStages; ++s) mbar_init(a_full + s, 4), mbar_init(a_empty + s, 1);
     for (int b = 0; b < 2; ++b) mbar_init(acc_full + b, 1), mbar_init(acc_empty + b, 4);
-    mbar_init(tb_full, 4);
-    mbar_init(tb_empty, kBTp);
+    for (int h = 0; h < 2; ++h) mbar_init(tb_full + h, 4), mbar_init(tb_empty + h, kBTp);
     mbar_init(w_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -665,8 +667,10 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
       if (lane == 0) {
         const int span = a_hi - a_lo + 1;
         const uint32_t gbytes = (uint32_t)(span < kBGA ? span : kBGA) * DSH * 128;
-        uint32_t bytes = (uint32_t)B::tma_bytes() + gbytes + (K == 0 ? (uint32_t)nv * DSH * 4 : 0u);
-        mbar_expect_tx(in_full + s, bytes);
+        // the MMA chain's operands first, on their own barrier; then the TP inputs
+        mbar_expect_tx(in_full + s, (uint32_t)B::in_off());
+        const uint32_t bytes_b = (uint32_t)(B::tma_bytes() - B::in_off()) + gbytes + (K == 0 ? 2u * (uint32_t)nv * DSH * 4 : 0u);
+        mbar_expect_tx(in_full_b + s, bytes_b);
         static_for<NO>([&](auto O) {
           constexpr int o = decltype(O)::value;
           static_for<ir_dim(A.out.v[o])>([&](auto M) {
@@ -677,16 +681,17 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
         for (int q = 0; q < A.n_s; ++q) tma_load_2d(st + B::sb_off() + q * kBoxBytes, &maps.sb, 32 * q, (int)e0, in_full + s);
         if constexpr (K == 0) {
 #pragma unroll
-          for (int l = 0; l < AR::NENV; ++l) tma_load_2d(st + B::in_off() + l * kBoxBytes, &maps.in[0], 32 * l, (int)e0, in_full + s);
-          bulk_load(st + B::y_off(), p.Y + e0 * DSH, (uint32_t)nv * DSH * 4, in_full + s);
+          for (int l = 0; l < AR::NENV; ++l) tma_load_2d(st + B::in_off() + l * kBoxBytes, &maps.in[0], 32 * l, (int)e0, in_full_b + s);
+          bulk_load(st + B::y_off(), p.Y + e0 * DSH, (uint32_t)nv * DSH * 4, in_full_b + s);
+          bulk_load(st + B::yb_off(), p.ybar + e0 * DSH, (uint32_t)nv * DSH * 4, in_full_b + s);
         } else {
           static_for<B::NI>([&](auto I) {
             constexpr int i = decltype(I)::value;
             constexpr int dim = ir_dim(A.in.v[i]);
-            tma_load_2d(st + B::v_off(i), &maps.in[i], 0, (int)(e0 * dim), in_full + s);
+            tma_load_2d(st + B::v_off(i), &maps.in[i], 0, (int)(e0 * dim), in_full_b + s);
           });
         }
-        bulk_load(st + B::g_off(), p.G + (int64_t)a_lo * DSH * 32, gbytes, in_full + s);
+        bulk_load(st + B::g_off(), p.G + (int64_t)a_lo * DSH * 32, gbytes, in_full_b + s);
       }
       if (++s == p.stages) s = 0, ph ^= 1;
     }
@@ -779,39 +784,47 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
       mbar_wait(acc_full + buf, (uint32_t)(t >> 1) & 1u);
       tc_fence_after();
       mbar_wait(in_full + s, ph);                      // (complete: its s-bar boxes are read here)
-      mbar_wait(tb_empty, ((uint32_t)t & 1u) ^ 1u);    // the TP warps are done with the previous tile
       const unsigned char* st = stage0 + (size_t)s * B::stage_bytes();
       const int e = lane;
-      static_for<NO>([&](auto O) {
-        constexpr int o = decltype(O)::value;
-        constexpr int B0 = F::base(o);
-        const int m3 = (qw - B0 + 4) & 3;
-        if (m3 < F::dim(o)) {
-          static_for<A.n_to[o]>([&](auto P) {
-            constexpr int pl = decltype(P)::value;
-            constexpr int q = F::path_of(o, pl);
-            float v[32];
-            tmem_ld32(tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(buf * B::acc_cols() + B::col_off(o) + 32 * pl), v);
-            const float sc = p.scale[o];
-            const int row = e * DT + A.t_off[q] + m3;
-            unsigned char* dst = tbt + (size_t)row * 128;
-            const unsigned char* sbr = st + B::sb_off() + pl * kBoxBytes + e * 128;
+      // two passes over the accumulator: edges 0-15 into half 0, then 16-31 into half 1, so that the
+      // TP warps work on one half while the other is refilled
+      for (int h = 0; h < 2; ++h) {
+        mbar_wait(tb_empty + h, ((uint32_t)t & 1u) ^ 1u);  // the TP warps are done with this half
+        const bool mine = (e >> 4) == h;
+        static_for<NO>([&](auto O) {
+          constexpr int o = decltype(O)::value;
+          constexpr int B0 = F::base(o);
+          const int m3 = (qw - B0 + 4) & 3;
+          if (m3 < F::dim(o)) {
+            static_for<A.n_to[o]>([&](auto P) {
+              constexpr int pl = decltype(P)::value;
+              constexpr int q = F::path_of(o, pl);
+              float v[32];
+              tmem_ld32(tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(buf * B::acc_cols() + B::col_off(o) + 32 * pl), v);
+              if (mine) {
+                const float sc = p.scale[o];
+                const int row = (e & 15) * DT + A.t_off[q] + m3;
+                unsigned char* dst = tbt + (size_t)h * (B::tb_bytes() / 2) + (size_t)row * 128;
+                const unsigned char* sbr = st + B::sb_off() + pl * kBoxBytes + e * 128;
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-              float4 w4 = make_float4(sc * v[4 * c4], sc * v[4 * c4 + 1], sc * v[4 * c4 + 2], sc * v[4 * c4 + 3]);
-              if constexpr (F::scalar(o)) {  // T-bar of the scalar paths += s-bar (same order as EPI_ADDX)
-                const float4 a4 = *reinterpret_cast<const float4*>(sbr + ((c4 ^ (e & 7)) << 4));
-                w4 = make_float4(w4.x + a4.x, w4.y + a4.y, w4.z + a4.z, w4.w + a4.w);
+                for (int c4 = 0; c4 < 8; ++c4) {
+                  float4 w4 = make_float4(sc * v[4 * c4], sc * v[4 * c4 + 1], sc * v[4 * c4 + 2], sc * v[4 * c4 + 3]);
+                  if constexpr (F::scalar(o)) {  // T-bar of the scalar paths += s-bar (same order as EPI_ADDX)
+                    const float4 a4 = *reinterpret_cast<const float4*>(sbr + ((c4 ^ (e & 7)) << 4));
+                    w4 = make_float4(w4.x + a4.x, w4.y + a4.y, w4.z + a4.z, w4.w + a4.w);
+                  }
+                  *reinterpret_cast<float4*>(dst + ((c4 ^ (row & 7)) << 4)) = w4;
+                }
               }
-              *reinterpret_cast<float4*>(dst + ((c4 ^ (row & 7)) << 4)) = w4;
-            }
-          });
-        }
-      });
+            });
+          }
+        });
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tb_full + h);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + buf);
-      if (lane == 0) mbar_arrive(tb_full);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(in_empty + s);
@@ -825,11 +838,15 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
     for (int t = 0; t < n_my; ++t) {
       const int64_t e0 = tile_e0(t);
       mbar_wait(in_full + s, ph);
-      mbar_wait(tb_full, (uint32_t)t & 1u);
+      mbar_wait(in_full_b + s, ph);
       const unsigned char* st = stage0 + (size_t)s * B::stage_bytes();
       const int* hdr = reinterpret_cast<const int*>(st + B::h_off());
       const int nv = hdr[32], a_lo = hdr[33];
-      for (int e = warp; e < nv; e += kBTp) {
+      for (int h = 0; h < 2; ++h) {
+      mbar_wait(tb_full + h, (uint32_t)t & 1u);
+      const unsigned char* tbh = tbt + (size_t)h * (B::tb_bytes() / 2);
+      const int e_end = 16 * h + 16 < nv ? 16 * h + 16 : nv;
+      for (int e = 16 * h + warp; e < e_end; e += kBTp) {
         const int ga = hdr[e];
         const float* gsrc = ga < kBGA ? reinterpret_cast<const float*>(st + B::g_off() + (size_t)ga * DSH * 128)
                                       : p.G + (int64_t)(a_lo + ga) * DSH * 32;
@@ -838,8 +855,8 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
         for (int m = 0; m < DSH; ++m) G[m] = gsrc[m * 32 + c], gp[m] = 0.f;
 #pragma unroll
         for (int q = 0; q < DT; ++q) {
-          const int row = e * DT + q;
-          tb[q] = *reinterpret_cast<const float*>(tbt + row * 128 + ((((c >> 2) ^ (row & 7))) << 4) + (c & 3) * 4);
+          const int row = (e & 15) * DT + q;
+          tb[q] = *reinterpret_cast<const float*>(tbh + row * 128 + ((((c >> 2) ^ (row & 7))) << 4) + (c & 3) * 4);
         }
         [[maybe_unused]] float we[AR::NENV], yv[DSH];
         if constexpr (K == 0) {
@@ -897,7 +914,8 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
 #pragma unroll
           for (int l = 0; l < AR::NENV; ++l) p.wbar[ge * AR::NW + l * 32 + c] = wb[l];
           constexpr int LP = DSH <= 1 ? 0 : DSH <= 2 ? 1 : DSH <= 4 ? 2 : DSH <= 8 ? 3 : 4;
-          if (mq < DSH && (lane & ((1 << (5 - LP)) - 1)) == 0) p.ybar[ge * DSH + mq] += sm;
+          if (mq < DSH && (lane & ((1 << (5 - LP)) - 1)) == 0)  // old Y-bar staged by the producer
+            p.ybar[ge * DSH + mq] = reinterpret_cast<const float*>(st + B::yb_off())[e * DSH + mq] + sm;
         } else {
           static_for<B::NI>([&](auto I) {
             constexpr int i = decltype(I)::value;
@@ -911,7 +929,8 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
         for (int m = 0; m < DSH; ++m) p.gp[(ge * DSH + m) * 32 + c] = gp[m];
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(tb_empty);
+      if (lane == 0) mbar_arrive(tb_empty + h);
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(in_empty + s);
