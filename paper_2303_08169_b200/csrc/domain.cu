@@ -175,14 +175,6 @@ void reserve_keep(DBuf<T>& b, size_t n, size_t used, cudaStream_t st) {
   nb.cap = 0;
 }
 
-int64_t scan_count(allegro_ctx* c, const int32_t* flag, int32_t* idx, int64_t n) {
-  exclusive_scan(c, flag, idx, n);
-  int32_t cnt = 0;
-  ALG_CUDA(cudaMemcpyAsync(&cnt, idx + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-  ALG_CUDA(cudaStreamSynchronize(c->stream));
-  return cnt;
-}
-
 // Exchange byte messages with the -/+ neighbours of one axis: send[d] -> nbr[d],
 // recv[d] <- nbr[d] (the neighbour's message in the opposite direction).
 void exchange(allegro_ctx* c, int axis, const void* send_m, size_t bytes_m, const void* send_p, size_t bytes_p,
@@ -204,20 +196,28 @@ void exchange(allegro_ctx* c, int axis, const void* send_m, size_t bytes_m, cons
   ALG_NCCL(N.GroupEnd());
 }
 
-// exchange the two message sizes, returns (from -, from +)
-void exchange_counts(allegro_ctx* c, int axis, int64_t n_m, int64_t n_p, int64_t* r_m, int64_t* r_p) {
-  Domain& D = c->dom;
-  D.cnt.reserve(8);
-  long long h[2] = {n_m, n_p};
-  ALG_CUDA(cudaMemcpyAsync(D.cnt.p, h, 2 * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
-  exchange(c, axis, D.cnt.p, 8, D.cnt.p + 1, 8, D.cnt.p + 2, 8, D.cnt.p + 3, 8);
-  long long r[2];
-  ALG_CUDA(cudaMemcpyAsync(r, D.cnt.p + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-  ALG_CUDA(cudaStreamSynchronize(c->stream));
-  *r_m = r[0];
-  *r_p = r[1];
+__global__ void k_pack_counts(const int32_t* __restrict__ a, const int32_t* __restrict__ b,
+                              const int32_t* __restrict__ extra, long long* __restrict__ out) {
+  out[0] = *a;
+  out[1] = *b;
+  out[4] = extra ? *extra : 0;
 }
 
+// The counts of one stage without a host round trip per count: the scans leave their totals on
+// the device (idx[n]); they are packed, the two message sizes are exchanged device-to-device with
+// the neighbours, and ONE read brings {n_m, n_p, r_m, r_p, extra} to the host.
+void stage_counts(allegro_ctx* c, int axis, const int32_t* tot_m, const int32_t* tot_p, const int32_t* tot_extra,
+                  int64_t out[5]) {
+  Domain& D = c->dom;
+  D.cnt.reserve(8);
+  k_pack_counts<<<1, 1, 0, c->stream>>>(tot_m, tot_p, tot_extra, D.cnt.p);
+  ALG_LAUNCH_CHECK();
+  exchange(c, axis, D.cnt.p, 8, D.cnt.p + 1, 8, D.cnt.p + 2, 8, D.cnt.p + 3, 8);
+  long long h[5];
+  ALG_CUDA(cudaMemcpyAsync(h, D.cnt.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  ALG_CUDA(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < 5; ++i) out[i] = h[i];
+}
 
 }  // namespace
 
@@ -375,11 +375,12 @@ void migrate(allegro_ctx* c) {
                                                     D.f2.p);
       ALG_LAUNCH_CHECK();
     }
-    const int64_t n_stay = scan_count(c, D.f0.p, D.i0.p, n);
-    const int64_t n_m = scan_count(c, D.f1.p, D.i1.p, n);
-    const int64_t n_p = scan_count(c, D.f2.p, D.i2.p, n);
-    D.sendbuf[0].reserve((n_m + 1) * sizeof(MigAtom));
-    D.sendbuf[1].reserve((n_p + 1) * sizeof(MigAtom));
+    // scans without host reads; buffers sized for the upper bound n (they only grow)
+    exclusive_scan(c, D.f0.p, D.i0.p, n);
+    exclusive_scan(c, D.f1.p, D.i1.p, n);
+    exclusive_scan(c, D.f2.p, D.i2.p, n);
+    D.sendbuf[0].reserve((n + 1) * sizeof(MigAtom));
+    D.sendbuf[1].reserve((n + 1) * sizeof(MigAtom));
     // stay-compaction into temporaries, then pack the leavers
     D.tpos.reserve(3 * n + 3), D.tvel.reserve(3 * n + 3), D.tgid.reserve(n + 1), D.tspec.reserve(n + 1);
     if (n > 0) {
@@ -389,16 +390,20 @@ void migrate(allegro_ctx* c) {
       k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, D.f2.p, D.i2.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
                                                    reinterpret_cast<MigAtom*>(D.sendbuf[1].p));
       // reuse the recv buffer as the stay staging (MigAtom layout)
-      D.recvbuf[0].reserve((n_stay + 1) * sizeof(MigAtom));
+      D.recvbuf[0].reserve((n + 1) * sizeof(MigAtom));
       k_mig_pack<<<ceil_div(n, 256), 256, 0, st>>>(n, D.f0.p, D.i0.p, c->pos.p, c->vel.p, c->gid.p, c->species.p,
                                                    reinterpret_cast<MigAtom*>(D.recvbuf[0].p));
       ALG_LAUNCH_CHECK();
+    }
+    int64_t cnt[5];
+    stage_counts(c, axis, D.i1.p + n, D.i2.p + n, D.i0.p + n, cnt);  // the one host read of this axis
+    const int64_t n_m = cnt[0], n_p = cnt[1], r_m = cnt[2], r_p = cnt[3], n_stay = cnt[4];
+    if (n > 0) {
+      ProfScope ps_(&c->prof, st, PK_HALO, 0, 112.0 * n_stay);
       k_mig_unpack<<<ceil_div(std::max<int64_t>(n_stay, 1), 256), 256, 0, st>>>(
           n_stay, reinterpret_cast<MigAtom*>(D.recvbuf[0].p), 0, c->pos.p, c->vel.p, c->gid.p, c->species.p);
       ALG_LAUNCH_CHECK();
     }
-    int64_t r_m = 0, r_p = 0;
-    exchange_counts(c, axis, n_m, n_p, &r_m, &r_p);
     const int64_t n_new = n_stay + r_m + r_p;
     // owned capacity has 25 % slack (select_owned); growing here would discard content
     if ((size_t)(3 * n_new + 3) > c->pos.cap || (size_t)(3 * n_new + 3) > c->vel.cap || (size_t)(n_new + 1) > c->gid.cap ||
@@ -443,19 +448,17 @@ void halo_exchange(allegro_ctx* c) {
                                                         D.f1.p);
       ALG_LAUNCH_CHECK();
     }
-    const int64_t n_m = scan_count(c, D.f0.p, D.i0.p, n_cur);
-    const int64_t n_p = scan_count(c, D.f1.p, D.i1.p, n_cur);
-    S.n_send[0] = n_m;
-    S.n_send[1] = n_p;
-    S.send_idx[0].reserve(n_m + 1);
-    S.send_idx[1].reserve(n_p + 1);
-    D.sendbuf[0].reserve((n_m + 1) * sizeof(HaloAtom));
-    D.sendbuf[1].reserve((n_p + 1) * sizeof(HaloAtom));
+    exclusive_scan(c, D.f0.p, D.i0.p, n_cur);  // totals stay on the device (stage_counts below)
+    exclusive_scan(c, D.f1.p, D.i1.p, n_cur);
+    S.send_idx[0].reserve(n_cur + 1);
+    S.send_idx[1].reserve(n_cur + 1);
+    D.sendbuf[0].reserve((n_cur + 1) * sizeof(HaloAtom));
+    D.sendbuf[1].reserve((n_cur + 1) * sizeof(HaloAtom));
     // "-" message: atoms near the lower face, shifted by +L when wrapping; "+" message: -L
     const int sh_m = D.c[axis] == 0 ? +1 : 0;
     const int sh_p = D.c[axis] == D.P[axis] - 1 ? -1 : 0;
     if (n_cur > 0) {
-      ProfScope ps_(&c->prof, st, PK_HALO, 0, 40.0 * (n_m + n_p));
+      ProfScope ps_(&c->prof, st, PK_HALO, 0, 16.0 * n_cur);
       k_halo_pack<<<ceil_div(n_cur, 256), 256, 0, st>>>(n_cur, D.f0.p, D.i0.p, axis, c->box[axis], sh_m, c->apos.p,
                                                         c->agid.p, c->aspec.p, c->ashift.p,
                                                         reinterpret_cast<HaloAtom*>(D.sendbuf[0].p), S.send_idx[0].p);
@@ -464,8 +467,11 @@ void halo_exchange(allegro_ctx* c) {
                                                         reinterpret_cast<HaloAtom*>(D.sendbuf[1].p), S.send_idx[1].p);
       ALG_LAUNCH_CHECK();
     }
-    int64_t r_m = 0, r_p = 0;
-    exchange_counts(c, axis, n_m, n_p, &r_m, &r_p);
+    int64_t cnt[5];
+    stage_counts(c, axis, D.i0.p + n_cur, D.i1.p + n_cur, nullptr, cnt);  // the one host read of this stage
+    const int64_t n_m = cnt[0], n_p = cnt[1], r_m = cnt[2], r_p = cnt[3];
+    S.n_send[0] = n_m;
+    S.n_send[1] = n_p;
     S.n_recv[0] = r_m;
     S.n_recv[1] = r_p;
     D.recvbuf[0].reserve((r_m + 1) * sizeof(HaloAtom));

@@ -12,13 +12,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
 
-def test_two_gpu_decomposition_equals_one_gpu():
+@pytest.mark.parametrize("cfg,port", [("C2", 29533), ("CP", 29534)])
+def test_two_gpu_decomposition_equals_one_gpu(cfg, port):
+    """C2 (the 2-layer l=2 model, unfused TP path) and CP (the paper's 3-layer l=1 model at 6,912
+    atoms, the fused TP + TP-linear kernels)."""
     import torch
 
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "scripts", "check_multigpu.py"), "C2"]
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "scripts", "check_multigpu.py"), cfg]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-2000:]

@@ -295,9 +295,9 @@ def test_profiler_counts_launches(pb):
     prof = m.profile_read()
     assert m.launch_count() == sum(v[3] for v in prof.values()) > 20
     assert prof["gemm"][3] > 0 and prof["gemm"][0] > 0 and prof["gemm"][1] > 0
-    # 2 layers x 2 steps: layer 0 runs the fused TP + TP-linear kernel (3xTF32 default), layer 1 the TP kernel
-    assert prof["tp_fwd"][3] + prof["tp_lin_fwd"][3] == prof["tp_bwd"][3] == 2 * 2
-    assert prof["tp_lin_fwd"][3] == prof["gamma"][3]
+    # 2 layers x 2 steps: layer 0 runs the fused TP + TP-linear kernels (3xTF32 default), layer 1 the TP kernels
+    assert prof["tp_fwd"][3] + prof["tp_lin_fwd"][3] == prof["tp_bwd"][3] + prof["tp_lin_bwd"][3] == 2 * 2
+    assert prof["tp_lin_fwd"][3] == prof["gamma"][3] == prof["tp_lin_bwd"][3] == prof["env_adj"][3] == 2
 
 
 def test_nvt_step_matches_oracle(pb):
