@@ -236,7 +236,7 @@ int allegro_compute_energy_forces(allegro_ctx* c, int64_t n, int where, const in
       if (e_atom) ALG_CUDA(cudaMemcpyAsync(e_atom, c->e_atom.p, sizeof(double) * n, kout, c->stream));
     }
     ALG_CUDA(cudaStreamSynchronize(c->stream));
-    c->prof.flush();
+    c->prof.flush_if_large();
     return rc;
   });
 }
@@ -331,7 +331,7 @@ static int md_run(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
         break;
       }
       ++c->md_steps;
-      c->prof.flush();
+      c->prof.flush_if_large();
     }
     if (out) {
       out->steps_done = done;
@@ -349,7 +349,7 @@ static int md_run(allegro_ctx* c, int64_t n_steps, double dt, md_report* out) {
       out->n_local = c->n;
       out->n_rebuilds = c->n_rebuilds;
     }
-    c->prof.flush();
+    c->prof.flush_if_large();
     return rc;
   }
 }
@@ -500,7 +500,7 @@ int allegro_compute_energy_forces_batch(allegro_ctx* c, int64_t n_rep, int64_t n
     ALG_CUDA(cudaMemcpyAsync(forces, c->frc.p, sizeof(double) * 3 * n, kout, c->stream));
     if (e_atom) ALG_CUDA(cudaMemcpyAsync(e_atom, c->e_atom.p, sizeof(double) * n, kout, c->stream));
     ALG_CUDA(cudaStreamSynchronize(c->stream));
-    c->prof.flush();
+    c->prof.flush_if_large();
     return rc;
   });
 }
@@ -571,10 +571,10 @@ int pimd_step(allegro_ctx* c, int64_t n_steps, double dt, pimd_report* out) {
         break;
       }
       ++c->pimd_steps;
-      c->prof.flush();
+      c->prof.flush_if_large();
     }
     if (out) pimd_fill_report(c, done, out);
-    c->prof.flush();
+    c->prof.flush_if_large();
     return rc;
   });
 }

@@ -526,6 +526,187 @@ __global__ void __launch_bounds__(128) k_env_adj(TpArgs t) {
   env_adjoint<NL, LMAX, K>(t, r0, r1, lane, mm, Gb);
 }
 
+// ----------------------------------------------------------------- the last layer, fused
+// Layer L-1 has only scalar outputs (T = s) and no TP-linear, and its latent update is folded into
+// the read-out (below), so its whole forward + reverse is per CSR row: one warp per centre computes
+// Gamma_i, then per edge s (the TP), E_e, u-bar and E-bar (as k_energy_last), s-bar = T-bar and the
+// TP adjoint (V-bar^{L-1}, Gamma-bar in registers), and finally the environment adjoint of the row.
+// Same arithmetic in the same order as k_tp_fwd<L-1> + k_energy_last + k_tp_bwd<L-1> (bit-identical),
+// without their T, s-bar, Gamma and second V round trips through HBM.
+struct LastArgs {
+  TpArgs t;
+  const int32_t* species;
+  const float* x;     // x^{L-1} [E][D]
+  const float* u;     // [E]
+  const float* wout;  // [D]
+  const float* q;     // [fan_lat]: x rows, then the scalar rows (path, c)
+  double* e_atom;
+  float* ubar;
+  float* ebar;
+  double s0, s1, mu0, mu1;
+  float ra, sf;
+};
+
+template <int NL, int LMAX>
+__global__ void __launch_bounds__(128) k_last(LastArgs a) {
+  constexpr int K = NL - 1;
+  using AR = Arch<NL, LMAX, K>;
+  constexpr LayerArch A = AR::A;
+  constexpr int NS = A.n_s;  // every path of the last layer is scalar
+  static_assert(NS == A.n_paths && NS <= 3, "last layer: scalar paths only, <= 96 channels");
+  static_assert(A.t_off[NS > 1 ? NS - 1 : 0] == (NS > 1 ? NS - 1 : 0), "last layer: T index = path index");
+  const TpArgs& t = a.t;
+  const int lane = threadIdx.x & 31;
+  const int64_t ii = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (ii >= t.ch.n_c) return;
+  const int64_t at = t.ch.a0 + ii;
+  const int64_t r0 = t.row_ptr[at] - t.ch.e0, r1 = t.row_ptr[at + 1] - t.ch.e0;
+  const int z = a.species[at];
+  const double sig = z == 0 ? a.s0 : a.s1;
+  if (r1 <= r0) {
+    if (lane == 0) a.e_atom[at] = z == 0 ? a.mu0 : a.mu1;  // sig nbar^-1/2 * 0 + mu
+    return;
+  }
+  // Gamma_i (as k_tp_fwd)
+  float G[AR::DSH];
+#pragma unroll
+  for (int m = 0; m < AR::DSH; ++m) G[m] = 0.f;
+  {
+    EnvIn<NL, LMAX, K> nx;
+    fetch_env<NL, LMAX, K>(t, r0, lane, nx);
+    for (int64_t e = r0; e < r1; ++e) {
+      const EnvIn<NL, LMAX, K> cur = nx;
+      fetch_env<NL, LMAX, K>(t, e + 1 < r1 ? e + 1 : e, lane, nx);
+#pragma unroll
+      for (int m = 0; m < AR::DSH; ++m) G[m] = fmaf(cur.we[lm_l(m)], cur.y[m], G[m]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < AR::DSH; ++m) G[m] *= t.inv_sqrt_nbar;
+  // read-out constants (as k_energy_last)
+  const float eb = (float)sig * t.inv_sqrt_nbar;
+  const float4 w4 = reinterpret_cast<const float4*>(a.wout)[lane];
+  const float4 q4 = reinterpret_cast<const float4*>(a.q)[lane];
+  float qs[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) qs[k] = k < NS ? a.q[128 + lane + 32 * k] : 0.f;
+  float acc = 0.f, Gb[AR::DSH];
+#pragma unroll
+  for (int m = 0; m < AR::DSH; ++m) Gb[m] = 0.f;
+  struct In {
+    VIn<NL, LMAX, K> v;
+    float4 x4;
+    float ue;
+  };
+  auto fetch = [&](int64_t e, In& in) {
+    fetch_v<NL, LMAX, K>(t, e, lane, in.v);
+    in.x4 = reinterpret_cast<const float4*>(a.x + e * kD)[lane];
+    in.ue = a.u[e];
+  };
+  In nx;
+  fetch(r0, nx);
+  for (int64_t e = r0; e < r1; ++e) {
+    const In cur = nx;
+    fetch(e + 1 < r1 ? e + 1 : e, nx);
+    float v[AR::DIN];
+    expand_v<NL, LMAX, K>(cur.v, v);
+    // T = s (scalar outputs only)
+    float T[AR::DT];
+#pragma unroll
+    for (int q = 0; q < AR::DT; ++q) T[q] = 0.f;
+    static_for<A.n_paths>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      constexpr int L1 = A.path[q].a.l, L2 = A.path[q].b.l, LO = A.path[q].o.l;
+      constexpr int D2 = 2 * L2 + 1, D3 = 2 * LO + 1;
+      constexpr double alpha = csqrt(2.0 * LO + 1.0);
+      static_for<(2 * L1 + 1) * D2 * D3>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int m1 = i / (D2 * D3), m2 = (i / D3) % D2, m3 = i % D3;
+        constexpr float c = (float)(alpha * W3j<L1, L2, LO>::t.v[i]);
+        constexpr int it = A.t_off[q] + m3, iv = A.in_off[q] + m1, ig = A.sh_off[q] + m2;
+        if constexpr (c != 0.f) T[it] = fmaf(c * v[iv], G[ig], T[it]);
+      });
+    });
+    // E_e = a (x.w_out) + (b u / sqrt(fan)) ([x, s].q)
+    const float4 x4 = cur.x4;
+    float d1 = x4.x * w4.x;
+    d1 = fmaf(x4.y, w4.y, d1);
+    d1 = fmaf(x4.z, w4.z, d1);
+    d1 = fmaf(x4.w, w4.w, d1);
+    float d2 = x4.x * q4.x;
+    d2 = fmaf(x4.y, q4.y, d2);
+    d2 = fmaf(x4.z, q4.z, d2);
+    d2 = fmaf(x4.w, q4.w, d2);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d2 = fmaf(k < NS ? T[k < NS ? k : 0] : 0.f, qs[k], d2);  // qs = 0 beyond NS
+    d1 = warp_sum(d1);
+    d2 = warp_sum(d2);
+    acc += a.ra * d1 + a.sf * cur.ue * d2;
+    if (lane == 0) {
+      a.ubar[e] = eb * a.sf * d2;
+      a.ebar[e] = eb;
+    }
+    // T-bar = s-bar = E-bar u (b / sqrt(fan)) q_s; the TP adjoint (as k_tp_bwd)
+    float tb[AR::DT];
+#pragma unroll
+    for (int q = 0; q < AR::DT; ++q) tb[q] = 0.f;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) tb[k] = eb * cur.ue * a.sf * qs[k];
+    float vb[AR::DIN];
+#pragma unroll
+    for (int q = 0; q < AR::DIN; ++q) vb[q] = 0.f;
+    static_for<A.n_paths>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      constexpr int L1 = A.path[q].a.l, L2 = A.path[q].b.l, LO = A.path[q].o.l;
+      constexpr int D2 = 2 * L2 + 1, D3 = 2 * LO + 1;
+      constexpr double alpha = csqrt(2.0 * LO + 1.0);
+      static_for<(2 * L1 + 1) * D2 * D3>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int m1 = i / (D2 * D3), m2 = (i / D3) % D2, m3 = i % D3;
+        constexpr float c = (float)(alpha * W3j<L1, L2, LO>::t.v[i]);
+        constexpr int it = A.t_off[q] + m3, iv = A.in_off[q] + m1, ig = A.sh_off[q] + m2;
+        if constexpr (c != 0.f) {
+          const float ct = c * tb[it];
+          vb[iv] = fmaf(ct, G[ig], vb[iv]);
+          Gb[ig] = fmaf(ct, v[iv], Gb[ig]);
+        }
+      });
+    });
+    static_for<A.in.n>([&](auto I) {
+      constexpr int ii2 = decltype(I)::value;
+      constexpr int dim = ir_dim(A.in.v[ii2]);
+      constexpr int off = A.in.off(ii2);
+      constexpr int vbase = AR::v_base(ii2);
+      float* dst = t.Vb + (int64_t)vbase * t.e_cap + e * dim * kC + lane;
+#pragma unroll
+      for (int m = 0; m < dim; ++m) dst[m * kC] = vb[off + m];
+    });
+  }
+  if (lane == 0) a.e_atom[at] = sig * (double)t.inv_sqrt_nbar * (double)acc + (z == 0 ? a.mu0 : a.mu1);
+  constexpr int LP = AR::DSH <= 1 ? 0 : AR::DSH <= 2 ? 1 : AR::DSH <= 4 ? 2 : AR::DSH <= 8 ? 3 : 4;
+  env_adjoint<NL, LMAX, K>(t, r0, r1, lane, lane >> (5 - LP), Gb);
+}
+
+void last_dispatch(int NL, int LMAX, const LastArgs& a, cudaStream_t st, Profiler* prof, const LayerInfo& L) {
+  const unsigned blocks = (unsigned)((a.t.ch.n_c * 32 + 127) / 128);
+  if (blocks == 0) return;
+  const double E = (double)a.t.ch.n_e;
+  const int dsh = (LMAX + 1) * (LMAX + 1);
+  const double vin = (double)L.A.dim_in * kC, nenv = LMAX + 1;
+  // algorithmic: Gamma + TP + adjoint FMAs and the read-out dots; bytes: w_env + Y twice (Gamma, env
+  // adjoint), V, x, u in; V-bar, w-bar, Y-bar, u-bar, E-bar out
+  const double flops = E * (kC * 2.0 * (3.0 * L.tp_nnz + 3.0 * dsh) + 6.0 * 128);
+  const double bytes = 4.0 * E * (2.0 * (nenv * kC + dsh) + vin + 128 + 1 + vin + nenv * kC + 2.0 * dsh + 2);
+  {
+    ProfScope ps_(prof, st, PK_LAST, flops, bytes, "last layer (fused)");
+#define ALG_LAST(nl, lm) \
+  if (NL == nl && LMAX == lm) k_last<nl, lm><<<blocks, 128, 0, st>>>(a);
+    ALG_LAST(2, 1) ALG_LAST(2, 2) ALG_LAST(3, 0) ALG_LAST(3, 1) ALG_LAST(3, 2)
+#undef ALG_LAST
+  }
+  ALG_LAUNCH_CHECK();
+}
+
 // ----------------------------------------------------------------- A10 energies
 // Last layer folded into the linear read-out: with w_out = W_o1 W_o2 / sqrt(D 32)
 // and q = W_lat(L-1) w_out (all linear),
@@ -991,6 +1172,8 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   tp.e_cap = ecap;
   tp.inv_sqrt_nbar = inv_sqrt_nbar;
   const unsigned warp_blocks = (unsigned)((ch.n_c * 32 + 127) / 128);
+  const char* fl_env = std::getenv("ALLEGRO_FUSED_LAST");  // A/B switch: the last layer in one kernel
+  const bool fused_last = !fl_env || std::atoi(fl_env) != 0;
   // ---- layers (E6) ----
   for (int k = 0; k < M.n_layers; ++k) {
     const LayerInfo& L = M.L[k];
@@ -1022,7 +1205,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
       io.s = w.T.p;  // T_0e = s, [E][n_s C] (the latent update's second operand)
       io.tp_fma_per_edge = (double)L.tp_nnz * kC;
       tpl_fwd(M.n_layers, M.lmax, k, io, st, &c->prof);
-    } else {
+    } else if (!(k == M.n_layers - 1 && fused_last)) {  // (the fused last layer forms Gamma and s itself)
       tp_dispatch(M.n_layers, M.lmax, k, 0, tp, st, &c->prof, L);
     }
     if (k < M.n_layers - 1 && !fused) {
@@ -1055,7 +1238,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   const int nsc_last = LL.A.n_s * kC;
   if (nsc_last > 3 * 32) throw CudaError("k_energy_last holds at most 96 last-layer scalar channels (lmax <= 2)");
   const float sf_last = kResB / std::sqrt((float)LL.fan_lat);
-  if (warp_blocks) {
+  if (warp_blocks && !fused_last) {
     {
       ProfScope ps_(&c->prof, st, PK_ENERGY, 6.0 * 128 * E, (double)E * (512 + 8.0 * nsc_last + 16));
       k_energy_last<<<warp_blocks, 128, 0, st>>>(ch, c->row_ptr.p, c->species.p, x, w.T.p, nsc_last, w.u.p, M.w.wout,
@@ -1118,6 +1301,21 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
       tpl_bwd(M.n_layers, M.lmax, k, io, st, &c->prof);
       tp.gp = w.gp.p;
       tp_dispatch(M.n_layers, M.lmax, k, 3, tp, st, &c->prof, L);  // Gamma-bar + environment adjoint
+    } else if (k == M.n_layers - 1 && fused_last) {
+      LastArgs la;
+      la.t = tp;
+      la.species = c->species.p;
+      la.x = x;
+      la.u = w.u.p;
+      la.wout = M.w.wout;
+      la.q = M.w.q_last;
+      la.e_atom = c->e_atom.p;
+      la.ubar = w.ubar.p;
+      la.ebar = w.ebar.p;
+      la.s0 = M.sigma[0], la.s1 = M.sigma[1], la.mu0 = M.mu[0], la.mu1 = M.mu[1];
+      la.ra = kResA;
+      la.sf = sf_last;
+      last_dispatch(M.n_layers, M.lmax, la, st, &c->prof, L);
     } else if (k == M.n_layers - 1) {
       tp.Tb[0] = w.sbar.p;  // last layer: out = {0e}, T-bar = s-bar
     } else {
@@ -1135,7 +1333,7 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
         tp.Tb[o] = dst;
       }
     }
-    if (!fused_bwd) tp_dispatch(M.n_layers, M.lmax, k, 1, tp, st, &c->prof, L);
+    if (!fused_bwd && !(last && fused_last)) tp_dispatch(M.n_layers, M.lmax, k, 1, tp, st, &c->prof, L);
     {
       GemmArgs g = G(w.wbar.p, L.nw, M.w.envT[k], 128, L.nw, xbn, 1.f / std::sqrt(128.f), last ? EPI_R2 : EPI_ACC);
       if (last) {  // xbar^{L-1} = env^T part + Ebar (a w_out + u (b/sqrt(fan)) q_x)

@@ -33,12 +33,13 @@ enum ProfKind : int {
   PK_TPL_FWD,   // fused TP + TP-linear (tcgen05), forward
   PK_TPL_BWD,   // fused TP-linear^T + TP adjoint (tcgen05), backward
   PK_ENV_ADJ,   // Gamma-bar row sums + environment adjoint (fused path)
+  PK_LAST,      // last layer forward + read-out + reverse, one warp per row
   PK_COUNT
 };
 
 inline const char* prof_name(int k) {
   static const char* names[PK_COUNT] = {"wrap", "ghost", "cell", "edge_build", "scan", "geom", "gemm", "tp_fwd",
-                                        "tp_bwd", "energy", "rowdot", "geom_bwd", "force_gather", "verlet", "reduce", "halo", "gamma", "tp_lin_fwd", "tp_lin_bwd", "env_adj"};
+                                        "tp_bwd", "energy", "rowdot", "geom_bwd", "force_gather", "verlet", "reduce", "halo", "gamma", "tp_lin_fwd", "tp_lin_bwd", "env_adj", "last_layer"};
   return (k >= 0 && k < PK_COUNT) ? names[k] : "?";
 }
 
@@ -101,6 +102,12 @@ struct Profiler {
       pool.push_back(r.b);
     }
     pending.clear();
+  }
+  // the per-call paths defer the host-side reading of event pairs until the totals are read
+  // (allegro_profile_read): reading ~1,000 pairs after every MD step left the GPU idle for
+  // milliseconds inside the timed region of small boxes
+  void flush_if_large() {
+    if (pending.size() > 200000) flush();
   }
   void destroy() {
     flush();

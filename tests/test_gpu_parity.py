@@ -296,8 +296,9 @@ def test_profiler_counts_launches(pb):
     assert m.launch_count() == sum(v[3] for v in prof.values()) > 20
     assert prof["gemm"][3] > 0 and prof["gemm"][0] > 0 and prof["gemm"][1] > 0
     # 2 layers x 2 steps: layer 0 runs the fused TP + TP-linear kernels (3xTF32 default), layer 1 the TP kernels
-    assert prof["tp_fwd"][3] + prof["tp_lin_fwd"][3] == prof["tp_bwd"][3] + prof["tp_lin_bwd"][3] == 2 * 2
+    # and layer 1 (the last) the fused last-layer kernel (forward + read-out + reverse)
     assert prof["tp_lin_fwd"][3] == prof["gamma"][3] == prof["tp_lin_bwd"][3] == prof["env_adj"][3] == 2
+    assert prof["last_layer"][3] == 2 and prof["tp_fwd"][3] == prof["tp_bwd"][3] == prof["energy"][3] == 0
 
 
 def test_nvt_step_matches_oracle(pb):
@@ -356,20 +357,28 @@ def test_resnet_contraction_deterministic(pb):
 
 @pytest.mark.parametrize("cfg", ["C1", "C5"])
 def test_fused_tp_linear_matches_unfused(pb, cfg, monkeypatch):
-    """The fused TP + TP-linear kernel (tp_fused.cu) computes the same T (same FMA order) and the
-    same 3xTF32 contraction as the unfused TP kernel + GEMM: energies and forces agree to
-    rounding (in practice bit for bit), C1 (2, 1) and the bench's C5 (3, 1) at full size."""
+    """The fused kernels against the unfused path: the last layer in one kernel (k_last) is
+    bit-identical; the fused TP + TP-linear forward (same FMA order, same 3xTF32 contraction) gives
+    bit-identical energies; the fused backward re-associates the Gamma-bar row sum (per edge,
+    then over the row), so forces agree to rounding.  C1 (2, 1) and the bench's C5 (3, 1)."""
     s = configs.system(cfg)
     wf = configs.weight_file(cfg)
     m = pb.Allegro(wf, s.box, precision=pb.PREC_3XTF32, n_atoms=s.n)
     monkeypatch.setenv("ALLEGRO_FUSED_TP", "0")
+    monkeypatch.setenv("ALLEGRO_FUSED_TP_BWD", "0")
+    monkeypatch.setenv("ALLEGRO_FUSED_LAST", "0")
     e0, ea0, f0 = m.compute_energy_forces(s.pos, s.species)
+    # the fused last layer alone: the same arithmetic in the same order (bit-identical)
+    monkeypatch.setenv("ALLEGRO_FUSED_LAST", "1")
+    eL, eaL, fL = m.compute_energy_forces(s.pos, s.species)
+    assert eL == e0 and np.array_equal(eaL, ea0) and np.array_equal(fL, f0)
     monkeypatch.setenv("ALLEGRO_FUSED_TP", "1")
+    monkeypatch.setenv("ALLEGRO_FUSED_TP_BWD", "1")
     m.profile(True)
     e1, ea1, f1 = m.compute_energy_forces(s.pos, s.species)
     assert m.profile_read()["tp_lin_fwd"][3] > 0
     m.profile(False)
     print(f"{cfg}: fused vs unfused bitwise: E {e1 == e0}, F {np.array_equal(f1, f0)}, "
           f"max|dF| = {np.abs(f1 - f0).max():.3g}")
-    assert abs(e1 - e0) <= 1e-9 * np.abs(ea0).sum()
+    assert e1 == e0 and np.array_equal(ea1, ea0)
     assert np.abs(f1 - f0).max() <= 1e-6
