@@ -531,9 +531,10 @@ void launch(const TplIO& io, cudaStream_t st, Profiler* prof) {
 constexpr int kBTp = 12;
 constexpr int kBSplit0 = kBTp;
 constexpr int kBCopy0 = kBTp + 4;
-constexpr int kBProd = kBTp + 8;
+constexpr int kBProd = kBTp + 8;   // ring B producer (the TP inputs)
 constexpr int kBMma = kBTp + 9;
-constexpr int kBThreads = 32 * (kBTp + 10);
+constexpr int kBProdA = kBTp + 10; // ring A producer (the MMA chain's V-bar / s-bar boxes) + W images
+constexpr int kBThreads = 32 * (kBTp + 11);
 constexpr int kBAStages = 3;
 constexpr int kBGA = 8;  // Gamma rows staged per tile (atoms); wider spans read from L2
 
@@ -554,16 +555,19 @@ struct Bz {
     for (int q = 0; q < o; ++q) b += ir_dim(A.out.v[q]) * kBoxBytes;
     return b;
   }
+  // ring A stage (split / MMA / copy chain): V-bar^{k+1} boxes, one per (irrep, m3), then s-bar boxes
   static constexpr int sb_off() { return vb_off(NO); }
-  static constexpr int in_off() { return sb_off() + A.n_s * kBoxBytes; }
-  static constexpr int v_off(int i) { return in_off() + F::v_off(i); }
-  static constexpr int y_off() { return in_off() + AR::NENV * kBoxBytes; }
-  static constexpr int yb_off() { return y_off() + kTile * DSH * 4; }  // K == 0: Y-bar rows (read-modify-write)
-  static constexpr int g_off() { return K == 0 ? yb_off() + kTile * DSH * 4 : in_off() + F::v_off(NI); }
+  static constexpr int a_bytes() { return sb_off() + A.n_s * kBoxBytes; }
+  // ring B stage (the TP warps): V^k per in irrep (k >= 1) or w_edge boxes + Y + old Y-bar (k = 0),
+  // the Gamma rows of the tile's centres, and the header (centre slots, edge count, first centre)
+  static constexpr int v_off(int i) { return F::v_off(i); }
+  static constexpr int y_off() { return AR::NENV * kBoxBytes; }
+  static constexpr int yb_off() { return y_off() + kTile * DSH * 4; }
+  static constexpr int g_off() { return K == 0 ? yb_off() + kTile * DSH * 4 : F::v_off(NI); }
   static constexpr int h_off() { return g_off() + kBGA * DSH * 128; }
-  static constexpr int stage_bytes() { return (h_off() + 256 + 1023) / 1024 * 1024; }
+  static constexpr int b_bytes() { return (h_off() + 256 + 1023) / 1024 * 1024; }
+  static constexpr int b_tma_bytes() { return K == 0 ? AR::NENV * kBoxBytes : F::v_off(NI); }
   static constexpr int tb_bytes() { return kTile * DT * 128; }  // two 16-edge halves, double-buffered in turn
-  static constexpr int tma_bytes() { return in_off() + (K == 0 ? AR::NENV * kBoxBytes : F::v_off(NI)); }
 };
 
 template <int NL, int LMAX, int K>
@@ -581,7 +585,7 @@ struct TpbParams {
   const float* wimg[kMaxIr];
   uint32_t wbytes[kMaxIr];
   float scale[kMaxIr];
-  int n_tiles, stages;
+  int n_tiles, sa, sb;  // ring depths
 };
 
 struct TpbMaps {
@@ -604,11 +608,12 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
 #pragma unroll
   for (int o = 0; o < kMaxIr; ++o) woff[o + 1] = woff[o] + (o < NO ? p.wbytes[o] : 0u);
   unsigned char* w_img = base;
-  unsigned char* stage0 = base + ((woff[NO] + 1023u) & ~1023u);
-  unsigned char* tbt = stage0 + (size_t)p.stages * B::stage_bytes();
+  unsigned char* ringA = base + ((woff[NO] + 1023u) & ~1023u);
+  unsigned char* ringB = ringA + (size_t)p.sa * B::a_bytes();
+  unsigned char* tbt = ringB + (size_t)p.sb * B::b_bytes();
   uint64_t* bars = reinterpret_cast<uint64_t*>(tbt + B::tb_bytes());
-  uint64_t* in_full = bars;           // [4] the tile's V-bar and s-bar boxes (split / MMA / copy chain)
-  uint64_t* in_empty = in_full + 4;
+  uint64_t* in_full = bars;           // [4] ring A: the tile's V-bar and s-bar boxes
+  uint64_t* in_empty = in_full + 4;   // [4] released by the split and copy warps
   uint64_t* a_full = in_empty + 4;
   uint64_t* a_empty = a_full + kBAStages;
   uint64_t* acc_full = a_empty + kBAStages;
@@ -616,13 +621,14 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
   uint64_t* tb_full = acc_empty + 2;  // [2] T-bar halves (edges 0-15, 16-31)
   uint64_t* tb_empty = tb_full + 2;   // [2]
   uint64_t* w_full = tb_empty + 2;
-  uint64_t* in_full_b = w_full + 1;   // [4] the TP inputs (V^k or w_edge, Y, Y-bar, Gamma)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(in_full_b + 4);
+  uint64_t* in_full_b = w_full + 1;   // [4] ring B: the TP inputs
+  uint64_t* in_empty_b = in_full_b + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(in_empty_b + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s)
-      mbar_init(in_full + s, 1), mbar_init(in_full_b + s, 1), mbar_init(in_empty + s, kBTp + 8);
+    for (int s = 0; s < p.sa; ++s) mbar_init(in_full + s, 1), mbar_init(in_empty + s, 8);
+    for (int s = 0; s < p.sb; ++s) mbar_init(in_full_b + s, 1), mbar_init(in_empty_b + s, kBTp);
     for (int s = 0; s < kBAStages; ++s) mbar_init(a_full + s, 4), mbar_init(a_empty + s, 1);
     for (int b = 0; b < 2; ++b) mbar_init(acc_full + b, 1), mbar_init(acc_empty + b, 4);
     for (int h = 0; h < 2; ++h) mbar_init(tb_full + h, 4), mbar_init(tb_empty + h, kBTp);
@@ -638,12 +644,31 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
   const int n_my = p.n_tiles > (int)blockIdx.x ? (p.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   auto tile_e0 = [&](int t) -> int64_t { return (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kTile; };
 
-  if (warp == kBProd) {
-    // ---------------- producer ----------------
+  if (warp == kBProdA) {
+    // ---------------- ring A producer: the MMA chain's operands (and the W images) ----------------
     if (lane == 0) {
       mbar_expect_tx(w_full, woff[NO]);
       for (int o = 0; o < NO; ++o) bulk_load(w_img + woff[o], p.wimg[o], p.wbytes[o], w_full);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = 0; t < n_my; ++t) {
+        const int64_t e0 = tile_e0(t);
+        mbar_wait(in_empty + s, ph ^ 1);
+        unsigned char* st = ringA + (size_t)s * B::a_bytes();
+        mbar_expect_tx(in_full + s, (uint32_t)B::a_bytes());
+        static_for<NO>([&](auto O) {
+          constexpr int o = decltype(O)::value;
+          static_for<ir_dim(A.out.v[o])>([&](auto M) {
+            constexpr int m = decltype(M)::value;
+            tma_load_3d(st + B::vb_off(o) + m * kBoxBytes, &maps.vb[o], 0, m, (int)e0, in_full + s);
+          });
+        });
+        for (int q = 0; q < A.n_s; ++q) tma_load_2d(st + B::sb_off() + q * kBoxBytes, &maps.sb, 32 * q, (int)e0, in_full + s);
+        if (++s == p.sa) s = 0, ph ^= 1;
+      }
     }
+  } else if (warp == kBProd) {
+    // ---------------- ring B producer: the TP inputs ----------------
     int s = 0;
     uint32_t ph = 0;
     auto load_ci = [&](int t) -> int {
@@ -656,8 +681,8 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
       const int nv = (int)(p.n_e - e0 < kTile ? p.n_e - e0 : kTile);
       const int ci = ci_next;
       ci_next = load_ci(t + 1);
-      mbar_wait(in_empty + s, ph ^ 1);
-      unsigned char* st = stage0 + (size_t)s * B::stage_bytes();
+      mbar_wait(in_empty_b + s, ph ^ 1);
+      unsigned char* st = ringB + (size_t)s * B::b_bytes();
       int* hdr = reinterpret_cast<int*>(st + B::h_off());
       const int a_lo = __shfl_sync(0xffffffffu, ci, 0);
       const int a_hi = __shfl_sync(0xffffffffu, ci, nv - 1);
@@ -667,21 +692,10 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
       if (lane == 0) {
         const int span = a_hi - a_lo + 1;
         const uint32_t gbytes = (uint32_t)(span < kBGA ? span : kBGA) * DSH * 128;
-        // the MMA chain's operands first, on their own barrier; then the TP inputs
-        mbar_expect_tx(in_full + s, (uint32_t)B::in_off());
-        const uint32_t bytes_b = (uint32_t)(B::tma_bytes() - B::in_off()) + gbytes + (K == 0 ? 2u * (uint32_t)nv * DSH * 4 : 0u);
-        mbar_expect_tx(in_full_b + s, bytes_b);
-        static_for<NO>([&](auto O) {
-          constexpr int o = decltype(O)::value;
-          static_for<ir_dim(A.out.v[o])>([&](auto M) {
-            constexpr int m = decltype(M)::value;
-            tma_load_3d(st + B::vb_off(o) + m * kBoxBytes, &maps.vb[o], 0, m, (int)e0, in_full + s);
-          });
-        });
-        for (int q = 0; q < A.n_s; ++q) tma_load_2d(st + B::sb_off() + q * kBoxBytes, &maps.sb, 32 * q, (int)e0, in_full + s);
+        mbar_expect_tx(in_full_b + s, (uint32_t)B::b_tma_bytes() + gbytes + (K == 0 ? 2u * (uint32_t)nv * DSH * 4 : 0u));
         if constexpr (K == 0) {
 #pragma unroll
-          for (int l = 0; l < AR::NENV; ++l) tma_load_2d(st + B::in_off() + l * kBoxBytes, &maps.in[0], 32 * l, (int)e0, in_full_b + s);
+          for (int l = 0; l < AR::NENV; ++l) tma_load_2d(st + l * kBoxBytes, &maps.in[0], 32 * l, (int)e0, in_full_b + s);
           bulk_load(st + B::y_off(), p.Y + e0 * DSH, (uint32_t)nv * DSH * 4, in_full_b + s);
           bulk_load(st + B::yb_off(), p.ybar + e0 * DSH, (uint32_t)nv * DSH * 4, in_full_b + s);
         } else {
@@ -693,7 +707,7 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
         }
         bulk_load(st + B::g_off(), p.G + (int64_t)a_lo * DSH * 32, gbytes, in_full_b + s);
       }
-      if (++s == p.stages) s = 0, ph ^= 1;
+      if (++s == p.sb) s = 0, ph ^= 1;
     }
   } else if (warp >= kBSplit0 && warp < kBSplit0 + 4) {
     // ---------------- split: V-bar rows -> TF32 hi / lo in TMEM ----------------
@@ -702,7 +716,7 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
     uint32_t ph = 0, aph = 0;
     for (int t = 0; t < n_my; ++t) {
       mbar_wait(in_full + s, ph);
-      const unsigned char* st = stage0 + (size_t)s * B::stage_bytes();
+      const unsigned char* st = ringA + (size_t)s * B::a_bytes();
       static_for<NO>([&](auto O) {
         constexpr int o = decltype(O)::value;
         constexpr int B0 = F::base(o);
@@ -736,7 +750,7 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(in_empty + s);
-      if (++s == p.stages) s = 0, ph ^= 1;
+      if (++s == p.sa) s = 0, ph ^= 1;
     }
   } else if (warp == kBMma) {
     // ---------------- MMA issuer: D_o = A_o W_o^T ----------------
@@ -784,7 +798,7 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
       mbar_wait(acc_full + buf, (uint32_t)(t >> 1) & 1u);
       tc_fence_after();
       mbar_wait(in_full + s, ph);                      // (complete: its s-bar boxes are read here)
-      const unsigned char* st = stage0 + (size_t)s * B::stage_bytes();
+      const unsigned char* st = ringA + (size_t)s * B::a_bytes();
       const int e = lane;
       // two passes over the accumulator: edges 0-15 into half 0, then 16-31 into half 1, so that the
       // TP warps work on one half while the other is refilled
@@ -828,7 +842,7 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(in_empty + s);
-      if (++s == p.stages) s = 0, ph ^= 1;
+      if (++s == p.sa) s = 0, ph ^= 1;
     }
   } else if (warp < kBTp) {
     // ---------------- TP adjoint: warp per edge, lane = channel ----------------
@@ -837,9 +851,8 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
     uint32_t ph = 0;
     for (int t = 0; t < n_my; ++t) {
       const int64_t e0 = tile_e0(t);
-      mbar_wait(in_full + s, ph);
       mbar_wait(in_full_b + s, ph);
-      const unsigned char* st = stage0 + (size_t)s * B::stage_bytes();
+      const unsigned char* st = ringB + (size_t)s * B::b_bytes();
       const int* hdr = reinterpret_cast<const int*>(st + B::h_off());
       const int nv = hdr[32], a_lo = hdr[33];
       for (int h = 0; h < 2; ++h) {
@@ -862,7 +875,7 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
         if constexpr (K == 0) {
 #pragma unroll
           for (int l = 0; l < AR::NENV; ++l)
-            we[l] = *reinterpret_cast<const float*>(st + B::in_off() + l * kBoxBytes + e * 128 + (((c >> 2) ^ (e & 7)) << 4) + (c & 3) * 4);
+            we[l] = *reinterpret_cast<const float*>(st + l * kBoxBytes + e * 128 + (((c >> 2) ^ (e & 7)) << 4) + (c & 3) * 4);
 #pragma unroll
           for (int m = 0; m < DSH; ++m) yv[m] = reinterpret_cast<const float*>(st + B::y_off())[e * DSH + m];
 #pragma unroll
@@ -933,8 +946,8 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(in_empty + s);
-      if (++s == p.stages) s = 0, ph ^= 1;
+      if (lane == 0) mbar_arrive(in_empty_b + s);
+      if (++s == p.sb) s = 0, ph ^= 1;
     }
   }
   __syncthreads();
@@ -997,11 +1010,13 @@ void launch_bwd(const TpbIO& io, cudaStream_t st, Profiler* prof) {
       maps.in[i] = tc_map_f32(io.vin[i], 2, dims, strides, box);
     }
   }
-  const size_t fixed = 1024 + ((wsum + 1023) / 1024) * 1024 + B::tb_bytes() + 512;
-  int stages = (int)std::min<size_t>(4, (kSmemLimit - fixed) / B::stage_bytes());
-  if (stages < 2) throw CudaError("tpl_bwd: shared memory too small for two input stages");
-  p.stages = stages;
-  const size_t smem = fixed + (size_t)stages * B::stage_bytes();
+  const size_t fixed = 1024 + ((wsum + 1023) / 1024) * 1024 + B::tb_bytes() + 512 + 2 * (size_t)B::b_bytes();
+  // ring B: two stages; ring A (the latency-critical MMA chain) as deep as the rest allows (<= 4)
+  const int sa = (int)std::min<size_t>(4, (kSmemLimit - fixed) / B::a_bytes());
+  if (sa < 2) throw CudaError("tpl_bwd: shared memory too small for two stages per ring");
+  p.sa = sa;
+  p.sb = 2;
+  const size_t smem = fixed + (size_t)sa * B::a_bytes();
   int dev = 0;
   ALG_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};
