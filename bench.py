@@ -247,6 +247,8 @@ def main():
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: split the config's box over the GPUs (default: replicate it per GPU)")
     ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "fp32", "tf32"])
+    ap.add_argument("--skin", type=float, default=0.0,
+                    help="neighbour-list skin (A); the list is still rebuilt every step (NEXT-4 A/B of its cost)")
     ap.add_argument("--clock-interval-ms", type=int, default=200,
                     help="nvidia-smi sampling period during the timed region (0: off)")
     args = ap.parse_args()
@@ -282,7 +284,7 @@ def main():
     stream = torch.cuda.current_stream()
     prec = {"3xtf32": pb.PREC_3XTF32, "fp32": pb.PREC_FP32, "tf32": pb.PREC_TF32}[args.precision]
     m = pb.Allegro(wf, s.box, device=local, n_atoms=s.n, stream=stream.cuda_stream, precision=prec, rank=rank,
-                   world_size=ws, nccl_id=nccl_id, grid=grid)
+                   world_size=ws, nccl_id=nccl_id, grid=grid, skin=args.skin)
     m.md_set_state(s.species, s.pos, s.vel)
     r_w = m.md_step(args.warmup, DT_FS)
     edges_first = int(r_w.n_edges)

@@ -139,3 +139,18 @@ def test_single_pass_tf32_reported_not_gated(pb):
     rel_e = abs(e - ref["energy"]) / np.abs(ref["e_atom"]).sum()
     print(f"TF32 single pass on C2: max|dF| = {err:.3g} eV/A (bar 1e-4), rel dE = {rel_e:.3g} (bar 1e-5)")
     assert np.all(np.isfinite(F)) and err < 0.1
+
+
+def test_skin_edges_contribute_exact_zeros(pb):
+    """NEXT-4: a neighbour-list skin adds edges with r_c < d <= r_c + skin; the
+    envelope makes u = u' = 0 there, so x = w = V = 0 on them and their g is exactly 0 (§8(c)
+    "exact zero beyond r_c").  Energies, per-atom energies and forces with skin 0.5 A equal skin 0
+    bit for bit (the extra terms are exact zeros in every fixed-order sum)."""
+    s = configs.system("C2")
+    wf = configs.weight_file("C2")
+    m0 = pb.Allegro(wf, s.box)
+    m1 = pb.Allegro(wf, s.box, skin=0.5)
+    e0, a0, f0 = m0.compute_energy_forces(s.pos, s.species)
+    e1, a1, f1 = m1.compute_energy_forces(s.pos, s.species)
+    assert len(m1.get_edges()[0]) > 1.2 * len(m0.get_edges()[0])
+    assert e1 == e0 and np.array_equal(a1, a0) and np.array_equal(f1, f0)
