@@ -184,7 +184,7 @@ void allegro_destroy(allegro_ctx* c) {
   for (auto& b : c->scan_lv) b.release();
   Workspace& w = c->ws;
   for (DBuf<float>* b : {&w.z, &w.a1, &w.h1, &w.a2, &w.h2, &w.m, &w.u, &w.Y, &w.xa, &w.xb, &w.T, &w.xbar_a, &w.xbar_b,
-                         &w.sbar, &w.vbar_a, &w.vbar_b, &w.wbar, &w.ybar, &w.ubar, &w.zbar, &w.ab2, &w.ab1, &w.ee, &w.ebar, &w.gp})
+                         &w.sbar, &w.vbar_a, &w.vbar_b, &w.wbar, &w.ybar, &w.ubar, &w.zbar, &w.ab2, &w.ab1, &w.ee, &w.ebar, &w.gp, &w.dotp})
     b->release();
   for (int k = 0; k < kMaxLayers; ++k) {
     w.w[k].release();

@@ -79,6 +79,7 @@ struct DevWeights {
   Wt lat[kMaxLayers];             // [128 + n_s*C][128], scalar rows in (q, c) order
   Wt latT_x[kMaxLayers];          // [128][128]
   Wt latT_s[kMaxLayers];          // [128][n_s*C]
+  Wt latenvT[kMaxLayers];         // [128 + nw][128]: latT_x stacked over envT (the merged x-bar contraction)
   float* wout = nullptr;          // [128] = W_o1 W_o2 / (sqrt(128) sqrt(32))
   // last layer folded into the linear read-out: q = W_lat(L-1) w_out
   float* q_last = nullptr;        // [fan_lat(L-1)] device row order (x rows, then scalar rows (q, c))
@@ -103,7 +104,7 @@ struct Workspace {
   DBuf<float> xa, xb;
   DBuf<float> w[kMaxLayers], h[kMaxLayers], V[kMaxLayers], G[kMaxLayers];
   DBuf<float> T;
-  DBuf<float> xbar_a, xbar_b, sbar, vbar_a, vbar_b, wbar, ybar, ubar, zbar, ab2, ab1, ee, ebar, gp;
+  DBuf<float> xbar_a, xbar_b, sbar, vbar_a, vbar_b, wbar, ybar, ubar, zbar, ab2, ab1, ee, ebar, gp, dotp;
 };
 
 // Spatial domain decomposition (§2.4).

@@ -19,6 +19,7 @@ enum GemmEpi : int {
   EPI_ADDX = 7,       // C = s acc + X
   EPI_DSILU = 8,      // C = (u ? u[r] : 1) s acc SiLU'(X)
   EPI_R2 = 9,         // C = s acc + rs2[r] (vec1[col] + u[r] vec2[col])   (rank-2 affine term)
+  EPI_ACCX = 10,      // C = s acc + alpha X   (the latent-transpose + env-transpose contraction, one K)
 };
 
 struct GemmArgs {
@@ -46,6 +47,13 @@ struct GemmArgs {
   int epi = EPI_STORE;
   int silu_a = 0;  // A holds pre-activations: the contraction multiplies SiLU(A) (applied on load)
   int single_pass = 0;  // tcgen05 path: one TF32 MMA (a_hi w_hi) instead of 3xTF32 (ALLEGRO_PREC_TF32)
+  // tcgen05 path: A rows scaled before the hi/lo split -- columns [0, K1) by arow_c1 * arow_u[r],
+  // columns [K1, K) by arow_c2 (two contractions of different scale in one accumulator)
+  const float* arow_u = nullptr;
+  float arow_c1 = 1.f, arow_c2 = 1.f;
+  // row-dot of an output split over N-tiles: each tile writes its partial to dot_part[r][tile] and
+  // the host adds dot_out[r] += dot_coef sum_tile dot_part[r][tile] (fixed order) after the launch
+  float* dot_part = nullptr;
 };
 
 void gemm(const GemmArgs& g, cudaStream_t st, Profiler* prof);

@@ -228,6 +228,22 @@ __device__ __forceinline__ void pf_lines(const float* base, int nlines, int lane
   if (lane < nlines) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + lane * kC));
 }
 
+// L2 prefetch of edge e's environment operands: the w_env rows (lanes 0 .. NENV-1), the Y and Y-bar
+// lines (the next two lanes); issued a few edges ahead of the register pipeline of the row loops,
+// it holds no registers (the row kernels have one edge of loads in flight per warp otherwise)
+#ifndef ALG_ROW_PFD
+#define ALG_ROW_PFD 3
+#endif
+template <int NL, int LMAX, int K>
+__device__ __forceinline__ void prefetch_env(const TpArgs& t, int64_t e, int lane, bool ybar) {
+  using AR = Arch<NL, LMAX, K>;
+  const float* p = nullptr;
+  if (lane < AR::NENV) p = t.w + e * AR::NW + AR::ENV_OFF + lane * kC;
+  else if (lane == AR::NENV) p = t.Y + e * AR::DSH;
+  else if (lane == AR::NENV + 1 && ybar) p = t.ybar + e * AR::DSH;
+  if (p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <int NL, int LMAX, int K, bool TB>
 __device__ __forceinline__ void prefetch_edge(const TpArgs& t, int64_t e, int lane) {
   using AR = Arch<NL, LMAX, K>;
@@ -307,9 +323,12 @@ __global__ void __launch_bounds__(128) k_tp_fwd(TpArgs t) {
   if (r1 > r0) {
     EnvIn<NL, LMAX, K> nx;
     fetch_env<NL, LMAX, K>(t, r0, lane, nx);
+    for (int64_t e = r1 - 1 < r0 + ALG_ROW_PFD ? r1 - 1 : r0 + ALG_ROW_PFD; e > r0; --e)
+      prefetch_env<NL, LMAX, K>(t, e, lane, false);
     for (int64_t e = r0; e < r1; ++e) {
       const EnvIn<NL, LMAX, K> cur = nx;
       fetch_env<NL, LMAX, K>(t, e + 1 < r1 ? e + 1 : e, lane, nx);
+      if (e + 1 + ALG_ROW_PFD < r1) prefetch_env<NL, LMAX, K>(t, e + 1 + ALG_ROW_PFD, lane, false);
 #pragma unroll
       for (int m = 0; m < AR::DSH; ++m) G[m] = fmaf(cur.we[lm_l(m)], cur.y[m], G[m]);
     }
@@ -400,9 +419,12 @@ __device__ __forceinline__ void env_adjoint(const TpArgs& t, int64_t r0, int64_t
   };
   EnvB en;
   fetch_envb(r0, en);
+  for (int64_t e = r1 - 1 < r0 + ALG_ROW_PFD ? r1 - 1 : r0 + ALG_ROW_PFD; e > r0; --e)
+    prefetch_env<NL, LMAX, K>(t, e, lane, true);
   for (int64_t e = r0; e < r1; ++e) {
     const EnvB cur = en;
     fetch_envb(e + 1 < r1 ? e + 1 : e, en);
+    if (e + 1 + ALG_ROW_PFD < r1) prefetch_env<NL, LMAX, K>(t, e + 1 + ALG_ROW_PFD, lane, true);
     float wb[AR::NENV];
 #pragma unroll
     for (int l = 0; l < AR::NENV; ++l) wb[l] = 0.f;
@@ -513,11 +535,15 @@ __global__ void __launch_bounds__(128) k_env_adj(TpArgs t) {
   float Gb[AR::DSH], nx[AR::DSH];
 #pragma unroll
   for (int m = 0; m < AR::DSH; ++m) Gb[m] = 0.f, nx[m] = t.gp[(r0 * AR::DSH + m) * kC + lane];
-  for (int64_t e = r0; e < r1; ++e) {  // pipelined one edge ahead
+  for (int64_t e = r0 + 1; e < r1 && e <= r0 + ALG_ROW_PFD; ++e)
+    if (lane < AR::DSH) asm volatile("prefetch.global.L2 [%0];" ::"l"(t.gp + (e * AR::DSH + lane) * kC));
+  for (int64_t e = r0; e < r1; ++e) {  // pipelined one edge ahead (+ L2 prefetch further ahead)
     float cur[AR::DSH];
 #pragma unroll
     for (int m = 0; m < AR::DSH; ++m) cur[m] = nx[m];
     const int64_t en = e + 1 < r1 ? e + 1 : e;
+    if (lane < AR::DSH && e + 1 + ALG_ROW_PFD < r1)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(t.gp + ((e + 1 + ALG_ROW_PFD) * AR::DSH + lane) * kC));
 #pragma unroll
     for (int m = 0; m < AR::DSH; ++m) nx[m] = t.gp[(en * AR::DSH + m) * kC + lane];
 #pragma unroll
@@ -605,9 +631,26 @@ __global__ void __launch_bounds__(128) k_last(LastArgs a) {
   };
   In nx;
   fetch(r0, nx);
+  auto pf = [&](int64_t e) {  // V rows (lanes 0 .. DIN-1) and the x row (4 lines) of edge e
+    const float* q = nullptr;
+    if (lane < AR::DIN) {
+      int ii2 = 0, m = lane;
+      static_for<A.in.n>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        constexpr int dim = ir_dim(A.in.v[i]);
+        constexpr int off = A.in.off(i);
+        if (lane >= off && lane < off + dim) ii2 = AR::v_base(i), m = lane - off, q = t.V + (int64_t)ii2 * t.e_cap + (e * dim + m) * kC;
+      });
+    } else if (lane < AR::DIN + 4) {
+      q = a.x + e * kD + (lane - AR::DIN) * 32;
+    }
+    if (q) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+  };
+  for (int64_t e = r0 + 1; e < r1 && e <= r0 + ALG_ROW_PFD; ++e) pf(e);
   for (int64_t e = r0; e < r1; ++e) {
     const In cur = nx;
     fetch(e + 1 < r1 ? e + 1 : e, nx);
+    if (e + 1 + ALG_ROW_PFD < r1) pf(e + 1 + ALG_ROW_PFD);
     float v[AR::DIN];
     expand_v<NL, LMAX, K>(cur.v, v);
     // T = s (scalar outputs only)
@@ -1032,7 +1075,7 @@ void run_gemm(const Model& M, const GemmArgs& g_in, const Wt& w, cudaStream_t st
     return !e || std::atoi(e) != 0;
   }();
   if (tc_mode(M.precision) &&
-      (!g.dotv || (fuse_dot && w.tc.n_tiles == 1 && (fuse_r2 || g.epi != EPI_R2)))) {
+      (!g.dotv || (g.dot_part && fuse_dot) || (fuse_dot && w.tc.n_tiles == 1 && (fuse_r2 || g.epi != EPI_R2)))) {
     tc_gemm(g, w.tc, st, prof);  // the row-dot (if any) is fused into the epilogue
     return;
   }
@@ -1066,7 +1109,7 @@ size_t floats_per_edge(const Model& M) {
     nsmax = std::max(nsmax, (size_t)L.A.n_s * kC);
   }
   f += tmax + 2 * 128 + nsmax + 2 * vmax + nwmax + dsh + 1 + 64 + 32 + 1;
-  f += dsh * kC;  // gp (fused backward)
+  f += dsh * kC + 4;  // gp (fused backward), row-dot partials
   return f;
 }
 
@@ -1106,6 +1149,7 @@ void reserve_ws(allegro_ctx* c, size_t e_cap, size_t a_cap) {
   w.ab1.reserve(e_cap * 32);
   w.ebar.reserve(e_cap);
   w.gp.reserve(e_cap * dsh * kC);
+  w.dotp.reserve(e_cap * 4);  // row-dot partials of a contraction split over N-tiles
   w.e_cap = e_cap;
   w.a_cap = a_cap;
 }
@@ -1255,13 +1299,21 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     const LayerInfo& L = M.L[k];
     const bool last = k == M.n_layers - 1;
     const float sl = 1.f / std::sqrt((float)L.fan_lat);
+    // merged x-bar contraction (3xTF32): the latent transpose and the env transpose of this layer
+    // accumulate in ONE contraction over K = 128 + nw (A = [b u x-bar^{k+1} / sqrt(fan) | w-bar / sqrt(D)],
+    // rows scaled before the TF32 split), so the partial x-bar^k never round-trips HBM
+    const char* mx_env = std::getenv("ALLEGRO_MERGE_XBAR");
+    const bool merge_x = !last && M.precision == ALLEGRO_PREC_3XTF32 && (!mx_env || std::atoi(mx_env) != 0);
     if (!last) {
-      GemmArgs g = G(xb, 128, M.w.latT_x[k], 128, 128, xbn, sl, EPI_URESID);
-      g.X = xb;
-      g.u = w.u.p;
-      g.alpha = kResA;
-      g.beta = kResB;
-      run_gemm(M, g, *last_w, st, &c->prof);
+      GemmArgs g;
+      if (!merge_x) {
+        g = G(xb, 128, M.w.latT_x[k], 128, 128, xbn, sl, EPI_URESID);
+        g.X = xb;
+        g.u = w.u.p;
+        g.alpha = kResA;
+        g.beta = kResB;
+        run_gemm(M, g, *last_w, st, &c->prof);
+      }
       g = G(xb, 128, M.w.latT_s[k], L.A.n_s * kC, 128, w.sbar.p, sl, EPI_USCALE);
       g.u = w.u.p;
       g.beta = kResB;
@@ -1334,7 +1386,22 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
       }
     }
     if (!fused_bwd && !(last && fused_last)) tp_dispatch(M.n_layers, M.lmax, k, 1, tp, st, &c->prof, L);
-    {
+    if (merge_x) {
+      GemmArgs g = G(xb, 128, M.w.latenvT[k], 128, 128 + L.nw, xbn, 1.f, EPI_ACCX);
+      g.K1 = 128;
+      g.A2 = w.wbar.p;
+      g.lda2 = L.nw;
+      g.arow_u = w.u.p;
+      g.arow_c1 = kResB * sl;
+      g.arow_c2 = 1.f / std::sqrt(128.f);
+      g.X = xb;
+      g.alpha = kResA;
+      g.dotv = k >= 1 ? w.h[k - 1].p : w.m.p;
+      g.dot_coef = k >= 1 ? kResB : 1.f;
+      g.dot_out = w.ubar.p;
+      g.dot_part = w.dotp.p;
+      run_gemm(M, g, *last_w, st, &c->prof);
+    } else {
       GemmArgs g = G(w.wbar.p, L.nw, M.w.envT[k], 128, L.nw, xbn, 1.f / std::sqrt(128.f), last ? EPI_R2 : EPI_ACC);
       if (last) {  // xbar^{L-1} = env^T part + Ebar (a w_out + u (b/sqrt(fan)) q_x)
         g.rs2 = w.ebar.p;

@@ -69,6 +69,7 @@ struct TcParams {
   const float* wimg;   // N-tile images (hi | lo), tile_floats apart
   size_t tile_floats;
   int n_tiles;         // CTAs blockIdx % n_tiles = N-tile of the same M-tiles (siblings share A via L2)
+  int n_tiles_total;   // N-tiles of the whole contraction (row-dot partials when > 1)
   int tile_base;       // first N-tile of this launch
   int N_t;             // tile width (multiple of 16)
   int nK;              // K-blocks of 32
@@ -105,6 +106,7 @@ __device__ __forceinline__ void epi_apply(const GemmArgs& g, float* v, const flo
       case EPI_ADDX: out[j] = pv + xin[j]; break;
       case EPI_DSILU: out[j] = ur * pv * dsilu(xin[j]); break;
       case EPI_R2: out[j] = pv + xin[j]; break;  // xin = rs2 (vec1 + u vec2), prepared by the caller
+      case EPI_ACCX: out[j] = pv + g.alpha * xin[j]; break;
       default: out[j] = pv; break;
     }
   }
@@ -330,8 +332,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int row = warp * 32 + lane;  // TMEM lane quarter = warp
     int s = 0, j = 0;
     uint32_t ph = 0, aph = 0;
+    auto row_scale_u = [&](int tt) -> float {  // arow_u of this thread's row of tile tt (loaded a tile ahead)
+      const int64_t rr = (int64_t)(grp + tt * n_grp) * ROWS + row;
+      return (p.g.arow_u != nullptr && tt < n_my && rr < p.g.M) ? __ldg(p.g.arow_u + rr) : 1.f;
+    };
+    float ru_next = row_scale_u(0);
     for (int t = 0; t < n_my; ++t) {
+      const float ru = ru_next;
+      ru_next = row_scale_u(t + 1);
       for (int kb = 0; kb < p.nK; ++kb) {
+        const float rsc = p.g.arow_u == nullptr ? 1.f : (kb < p.nK1 ? p.g.arow_c1 * ru : p.g.arow_c2);
         mbar_wait(raw_full + s, ph);
         const unsigned char* raw = stage0 + (size_t)s * STAGE_BYTES;
         uint32_t hi[32], lo[32];
@@ -342,6 +352,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (p.g.silu_a) {  // pre-activation operand (SiLU(0) = 0 keeps the zero-filled tail zero)
 #pragma unroll
             for (int e = 0; e < 4; ++e) x[e] = silu(x[e]);
+          }
+          if (p.g.arow_u != nullptr) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[e] *= rsc;
           }
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -378,7 +392,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- epilogue warpgroup (warps 4..7) ----------------
     const int q = warp & 3;  // TMEM lane quarter
     const GemmArgs& g = p.g;
-    constexpr bool kX = EPI == EPI_RESID || EPI == EPI_URESID || EPI == EPI_ADDX || EPI == EPI_DSILU;
+    constexpr bool kX = EPI == EPI_RESID || EPI == EPI_URESID || EPI == EPI_ADDX || EPI == EPI_DSILU || EPI == EPI_ACCX;
     constexpr bool kAuxEpi = EPI == EPI_SILU || EPI == EPI_UMUL_SAVE || EPI == EPI_RESID;
     const bool want_aux = kAuxEpi && g.aux != nullptr;
     unsigned char* buf = out_stage + (size_t)(2 * q) * STAGE_OUT_BYTES;  // [8][4 KB]: two slots per warp
@@ -546,7 +560,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if ((lane & 7) == i) mine = t8;
         }
         const int64_t rr = row0 + (lane >> 3) + 4 * (lane & 7);
-        if (rr < g.M) g.dot_out[rr] += g.dot_coef * mine;  // host: one N-tile
+        if (rr < g.M) {
+          if (p.n_tiles_total > 1) g.dot_part[rr * p.n_tiles_total + tile] = mine;  // summed by k_dot_parts
+          else g.dot_out[rr] += g.dot_coef * mine;
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -559,6 +576,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem, p.tmem_cols);
   }
+}
+
+__global__ void k_dot_parts(int64_t M, int nt, const float* __restrict__ part, float coef, float* __restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= M) return;
+  float sdot = part[r * nt];
+  for (int t = 1; t < nt; ++t) sdot += part[r * nt + t];
+  out[r] += coef * sdot;
 }
 
 // ------------------------------------------------------------------ host side
@@ -692,7 +717,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const size_t w_bytes = w.tile_bytes;
   const size_t w_round = (w_bytes + 1023) & ~(size_t)1023;
   const bool has_x = g.epi == EPI_RESID || g.epi == EPI_URESID || g.epi == EPI_ADDX || g.epi == EPI_DSILU ||
-                     g.epi == EPI_ACC;
+                     g.epi == EPI_ACC || g.epi == EPI_ACCX;
   const size_t out_bytes = 8 * (size_t)STAGE_OUT_BYTES + (has_x ? (size_t)X_STAGES * X_STAGE_BYTES : 0);
   int stages = (int)((SMEM_LIMIT - SMEM_RESERVE - w_round - out_bytes) / STAGE_BYTES);
   stages = std::min(stages, g_tc_tuning.max_stages);
@@ -703,7 +728,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
     if (!g_attr_set[dev]) {  // the function attribute is per device
 #define ALG_SET(e) ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<e>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
       ALG_SET(EPI_STORE) ALG_SET(EPI_SILU) ALG_SET(EPI_UMUL_SAVE) ALG_SET(EPI_RESID) ALG_SET(EPI_URESID)
-      ALG_SET(EPI_USCALE) ALG_SET(EPI_ACC) ALG_SET(EPI_ADDX) ALG_SET(EPI_DSILU) ALG_SET(EPI_R2)
+      ALG_SET(EPI_USCALE) ALG_SET(EPI_ACC) ALG_SET(EPI_ADDX) ALG_SET(EPI_DSILU) ALG_SET(EPI_R2) ALG_SET(EPI_ACCX)
 #undef ALG_SET
       ALG_CUDA(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev));
       g_attr_set[dev] = true;
@@ -740,7 +765,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   p.store_hint = g_tc_tuning.store_hint;
   const CUtensorMap mC = p.tma_store ? make_map(g.C, g.M, g.N, g.N, 32) : mA;
   const CUtensorMap mAux = (p.tma_store && aux_epi) ? make_map(g.aux, g.M, g.N, g.N, 32) : mA;
-  if (g.dotv && w.n_tiles != 1) throw CudaError("tc_gemm: the fused row-dot needs a single N-tile");
+  if (g.dotv && w.n_tiles != 1 && !g.dot_part) throw CudaError("tc_gemm: a row-dot over N-tiles needs dot_part");
   // one launch; CTA b handles N-tile b % n_tiles of M-tile group b / n_tiles
   // (ALLEGRO_TC_COSCHED=0: one launch per N-tile, for A/B measurements)
   static const bool cosched = [] {
@@ -753,6 +778,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const double mn = (double)g.M * g.N;
   const int n_io = 1 + (g.aux != nullptr) + (g.X != nullptr) + (g.epi == EPI_ACC);
   p.n_tiles = per_launch;
+  p.n_tiles_total = w.n_tiles;
   p.wimg = w.dev;
   p.tile_floats = w.tile_bytes / 4;
   for (int tb = 0; tb < w.n_tiles; tb += per_launch) {
@@ -767,10 +793,15 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
 #define ALG_EPI(e) \
   case e: k_tc_gemm<e><<<grid, TC_THREADS, smem, st>>>(mA, mA2, mX, mC, mAux, p); break;
       ALG_EPI(EPI_STORE) ALG_EPI(EPI_SILU) ALG_EPI(EPI_UMUL_SAVE) ALG_EPI(EPI_RESID) ALG_EPI(EPI_URESID)
-      ALG_EPI(EPI_USCALE) ALG_EPI(EPI_ACC) ALG_EPI(EPI_ADDX) ALG_EPI(EPI_DSILU) ALG_EPI(EPI_R2)
+      ALG_EPI(EPI_USCALE) ALG_EPI(EPI_ACC) ALG_EPI(EPI_ADDX) ALG_EPI(EPI_DSILU) ALG_EPI(EPI_R2) ALG_EPI(EPI_ACCX)
 #undef ALG_EPI
       default: throw CudaError("tc_gemm: unknown epilogue");
     }
+    ALG_LAUNCH_CHECK();
+  }
+  if (g.dotv && w.n_tiles > 1) {  // dot_out[r] += coef (partial_0 + partial_1 + ...), fixed order
+    ProfScope ps(prof, st, PK_ROWDOT, (double)g.M * w.n_tiles, 4.0 * (double)g.M * (w.n_tiles + 2));
+    k_dot_parts<<<ceil_div(g.M, 256), 256, 0, st>>>(g.M, w.n_tiles, g.dot_part, g.dot_coef, g.dot_out);
     ALG_LAUNCH_CHECK();
   }
 }

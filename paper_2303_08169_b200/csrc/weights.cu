@@ -206,6 +206,12 @@ void load_model(allegro_ctx* c, const char* path) {
     std::vector<float> hx(hl.begin(), hl.begin() + (size_t)D * D);
     std::vector<float> hs(hl.begin() + (size_t)D * D, hl.end());
     W.latT_x[k] = make_wt(W, transpose(hx, D, D), D, D, tc);
+    {  // [latT_x; envT] stacked along K: x-bar^k = a x-bar^{k+1} + [b u x-bar^{k+1} / sqrt(fan) | w-bar / sqrt(D)] W
+      std::vector<float> st = transpose(hx, D, D);
+      const std::vector<float> et = transpose(h, D, li.nw);
+      st.insert(st.end(), et.begin(), et.end());
+      W.latenvT[k] = make_wt(W, st, D + li.nw, D, tc);
+    }
     W.latT_s[k] = make_wt(W, transpose(hs, C * A.n_s, D), D, C * A.n_s, tc);
   }
   {

@@ -12,10 +12,11 @@ from oracle import allegro as oa, weights_io
 from synth import configs
 
 
-def run(m, s, fwd, bwd, last):
+def run(m, s, fwd, bwd, last, merge="1"):
     os.environ["ALLEGRO_FUSED_TP"] = fwd
     os.environ["ALLEGRO_FUSED_TP_BWD"] = bwd
     os.environ["ALLEGRO_FUSED_LAST"] = last
+    os.environ["ALLEGRO_MERGE_XBAR"] = merge
     return m.compute_energy_forces(s.pos, s.species)
 
 
@@ -23,9 +24,9 @@ for cfg in sys.argv[1:] or ["C1", "C2"]:
     s = configs.system(cfg)
     wf = configs.weight_file(cfg)
     m = pb.Allegro(wf, s.box, precision=pb.PREC_3XTF32, n_atoms=s.n)
-    e0, ea0, f0 = run(m, s, "0", "0", "0")
-    eL, eaL, fL = run(m, s, "0", "0", "1")
-    e1, ea1, f1 = run(m, s, "-1", "-1", "1")
+    e0, ea0, f0 = run(m, s, "0", "0", "0", "0")
+    eL, eaL, fL = run(m, s, "0", "0", "1", "0")
+    e1, ea1, f1 = run(m, s, "-1", "-1", "1", "1")
     line = (f"{cfg}: last layer fused vs not: bitwise E {eL == e0} E_i {np.array_equal(eaL, ea0)} F {np.array_equal(fL, f0)}"
             f" | all fused vs none: bitwise E {e1 == e0} F {np.array_equal(f1, f0)} max|dF| {np.abs(f1 - f0).max():.3g}")
     if s.n < 2000:

@@ -360,13 +360,15 @@ def test_fused_tp_linear_matches_unfused(pb, cfg, monkeypatch):
     """The fused kernels against the unfused path: the last layer in one kernel (k_last) is
     bit-identical; the fused TP + TP-linear forward (same FMA order, same 3xTF32 contraction) gives
     bit-identical energies; the fused backward re-associates the Gamma-bar row sum (per edge,
-    then over the row), so forces agree to rounding.  C1 (2, 1) and the bench's C5 (3, 1)."""
+    then over the row) and the merged x-bar contraction scales A rows before the TF32 split, so
+    forces agree to rounding.  C1 (2, 1) and the bench's C5 (3, 1)."""
     s = configs.system(cfg)
     wf = configs.weight_file(cfg)
     m = pb.Allegro(wf, s.box, precision=pb.PREC_3XTF32, n_atoms=s.n)
     monkeypatch.setenv("ALLEGRO_FUSED_TP", "0")
     monkeypatch.setenv("ALLEGRO_FUSED_TP_BWD", "0")
     monkeypatch.setenv("ALLEGRO_FUSED_LAST", "0")
+    monkeypatch.setenv("ALLEGRO_MERGE_XBAR", "0")
     e0, ea0, f0 = m.compute_energy_forces(s.pos, s.species)
     # the fused last layer alone: the same arithmetic in the same order (bit-identical)
     monkeypatch.setenv("ALLEGRO_FUSED_LAST", "1")
@@ -374,6 +376,7 @@ def test_fused_tp_linear_matches_unfused(pb, cfg, monkeypatch):
     assert eL == e0 and np.array_equal(eaL, ea0) and np.array_equal(fL, f0)
     monkeypatch.setenv("ALLEGRO_FUSED_TP", "1")
     monkeypatch.setenv("ALLEGRO_FUSED_TP_BWD", "1")
+    monkeypatch.setenv("ALLEGRO_MERGE_XBAR", "1")
     m.profile(True)
     e1, ea1, f1 = m.compute_energy_forces(s.pos, s.species)
     assert m.profile_read()["tp_lin_fwd"][3] > 0
