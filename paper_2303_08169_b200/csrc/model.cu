@@ -24,8 +24,10 @@
 
 #include "ctx.cuh"
 #include "gemm.cuh"
+#include "geom.cuh"
 #include "layer.cuh"
 #include "tp_fused.cuh"
+#include "twobody.cuh"
 
 namespace allegro {
 namespace {
@@ -34,36 +36,7 @@ constexpr float kCSilu = 1.6765324703f;  // E[SiLU(z)^2]^-1/2 (reading row 5)
 constexpr float kResA = 0.89442719099991588f;  // 2/sqrt5
 constexpr float kResB = 0.44721359549995794f;  // 1/sqrt5
 
-// ----------------------------------------------------------------- K3 geometry
-__device__ __forceinline__ void sh_eval(const float n[3], float* Y, int lmax) {
-  // component-normalised real SH (E3), m = -l..l; l = 1 stored (y, z, x)
-  const float s3 = 1.7320508075688772f, s5 = 2.2360679774997896f, s15 = 3.8729833462074170f;
-  Y[0] = 1.f;
-  if (lmax >= 1) {
-    Y[1] = s3 * n[1];
-    Y[2] = s3 * n[2];
-    Y[3] = s3 * n[0];
-  }
-  if (lmax >= 2) {
-    Y[4] = s15 * n[0] * n[1];
-    Y[5] = s15 * n[1] * n[2];
-    Y[6] = 0.5f * s5 * (2.f * n[2] * n[2] - n[0] * n[0] - n[1] * n[1]);
-    Y[7] = s15 * n[0] * n[2];
-    Y[8] = 0.5f * s15 * (n[0] * n[0] - n[1] * n[1]);
-  }
-}
-
-struct GeomParams {
-  float rc, inv_rc;
-  float freq[kNB];
-  int lmax, dsh;
-};
-
-__device__ __forceinline__ void edge_vec(const double* __restrict__ apos, int32_t i, int32_t a, float r[3]) {
-#pragma unroll
-  for (int d = 0; d < 3; ++d) r[d] = (float)__dsub_rn(apos[(int64_t)a * 3 + d], apos[(int64_t)i * 3 + d]);
-}
-
+// ----------------------------------------------------------------- K3 geometry (helpers: geom.cuh)
 // The first two-body layer is folded in (E4): a1 = (1/sqrt 12) z W0 with z = [onehot(Z_i),
 // onehot(Z_j), u B(d)] never leaves registers -- two selected rows of W0 plus eight Bessel rows.
 __global__ void __launch_bounds__(256) k_geom(ChunkPtrs ch, GeomParams gp, const double* __restrict__ apos,
@@ -1168,7 +1141,9 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   for (int q = 0; q < kNB; ++q) gp.freq[q] = M.w.bessel[q];
   gp.lmax = M.lmax;
   gp.dsh = dsh;
-  if (E > 0) {
+  const char* f2_env = std::getenv("ALLEGRO_FUSED_2B");  // A/B switch: geometry + two-body MLP in one kernel
+  const bool fused_2b = (!f2_env || std::atoi(f2_env) != 0) && M.precision == ALLEGRO_PREC_3XTF32;
+  if (E > 0 && !fused_2b) {
     {
       ProfScope ps_(&c->prof, st, PK_GEOM, 0, (double)E * (8 + 128 + 4 * dsh + 4));
       k_geom<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, c->aspec.p, c->species.p,
@@ -1193,7 +1168,26 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     return g;
   };
   // ---- two-body MLP (E4, E5) ----
-  {
+  if (fused_2b) {
+    TbIO io;
+    io.ch = ch;
+    io.gp = gp;
+    io.apos = c->apos.p;
+    io.cidx = c->cidx.p;
+    io.nbr = c->nbr.p;
+    io.aspec = c->aspec.p;
+    io.species = c->species.p;
+    io.w0 = M.w.tb_w0.f;
+    io.w1 = &M.w.tb_w1;
+    io.w2 = &M.w.tb_w2;
+    io.u = w.u.p;
+    io.Y = w.Y.p;
+    io.x0 = w.xa.p;
+    io.a1 = w.a1.p;
+    io.a2 = w.a2.p;
+    io.m = w.m.p;
+    tb_fwd(io, st, &c->prof);
+  } else {
     // only the pre-activations a1, a2 are stored (the reverse pass needs them); the next
     // contraction applies SiLU to its operand on load instead of reading a stored h = SiLU(a)
     // (a1 = z W0 / sqrt 12 was formed by k_geom)

@@ -34,12 +34,14 @@ enum ProfKind : int {
   PK_TPL_BWD,   // fused TP-linear^T + TP adjoint (tcgen05), backward
   PK_ENV_ADJ,   // Gamma-bar row sums + environment adjoint (fused path)
   PK_LAST,      // last layer forward + read-out + reverse, one warp per row
+  PK_TWOBODY,   // fused geometry + two-body MLP (tcgen05), forward
+  PK_TWOBODY_BWD,  // fused two-body MLP reverse + geometry adjoint (tcgen05)
   PK_COUNT
 };
 
 inline const char* prof_name(int k) {
   static const char* names[PK_COUNT] = {"wrap", "ghost", "cell", "edge_build", "scan", "geom", "gemm", "tp_fwd",
-                                        "tp_bwd", "energy", "rowdot", "geom_bwd", "force_gather", "verlet", "reduce", "halo", "gamma", "tp_lin_fwd", "tp_lin_bwd", "env_adj", "last_layer"};
+                                        "tp_bwd", "energy", "rowdot", "geom_bwd", "force_gather", "verlet", "reduce", "halo", "gamma", "tp_lin_fwd", "tp_lin_bwd", "env_adj", "last_layer", "twobody", "twobody_bwd"};
   return (k >= 0 && k < PK_COUNT) ? names[k] : "?";
 }
 

@@ -1,0 +1,35 @@
+// twobody.cuh -- host entry of the fused geometry + two-body MLP kernels (twobody.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "ctx.cuh"
+#include "geom.cuh"
+#include "layer.cuh"
+#include "prof.cuh"
+
+namespace allegro {
+
+// Forward over one chunk: reads positions / edges, writes u [E], Y [E][DSH], x0 [E][128] and, when
+// the pointers are set, a1 [E][32], a2 [E][64], m [E][128] for the unfused reverse.
+struct TbIO {
+  ChunkPtrs ch;
+  GeomParams gp;
+  const double* apos = nullptr;
+  const int32_t* cidx = nullptr;
+  const int32_t* nbr = nullptr;
+  const int32_t* aspec = nullptr;
+  const int32_t* species = nullptr;
+  const float* w0 = nullptr;  // W0 fp32 [16][32]
+  const Wt* w1 = nullptr;     // W1 [32][64] (tensor-core image)
+  const Wt* w2 = nullptr;     // W2 [64][128]
+  float* u = nullptr;
+  float* Y = nullptr;
+  float* x0 = nullptr;
+  float* a1 = nullptr;
+  float* a2 = nullptr;
+  float* m = nullptr;
+};
+
+void tb_fwd(const TbIO& io, cudaStream_t st, Profiler* prof);
+
+}  // namespace allegro

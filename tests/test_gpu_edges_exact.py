@@ -144,8 +144,10 @@ def test_single_pass_tf32_reported_not_gated(pb):
 def test_skin_edges_contribute_exact_zeros(pb):
     """NEXT-4: a neighbour-list skin adds edges with r_c < d <= r_c + skin; the
     envelope makes u = u' = 0 there, so x = w = V = 0 on them and their g is exactly 0 (§8(c)
-    "exact zero beyond r_c").  Energies, per-atom energies and forces with skin 0.5 A equal skin 0
-    bit for bit (the extra terms are exact zeros in every fixed-order sum)."""
+    "exact zero beyond r_c").  Energies and per-atom energies with skin 0.5 A equal skin 0 bit for
+    bit; the forces' lane-strided edge reductions (force gather, Gamma-bar row sums) hand the
+    same nonzero terms to different lanes once zeros are interleaved, so they agree to fp32
+    re-association (measured on a B200: energies bitwise, forces not)."""
     s = configs.system("C2")
     wf = configs.weight_file("C2")
     m0 = pb.Allegro(wf, s.box)
@@ -153,4 +155,8 @@ def test_skin_edges_contribute_exact_zeros(pb):
     e0, a0, f0 = m0.compute_energy_forces(s.pos, s.species)
     e1, a1, f1 = m1.compute_energy_forces(s.pos, s.species)
     assert len(m1.get_edges()[0]) > 1.2 * len(m0.get_edges()[0])
-    assert e1 == e0 and np.array_equal(a1, a0) and np.array_equal(f1, f0)
+    assert e1 == e0 and np.array_equal(a1, a0)
+    rms = float(np.sqrt((f0**2).sum(1).mean()))
+    err = float(np.abs(f1 - f0).max())
+    print(f"skin 0.5 vs 0: max|dF| = {err:.3g} eV/A (RMS|F| = {rms:.3g})")
+    assert err <= 1e-6 * max(1.0, rms)
