@@ -11,7 +11,13 @@ namespace {
 constexpr int BM = 128, BK = 16, NT = 256;
 
 // sigmoid via exp2 + fast reciprocal (a few ulp; the parity tolerance is ~1e-6 relative)
-__device__ __forceinline__ float sigm(float t) { return __fdividef(1.f, 1.f + exp2f(-1.4426950408889634f * t)); }
+// exp2f(x) is MUFU.EX2 for x >= -126 plus a denormal-result fix-up below; 1 + 2^x rounds to 1 there
+// anyway, so the bare ex2.approx.ftz gives the same sigmoid bits with three fewer instructions
+__device__ __forceinline__ float sigm(float t) {
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * t));
+  return __fdividef(1.f, 1.f + e);
+}
 __device__ __forceinline__ float silu(float t) { return t * sigm(t); }
 __device__ __forceinline__ float dsilu(float t) {
   const float s = sigm(t);

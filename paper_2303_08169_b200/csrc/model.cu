@@ -848,59 +848,10 @@ __global__ void __launch_bounds__(256) k_geom_bwd(ChunkPtrs ch, GeomParams gp, c
     }
   }
   const int64_t ge = ch.e0 + e;
-  float r[3];
+  float r[3], yb[9];
   edge_vec(apos, cidx[ge], nbr[ge], r);
-  const float d = sqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-  const float inv = 1.f / d;
-  const float n[3] = {r[0] * inv, r[1] * inv, r[2] * inv};
-  const float x = d * gp.inv_rc;
-  float uu = 0.f, du = 0.f;
-  if (x < 1.f) {
-    const float x2 = x * x, x3 = x2 * x, x5 = x3 * x2, x6 = x3 * x3;
-    uu = 1.f - 28.f * x6 + 48.f * x6 * x - 21.f * x6 * x2;
-    du = -168.f * gp.inv_rc * x5 * (1.f - x) * (1.f - x);
-  }
-  float ub = ubar[e];
-  float db = 0.f;
-  const float pre = 2.f * gp.inv_rc;
-#pragma unroll
-  for (int q = 0; q < kNB; ++q) {
-    const float k = gp.freq[q] * gp.inv_rc;
-    float sn, cs;
-    sincosf(k * d, &sn, &cs);
-    const float B = pre * sn * inv;
-    const float dB = pre * (k * cs * inv - sn * inv * inv);
-    const float zb = s0 * zbar[q];
-    ub = fmaf(zb, B, ub);
-    db = fmaf(uu * zb, dB, db);
-  }
-  db = fmaf(ub, du, db);
-  float gx = db * n[0], gy = db * n[1], gz = db * n[2];
-  // sum_m Ybar[m] dY_m/dr,  dY^l/dr = (grad P_l(n) - l Y^l n) / d
-  if (gp.lmax >= 1) {
-    const float s3 = 1.7320508075688772f;
-    const float* yb = ybar + e * gp.dsh;
-    const float b1 = yb[1], b2 = yb[2], b3 = yb[3];
-    const float dot1 = b1 * n[1] + b2 * n[2] + b3 * n[0];  // sum_m yb_m Y_m / sqrt3
-    gx += s3 * inv * (b3 - dot1 * n[0]);
-    gy += s3 * inv * (b1 - dot1 * n[1]);
-    gz += s3 * inv * (b2 - dot1 * n[2]);
-    if (gp.lmax >= 2) {
-      const float s5 = 2.2360679774997896f, s15 = 3.8729833462074170f;
-      const float c0 = yb[4], c1 = yb[5], c2 = yb[6], c3 = yb[7], c4 = yb[8];
-      float Y2[5] = {s15 * n[0] * n[1], s15 * n[1] * n[2], 0.5f * s5 * (2.f * n[2] * n[2] - n[0] * n[0] - n[1] * n[1]),
-                     s15 * n[0] * n[2], 0.5f * s15 * (n[0] * n[0] - n[1] * n[1])};
-      const float sy = c0 * Y2[0] + c1 * Y2[1] + c2 * Y2[2] + c3 * Y2[3] + c4 * Y2[4];
-      // grad P2 at n
-      const float px = s15 * (c0 * n[1] + c3 * n[2]) + 0.5f * s5 * c2 * (-2.f * n[0]) + 0.5f * s15 * c4 * (2.f * n[0]);
-      const float py = s15 * (c0 * n[0] + c1 * n[2]) + 0.5f * s5 * c2 * (-2.f * n[1]) + 0.5f * s15 * c4 * (-2.f * n[1]);
-      const float pz = s15 * (c1 * n[1] + c3 * n[0]) + 0.5f * s5 * c2 * (4.f * n[2]);
-      gx += inv * (px - 2.f * sy * n[0]);
-      gy += inv * (py - 2.f * sy * n[1]);
-      gz += inv * (pz - 2.f * sy * n[2]);
-    }
-  }
-  reinterpret_cast<float4*>(g)[ge] = make_float4(gx, gy, gz, 0.f);  // [E][4]: one 16-B load per reverse gather
+  load_ybar(ybar, e, gp.dsh, yb);
+  geom_bwd_tail(gp, r, ubar[e], yb, s0, zbar, g, ge);
 }
 
 // ----------------------------------------------------------------- A12 force gather
@@ -1142,7 +1093,8 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
   gp.lmax = M.lmax;
   gp.dsh = dsh;
   const char* f2_env = std::getenv("ALLEGRO_FUSED_2B");  // A/B switch: geometry + two-body MLP in one kernel
-  const bool fused_2b = (!f2_env || std::atoi(f2_env) != 0) && M.precision == ALLEGRO_PREC_3XTF32;
+  const int f2_mask = (f2_env ? std::atoi(f2_env) : 3) * (M.precision == ALLEGRO_PREC_3XTF32 ? 1 : 0);
+  const bool fused_2b = f2_mask & 1, fused_2b_bwd = (f2_mask >> 1) & 1;  // bit 0: forward, bit 1: reverse
   if (E > 0 && !fused_2b) {
     {
       ProfScope ps_(&c->prof, st, PK_GEOM, 0, (double)E * (8 + 128 + 4 * dsh + 4));
@@ -1168,8 +1120,9 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     return g;
   };
   // ---- two-body MLP (E4, E5) ----
-  if (fused_2b) {
-    TbIO io;
+  TbIO tbio;
+  {
+    TbIO& io = tbio;
     io.ch = ch;
     io.gp = gp;
     io.apos = c->apos.p;
@@ -1183,10 +1136,12 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     io.u = w.u.p;
     io.Y = w.Y.p;
     io.x0 = w.xa.p;
-    io.a1 = w.a1.p;
-    io.a2 = w.a2.p;
+    io.a1 = fused_2b_bwd ? nullptr : w.a1.p;  // the fused reverse recomputes a1, a2
+    io.a2 = fused_2b_bwd ? nullptr : w.a2.p;
     io.m = w.m.p;
-    tb_fwd(io, st, &c->prof);
+  }
+  if (fused_2b) {
+    tb_fwd(tbio, st, &c->prof);
   } else {
     // only the pre-activations a1, a2 are stored (the reverse pass needs them); the next
     // contraction applies SiLU to its operand on load instead of reading a stored h = SiLU(a)
@@ -1414,6 +1369,17 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     std::swap(vb, vbn);
   }
   // ---- two-body reverse (its u-gradient row-dot ran in layer 0's env^T epilogue) ----
+  if (fused_2b_bwd) {
+    TbbIO bo;
+    bo.w2t = &M.w.tb_w2T;
+    bo.w1t = &M.w.tb_w1T;
+    bo.xbar = xb;
+    bo.ubar = w.ubar.p;
+    bo.ybar = w.ybar.p;
+    bo.g = c->g.p;
+    tb_bwd(tbio, bo, st, &c->prof);
+    return;
+  }
   {
     GemmArgs g = G(xb, 128, M.w.tb_w2T, 64, 128, w.ab2.p, kCSilu / std::sqrt(64.f), EPI_DSILU);
     g.X = w.a2.p;

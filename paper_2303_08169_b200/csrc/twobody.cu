@@ -35,7 +35,13 @@ constexpr int kTbThreads = 32 * 9;
 constexpr int kBox = 32 * 128;  // [32 rows x 32 fp32] staging box
 constexpr float kCSiluTb = 1.6765324703f;
 
-__device__ __forceinline__ float sigm_tb(float t) { return __fdividef(1.f, 1.f + exp2f(-1.4426950408889634f * t)); }
+// exp2f(x) is MUFU.EX2 for x >= -126 plus a denormal-result fix-up below; 1 + 2^x rounds to 1 there
+// anyway, so the bare ex2.approx.ftz gives the same sigmoid bits with three fewer instructions
+__device__ __forceinline__ float sigm_tb(float t) {
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * t));
+  return __fdividef(1.f, 1.f + e);
+}
 __device__ __forceinline__ float silu_tb(float t) { return t * sigm_tb(t); }
 
 struct TbParams {
@@ -92,12 +98,11 @@ __device__ __forceinline__ uint32_t idesc_n(uint32_t N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
 }
 
-// the geometry of one edge and its first two-body layer, exactly as k_geom (model.cu)
-__device__ __forceinline__ void geom_row(const TbParams& p, const float (*sw)[32], int64_t e, float& uu, float* y,
-                                         float* a1) {
-  const int64_t ge = p.ch.e0 + e;
-  const int32_t i = p.cidx[ge], a = p.nbr[ge];
-  float r[3];
+// the geometry of one edge and its first two-body layer, exactly as k_geom (model.cu); s4 = W0 rows
+// 0..11 as float4 (SMEM in the forward, global / L1 broadcast in the reverse); Y only when y != nullptr
+template <bool kY>
+__device__ __forceinline__ void geom_row(const TbParams& p, const float4* s4, int32_t i, int32_t a, float& uu, float* y,
+                                         float* a1, float* r) {
   edge_vec(p.apos, i, a, r);
   const float d = sqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
   const float x = d * p.gp.inv_rc;
@@ -111,7 +116,6 @@ __device__ __forceinline__ void geom_row(const TbParams& p, const float (*sw)[32
   float zb[kNB];
 #pragma unroll
   for (int q = 0; q < kNB; ++q) zb[q] = uu * pre * sinf(p.gp.freq[q] * d * p.gp.inv_rc);
-  const float4* s4 = reinterpret_cast<const float4*>(&sw[0][0]);
 #pragma unroll
   for (int c4 = 0; c4 < 8; ++c4) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -131,9 +135,33 @@ __device__ __forceinline__ void geom_row(const TbParams& p, const float (*sw)[32
     a1[4 * c4 + 2] = p.s0 * acc.z;
     a1[4 * c4 + 3] = p.s0 * acc.w;
   }
-  const float inv = 1.f / d;
-  const float nv[3] = {r[0] * inv, r[1] * inv, r[2] * inv};
-  sh_eval(nv, y, p.gp.lmax);
+  if constexpr (kY) {
+    const float inv = 1.f / d;
+    const float nv[3] = {r[0] * inv, r[1] * inv, r[2] * inv};
+    sh_eval(nv, y, p.gp.lmax);
+  }
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* ptr) { asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr)); }
+
+// The edge endpoints of a group's NEXT tile are loaded one tile ahead, and once they have arrived the
+// positions / species they point at are prefetched into L1: the dependent index -> position gather
+// is otherwise exposed on every tile (the row warps are few; their latency is the kernel's bound).
+struct NextIdx {
+  int32_t i = 0, a = 0;
+  __device__ __forceinline__ void load(const TbParams& p, int64_t e) {
+    if (e < p.ch.n_e) i = __ldg(p.cidx + p.ch.e0 + e), a = __ldg(p.nbr + p.ch.e0 + e);
+  }
+  __device__ __forceinline__ void prefetch(const TbParams& p) const {
+    prefetch_l1(p.apos + (int64_t)i * 3);
+    prefetch_l1(p.apos + (int64_t)a * 3);
+    prefetch_l1(p.species + i);
+    prefetch_l1(p.aspec + a);
+  }
+};
+
+__device__ __forceinline__ int64_t tile_row(int t, int qw, int lane) {
+  return (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kRows + qw * 32 + lane;
 }
 
 // one [32 rows x 32 fp32] box of this warp's rows (thread = row) through a swizzled SMEM slot
@@ -217,20 +245,26 @@ __global__ void __launch_bounds__(kTbThreads, 1) k_tb_fwd(const __grid_constant_
     const int g = warp >> 2, q = warp & 3;
     const uint32_t b = tmem + 256u * g + ((uint32_t)(q * 32) << 16);
     int n_st = 0;
+    NextIdx nx;
+    if (g < n_my) nx.load(p, tile_row(g, q, lane));
     for (int t = g; t < n_my; t += 2) {
       const uint32_t ph = (uint32_t)(t >> 1) & 1u;
       const int64_t e0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kRows;
       const int64_t e = e0 + q * 32 + lane;
       const bool valid = e < p.ch.n_e;
-      float uu = 0.f, y[9], a[32];
+      const int32_t ci = nx.i, ca = nx.a;
+      if (t + 2 < n_my) nx.load(p, tile_row(t + 2, q, lane));
+      float uu = 0.f, y[9], a[32], r[3];
 #pragma unroll
       for (int c = 0; c < 32; ++c) a[c] = 0.f;
       if (valid) {
-        geom_row(p, sw, e, uu, y, a);
+        geom_row<true>(p, reinterpret_cast<const float4*>(&sw[0][0]), ci, ca, uu, y, a, r);
         p.u[e] = uu;
         if (p.gp.dsh == 4) reinterpret_cast<float4*>(p.Y)[e] = make_float4(y[0], y[1], y[2], y[3]);
         else
-          for (int k = 0; k < p.gp.dsh; ++k) p.Y[e * p.gp.dsh + k] = y[k];
+#pragma unroll
+          for (int k = 0; k < 9; ++k)
+            if (k < p.gp.dsh) p.Y[e * p.gp.dsh + k] = y[k];
       }
       unsigned char* slot0 = slots + (size_t)(2 * warp) * kBox;
       auto next_slot = [&]() -> unsigned char* {  // the slot used two stores ago has been read
@@ -252,6 +286,7 @@ __global__ void __launch_bounds__(kTbThreads, 1) k_tb_fwd(const __grid_constant_
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(a1_full + g);
+      if (t + 2 < n_my) nx.prefetch(p);
       // a2 = s1 D1; A2 = SiLU(a2) (two K-blocks)
       mbar_wait(d1_full + g, ph);
       tc_fence_after();
@@ -291,6 +326,243 @@ __global__ void __launch_bounds__(kTbThreads, 1) k_tb_fwd(const __grid_constant_
   }
   __syncthreads();
   if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Reverse: per 128-edge tile (thread = edge row), with a1 and a2 recomputed from the geometry:
+//   ab2 = u (s2 xbar0 W2^T) dsilu(a2);  ab1 = (s1 ab2 W1^T) dsilu(a1);  zbar = ab1 W0[Bessel]^T;
+//   g = geometry adjoint (geom_bwd_tail, shared with k_geom_bwd)
+// -- the arithmetic and order of the unfused reverse (two EPI_DSILU contractions + k_geom_bwd), so
+// g is bit-identical to it.  The u-gradient <xbar0, m> stays in layer 0's env^T epilogue (ubar in).
+// Warps 0-7: two groups of four row warps, alternate tiles; warps 8 / 9: MMA issuer of group 0 / 1.
+// TMEM per group (256 columns): A1 [0, 64), D1 [64, 128) (kept: a2 = s1 D1 is re-read for dsilu),
+// xbar0 K-blocks {0, 1} then {2, 3} split into [128, 256), D3 [0, 64) (A1 consumed), A4 (ab2 split)
+// [128, 256), D4 [64, 96) (D1 read by then).  xbar0 arrives by per-warp TMA boxes, one tile ahead.
+struct TbbParams {
+  TbParams f;      // geometry inputs and the forward weights (f.w1img: W1)
+  const float* w2t_img;  // W2^T [128][64] image (N 64, 4 K-blocks)
+  const float* w1t_img;  // W1^T [64][32] image (N 32, 2 K-blocks)
+  uint32_t w2t_bytes, w1t_bytes;
+  float s3, s4;    // c / sqrt 64, c / sqrt 32
+  const float* ubar;
+  const float* ybar;
+  float* g;
+};
+
+__device__ __forceinline__ float dsilu_tb(float t) {
+  const float s = sigm_tb(t);
+  return s * (1.f + t * (1.f - s));
+}
+
+// split 32 fp32 values read from a swizzled [32 rows x 32 fp32] SMEM box (this thread's row) into TMEM
+__device__ __forceinline__ void split_box(uint32_t taddr, const unsigned char* box, int lane) {
+  float x[32];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 v = *reinterpret_cast<const float4*>(box + lane * 128 + ((c ^ (lane & 7)) << 4));
+    x[4 * c] = v.x, x[4 * c + 1] = v.y, x[4 * c + 2] = v.z, x[4 * c + 3] = v.w;
+  }
+  split_store(taddr, x);
+}
+
+__global__ void __launch_bounds__(32 * 8, 1) k_tb_bwd(const __grid_constant__ CUtensorMap map_xbar, const TbbParams q) {
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  const TbParams& p = q.f;
+  // no alignment slack: the dynamic window starts 1024-aligned (after the reserved 1 KB) -- checked
+  if (smem_u32(smem_dyn) & 1023u) __trap();
+  unsigned char* w1s = smem_dyn;
+  unsigned char* w2ts = w1s + ((p.w1bytes + 1023u) & ~1023u);
+  unsigned char* w1ts = w2ts + ((q.w2t_bytes + 1023u) & ~1023u);
+  unsigned char* slots = w1ts + ((q.w1t_bytes + 1023u) & ~1023u);  // [8 warps][4 K-blocks][4 KB]
+  float(*sw)[32] = reinterpret_cast<float(*)[32]>(slots + 32 * kBox);      // W0 rows 0..11 [12][32]
+  float(*swt)[kNB] = reinterpret_cast<float(*)[kNB]>(slots + 32 * kBox + 12 * 32 * 4);  // W0 rows 4..11^T [32][8]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + 32 * kBox + 12 * 32 * 4 + 32 * kNB * 4);
+  uint64_t* a1_full = bars;        // [2]
+  uint64_t* d1_full = bars + 2;    // [2]
+  uint64_t* x3a_full = bars + 4;   // [2]
+  uint64_t* x3a_empty = bars + 6;  // [2]
+  uint64_t* x3b_full = bars + 8;   // [2]
+  uint64_t* d3_full = bars + 10;   // [2]
+  uint64_t* a4_full = bars + 12;   // [2]
+  uint64_t* d4_full = bars + 14;   // [2]
+  uint64_t* xb_full = bars + 16;   // [8] per row warp
+  uint64_t* w_full = bars + 24;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = threadIdx.x; t < 12 * 32; t += blockDim.x) sw[t / 32][t % 32] = p.w0[t];
+  for (int t = threadIdx.x; t < kNB * 32; t += blockDim.x) swt[t % 32][t / 32] = p.w0[4 * 32 + t];
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(a1_full + g, 4), mbar_init(d1_full + g, 1), mbar_init(x3a_full + g, 4), mbar_init(x3a_empty + g, 1);
+      mbar_init(x3b_full + g, 4), mbar_init(d3_full + g, 1), mbar_init(a4_full + g, 4), mbar_init(d4_full + g, 1);
+    }
+    for (int w = 0; w < 8; ++w) mbar_init(xb_full + w, 1);
+    mbar_init(w_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_my = p.n_tiles > (int)blockIdx.x ? (p.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  {
+    // ---------------- row warps (warp 0 of each group also issues the group's MMAs) ----------------
+    if (warp == 0 && lane == 0) {
+      mbar_expect_tx(w_full, p.w1bytes + q.w2t_bytes + q.w1t_bytes);
+      bulk_load(w1s, p.w1img, p.w1bytes, w_full);
+      bulk_load(w2ts, q.w2t_img, q.w2t_bytes, w_full);
+      bulk_load(w1ts, q.w1t_img, q.w1t_bytes, w_full);
+    }
+    const int g = warp >> 2, qw = warp & 3;
+    const bool issuer = qw == 0;
+    const uint32_t bm = tmem + 256u * g;  // the group's TMEM base (lane 0) for the MMAs
+    uint32_t L = 0;
+    if (issuer) {
+      mbar_wait(w_full, 0);
+      tc_fence_after();
+      __syncwarp();
+      L = elect_leader();
+    }
+    const uint64_t dw1 = sdesc(smem_u32(w1s)), dw2t = sdesc(smem_u32(w2ts)), dw1t = sdesc(smem_u32(w1ts));
+    const uint64_t kb64 = (uint64_t)((2 * 64 * 128) >> 4), kb32 = (uint64_t)((2 * 32 * 128) >> 4);
+    const uint32_t b = tmem + 256u * g + ((uint32_t)(qw * 32) << 16);
+    unsigned char* myslots = slots + (size_t)(4 * warp) * kBox;
+    auto load_xbar = [&](int t) {  // this warp's 32 rows of tile t: four [32 x 32] boxes
+      if (lane == 0 && t < n_my) {
+        const int row0 = ((int)blockIdx.x + t * (int)gridDim.x) * kRows + qw * 32;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(xb_full + warp, 4 * kBox);
+        for (int kb = 0; kb < 4; ++kb) tma_load_2d(myslots + kb * kBox, &map_xbar, 32 * kb, row0, xb_full + warp);
+      }
+    };
+    load_xbar(g);
+    NextIdx nx;
+    if (g < n_my) nx.load(p, tile_row(g, qw, lane));
+    for (int t = g; t < n_my; t += 2) {
+      const uint32_t ph = (uint32_t)(t >> 1) & 1u;
+      const int64_t e = tile_row(t, qw, lane);
+      const bool valid = e < p.ch.n_e;
+      const int32_t ci = nx.i, ca = nx.a;
+      if (t + 2 < n_my) nx.load(p, tile_row(t + 2, qw, lane));
+      float uu = 0.f, a1[32], x[32], r[3] = {0.f, 0.f, 0.f}, ub = 0.f, yb[9];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) a1[c] = 0.f;
+      if (valid) {
+        ub = __ldg(q.ubar + e);  // consumed at the end of the tile: in flight across the MMA chain
+        load_ybar(q.ybar, e, p.gp.dsh, yb);
+        geom_row<false>(p, reinterpret_cast<const float4*>(&sw[0][0]), ci, ca, uu, nullptr, a1, r);
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {  // SiLU(a1) for MMA1 and dsilu(a1) for ab1, one sigmoid each
+        const float sg = sigm_tb(a1[c]);
+        x[c] = a1[c] * sg;
+        a1[c] = sg * (1.f + a1[c] * (1.f - sg));
+      }
+      tc_fence_after();
+      split_store(b, x);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a1_full + g);
+      if (issuer) {
+        mbar_wait(a1_full + g, ph);
+        tc_fence_after();
+        mma_kblock(L, bm + 64, bm, dw1, 64, idesc_n(64), true);  // D1 = SiLU(a1) W1
+        mma_commit_w(L, d1_full + g);
+      }
+      // xbar0 K-blocks 0, 1 -> [128, 256) (free: the previous tile's MMA4 completed)
+      mbar_wait(xb_full + warp, ph);
+      split_box(b + 128, myslots, lane);
+      split_box(b + 192, myslots + kBox, lane);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(x3a_full + g);
+      if (issuer) {
+        mbar_wait(d1_full + g, ph);  // MMA1 done: D3 may overwrite A1
+        mbar_wait(x3a_full + g, ph);
+        tc_fence_after();
+        mma_kblock(L, bm, bm + 128, dw2t, 64, idesc_n(64), true);  // D3 = xbar0 W2^T, K-blocks 0, 1
+        mma_kblock(L, bm, bm + 192, dw2t + kb64, 64, idesc_n(64), false);
+        mma_commit_w(L, x3a_empty + g);
+      }
+      mbar_wait(x3a_empty + g, ph);
+      tc_fence_after();
+      split_box(b + 128, myslots + 2 * kBox, lane);
+      split_box(b + 192, myslots + 3 * kBox, lane);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(x3b_full + g);
+      if (issuer) {
+        mbar_wait(x3b_full + g, ph);
+        tc_fence_after();
+        mma_kblock(L, bm, bm + 128, dw2t + 2 * kb64, 64, idesc_n(64), false);  // K-blocks 2, 3
+        mma_kblock(L, bm, bm + 192, dw2t + 3 * kb64, 64, idesc_n(64), false);
+        mma_commit_w(L, d3_full + g);
+      }
+      load_xbar(t + 2);  // the slots are read: fetch the group's next tile
+      if (t + 2 < n_my) nx.prefetch(p);
+      // ab2 = u (s3 D3) dsilu(a2), a2 = s1 D1 -> A4 [128, 256)
+      mbar_wait(d3_full + g, ph);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float d1[32], d3[32];
+        tmem_ld32(b + 64 + 32 * h, d1);
+        tmem_ld32(b + 32 * h, d3);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float a2 = p.s1 * d1[c];
+          x[c] = uu * (q.s3 * d3[c]) * dsilu_tb(a2);
+        }
+        split_store(b + 128 + 64 * h, x);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a4_full + g);
+      if (issuer) {
+        mbar_wait(a4_full + g, ph);
+        tc_fence_after();
+        mma_kblock(L, bm + 64, bm + 128, dw1t, 32, idesc_n(32), true);  // D4 = ab2 W1^T
+        mma_kblock(L, bm + 64, bm + 192, dw1t + kb32, 32, idesc_n(32), false);
+        mma_commit_w(L, d4_full + g);
+      }
+      // ab1 = (s4 D4) dsilu(a1); zbar; g
+      mbar_wait(d4_full + g, ph);
+      tc_fence_after();
+      tmem_ld32(b + 64, x);
+      tc_fence_before();
+      if (valid) {
+        float zbar[kNB];
+#pragma unroll
+        for (int k = 0; k < kNB; ++k) zbar[k] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float ab1 = 1.f * (q.s4 * x[j]) * a1[j];  // a1[j] holds dsilu(a1_j)
+          const float4* wj = reinterpret_cast<const float4*>(&swt[j][0]);
+#pragma unroll
+          for (int h = 0; h < kNB / 4; ++h) {
+            const float4 w4 = wj[h];
+            zbar[4 * h] = fmaf(ab1, w4.x, zbar[4 * h]);
+            zbar[4 * h + 1] = fmaf(ab1, w4.y, zbar[4 * h + 1]);
+            zbar[4 * h + 2] = fmaf(ab1, w4.z, zbar[4 * h + 2]);
+            zbar[4 * h + 3] = fmaf(ab1, w4.w, zbar[4 * h + 3]);
+          }
+        }
+        geom_bwd_tail(p.gp, r, ub, yb, p.s0, zbar, q.g, p.ch.e0 + e);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -365,6 +637,65 @@ void tb_fwd(const TbIO& io, cudaStream_t st, Profiler* prof) {
   if (std::getenv("ALLEGRO_SYNC_CHECK")) {
     const cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) throw CudaError(std::string("k_tb_fwd: ") + cudaGetErrorString(e));
+  }
+}
+
+void tb_bwd(const TbIO& io, const TbbIO& bo, cudaStream_t st, Profiler* prof) {
+  const int64_t E = io.ch.n_e;
+  if (E <= 0) return;
+  if (io.w1->tc.N_t != 64 || io.w1->tc.n_tiles != 1 || bo.w2t->tc.N_t != 64 || bo.w2t->tc.n_tiles != 1 ||
+      bo.w2t->tc.K != 128 || bo.w1t->tc.N_t != 32 || bo.w1t->tc.n_tiles != 1 || bo.w1t->tc.K != 64)
+    throw CudaError("tb_bwd: unexpected two-body weight images");
+  TbbParams q;
+  std::memset(&q, 0, sizeof(q));
+  TbParams& p = q.f;
+  p.ch = io.ch;
+  p.gp = io.gp;
+  p.apos = io.apos;
+  p.cidx = io.cidx;
+  p.nbr = io.nbr;
+  p.aspec = io.aspec;
+  p.species = io.species;
+  p.w0 = io.w0;
+  p.s0 = 1.f / std::sqrt(12.f);
+  p.s1 = kCSiluTb / std::sqrt(32.f);
+  p.w1img = io.w1->tc.dev;
+  p.w1bytes = (uint32_t)io.w1->tc.tile_bytes;
+  p.n_tiles = (int)((E + kRows - 1) / kRows);
+  q.w2t_img = bo.w2t->tc.dev;
+  q.w1t_img = bo.w1t->tc.dev;
+  q.w2t_bytes = (uint32_t)bo.w2t->tc.tile_bytes;
+  q.w1t_bytes = (uint32_t)bo.w1t->tc.tile_bytes;
+  q.s3 = kCSiluTb / std::sqrt(64.f);
+  q.s4 = kCSiluTb / std::sqrt(32.f);
+  q.ubar = bo.ubar;
+  q.ybar = bo.ybar;
+  q.g = bo.g;
+  const CUtensorMap mx = map_rows(bo.xbar, E, 128);
+  const size_t smem = ((p.w1bytes + 1023) & ~1023u) + ((q.w2t_bytes + 1023) & ~1023u) +
+                      ((q.w1t_bytes + 1023) & ~1023u) + 32 * kBox + 12 * 32 * 4 + 32 * kNB * 4 + 256;
+  int dev = 0;
+  ALG_CUDA(cudaGetDevice(&dev));
+  static bool attr[64] = {};
+  static int nsm[64] = {};
+  if (!attr[dev]) {
+    ALG_CUDA(cudaFuncSetAttribute(k_tb_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
+    attr[dev] = true;
+  }
+  const int grid = std::max(1, std::min(p.n_tiles, nsm[dev]));
+  {
+    // algorithmic: three contractions (MMA1 recompute, x-bar W2^T, ab2 W1^T); bytes: x-bar0, u-bar,
+    // Y-bar, positions / indices in, g out
+    const double flops = 2.0 * E * (32.0 * 64 + 128.0 * 64 + 64.0 * 32);
+    const double bytes = (double)E * (8 + 2 * 24 + 512 + 4 + 4.0 * p.gp.dsh + 16);
+    ProfScope ps_(prof, st, PK_TWOBODY_BWD, flops, bytes, "two-body bwd (fused)");
+    k_tb_bwd<<<grid, 32 * 8, smem, st>>>(mx, q);
+  }
+  ALG_LAUNCH_CHECK();
+  if (std::getenv("ALLEGRO_SYNC_CHECK")) {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) throw CudaError(std::string("k_tb_bwd: ") + cudaGetErrorString(e));
   }
 }
 

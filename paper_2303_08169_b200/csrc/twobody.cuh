@@ -32,4 +32,18 @@ struct TbIO {
 
 void tb_fwd(const TbIO& io, cudaStream_t st, Profiler* prof);
 
+// Reverse over the same chunk (TbIO: geometry inputs, w0, w1; its outputs are not used): x-bar0
+// [E][128] (the latent gradient after layer 0), u-bar [E] (complete: <x-bar0, m> included), Y-bar
+// [E][DSH] in; g [E][4] out.
+struct TbbIO {
+  const Wt* w2t = nullptr;  // W2^T [128][64]
+  const Wt* w1t = nullptr;  // W1^T [64][32]
+  const float* xbar = nullptr;
+  const float* ubar = nullptr;
+  const float* ybar = nullptr;
+  float* g = nullptr;
+};
+
+void tb_bwd(const TbIO& io, const TbbIO& bo, cudaStream_t st, Profiler* prof);
+
 }  // namespace allegro

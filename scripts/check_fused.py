@@ -28,8 +28,8 @@ for cfg in sys.argv[1:] or ["C1", "C2"]:
     m = pb.Allegro(wf, s.box, precision=pb.PREC_3XTF32, n_atoms=s.n)
     e0, ea0, f0 = run(m, s, "0", "0", "0", "0")
     eL, eaL, fL = run(m, s, "0", "0", "1", "0")
-    eT, eaT, fT = run(m, s, "0", "0", "0", "0", "1")
-    e1, ea1, f1 = run(m, s, "-1", "-1", "1", "1", "1")
+    eT, eaT, fT = run(m, s, "0", "0", "0", "0", "3")
+    e1, ea1, f1 = run(m, s, "-1", "-1", "1", "1", "3")
     line = (f"{cfg}: last layer fused vs not: bitwise E {eL == e0} E_i {np.array_equal(eaL, ea0)} F {np.array_equal(fL, f0)}"
             f" | two-body fused vs not: bitwise E {eT == e0} E_i {np.array_equal(eaT, ea0)} F {np.array_equal(fT, f0)}"
             f" | all fused vs none: bitwise E {e1 == e0} F {np.array_equal(f1, f0)} max|dF| {np.abs(f1 - f0).max():.3g}")
