@@ -14,12 +14,13 @@ from __future__ import annotations
 
 import csv
 import json
+import re
 import sys
 from collections import defaultdict
 
 # kernel-name substring -> class (prof.cuh prof_name); first match wins
 CLASSES = [
-    ("k_tpl_fwd", "tp_lin_fwd"), ("k_tpl_bwd", "tp_lin_bwd"), ("k_env_adj", "env_adj"), ("k_last", "last_layer"),
+    ("k_tb_fwd", "twobody"), ("k_tb_bwd", "twobody_bwd"), ("k_tpl_fwd", "tp_lin_fwd"), ("k_tpl_bwd", "tp_lin_bwd"), ("k_env_adj", "env_adj"), ("k_last", "last_layer"),
     ("true>", "gamma"), ("k_tc_gemm", "gemm"), ("k_gemm", "gemm"), ("k_tp_fwd", "tp_fwd"), ("k_tp_bwd", "tp_bwd"),
     ("k_energy", "energy"), ("k_rowdot", "rowdot"), ("k_geom_bwd", "geom_bwd"), ("k_geom", "geom"),
     ("k_force", "force_gather"), ("k_edge", "edge_build"), ("k_cell", "cell"), ("scan_", "scan"),
@@ -30,6 +31,8 @@ CLASSES = [
 
 
 def classify(name: str) -> str:
+    if re.search(r"k_tp_fwd<\d+, \d+, \d+, (1|true)>", name):  # the Gamma-only instantiation
+        return "gamma"
     for sub, cls in CLASSES:
         if sub in name:
             return cls
