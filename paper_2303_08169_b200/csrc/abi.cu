@@ -177,6 +177,7 @@ void allegro_destroy(allegro_ctx* c) {
   c->key_pad.release();
   c->key.release();
   c->g.release();
+  c->gT.release();
   c->flags.release();
   c->red.release();
   c->e_atom.release();

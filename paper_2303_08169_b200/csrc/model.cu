@@ -16,7 +16,7 @@
 //   A10 k_energy      E_e = x^L . w_out, E_i = sigma nbar^-1/2 sum E_e + mu      E7-E8
 //   A11 reverse mode  the same chain transposed (W^T GEMMs, k_tp_bwd), k_geom_bwd E9
 // then over all atoms:
-//   A12 k_force_warp  F_a = sum_{e in row a} (g_e - g_rev(e)), fixed-order warp sum (fp64)
+//   A12 k_force_warp  F_a = sum_{e in row a} (g_e - gT_e), gT_e = g_rev(e), fixed-order warp sum (fp64)
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -808,7 +808,8 @@ __global__ void __launch_bounds__(256) k_geom_bwd(ChunkPtrs ch, GeomParams gp, c
                                                   const int32_t* __restrict__ cidx, const int32_t* __restrict__ nbr,
                                                   const float* __restrict__ ubar, const float* __restrict__ w0, float s0,
                                                   const float* __restrict__ ab1, const float* __restrict__ ybar,
-                                                  float* __restrict__ g) {
+                                                  float* __restrict__ g, const int32_t* __restrict__ rev,
+                                                  float* __restrict__ gT) {
   __shared__ __align__(16) float swt[32][kNB];  // W0 Bessel rows 4..11, transposed: [j][q], broadcast float4 reads
   __shared__ float4 stile[256 * 8];             // the block's ab1 rows (coalesced load), XOR-swizzled by row % 8
   for (int t = threadIdx.x; t < kNB * 32; t += blockDim.x) swt[t % 32][t / 32] = w0[4 * 32 + t];
@@ -851,25 +852,31 @@ __global__ void __launch_bounds__(256) k_geom_bwd(ChunkPtrs ch, GeomParams gp, c
   float r[3], yb[9];
   edge_vec(apos, cidx[ge], nbr[ge], r);
   load_ybar(ybar, e, gp.dsh, yb);
-  geom_bwd_tail(gp, r, ubar[e], yb, s0, zbar, g, ge);
+  geom_bwd_tail(gp, r, ubar[e], yb, s0, zbar, g, ge, __ldg(rev + ge), gT);
+}
+
+// A/B switch: the producer of g scatters it to the reverse edge's slot (default) or the force gather
+// gathers it through rev
+bool force_scatter() {
+  static const bool on = [] {
+    const char* e = std::getenv("ALLEGRO_FORCE_SCATTER");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
 }
 
 // ----------------------------------------------------------------- A12 force gather
-// Warp per atom: the lanes stride the atom's CSR row (coalesced g reads, 32 reverse-edge
-// gathers in flight) and the fp64 partial sums are combined by a fixed butterfly, so the
-// result is deterministic (and independent of the chunking).
-// F_a = sum_{e in row a} (g_e - g_rev(e)) (+ the returned ghost forces); rev = -1: no reverse edge.
-__global__ void k_force_warp(int64_t n, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ rev,
-                             const float* __restrict__ g, const long long* __restrict__ acc, double* __restrict__ F,
-                             int* __restrict__ flags) {
+// A/B variant without the producer-side scatter (ALLEGRO_FORCE_SCATTER=0): the reverse operand is
+// gathered through rev (a dependent index -> 16-B gather round trip per edge); same sums, same order.
+__global__ void k_force_warp_rev(int64_t n, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ rev,
+                                 const float* __restrict__ g, const long long* __restrict__ acc,
+                                 double* __restrict__ F, int* __restrict__ flags) {
   const int lane = threadIdx.x & 31;
   const int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= n) return;
   double f[3] = {0, 0, 0};
   const int64_t r0 = row_ptr[a], r1 = row_ptr[a + 1];
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  // Four edges per lane per round: all reverse indices, then all 16-B gathers in flight before the
-  // first use (each lane still adds its edges in the order r0 + lane, + 32, + 64, ...).
   for (int64_t base = r0; base < r1; base += 128) {
     int32_t rr[4];
     float4 a4[4], b4[4];
@@ -881,6 +888,56 @@ __global__ void k_force_warp(int64_t n, const int32_t* __restrict__ row_ptr, con
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) b4[k] = rr[k] >= 0 ? __ldg(g4 + rr[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (base + lane + 32 * k < r1) {
+        f[0] += (double)a4[k].x - (double)b4[k].x;
+        f[1] += (double)a4[k].y - (double)b4[k].y;
+        f[2] += (double)a4[k].z - (double)b4[k].z;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) f[d] += __shfl_xor_sync(0xffffffffu, f[d], o);
+  if (lane == 0) {
+    bool bad = false;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double v = f[d] + (acc != nullptr ? (double)acc[a * 3 + d] * (1.0 / kFixScale) : 0.0);
+      F[a * 3 + d] = v;
+      bad = bad || !isfinite(v);
+    }
+    if (bad) atomicOr(flags + 2, 1);
+  }
+}
+
+// Warp per atom: the lanes stride the atom's CSR row and the fp64 partial sums are combined by a
+// fixed butterfly, so the result is deterministic (and independent of the chunking).
+// F_a = sum_{e in row a} (g_e - g_rev(e)) (+ the returned ghost forces).  g_rev(e) is read from gT[e]
+// (= g[rev[e]], or 0 without a reverse edge), which the producer of g scattered, so both operands
+// stream sequentially: no dependent index -> gather round trip.
+__global__ void k_force_warp(int64_t n, const int32_t* __restrict__ row_ptr, const float* __restrict__ g,
+                             const float* __restrict__ gT, const long long* __restrict__ acc, double* __restrict__ F,
+                             int* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (a >= n) return;
+  double f[3] = {0, 0, 0};
+  const int64_t r0 = row_ptr[a], r1 = row_ptr[a + 1];
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* t4 = reinterpret_cast<const float4*>(gT);
+  // Four edges per lane per round, all eight 16-B loads in flight before the first use (each lane
+  // adds its edges in the order r0 + lane, + 32, + 64, ...).
+  for (int64_t base = r0; base < r1; base += 128) {
+    float4 a4[4], b4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = base + lane + 32 * k;
+      a4[k] = e < r1 ? __ldg(g4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      b4[k] = e < r1 ? __ldg(t4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (base + lane + 32 * k < r1) {
@@ -1377,6 +1434,8 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     bo.ubar = w.ubar.p;
     bo.ybar = w.ybar.p;
     bo.g = c->g.p;
+    bo.rev = c->rev.p;
+    bo.gT = force_scatter() ? c->gT.p : nullptr;
     tb_bwd(tbio, bo, st, &c->prof);
     return;
   }
@@ -1394,7 +1453,8 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     {
       ProfScope ps_(&c->prof, st, PK_GEOM_BWD, 0, (double)E * (8 + 4 + 128 + 4 * dsh + 16));
       k_geom_bwd<<<ceil_div(E, 256), 256, 0, st>>>(ch, gp, c->apos.p, c->cidx.p, c->nbr.p, w.ubar.p, M.w.tb_w0.f,
-                                                 1.f / std::sqrt(12.f), w.ab1.p, w.ybar.p, c->g.p);
+                                                 1.f / std::sqrt(12.f), w.ab1.p, w.ybar.p, c->g.p, c->rev.p,
+                                                 force_scatter() ? c->gT.p : nullptr);
     }
     ALG_LAUNCH_CHECK();
   }
@@ -1442,9 +1502,15 @@ void compute_forces(allegro_ctx* c, bool defer_e) {
   if (c->dom.multi) ghost_force_return(c);
   if (n > 0) {
     {
-      ProfScope ps_(&c->prof, st, PK_FORCE, 0, 24.0 * n + 8.0 * n + 28.0 * E);  // algorithmic: g_e, g_rev (12 B each), rev
-      k_force_warp<<<ceil_div(n * 32, 256), 256, 0, st>>>(n, c->row_ptr.p, c->rev.p, c->g.p,
-                                                        c->dom.multi ? c->dom.acc.p : nullptr, c->frc.p, c->flags.p);
+      // algorithmic: g_e, g_rev (12 B each); + rev (4 B) on the gather variant
+      ProfScope ps_(&c->prof, st, PK_FORCE, 0, 24.0 * n + 8.0 * n + (force_scatter() ? 24.0 : 28.0) * E);
+      if (force_scatter())
+        k_force_warp<<<ceil_div(n * 32, 256), 256, 0, st>>>(n, c->row_ptr.p, c->g.p, c->gT.p,
+                                                          c->dom.multi ? c->dom.acc.p : nullptr, c->frc.p, c->flags.p);
+      else
+        k_force_warp_rev<<<ceil_div(n * 32, 256), 256, 0, st>>>(n, c->row_ptr.p, c->rev.p, c->g.p,
+                                                              c->dom.multi ? c->dom.acc.p : nullptr, c->frc.p,
+                                                              c->flags.p);
     }
     ALG_LAUNCH_CHECK();
   }

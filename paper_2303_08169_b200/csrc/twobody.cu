@@ -350,6 +350,8 @@ struct TbbParams {
   const float* ubar;
   const float* ybar;
   float* g;
+  const int32_t* rev;
+  float* gT;
 };
 
 __device__ __forceinline__ float dsilu_tb(float t) {
@@ -450,10 +452,12 @@ __global__ void __launch_bounds__(32 * 8, 1) k_tb_bwd(const __grid_constant__ CU
       const int32_t ci = nx.i, ca = nx.a;
       if (t + 2 < n_my) nx.load(p, tile_row(t + 2, qw, lane));
       float uu = 0.f, a1[32], x[32], r[3] = {0.f, 0.f, 0.f}, ub = 0.f, yb[9];
+      int32_t rv = -1;
 #pragma unroll
       for (int c = 0; c < 32; ++c) a1[c] = 0.f;
       if (valid) {
         ub = __ldg(q.ubar + e);  // consumed at the end of the tile: in flight across the MMA chain
+        rv = __ldg(q.rev + p.ch.e0 + e);
         load_ybar(q.ybar, e, p.gp.dsh, yb);
         geom_row<false>(p, reinterpret_cast<const float4*>(&sw[0][0]), ci, ca, uu, nullptr, a1, r);
       }
@@ -556,7 +560,7 @@ __global__ void __launch_bounds__(32 * 8, 1) k_tb_bwd(const __grid_constant__ CU
             zbar[4 * h + 3] = fmaf(ab1, w4.w, zbar[4 * h + 3]);
           }
         }
-        geom_bwd_tail(p.gp, r, ub, yb, p.s0, zbar, q.g, p.ch.e0 + e);
+        geom_bwd_tail(p.gp, r, ub, yb, p.s0, zbar, q.g, p.ch.e0 + e, rv, q.gT);
       }
       __syncwarp();
     }
@@ -671,6 +675,8 @@ void tb_bwd(const TbIO& io, const TbbIO& bo, cudaStream_t st, Profiler* prof) {
   q.ubar = bo.ubar;
   q.ybar = bo.ybar;
   q.g = bo.g;
+  q.rev = bo.rev;
+  q.gT = bo.gT;
   const CUtensorMap mx = map_rows(bo.xbar, E, 128);
   const size_t smem = ((p.w1bytes + 1023) & ~1023u) + ((q.w2t_bytes + 1023) & ~1023u) +
                       ((q.w1t_bytes + 1023) & ~1023u) + 32 * kBox + 12 * 32 * 4 + 32 * kNB * 4 + 256;

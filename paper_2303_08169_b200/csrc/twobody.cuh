@@ -42,6 +42,8 @@ struct TbbIO {
   const float* ubar = nullptr;
   const float* ybar = nullptr;
   float* g = nullptr;
+  const int32_t* rev = nullptr;  // [E] reverse edge (global index) or -1
+  float* gT = nullptr;           // [E][4] g scattered to the reverse edge's slot
 };
 
 void tb_bwd(const TbIO& io, const TbbIO& bo, cudaStream_t st, Profiler* prof);
