@@ -167,7 +167,7 @@ struct allegro_ctx {
   allegro::DBuf<int32_t> nb_count, nb_pad, row_ptr, nbr, cidx, rev;
   allegro::DBuf<unsigned long long> key_pad, key;
   allegro::DBuf<float> g;                    // [E][4] dE/dr_e (x, y, z, pad)
-  allegro::DBuf<float> gT;                   // [E][4] gT[e] = g[rev[e]] (0 without a reverse edge), scattered by
+  allegro::DBuf<float> gT;                   // [E][3] gT[e] = g[rev[e]] (0 without a reverse edge), scattered by
                                              // the producer of g so the force gather streams both arrays
   std::vector<int32_t> h_row_ptr;
   std::vector<int64_t> chunk_a0;             // first centre atom of each model chunk (last evaluation)

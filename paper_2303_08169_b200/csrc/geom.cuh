@@ -57,8 +57,8 @@ __device__ __forceinline__ void load_ybar(const float* __restrict__ ybar, int64_
 // The geometry adjoint of one edge (global index ge, edge vector r), given zbar = ab1 W0[Bessel
 // rows]^T, its u-bar and Y-bar: the u / B chain rule, the envelope derivative and the Y-bar term;
 // writes g [E][4] (shared by k_geom_bwd and the fused two-body reverse, so both give the same bits).
-// rr = rev[ge]: g is also stored at gT[rr] (the reverse edge's slot), or gT[ge] = 0 when the edge has
-// no reverse (rev is an involution, so every gT slot has exactly one writer).
+// rr = rev[ge]: g is also stored at gT[rr] (the reverse edge's slot, [E][3] packed), or gT[ge] = 0
+// when the edge has no reverse (rev is an involution, so every gT slot has exactly one writer).
 __device__ __forceinline__ void geom_bwd_tail(const GeomParams& gp, const float r[3], float ub, const float* yb,
                                               float s0, const float* zbar, float* __restrict__ g, int64_t ge,
                                               int32_t rr, float* __restrict__ gT) {
@@ -112,9 +112,11 @@ __device__ __forceinline__ void geom_bwd_tail(const GeomParams& gp, const float 
   }
   const float4 g4 = make_float4(gx, gy, gz, 0.f);
   reinterpret_cast<float4*>(g)[ge] = g4;
-  if (gT != nullptr) {
-    if (rr >= 0) reinterpret_cast<float4*>(gT)[rr] = g4;
-    else reinterpret_cast<float4*>(gT)[ge] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (gT != nullptr) {  // packed [E][3]: the force gather reads 12 B per edge from it
+    const int64_t t = 3 * (rr >= 0 ? (int64_t)rr : ge);
+    gT[t] = rr >= 0 ? gx : 0.f;
+    gT[t + 1] = rr >= 0 ? gy : 0.f;
+    gT[t + 2] = rr >= 0 ? gz : 0.f;
   }
 }
 

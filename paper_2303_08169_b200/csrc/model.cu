@@ -927,16 +927,17 @@ __global__ void k_force_warp(int64_t n, const int32_t* __restrict__ row_ptr, con
   double f[3] = {0, 0, 0};
   const int64_t r0 = row_ptr[a], r1 = row_ptr[a + 1];
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  const float4* t4 = reinterpret_cast<const float4*>(gT);
-  // Four edges per lane per round, all eight 16-B loads in flight before the first use (each lane
-  // adds its edges in the order r0 + lane, + 32, + 64, ...).
+  // Four edges per lane per round, all loads in flight before the first use (each lane adds its
+  // edges in the order r0 + lane, + 32, + 64, ...); gT is packed [E][3] (12 B per edge)
   for (int64_t base = r0; base < r1; base += 128) {
-    float4 a4[4], b4[4];
+    float4 a4[4];
+    float3 b4[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t e = base + lane + 32 * k;
       a4[k] = e < r1 ? __ldg(g4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-      b4[k] = e < r1 ? __ldg(t4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      b4[k] = e < r1 ? make_float3(__ldg(gT + 3 * e), __ldg(gT + 3 * e + 1), __ldg(gT + 3 * e + 2))
+                     : make_float3(0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {

@@ -446,7 +446,7 @@ void build_neighbors(allegro_ctx* c) {
   c->cidx.reserve(E + 1);
   c->rev.reserve(E + 1);
   c->g.reserve(4 * (size_t)E + 4);  // [E][4] (x, y, z, pad)
-  c->gT.reserve(4 * (size_t)E + 4);
+  c->gT.reserve(3 * (size_t)E + 4);
   if (n > 0) {
     {
       ProfScope ps_(&c->prof, st, PK_EDGE, 0, 4.0 * n);
