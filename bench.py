@@ -446,7 +446,7 @@ def main():
         "kernels": kernels,
         "gpu_launches": launches,
         "shapes": [{"tag": t, "ms_per_step": round(ms_ / n_prof, 3), "gbs": round(by / max(ms_, 1e-9) / 1e6, 1),
-                    "launches_per_step": n_ / n_prof} for t, ms_, by, n_ in detail[:24]],
+                    "launches_per_step": n_ / n_prof} for t, ms_, by, n_ in detail[:40]],
         "profiled_steps": n_prof,
         "edges": {"first": edges_first, "profiled": edges_prof, "last": edges_last,
                   "edges_per_s": round(0.5 * (edges_first + edges_last) * args.steps / (ms_max / 1e3), 1)},

@@ -127,6 +127,10 @@ struct Domain {
   DBuf<int32_t> flag, pos_idx;
   DBuf<long long> acc;          // [n + G][3] fixed-point ghost-force accumulators
   DBuf<long long> cnt;          // scratch counts
+  DBuf<long long> hs;           // halo message-path state (domain.cu: n_cur, overflow, per-stage counts)
+  double cap_scale = 1.0;       // halo message capacity scale (doubled on overflow, on every rank)
+  DBuf<long long> ms;           // migration message-path state (owned count, stayers, overflow)
+  DBuf<unsigned char> mstage;   // migration stayers staging (MigAtom)
   DBuf<double> red;             // allreduce scratch
   // migration / halo scratch (per ctx, so ctxs on different devices or threads never share it)
   DBuf<double> tpos, tvel;
