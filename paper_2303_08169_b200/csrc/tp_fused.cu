@@ -586,6 +586,7 @@ struct TpbParams {
   uint32_t wbytes[kMaxIr];
   float scale[kMaxIr];
   int n_tiles, sa, sb;  // ring depths
+  int rr;               // TP warps take the tile's edges round-robin across both T-bar halves
 };
 
 struct TpbMaps {
@@ -855,11 +856,30 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
       const unsigned char* st = ringB + (size_t)s * B::b_bytes();
       const int* hdr = reinterpret_cast<const int*>(st + B::h_off());
       const int nv = hdr[32], a_lo = hdr[33];
-      for (int h = 0; h < 2; ++h) {
-      mbar_wait(tb_full + h, (uint32_t)t & 1u);
-      const unsigned char* tbh = tbt + (size_t)h * (B::tb_bytes() / 2);
-      const int e_end = 16 * h + 16 < nv ? 16 * h + 16 : nv;
-      for (int e = 16 * h + warp; e < e_end; e += kBTp) {
+      // the tile's 32 edges over the kBTp warps round-robin across both T-bar halves (edges w, w + 12,
+      // w + 24: three rounds instead of two per half, i.e. 32 edges in 36 slots, not 48); a warp
+      // releases half 0 when it moves to its first half-1 edge (every warp has edges in both)
+      mbar_wait(tb_full + 0, (uint32_t)t & 1u);
+      bool in_h1 = false;
+      for (int r = 0; r < 4; ++r) {
+        int e;
+        if (p.rr) {  // round-robin over the whole tile (default)
+          e = warp + r * kBTp;
+          if (e >= 2 * 16) break;
+        } else {  // A/B: each half in turn, edges 16 h + w (+ 12)
+          e = 16 * (r >> 1) + warp + (r & 1) * kBTp;
+          if (e >= 16 * (r >> 1) + 16) continue;
+        }
+        const int h = e >> 4;
+        if (h == 1 && !in_h1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tb_empty + 0);
+          mbar_wait(tb_full + 1, (uint32_t)t & 1u);
+          in_h1 = true;
+        }
+        if (e >= nv) continue;
+        const unsigned char* tbh = tbt + (size_t)h * (B::tb_bytes() / 2);
+        {
         const int ga = hdr[e];
         const float* gsrc = ga < kBGA ? reinterpret_cast<const float*>(st + B::g_off() + (size_t)ga * DSH * 128)
                                       : p.G + (int64_t)(a_lo + ga) * DSH * 32;
@@ -941,9 +961,10 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
 #pragma unroll
         for (int m = 0; m < DSH; ++m) p.gp[(ge * DSH + m) * 32 + c] = gp[m];
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tb_empty + h);
       }
+      static_assert(kBTp > 8 && kBTp <= 16, "every TP warp needs an edge in each T-bar half");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tb_empty + 1);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(in_empty_b + s);
@@ -1016,6 +1037,13 @@ void launch_bwd(const TpbIO& io, cudaStream_t st, Profiler* prof) {
   if (sa < 2) throw CudaError("tpl_bwd: shared memory too small for two stages per ring");
   p.sa = sa;
   p.sb = 2;
+  {
+    static const int rr = [] {
+      const char* e = std::getenv("ALLEGRO_TPB_RR");
+      return (!e || std::atoi(e) != 0) ? 1 : 0;
+    }();
+    p.rr = rr;
+  }
   const size_t smem = fixed + (size_t)sa * B::a_bytes();
   int dev = 0;
   ALG_CUDA(cudaGetDevice(&dev));
