@@ -25,6 +25,8 @@ OBJDIR = os.path.join(ROOT, "build", "obj")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-Wall", "-I", os.path.join(ROOT, "include")]
+# build-time A/B switches for measurements (e.g. ALLEGRO_NVCC_DEFS="-DALG_MBAR_HINT=20000"); rebuild with --force
+FLAGS += os.environ.get("ALLEGRO_NVCC_DEFS", "").split()
 
 
 def nvcc() -> str:

@@ -528,13 +528,25 @@ void launch(const TplIO& io, cudaStream_t st, Profiler* prof) {
 //   warps 12-15 split: V-bar rows (TMA boxes, one per (o, m3)) -> TF32 hi / lo -> TMEM A stage
 //   warps 16-19 T-bar copy: tcgen05.ld of D (thread = row), scale, + s-bar, -> SMEM tile
 //   warp 20     producer (TMA / bulk loads), warp 21 TMEM allocator + MMA issuer
-constexpr int kBTp = 12;
-constexpr int kBSplit0 = kBTp;
-constexpr int kBCopy0 = kBTp + 4;
-constexpr int kBProd = kBTp + 8;   // ring B producer (the TP inputs)
-constexpr int kBMma = kBTp + 9;
-constexpr int kBProdA = kBTp + 10; // ring A producer (the MMA chain's V-bar / s-bar boxes) + W images
-constexpr int kBThreads = 32 * (kBTp + 11);
+// TP warps of k_tpl_bwd per layer (build-time A/B): layer 0 (w (x) Y inputs, w-bar / Y-bar outputs)
+// is TP-warp-bound and takes 16 (one edge per warp per T-bar half); layer >= 1 is closer to its HBM
+// bound and runs faster with 12 (more registers per thread for the rest)
+#ifndef ALG_TPB_WARPS0
+#define ALG_TPB_WARPS0 16
+#endif
+#ifndef ALG_TPB_WARPS1
+#define ALG_TPB_WARPS1 12
+#endif
+template <int K>
+struct BW {
+  static constexpr int Tp = K == 0 ? ALG_TPB_WARPS0 : ALG_TPB_WARPS1;
+  static constexpr int Split0 = Tp;
+  static constexpr int Copy0 = Tp + 4;
+  static constexpr int Prod = Tp + 8;   // ring B producer (the TP inputs)
+  static constexpr int Mma = Tp + 9;
+  static constexpr int ProdA = Tp + 10; // ring A producer (the MMA chain's V-bar / s-bar boxes) + W images
+  static constexpr int Threads = 32 * (Tp + 11);
+};
 constexpr int kBAStages = 3;
 constexpr int kBGA = 8;  // Gamma rows staged per tile (atoms); wider spans read from L2
 
@@ -587,6 +599,8 @@ struct TpbParams {
   float scale[kMaxIr];
   int n_tiles, sa, sb;  // ring depths
   int rr;               // TP warps take the tile's edges round-robin across both T-bar halves
+  int diag;             // timing diagnostics (ALLEGRO_TPB_DIAG, wrong results): bit0 TP warps skip the
+                        // edge work, bit1 copy warps skip the TMEM reads / T-bar stores
 };
 
 struct TpbMaps {
@@ -596,7 +610,9 @@ struct TpbMaps {
 };
 
 template <int NL, int LMAX, int K>
-__global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant__ TpbMaps maps, const TpbParams p) {
+__global__ void __launch_bounds__(BW<K>::Threads, 1) k_tpl_bwd(const __grid_constant__ TpbMaps maps, const TpbParams p) {
+  constexpr int kBTp = BW<K>::Tp, kBSplit0 = BW<K>::Split0, kBCopy0 = BW<K>::Copy0, kBProd = BW<K>::Prod,
+                kBMma = BW<K>::Mma, kBProdA = BW<K>::ProdA;
   using B = Bz<NL, LMAX, K>;
   using F = Fz<NL, LMAX, K>;
   using AR = Arch<NL, LMAX, K>;
@@ -725,22 +741,26 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
         mbar_wait(a_empty + j, aph ^ 1);
         if (m3 < F::dim(o)) {
           const unsigned char* row = st + B::vb_off(o) + m3 * kBoxBytes + lane * 128;
-          uint32_t hi[32], lo[32];
-#pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4) {
-            const float4 v = *reinterpret_cast<const float4*>(row + ((c4 ^ (lane & 7)) << 4));
-            const float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint32_t h = __float_as_uint(x[q]) & 0xffffe000u;
-              hi[4 * c4 + q] = h;
-              lo[4 * c4 + q] = __float_as_uint(x[q] - __uint_as_float(h));
-            }
-          }
-          tc_fence_after();
           const uint32_t ta = tmem_a + (uint32_t)(j * kATm) + ((uint32_t)(qw * 32) << 16);
-          tmem_st32(ta, hi);
-          tmem_st32(ta + 32, lo);
+          tc_fence_after();
+#pragma unroll
+          for (int hc = 0; hc < 2; ++hc) {  // two 16-column chunks (register budget of 16 TP warps)
+            uint32_t hi[16], lo[16];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const int cc = 4 * hc + c4;
+              const float4 v = *reinterpret_cast<const float4*>(row + ((cc ^ (lane & 7)) << 4));
+              const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t h = __float_as_uint(x[q]) & 0xffffe000u;
+                hi[4 * c4 + q] = h;
+                lo[4 * c4 + q] = __float_as_uint(x[q] - __uint_as_float(h));
+              }
+            }
+            tmem_st16(ta + 16 * hc, hi);
+            tmem_st16(ta + 32 + 16 * hc, lo);
+          }
           tmem_st_wait();
         }
         tc_fence_before();
@@ -810,25 +830,31 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
           constexpr int o = decltype(O)::value;
           constexpr int B0 = F::base(o);
           const int m3 = (qw - B0 + 4) & 3;
-          if (m3 < F::dim(o)) {
+          if (m3 < F::dim(o) && !(p.diag & 2)) {
             static_for<A.n_to[o]>([&](auto P) {
               constexpr int pl = decltype(P)::value;
               constexpr int q = F::path_of(o, pl);
-              float v[32];
-              tmem_ld32(tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(buf * B::acc_cols() + B::col_off(o) + 32 * pl), v);
-              if (mine) {
-                const float sc = p.scale[o];
-                const int row = (e & 15) * DT + A.t_off[q] + m3;
-                unsigned char* dst = tbt + (size_t)h * (B::tb_bytes() / 2) + (size_t)row * 128;
-                const unsigned char* sbr = st + B::sb_off() + pl * kBoxBytes + e * 128;
 #pragma unroll
-                for (int c4 = 0; c4 < 8; ++c4) {
-                  float4 w4 = make_float4(sc * v[4 * c4], sc * v[4 * c4 + 1], sc * v[4 * c4 + 2], sc * v[4 * c4 + 3]);
-                  if constexpr (F::scalar(o)) {  // T-bar of the scalar paths += s-bar (same order as EPI_ADDX)
-                    const float4 a4 = *reinterpret_cast<const float4*>(sbr + ((c4 ^ (e & 7)) << 4));
-                    w4 = make_float4(w4.x + a4.x, w4.y + a4.y, w4.z + a4.z, w4.w + a4.w);
+              for (int hc = 0; hc < 2; ++hc) {  // 16-column chunks (register budget of 16 TP warps)
+                float v[16];
+                tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) +
+                              (uint32_t)(buf * B::acc_cols() + B::col_off(o) + 32 * pl + 16 * hc),
+                          v);
+                if (mine) {
+                  const float sc = p.scale[o];
+                  const int row = (e & 15) * DT + A.t_off[q] + m3;
+                  unsigned char* dst = tbt + (size_t)h * (B::tb_bytes() / 2) + (size_t)row * 128;
+                  const unsigned char* sbr = st + B::sb_off() + pl * kBoxBytes + e * 128;
+#pragma unroll
+                  for (int c4 = 0; c4 < 4; ++c4) {
+                    const int cc = 4 * hc + c4;
+                    float4 w4 = make_float4(sc * v[4 * c4], sc * v[4 * c4 + 1], sc * v[4 * c4 + 2], sc * v[4 * c4 + 3]);
+                    if constexpr (F::scalar(o)) {  // T-bar of the scalar paths += s-bar (same order as EPI_ADDX)
+                      const float4 a4 = *reinterpret_cast<const float4*>(sbr + ((cc ^ (e & 7)) << 4));
+                      w4 = make_float4(w4.x + a4.x, w4.y + a4.y, w4.z + a4.z, w4.w + a4.w);
+                    }
+                    *reinterpret_cast<float4*>(dst + ((cc ^ (row & 7)) << 4)) = w4;
                   }
-                  *reinterpret_cast<float4*>(dst + ((c4 ^ (row & 7)) << 4)) = w4;
                 }
               }
             });
@@ -856,9 +882,9 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
       const unsigned char* st = ringB + (size_t)s * B::b_bytes();
       const int* hdr = reinterpret_cast<const int*>(st + B::h_off());
       const int nv = hdr[32], a_lo = hdr[33];
-      // the tile's 32 edges over the kBTp warps round-robin across both T-bar halves (edges w, w + 12,
-      // w + 24: three rounds instead of two per half, i.e. 32 edges in 36 slots, not 48); a warp
-      // releases half 0 when it moves to its first half-1 edge (every warp has edges in both)
+      // the tile's 32 edges over the kBTp warps round-robin across both T-bar halves (with 12 warps:
+      // edges w, w + 12, w + 24, three rounds instead of two per half; with 16: one edge per half); a
+      // warp releases half 0 when it moves to its first half-1 edge (every warp has edges in both)
       mbar_wait(tb_full + 0, (uint32_t)t & 1u);
       bool in_h1 = false;
       for (int r = 0; r < 4; ++r) {
@@ -877,7 +903,7 @@ __global__ void __launch_bounds__(kBThreads, 1) k_tpl_bwd(const __grid_constant_
           mbar_wait(tb_full + 1, (uint32_t)t & 1u);
           in_h1 = true;
         }
-        if (e >= nv) continue;
+        if (e >= nv || (p.diag & 1)) continue;
         const unsigned char* tbh = tbt + (size_t)h * (B::tb_bytes() / 2);
         {
         const int ga = hdr[e];
@@ -1043,8 +1069,13 @@ void launch_bwd(const TpbIO& io, cudaStream_t st, Profiler* prof) {
       return (!e || std::atoi(e) != 0) ? 1 : 0;
     }();
     p.rr = rr;
+    const char* dg = std::getenv("ALLEGRO_TPB_DIAG");
+    p.diag = dg ? std::atoi(dg) : 0;
   }
   const size_t smem = fixed + (size_t)sa * B::a_bytes();
+  if (std::getenv("ALLEGRO_TPB_INFO"))
+    std::fprintf(stderr, "[tpl_bwd K=%d] W %u B, ring A %d x %d B, ring B %d x %d B, T-bar %d B, smem %zu B\n", K,
+                 wsum, sa, B::a_bytes(), p.sb, B::b_bytes(), B::tb_bytes(), smem);
   int dev = 0;
   ALG_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};
@@ -1068,7 +1099,7 @@ void launch_bwd(const TpbIO& io, cudaStream_t st, Profiler* prof) {
     else bytes += 2.0 * A.dim_in * 128;                                      // V^k in, V-bar^k out
     bytes += (double)B::DSH * 128;                                           // Gamma-bar terms out
     ProfScope ps_(prof, st, PK_TPL_BWD, flops, bytes * E, tag);
-    k_tpl_bwd<NL, LMAX, K><<<grid, kBThreads, smem, st>>>(maps, p);
+    k_tpl_bwd<NL, LMAX, K><<<grid, BW<K>::Threads, smem, st>>>(maps, p);
   }
   ALG_LAUNCH_CHECK();
   if (std::getenv("ALLEGRO_SYNC_CHECK")) {
