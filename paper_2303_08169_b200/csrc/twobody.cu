@@ -572,6 +572,307 @@ __global__ void __launch_bounds__(32 * 8, 1) k_tb_bwd(const __grid_constant__ CU
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// k_tb_bwd2: the same reverse with each row's columns split over TWO warps per lane quarter (16 row
+// warps = 2 groups x 8): the kernel is bound by the row warps' ALU issue (35 % issue-active with 8
+// warps), and TMEM holds only two tiles' chains, so more warps must share a tile's rows.  Warp
+// j = 0..7 of group g: lane quarter j & 3, column half hf = j >> 2.  Each computes the geometry
+// (duplicated), its 16 columns of a1 / dsilu(a1) / ab1, its two x-bar0 K-blocks and its 32 columns
+// of ab2; the zbar chain (j = 0..31, the unfused order) runs j < 16 in the hf = 0 warp, which hands
+// its partial sums to the hf = 1 warp through shared memory, which finishes the chain and the
+// geometry adjoint.  Bit-identical to k_tb_bwd.
+__device__ __forceinline__ void geom_core(const TbParams& p, int32_t i, int32_t a, float* r, float& uu, float* zb,
+                                          int& zi, int& zj) {
+  edge_vec(p.apos, i, a, r);
+  const float d = sqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  const float x = d * p.gp.inv_rc;
+  uu = 0.f;
+  if (x < 1.f) {
+    const float x2 = x * x, x3 = x2 * x, x6 = x3 * x3;
+    uu = 1.f - 28.f * x6 + 48.f * x6 * x - 21.f * x6 * x2;
+  }
+  zi = p.species[i], zj = p.aspec[a];
+  const float pre = 2.f * p.gp.inv_rc / d;
+#pragma unroll
+  for (int q = 0; q < kNB; ++q) zb[q] = uu * pre * sinf(p.gp.freq[q] * d * p.gp.inv_rc);
+}
+
+// columns 16 hf .. 16 hf + 15 of a1 (the arithmetic of geom_row, per 4-column group)
+__device__ __forceinline__ void a1_half(const TbParams& p, const float4* s4, int hf, const float* zb, int zi, int zj,
+                                        float* a1) {
+#pragma unroll
+  for (int k4 = 0; k4 < 4; ++k4) {
+    const int c4 = 4 * hf + k4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (zi < 2) acc = s4[zi * 8 + c4];
+    if (zj < 2) {
+      const float4 b = s4[(2 + zj) * 8 + c4];
+      acc = make_float4(acc.x + b.x, acc.y + b.y, acc.z + b.z, acc.w + b.w);
+    }
+#pragma unroll
+    for (int q = 0; q < kNB; ++q) {
+      const float4 wq = s4[(4 + q) * 8 + c4];
+      acc = make_float4(fmaf(zb[q], wq.x, acc.x), fmaf(zb[q], wq.y, acc.y), fmaf(zb[q], wq.z, acc.z),
+                        fmaf(zb[q], wq.w, acc.w));
+    }
+    a1[4 * k4 + 0] = p.s0 * acc.x;
+    a1[4 * k4 + 1] = p.s0 * acc.y;
+    a1[4 * k4 + 2] = p.s0 * acc.z;
+    a1[4 * k4 + 3] = p.s0 * acc.w;
+  }
+}
+
+__device__ __forceinline__ void split_store16(uint32_t taddr_hi, uint32_t taddr_lo, const float* x) {
+  uint32_t hi[16], lo[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const uint32_t h = __float_as_uint(x[c]) & 0xffffe000u;
+    hi[c] = h;
+    lo[c] = __float_as_uint(x[c] - __uint_as_float(h));
+  }
+  tmem_st16(taddr_hi, hi);
+  tmem_st16(taddr_lo, lo);
+}
+
+// one swizzled [32 x 32] box row -> hi / lo TMEM (two 16-column halves: register budget)
+__device__ __forceinline__ void split_box16(uint32_t taddr, const unsigned char* box, int lane) {
+#pragma unroll
+  for (int hc = 0; hc < 2; ++hc) {
+    float x[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = 4 * hc + k;
+      const float4 v = *reinterpret_cast<const float4*>(box + lane * 128 + ((c ^ (lane & 7)) << 4));
+      x[4 * k] = v.x, x[4 * k + 1] = v.y, x[4 * k + 2] = v.z, x[4 * k + 3] = v.w;
+    }
+    split_store16(taddr + 16 * hc, taddr + 32 + 16 * hc, x);
+  }
+}
+
+constexpr int kTb2Warps = 16;
+
+__global__ void __launch_bounds__(32 * kTb2Warps, 1) k_tb_bwd2(const __grid_constant__ CUtensorMap map_xbar,
+                                                              const TbbParams q) {
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  const TbParams& p = q.f;
+  if (smem_u32(smem_dyn) & 1023u) __trap();
+  unsigned char* w1s = smem_dyn;
+  unsigned char* w2ts = w1s + ((p.w1bytes + 1023u) & ~1023u);
+  unsigned char* w1ts = w2ts + ((q.w2t_bytes + 1023u) & ~1023u);
+  unsigned char* slots = w1ts + ((q.w1t_bytes + 1023u) & ~1023u);  // [16 warps][2 K-blocks][4 KB]
+  float(*sw)[32] = reinterpret_cast<float(*)[32]>(slots + 32 * kBox);
+  float(*swt)[kNB] = reinterpret_cast<float(*)[kNB]>(slots + 32 * kBox + 12 * 32 * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + 32 * kBox + 12 * 32 * 4 + 32 * kNB * 4);
+  uint64_t* a1_full = bars;        // [2]
+  uint64_t* d1_full = bars + 2;    // [2]
+  uint64_t* x3a_full = bars + 4;   // [2]
+  uint64_t* x3a_empty = bars + 6;  // [2]
+  uint64_t* x3b_full = bars + 8;   // [2]
+  uint64_t* d3_full = bars + 10;   // [2]
+  uint64_t* a4_full = bars + 12;   // [2]
+  uint64_t* d4_full = bars + 14;   // [2]
+  uint64_t* xb_full = bars + 16;   // [16] per row warp
+  uint64_t* w_full = bars + 32;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 33);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = threadIdx.x; t < 12 * 32; t += blockDim.x) sw[t / 32][t % 32] = p.w0[t];
+  for (int t = threadIdx.x; t < kNB * 32; t += blockDim.x) swt[t % 32][t / 32] = p.w0[4 * 32 + t];
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(a1_full + g, 8), mbar_init(d1_full + g, 1), mbar_init(x3a_full + g, 8), mbar_init(x3a_empty + g, 1);
+      mbar_init(x3b_full + g, 8), mbar_init(d3_full + g, 1), mbar_init(a4_full + g, 8), mbar_init(d4_full + g, 1);
+    }
+    for (int w = 0; w < kTb2Warps; ++w) mbar_init(xb_full + w, 1);
+    mbar_init(w_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_my = p.n_tiles > (int)blockIdx.x ? (p.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  if (warp == 0 && lane == 0) {
+    mbar_expect_tx(w_full, p.w1bytes + q.w2t_bytes + q.w1t_bytes);
+    bulk_load(w1s, p.w1img, p.w1bytes, w_full);
+    bulk_load(w2ts, q.w2t_img, q.w2t_bytes, w_full);
+    bulk_load(w1ts, q.w1t_img, q.w1t_bytes, w_full);
+  }
+  const int g = warp >> 3, j8 = warp & 7, qw = j8 & 3, hf = j8 >> 2;
+  const bool issuer = j8 == 0;
+  const uint32_t bm = tmem + 256u * g;
+  uint32_t L = 0;
+  if (issuer) {
+    mbar_wait(w_full, 0);
+    tc_fence_after();
+    __syncwarp();
+    L = elect_leader();
+  }
+  const uint64_t dw1 = sdesc(smem_u32(w1s)), dw2t = sdesc(smem_u32(w2ts)), dw1t = sdesc(smem_u32(w1ts));
+  const uint64_t kb64 = (uint64_t)((2 * 64 * 128) >> 4), kb32 = (uint64_t)((2 * 32 * 128) >> 4);
+  const uint32_t b = bm + ((uint32_t)(qw * 32) << 16);
+  unsigned char* myslots = slots + (size_t)(2 * warp) * kBox;
+  // the zbar hand-off (hf = 0 -> hf = 1 warp of the same quarter) uses the hf = 0 warp's first slot
+  float* zhand = reinterpret_cast<float*>(slots + (size_t)(2 * (8 * g + qw)) * kBox) + lane * kNB;
+  const int pair_bar = 1 + 4 * g + qw;  // named barrier of the (hf = 0, hf = 1) warp pair
+  auto load_xbar = [&](int t) {  // this warp's 32 rows of tile t: K-blocks hf and 2 + hf
+    if (lane == 0 && t < n_my) {
+      const int row0 = ((int)blockIdx.x + t * (int)gridDim.x) * kRows + qw * 32;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(xb_full + warp, 2 * kBox);
+      tma_load_2d(myslots, &map_xbar, 32 * hf, row0, xb_full + warp);
+      tma_load_2d(myslots + kBox, &map_xbar, 32 * (2 + hf), row0, xb_full + warp);
+    }
+  };
+  auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
+  load_xbar(g);
+  NextIdx nx;
+  if (g < n_my) nx.load(p, tile_row(g, qw, lane));
+  for (int t = g; t < n_my; t += 2) {
+    const uint32_t ph = (uint32_t)(t >> 1) & 1u;
+    const int64_t e = tile_row(t, qw, lane);
+    const bool valid = e < p.ch.n_e;
+    const int32_t ci = nx.i, ca = nx.a;
+    if (t + 2 < n_my) nx.load(p, tile_row(t + 2, qw, lane));
+    float uu = 0.f, da1[16], x[16], r[3] = {0.f, 0.f, 0.f}, ub = 0.f, yb[9];
+    int32_t rv = -1;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) da1[c] = 0.f;
+    if (valid) {
+      if (hf == 1) {  // the geometry adjoint's inputs, in flight across the MMA chain
+        ub = __ldg(q.ubar + e);
+        rv = __ldg(q.rev + p.ch.e0 + e);
+        load_ybar(q.ybar, e, p.gp.dsh, yb);
+      }
+      float zb[kNB];
+      int zi, zj;
+      geom_core(p, ci, ca, r, uu, zb, zi, zj);
+      a1_half(p, reinterpret_cast<const float4*>(&sw[0][0]), hf, zb, zi, zj, da1);
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {  // SiLU(a1) for MMA1 and dsilu(a1) for ab1, one sigmoid each
+      const float sg = sigm_tb(da1[c]);
+      x[c] = da1[c] * sg;
+      da1[c] = sg * (1.f + da1[c] * (1.f - sg));
+    }
+    tc_fence_after();
+    split_store16(b + 16 * hf, b + 32 + 16 * hf, x);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(a1_full + g);
+    if (issuer) {
+      mbar_wait(a1_full + g, ph);
+      tc_fence_after();
+      mma_kblock(L, bm + 64, bm, dw1, 64, idesc_n(64), true);  // D1 = SiLU(a1) W1
+      mma_commit_w(L, d1_full + g);
+    }
+    // xbar0 K-block hf -> [128 + 64 hf, ...) (free: the previous tile's MMA4 completed)
+    mbar_wait(xb_full + warp, ph);
+    split_box16(b + 128 + 64 * hf, myslots, lane);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(x3a_full + g);
+    if (issuer) {
+      mbar_wait(d1_full + g, ph);  // MMA1 done: D3 may overwrite A1
+      mbar_wait(x3a_full + g, ph);
+      tc_fence_after();
+      mma_kblock(L, bm, bm + 128, dw2t, 64, idesc_n(64), true);  // D3 = xbar0 W2^T, K-blocks 0, 1
+      mma_kblock(L, bm, bm + 192, dw2t + kb64, 64, idesc_n(64), false);
+      mma_commit_w(L, x3a_empty + g);
+    }
+    mbar_wait(x3a_empty + g, ph);
+    tc_fence_after();
+    split_box16(b + 128 + 64 * hf, myslots + kBox, lane);  // K-block 2 + hf
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(x3b_full + g);
+    if (issuer) {
+      mbar_wait(x3b_full + g, ph);
+      tc_fence_after();
+      mma_kblock(L, bm, bm + 128, dw2t + 2 * kb64, 64, idesc_n(64), false);  // K-blocks 2, 3
+      mma_kblock(L, bm, bm + 192, dw2t + 3 * kb64, 64, idesc_n(64), false);
+      mma_commit_w(L, d3_full + g);
+    }
+    if (hf == 1) {  // the hf = 0 warp's slots carry the zbar hand-off: it refills them later
+      load_xbar(t + 2);
+    }
+    if (t + 2 < n_my) nx.prefetch(p);
+    // ab2 columns 32 hf .. 32 hf + 31 = u (s3 D3) dsilu(s1 D1) -> A4 K-block hf
+    mbar_wait(d3_full + g, ph);
+    tc_fence_after();
+#pragma unroll
+    for (int hc = 0; hc < 2; ++hc) {
+      float d1[16], d3[16];
+      tmem_ld16(b + 64 + 32 * hf + 16 * hc, d1);
+      tmem_ld16(b + 32 * hf + 16 * hc, d3);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const float a2 = p.s1 * d1[c];
+        x[c] = uu * (q.s3 * d3[c]) * dsilu_tb(a2);
+      }
+      split_store16(b + 128 + 64 * hf + 16 * hc, b + 128 + 64 * hf + 32 + 16 * hc, x);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(a4_full + g);
+    if (issuer) {
+      mbar_wait(a4_full + g, ph);
+      tc_fence_after();
+      mma_kblock(L, bm + 64, bm + 128, dw1t, 32, idesc_n(32), true);  // D4 = ab2 W1^T
+      mma_kblock(L, bm + 64, bm + 192, dw1t + kb32, 32, idesc_n(32), false);
+      mma_commit_w(L, d4_full + g);
+    }
+    // ab1 columns 16 hf .. 16 hf + 15 = (s4 D4) dsilu(a1); the zbar chain over j in order
+    mbar_wait(d4_full + g, ph);
+    tc_fence_after();
+    tmem_ld16(b + 64 + 16 * hf, x);
+    tc_fence_before();
+    float zbar[kNB];
+    if (hf == 1) {
+      pair_sync();  // the hf = 0 warp's partial sums are in shared memory
+#pragma unroll
+      for (int k = 0; k < kNB; ++k) zbar[k] = zhand[k];
+      pair_sync();  // read: the hf = 0 warp may refill its slots
+    } else {
+#pragma unroll
+      for (int k = 0; k < kNB; ++k) zbar[k] = 0.f;
+    }
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const int j = 16 * hf + jj;
+      const float ab1 = 1.f * (q.s4 * x[jj]) * da1[jj];
+      const float4* wj = reinterpret_cast<const float4*>(&swt[j][0]);
+#pragma unroll
+      for (int h = 0; h < kNB / 4; ++h) {
+        const float4 w4 = wj[h];
+        zbar[4 * h] = fmaf(ab1, w4.x, zbar[4 * h]);
+        zbar[4 * h + 1] = fmaf(ab1, w4.y, zbar[4 * h + 1]);
+        zbar[4 * h + 2] = fmaf(ab1, w4.z, zbar[4 * h + 2]);
+        zbar[4 * h + 3] = fmaf(ab1, w4.w, zbar[4 * h + 3]);
+      }
+    }
+    if (hf == 0) {
+#pragma unroll
+      for (int k = 0; k < kNB; ++k) zhand[k] = zbar[k];
+      pair_sync();
+      pair_sync();
+      load_xbar(t + 2);
+    } else if (valid) {
+      geom_bwd_tail(p.gp, r, ub, yb, p.s0, zbar, q.g, p.ch.e0 + e, rv, q.gT);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 CUtensorMap map_rows(const float* ptr, int64_t rows, int cols) {
   const uint64_t dims[2] = {(uint64_t)cols, (uint64_t)rows};
   const uint64_t strides[1] = {(uint64_t)cols * 4};
@@ -679,13 +980,18 @@ void tb_bwd(const TbIO& io, const TbbIO& bo, cudaStream_t st, Profiler* prof) {
   q.gT = bo.gT;
   const CUtensorMap mx = map_rows(bo.xbar, E, 128);
   const size_t smem = ((p.w1bytes + 1023) & ~1023u) + ((q.w2t_bytes + 1023) & ~1023u) +
-                      ((q.w1t_bytes + 1023) & ~1023u) + 32 * kBox + 12 * 32 * 4 + 32 * kNB * 4 + 256;
+                      ((q.w1t_bytes + 1023) & ~1023u) + 32 * kBox + 12 * 32 * 4 + 32 * kNB * 4 + 512;
   int dev = 0;
   ALG_CUDA(cudaGetDevice(&dev));
+  static const bool split2 = [] {  // A/B switch: each row's columns over two warps (default)
+    const char* e = std::getenv("ALLEGRO_TB_BWD_SPLIT");
+    return !e || std::atoi(e) != 0;
+  }();
   static bool attr[64] = {};
   static int nsm[64] = {};
   if (!attr[dev]) {
     ALG_CUDA(cudaFuncSetAttribute(k_tb_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ALG_CUDA(cudaFuncSetAttribute(k_tb_bwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
     attr[dev] = true;
   }
@@ -696,7 +1002,8 @@ void tb_bwd(const TbIO& io, const TbbIO& bo, cudaStream_t st, Profiler* prof) {
     const double flops = 2.0 * E * (32.0 * 64 + 128.0 * 64 + 64.0 * 32);
     const double bytes = (double)E * (8 + 2 * 24 + 512 + 4 + 4.0 * p.gp.dsh + 16);
     ProfScope ps_(prof, st, PK_TWOBODY_BWD, flops, bytes, "two-body bwd (fused)");
-    k_tb_bwd<<<grid, 32 * 8, smem, st>>>(mx, q);
+    if (split2) k_tb_bwd2<<<grid, 32 * kTb2Warps, smem, st>>>(mx, q);
+    else k_tb_bwd<<<grid, 32 * 8, smem, st>>>(mx, q);
   }
   ALG_LAUNCH_CHECK();
   if (std::getenv("ALLEGRO_SYNC_CHECK")) {
