@@ -77,6 +77,7 @@ struct TcParams {
   int n_tiles;         // CTAs blockIdx % n_tiles = N-tile of the same M-tiles (siblings share A via L2)
   int n_tiles_total;   // N-tiles of the whole contraction (row-dot partials when > 1)
   int tile_base;       // first N-tile of this launch
+  int N_img;           // N rows of this CTA's W image (= N_t, or N_t / 2 for a CTA pair)
   int N_t;             // tile width (multiple of 16)
   int nK;              // K-blocks of 32
   int nK1;             // K-blocks coming from A (rest from A2)
@@ -187,13 +188,15 @@ __device__ __forceinline__ void scatter_rows_dot(unsigned char* buf, float* dst,
 // MODE 0: 3xTF32 (a_hi w_lo, a_lo w_hi, a_hi w_hi); 1: stacked (a_hi [w_hi | w_lo] into the
 // adjacent accumulators [D | D'], then a_lo w_hi into D; the epilogue adds D + D'); 2: single-pass
 // TF32 (a_hi w_hi; ALLEGRO_PREC_TF32, reported, not gated: SURVEY.md App. C); 4: no MMAs.
-template <int MODE>
+template <int MODE, int PAIR>
 __device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uint32_t tmem_a, uint32_t wimg, int n_my,
                                            uint64_t* a_full, uint64_t* a_empty, uint64_t* acc_full,
                                            uint64_t* acc_empty) {
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.N_t >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
+  // PAIR: M = 256 over the CTA pair (each CTA's 128 rows), N = the full N_t (each CTA holds N_t / 2 of W)
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.N_t >> 3) << 17) |
+                         ((uint32_t)((PAIR ? 2 * ROWS : ROWS) >> 4) << 24);
   const uint32_t idesc2 = idesc + ((uint32_t)(p.N_t >> 3) << 17);  // width 2 N_t (stacked)
-  const uint32_t wblk = (uint32_t)p.N_t * 128;                      // bytes of one W half-block (hi or lo)
+  const uint32_t wblk = (uint32_t)p.N_img * 128;                    // bytes of one W half-block (hi or lo)
   const uint64_t desc0 = sdesc(wimg);
   const uint64_t dlo = (uint64_t)(wblk >> 4);                        // descriptor step hi -> lo
   __syncwarp();
@@ -203,12 +206,14 @@ __device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uin
   for (int t = 0; t < n_my; ++t) {
     const int a = t % p.n_acc;
     const uint32_t acph = (uint32_t)(t / p.n_acc) & 1u;
-    mbar_wait(acc_empty + a, acph ^ 1);
+    if (PAIR) mbar_wait_cluster(acc_empty + a, acph ^ 1);  // both CTAs' epilogues released it
+    else mbar_wait(acc_empty + a, acph ^ 1);
     __syncwarp();
     tc_fence_after();
     const uint32_t d = tmem + (uint32_t)(a * p.acc_cols);
     for (int kb = 0; kb < p.nK; ++kb) {
-      mbar_wait(a_full + j, aph);
+      if (PAIR) mbar_wait_cluster(a_full + j, aph);  // both CTAs' split warps filled stage j
+      else mbar_wait(a_full + j, aph);
       __syncwarp();
       tc_fence_after();
       const uint32_t ahi = tmem_a + (uint32_t)(j * A_TMEM_COLS), alo = ahi + 32;
@@ -218,7 +223,11 @@ __device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uin
         const uint64_t dwh = dkb + (uint64_t)(k * 2);  // +32 bytes = 8 tf32 of a W row
         const uint64_t dwl = dwh + dlo;
         const uint32_t acc = (kb | k) ? 1u : 0u;
-        if constexpr (MODE == 0) {
+        if constexpr (MODE == 0 && PAIR) {
+          mma2_tf32_ts_w(L, d, ahi + 8 * k, dwl, idesc, acc);
+          mma2_tf32_ts_w(L, d, alo + 8 * k, dwh, idesc, 1u);
+          mma2_tf32_ts_w(L, d, ahi + 8 * k, dwh, idesc, 1u);
+        } else if constexpr (MODE == 0) {
           mma_tf32_ts_w(L, d, ahi + 8 * k, dwl, idesc, acc);
           mma_tf32_ts_w(L, d, alo + 8 * k, dwh, idesc, 1u);
           mma_tf32_ts_w(L, d, ahi + 8 * k, dwh, idesc, 1u);
@@ -229,14 +238,19 @@ __device__ __forceinline__ void mma_issuer(const TcParams& p, uint32_t tmem, uin
           mma_tf32_ts_w(L, d, ahi + 8 * k, dwh, idesc, acc);  // single-pass TF32: a_hi w_hi only
         }
       }
-      mma_commit_w(L, a_empty + j);
-      if (kb == p.nK - 1) mma_commit_w(L, acc_full + a);
+      if constexpr (PAIR) {  // multicast: both CTAs' split warps / epilogues see the completion
+        mma2_commit_w(L, a_empty + j);
+        if (kb == p.nK - 1) mma2_commit_w(L, acc_full + a);
+      } else {
+        mma_commit_w(L, a_empty + j);
+        if (kb == p.nK - 1) mma_commit_w(L, acc_full + a);
+      }
       if (++j == p.a_stages) j = 0, aph ^= 1;
     }
   }
 }
 
-template <int EPI>
+template <int EPI, int PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapA2,
               const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapC,
@@ -258,7 +272,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* w_full = acc_empty + 4;
   uint64_t* x_full = w_full + 1;                      // [X_STAGES]
   uint64_t* x_empty = x_full + X_STAGES;              // [X_STAGES]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_empty + X_STAGES);
+  uint64_t* peer_w = x_empty + X_STAGES;              // PAIR: the peer CTA's W half has landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(peer_w + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -267,33 +282,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(raw_empty + s, 4);
     }
     for (int s = 0; s < p.a_stages; ++s) {
-      mbar_init(a_full + s, 4);
+      mbar_init(a_full + s, PAIR ? 8 : 4);
       mbar_init(a_empty + s, 1);
     }
     for (int a = 0; a < p.n_acc; ++a) {
       mbar_init(acc_full + a, 1);
-      mbar_init(acc_empty + a, 4);
+      mbar_init(acc_empty + a, PAIR ? 8 : 4);
     }
     mbar_init(w_full, 1);
+    mbar_init(peer_w, 1);
     for (int s2 = 0; s2 < X_STAGES; ++s2) {
       mbar_init(x_full + s2, 1);
       mbar_init(x_empty + s2, 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 9) tmem_alloc(tmem_slot, p.tmem_cols);
+  if (warp == 9) {
+    if (PAIR) tmem_alloc2(tmem_slot, p.tmem_cols);  // the same columns in both CTAs of the pair
+    else tmem_alloc(tmem_slot, p.tmem_cols);
+  }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // both CTAs' barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmem_a = tmem + (uint32_t)(p.n_acc * p.acc_cols);  // A ring after the accumulators
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
 
-  // sibling CTAs (one per N-tile) walk the same M-tiles in step, so A is read from HBM once
-  const int tile = p.tile_base + (int)blockIdx.x % p.n_tiles, grp = (int)blockIdx.x / p.n_tiles;
-  const int n_grp = (int)gridDim.x / p.n_tiles;
-  const int col0 = tile * p.N_t;
+  // sibling CTAs (one per N-tile) walk the same M-tiles in step, so A is read from HBM once; a CTA
+  // PAIR (cluster of 2) instead walks M-tile pairs: CTA r takes M-tile 2 u + r of pair-unit u and
+  // holds W's N-half r, the pair's M = 256 MMAs produce all N_t columns of both CTAs' rows
+  const int tile = PAIR ? (int)crank : p.tile_base + (int)blockIdx.x % p.n_tiles;
+  const int grp = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x / p.n_tiles;
+  const int n_grp = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x / p.n_tiles;
+  const int col0 = PAIR ? 0 : tile * p.N_t;
   const float* wimg_g = p.wimg + (size_t)tile * p.tile_floats;
-  const int n_my = p.n_mtiles > grp ? (p.n_mtiles - 1 - grp) / n_grp + 1 : 0;
+  const int n_units = PAIR ? (p.n_mtiles + 1) / 2 : p.n_mtiles;
+  const int n_my = n_units > grp ? (n_units - 1 - grp) / n_grp + 1 : 0;
+  auto mt = [&](int tt) -> int { return PAIR ? 2 * (grp + tt * n_grp) + (int)crank : grp + tt * n_grp; };
 
   if (warp == 8) {
     // ---------------- TMA producer ----------------
@@ -307,7 +333,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int t = 0; t < n_my; ++t) {
-        const int m0 = (grp + t * n_grp) * ROWS;
+        const int m0 = mt(t) * ROWS;
         for (int kb = 0; kb < p.nK; ++kb) {
           mbar_wait(raw_empty + s, ph ^ 1);
           unsigned char* dst = stage0 + (size_t)s * STAGE_BYTES;
@@ -324,7 +350,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int s2 = 0;
       uint32_t ph = 0;
       for (int t = 0; t < n_my; ++t) {
-        const int m0 = (grp + t * n_grp) * ROWS;
+        const int m0 = mt(t) * ROWS;
         for (int c0 = 0; c0 < p.N_t; c0 += 32) {
           mbar_wait(x_empty + s2, ph ^ 1);
           mbar_expect_tx(x_full + s2, X_STAGE_BYTES);
@@ -339,7 +365,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     int s = 0, j = 0;
     uint32_t ph = 0, aph = 0;
     auto row_scale_u = [&](int tt) -> float {  // arow_u of this thread's row of tile tt (loaded a tile ahead)
-      const int64_t rr = (int64_t)(grp + tt * n_grp) * ROWS + row;
+      const int64_t rr = (int64_t)mt(tt) * ROWS + row;
       return (p.g.arow_u != nullptr && tt < n_my && rr < p.g.M) ? __ldg(p.g.arow_u + rr) : 1.f;
     };
     float ru_next = row_scale_u(0);
@@ -382,18 +408,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(a_full + j);
+        if (lane == 0) {
+          if (PAIR) mbar_arrive_cluster(a_full + j, 0);  // the leader CTA's MMA warp waits for both
+          else mbar_arrive(a_full + j);
+        }
         if (++j == p.a_stages) j = 0, aph ^= 1;
       }
     }
   } else if (warp == 9) {
     // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
     mbar_wait(w_full, 0);
-    tc_fence_after();
-    if (p.diag & 1) mma_issuer<4>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
-    else if (p.g.single_pass) mma_issuer<2>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
-    else if (p.stack) mma_issuer<1>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
-    else mma_issuer<0>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
+    if constexpr (PAIR) {
+      if (crank != 0) {  // the peer CTA issues nothing: it reports its W half to the leader
+        if (lane == 0) mbar_arrive_cluster(peer_w, 0);
+      } else {
+        mbar_wait_cluster(peer_w, 0);
+        tc_fence_after();
+        mma_issuer<0, 1>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
+      }
+    } else {
+      tc_fence_after();
+      if (p.diag & 1) mma_issuer<4, 0>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
+      else if (p.g.single_pass) mma_issuer<2, 0>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
+      else if (p.stack) mma_issuer<1, 0>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
+      else mma_issuer<0, 0>(p, tmem, tmem_a, smem_u32(w_img), n_my, a_full, a_empty, acc_full, acc_empty);
+    }
   } else {
     // ---------------- epilogue warpgroup (warps 4..7) ----------------
     const int q = warp & 3;  // TMEM lane quarter
@@ -408,11 +447,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // per-row scalars (u, and rs2 for EPI_R2) are loaded one tile ahead: a load issued at the
     // tile start would stall the epilogue warps for a full DRAM round trip every tile
     auto row_u = [&](int tt) -> float {
-      const int64_t rr = (int64_t)(grp + tt * n_grp) * ROWS + q * 32 + lane;
+      const int64_t rr = (int64_t)mt(tt) * ROWS + q * 32 + lane;
       return (tt < n_my && rr < g.M && g.u != nullptr) ? __ldg(g.u + rr) : 1.f;
     };
     auto row_rs2 = [&](int tt) -> float {
-      const int64_t rr = (int64_t)(grp + tt * n_grp) * ROWS + q * 32 + lane;
+      const int64_t rr = (int64_t)mt(tt) * ROWS + q * 32 + lane;
       return (EPI == EPI_R2 && tt < n_my && rr < g.M) ? __ldg(g.rs2 + rr) : 0.f;
     };
     float u_next = row_u(0), rs2_next = row_rs2(0);
@@ -425,7 +464,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       rs2_next = row_rs2(t + 1);
       mbar_wait(acc_full + a, acph);
       tc_fence_after();
-      const int64_t row0 = (int64_t)(grp + t * n_grp) * ROWS + q * 32;
+      const int64_t row0 = (int64_t)mt(t) * ROWS + q * 32;
       const int64_t r = row0 + lane;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * p.acc_cols);
       float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // row-dot partials, rows (lane>>3)+4i
@@ -442,7 +481,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
           // warm L2 with the next chunk's [32 x 32] block (one 128-B line per lane, no registers held)
           const int tn = c0 + 32 < p.N_t ? t : t + 1, cn = c0 + 32 < p.N_t ? c0 + 32 : 0;
-          const int64_t rn = (int64_t)(grp + tn * n_grp) * ROWS + q * 32 + lane;
+          const int64_t rn = (int64_t)mt(tn) * ROWS + q * 32 + lane;
           if (tn < n_my && rn < g.M)
             asm volatile("prefetch.global.L2 [%0];" ::"l"(g.dotv + rn * g.N + col0 + cn));
         }
@@ -573,14 +612,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty + a);
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_cluster(acc_empty + a, 0);  // the leader reuses it once both CTAs read it
+        else mbar_arrive(acc_empty + a);
+      }
     }
     if (p.tma_store && lane == 0) bulk_wait0();  // the output is complete before the CTA retires
   }
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // the leader's last MMAs wrote into this CTA's TMEM
   if (warp == 9) {
     tc_fence_after();
-    tmem_dealloc(tmem, p.tmem_cols);
+    if (PAIR) tmem_dealloc2(tmem, p.tmem_cols);
+    else tmem_dealloc(tmem, p.tmem_cols);
   }
 }
 
@@ -732,17 +776,29 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   {
     std::lock_guard<std::mutex> lk(g_dev_mu);
     if (!g_attr_set[dev]) {  // the function attribute is per device
-#define ALG_SET(e) ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<e>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
+#define ALG_SET(e) ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<e, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
       ALG_SET(EPI_STORE) ALG_SET(EPI_SILU) ALG_SET(EPI_UMUL_SAVE) ALG_SET(EPI_RESID) ALG_SET(EPI_URESID)
       ALG_SET(EPI_USCALE) ALG_SET(EPI_ACC) ALG_SET(EPI_ADDX) ALG_SET(EPI_DSILU) ALG_SET(EPI_R2) ALG_SET(EPI_ACCX)
 #undef ALG_SET
+      ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<EPI_RESID, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
+      ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<EPI_ACCX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
       ALG_CUDA(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev));
       g_attr_set[dev] = true;
     }
   }
+  // CTA pair (cta_group::2) for a contraction split into two N-tiles: each CTA of a cluster pair
+  // holds one N-half of W and splits only its own A rows (instead of two sibling CTAs splitting the
+  // same rows); A/B switch ALLEGRO_TC_PAIR
+  static const bool pair_on = [] {  // off by default: measured slower
+    const char* e = std::getenv("ALLEGRO_TC_PAIR");
+    return e && std::atoi(e) != 0;
+  }();
+  const bool pair = pair_on && w.n_tiles == 2 && (g.epi == EPI_RESID || g.epi == EPI_ACCX) && !g.single_pass &&
+                    g_tc_tuning.diag == 0 && (w.N_t * 2) % 32 == 0;
   TcParams p;
   p.g = g;
-  p.N_t = w.N_t;
+  p.N_t = pair ? 2 * w.N_t : w.N_t;
+  p.N_img = w.N_t;
   p.nK = nK;
   p.nK1 = g.A2 ? g.K1 / BLK_K : nK;
   p.stages = stages;
@@ -751,11 +807,18 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   // stacked hi/lo MMAs where the tensor pipe paces the kernel (A/B on one B200,
   // profiles/r01_gemm_stack_ab.jsonl): N_t = 32 always, N_t = 64 from K = 64 (at K = 32 the
   // doubled accumulator read makes the epilogue the bottleneck)
-  p.stack = (g_tc_tuning.stack && (w.N_t == 32 || (w.N_t == 64 && g.K >= 64))) ? 1 : 0;
-  p.acc_cols = (p.stack ? 2 : 1) * ((w.N_t + 31) / 32 * 32);
+  p.stack = (!pair && g_tc_tuning.stack && (w.N_t == 32 || (w.N_t == 64 && g.K >= 64))) ? 1 : 0;
+  p.acc_cols = (p.stack ? 2 : 1) * ((p.N_t + 31) / 32 * 32);
   // TMEM: two accumulators + the A ring (64 columns per stage), power of two <= 512
   // a deeper accumulator ring for narrow tiles lets the MMAs run further ahead of the epilogue
   p.n_acc = std::max(2, std::min(g_tc_tuning.max_acc, (512 - 4 * A_TMEM_COLS) / p.acc_cols));
+  if (pair) {  // A/B: a deeper accumulator ring at the cost of A stages (ALLEGRO_TC_PAIR_ACC = 3)
+    static const int pacc = [] {
+      const char* e = std::getenv("ALLEGRO_TC_PAIR_ACC");
+      return e ? std::atoi(e) : 2;
+    }();
+    p.n_acc = std::max(2, std::min(pacc, (512 - 2 * A_TMEM_COLS) / p.acc_cols));
+  }
   int a_st = std::min(4, (512 - p.n_acc * p.acc_cols) / A_TMEM_COLS);
   if (a_st < 2) throw CudaError("tc_gemm: TMEM too small");
   p.a_stages = a_st;
@@ -771,33 +834,52 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   p.store_hint = g_tc_tuning.store_hint;
   const CUtensorMap mC = p.tma_store ? make_map(g.C, g.M, g.N, g.N, 32) : mA;
   const CUtensorMap mAux = (p.tma_store && aux_epi) ? make_map(g.aux, g.M, g.N, g.N, 32) : mA;
-  if (g.dotv && w.n_tiles != 1 && !g.dot_part) throw CudaError("tc_gemm: a row-dot over N-tiles needs dot_part");
+  if (g.dotv && w.n_tiles != 1 && !pair && !g.dot_part)
+    throw CudaError("tc_gemm: a row-dot over N-tiles needs dot_part");
   // one launch; CTA b handles N-tile b % n_tiles of M-tile group b / n_tiles
   // (ALLEGRO_TC_COSCHED=0: one launch per N-tile, for A/B measurements)
   static const bool cosched = [] {
     const char* e = std::getenv("ALLEGRO_TC_COSCHED");
     return !e || std::atoi(e) != 0;
   }();
-  const int per_launch = cosched ? w.n_tiles : 1;
-  const int groups = std::max(1, std::min(p.n_mtiles, g_num_sms[dev] / per_launch));
-  const int grid = groups * per_launch;
+  const int per_launch = pair ? w.n_tiles : (cosched ? w.n_tiles : 1);
+  const int groups = pair ? std::max(1, std::min((p.n_mtiles + 1) / 2, g_num_sms[dev] / 2))
+                          : std::max(1, std::min(p.n_mtiles, g_num_sms[dev] / per_launch));
+  const int grid = groups * (pair ? 2 : per_launch);
   const double mn = (double)g.M * g.N;
   const int n_io = 1 + (g.aux != nullptr) + (g.X != nullptr) + (g.epi == EPI_ACC);
-  p.n_tiles = per_launch;
-  p.n_tiles_total = w.n_tiles;
+  p.n_tiles = pair ? 1 : per_launch;
+  p.n_tiles_total = pair ? 1 : w.n_tiles;  // a pair's row-dot covers all N columns: no partials
   p.wimg = w.dev;
   p.tile_floats = w.tile_bytes / 4;
   for (int tb = 0; tb < w.n_tiles; tb += per_launch) {
     p.tile_base = tb;
     char tag[96];
-    std::snprintf(tag, sizeof(tag), "tc N=%d K=%d epi=%d A2=%d Nt=%d", g.N, g.K, g.epi, g.A2 ? 1 : 0, w.N_t);
+    std::snprintf(tag, sizeof(tag), "tc N=%d K=%d epi=%d A2=%d Nt=%d%s", g.N, g.K, g.epi, g.A2 ? 1 : 0, w.N_t,
+                  pair ? " pair" : "");
     const double frac = (double)per_launch / w.n_tiles;
     ProfScope ps(prof, st, PK_GEMM, frac * (2.0 * mn * g.K + (g.dotv ? 2.0 * mn : 0.0)),
                  frac * 4.0 * ((double)g.M * g.K + (double)g.K * g.N + mn * (n_io + (g.dotv ? 1 : 0)) + (g.dotv ? 2.0 * g.M : 0.0)),
                  tag);
+    if (pair) {  // cluster launch: two CTAs per cluster on one TPC
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)grid);
+      cfg.blockDim = dim3(TC_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (g.epi == EPI_RESID) ALG_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<EPI_RESID, 1>, mA, mA2, mX, mC, mAux, p));
+      else ALG_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<EPI_ACCX, 1>, mA, mA2, mX, mC, mAux, p));
+      ALG_LAUNCH_CHECK();
+      break;
+    }
     switch (g.epi) {
 #define ALG_EPI(e) \
-  case e: k_tc_gemm<e><<<grid, TC_THREADS, smem, st>>>(mA, mA2, mX, mC, mAux, p); break;
+  case e: k_tc_gemm<e, 0><<<grid, TC_THREADS, smem, st>>>(mA, mA2, mX, mC, mAux, p); break;
       ALG_EPI(EPI_STORE) ALG_EPI(EPI_SILU) ALG_EPI(EPI_UMUL_SAVE) ALG_EPI(EPI_RESID) ALG_EPI(EPI_URESID)
       ALG_EPI(EPI_USCALE) ALG_EPI(EPI_ACC) ALG_EPI(EPI_ADDX) ALG_EPI(EPI_DSILU) ALG_EPI(EPI_R2) ALG_EPI(EPI_ACCX)
 #undef ALG_EPI
@@ -805,7 +887,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
     }
     ALG_LAUNCH_CHECK();
   }
-  if (g.dotv && w.n_tiles > 1) {  // dot_out[r] += coef (partial_0 + partial_1 + ...), fixed order
+  if (g.dotv && w.n_tiles > 1 && !pair) {  // dot_out[r] += coef (partial_0 + partial_1 + ...), fixed order
     ProfScope ps(prof, st, PK_ROWDOT, (double)g.M * w.n_tiles, 4.0 * (double)g.M * (w.n_tiles + 2));
     k_dot_parts<<<ceil_div(g.M, 256), 256, 0, st>>>(g.M, w.n_tiles, g.dot_part, g.dot_coef, g.dot_out);
     ALG_LAUNCH_CHECK();

@@ -48,7 +48,16 @@ constexpr int kProdWarp = kTpWarps + 4;
 constexpr int kMmaWarp = kTpWarps + 5;
 constexpr int kThreads = 32 * (kTpWarps + 6);  // 22 warps
 constexpr int kATm = 64;            // TMEM columns of one A stage (hi 32 | lo 32)
-constexpr int kAStages = 4;         // TMEM A ring depth
+// TMEM of k_tpl_fwd: kAccBufs accumulator sets (NO x 32 columns each) + the A ring (64 columns per
+// stage); build-time A/B (ALG_TPF_ACCBUFS / ALG_TPF_ASTAGES)
+#ifndef ALG_TPF_ACCBUFS
+#define ALG_TPF_ACCBUFS 2
+#endif
+#ifndef ALG_TPF_ASTAGES
+#define ALG_TPF_ASTAGES 4
+#endif
+constexpr int kAccBufs = ALG_TPF_ACCBUFS;
+constexpr int kAStages = ALG_TPF_ASTAGES;  // TMEM A ring depth
 constexpr int kBoxBytes = 32 * 128; // one [32 x 32 fp32] TMA box
 constexpr size_t kSmemLimit = 227 * 1024;
 
@@ -163,12 +172,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* w_full = acc_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
+  static_assert(kAccBufs >= 1 && kAccBufs <= 2 && kAccBufs * F::acc_cols() + kAStages * kATm <= 512, "TMEM budget");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) mbar_init(in_full + s, 1), mbar_init(in_empty + s, kTpWarps);
     for (int s = 0; s < kAStages; ++s) mbar_init(a_full + s, kTpWarps), mbar_init(a_empty + s, 1);
-    for (int b = 0; b < 2; ++b) mbar_init(acc_full + b, 1), mbar_init(acc_empty + b, 4);
+    for (int b = 0; b < kAccBufs; ++b) mbar_init(acc_full + b, 1), mbar_init(acc_empty + b, 4);
     mbar_init(w_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -177,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_a = tmem + 2u * F::acc_cols();  // A ring after the two accumulator sets
+  const uint32_t tmem_a = tmem + (uint32_t)(kAccBufs * F::acc_cols());  // A ring after the accumulator sets
   const int n_my = p.n_tiles > (int)blockIdx.x ? (p.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
   if (warp == kProdWarp) {
@@ -350,8 +360,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
     int j = 0;
     uint32_t aph = 0;
     for (int t = 0; t < n_my; ++t) {
-      const int buf = t & 1;
-      mbar_wait(acc_empty + buf, ((uint32_t)(t >> 1) & 1u) ^ 1u);
+      const int buf = t % kAccBufs;
+      mbar_wait(acc_empty + buf, ((uint32_t)(t / kAccBufs) & 1u) ^ 1u);
       __syncwarp();
       tc_fence_after();
       static_for<NO>([&](auto O) {
@@ -385,8 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
     int n_st = 0;
     for (int t = 0; t < n_my; ++t) {
       const int64_t e0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kTile;
-      const int buf = t & 1;
-      mbar_wait(acc_full + buf, (uint32_t)(t >> 1) & 1u);
+      const int buf = t % kAccBufs;
+      mbar_wait(acc_full + buf, (uint32_t)(t / kAccBufs) & 1u);
       tc_fence_after();
       static_for<NO>([&](auto O) {
         constexpr int o = decltype(O)::value;
