@@ -93,6 +93,7 @@ struct TcParams {
   int has_x;           // the epilogue reads an [M][N] input (X, or old C) through the TMA ring
   int tma_store;       // the output C (and aux) leave by TMA stores of [32 x 32] boxes (no row-dot)
   int store_hint;      // TMA stores carry an L2 evict_first policy
+  int out_slots;       // output staging slots per epilogue warp (2, or 4: two C + aux groups in flight)
 };
 
 // v <- s v (the saved pre-activation "aux"); out <- epilogue(v, xin) (xin = X, or old C for EPI_ACC)
@@ -260,8 +261,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   unsigned char* base = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
   unsigned char* w_img = base;  // per K-block: [w_hi rows][w_lo rows]
   unsigned char* stage0 = base + ((p.w_bytes + 1023) & ~1023u);
-  unsigned char* out_stage = stage0 + (size_t)p.stages * STAGE_BYTES;  // [4 warps][2][4 KB]
-  unsigned char* x_stage = out_stage + 8 * STAGE_OUT_BYTES;            // [X_STAGES][16 KB] (if has_x)
+  unsigned char* out_stage = stage0 + (size_t)p.stages * STAGE_BYTES;  // [4 warps][out_slots][4 KB]
+  unsigned char* x_stage = out_stage + 4 * p.out_slots * STAGE_OUT_BYTES;  // [X_STAGES][16 KB] (if has_x)
   uint64_t* bars = reinterpret_cast<uint64_t*>(x_stage + (p.has_x ? X_STAGES * X_STAGE_BYTES : 0));
   uint64_t* raw_full = bars;                          // [stages]  TMA landed
   uint64_t* raw_empty = raw_full + p.stages;          // [stages]  split warps read it
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr bool kX = EPI == EPI_RESID || EPI == EPI_URESID || EPI == EPI_ADDX || EPI == EPI_DSILU || EPI == EPI_ACCX;
     constexpr bool kAuxEpi = EPI == EPI_SILU || EPI == EPI_UMUL_SAVE || EPI == EPI_RESID;
     const bool want_aux = kAuxEpi && g.aux != nullptr;
-    unsigned char* buf = out_stage + (size_t)(2 * q) * STAGE_OUT_BYTES;  // [8][4 KB]: two slots per warp
+    unsigned char* buf = out_stage + (size_t)(p.out_slots * q) * STAGE_OUT_BYTES;  // this warp's slots
     constexpr bool kIn = kX || EPI == EPI_ACC;  // epilogue reads a [M][N] input (X or old C)
     int xs = 0;
     uint32_t xph = 0;
@@ -539,10 +540,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           scatter_rows_dot(buf, g.C + col, g.N, row0, g.M, lane, out, nc, dq, acc8);
         } else if (p.tma_store) {  // [32 rows x 32 cols] boxes through this warp's two SMEM slots
           if (want_aux) {  // C and aux in one group; wait until the previous group has read both slots
-            unsigned char* tc = out_stage + (size_t)(2 * q) * STAGE_OUT_BYTES;
+            // with 4 slots two (C, aux) groups alternate: the group of two stores ago must be read
+            const int grp2 = p.out_slots == 4 ? (n_st & 1) : 0;
+            unsigned char* tc = out_stage + (size_t)(p.out_slots * q + 2 * grp2) * STAGE_OUT_BYTES;
             unsigned char* ta = tc + STAGE_OUT_BYTES;
-            if (n_st >= 1) {
-              if (lane == 0) bulk_wait_read0();
+            if (n_st >= (p.out_slots == 4 ? 2 : 1)) {
+              if (lane == 0) {
+                if (p.out_slots == 4) bulk_wait_read1();
+                else bulk_wait_read0();
+              }
               __syncwarp();
             }
 #pragma unroll
@@ -564,7 +570,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               bulk_commit();
             }
           } else {  // double-buffered: the slot of chunk n_st - 2 must have been read
-            unsigned char* tb = out_stage + (size_t)(2 * q + (n_st & 1)) * STAGE_OUT_BYTES;
+            unsigned char* tb = out_stage + (size_t)(p.out_slots * q + (n_st & 1)) * STAGE_OUT_BYTES;
             if (n_st >= 2) {
               if (lane == 0) bulk_wait_read1();
               __syncwarp();
@@ -768,7 +774,14 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const size_t w_round = (w_bytes + 1023) & ~(size_t)1023;
   const bool has_x = g.epi == EPI_RESID || g.epi == EPI_URESID || g.epi == EPI_ADDX || g.epi == EPI_DSILU ||
                      g.epi == EPI_ACC || g.epi == EPI_ACCX;
-  const size_t out_bytes = 8 * (size_t)STAGE_OUT_BYTES + (has_x ? (size_t)X_STAGES * X_STAGE_BYTES : 0);
+  const bool aux_epi0 = g.aux && (g.epi == EPI_SILU || g.epi == EPI_UMUL_SAVE || g.epi == EPI_RESID);
+  // A/B (ALLEGRO_TC_OUTSLOTS=4): two (C, aux) store groups in flight per epilogue warp
+  static const int outslots_env = [] {
+    const char* e = std::getenv("ALLEGRO_TC_OUTSLOTS");
+    return e ? std::atoi(e) : 2;
+  }();
+  const int out_slots = (aux_epi0 && outslots_env == 4) ? 4 : 2;
+  const size_t out_bytes = 4 * (size_t)out_slots * STAGE_OUT_BYTES + (has_x ? (size_t)X_STAGES * X_STAGE_BYTES : 0);
   int stages = (int)((SMEM_LIMIT - SMEM_RESERVE - w_round - out_bytes) / STAGE_BYTES);
   stages = std::min(stages, g_tc_tuning.max_stages);
   if (stages < 2) throw CudaError("tc_gemm: shared memory too small for 2 stages");
@@ -832,6 +845,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const bool aux_epi = g.aux && (g.epi == EPI_SILU || g.epi == EPI_UMUL_SAVE || g.epi == EPI_RESID);
   p.tma_store = (g_tc_tuning.tma_store && w.N_t % 32 == 0 && (p.diag & 2) == 0) ? 1 : 0;
   p.store_hint = g_tc_tuning.store_hint;
+  p.out_slots = out_slots;
   const CUtensorMap mC = p.tma_store ? make_map(g.C, g.M, g.N, g.N, 32) : mA;
   const CUtensorMap mAux = (p.tma_store && aux_epi) ? make_map(g.aux, g.M, g.N, g.N, 32) : mA;
   if (g.dotv && w.n_tiles != 1 && !pair && !g.dot_part)
