@@ -128,7 +128,8 @@ struct Domain {
   DBuf<long long> acc;          // [n + G][3] fixed-point ghost-force accumulators
   DBuf<long long> cnt;          // scratch counts
   DBuf<long long> hs;           // halo message-path state (domain.cu: n_cur, overflow, per-stage counts)
-  double cap_scale = 1.0;       // halo message capacity scale (doubled on overflow, on every rank)
+  double cap_scale = 1.0;       // halo message capacity scale (doubled on overflow, on every rank;
+                                // ALLEGRO_HALO_CAP_SCALE sets the start, a test hook)
   DBuf<long long> ms;           // migration message-path state (owned count, stayers, overflow)
   DBuf<unsigned char> mstage;   // migration stayers staging (MigAtom)
   DBuf<double> red;             // allreduce scratch

@@ -16,6 +16,8 @@
 // A face neighbour that is this rank (p_alpha = 1) is served by a device copy.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -477,6 +479,7 @@ void domain_setup(allegro_ctx* c, const void* nccl_id) {
   Domain& D = c->dom;
   const allegro_params& p = c->prm;
   D.multi = p.world_size > 1;
+  if (const char* e = std::getenv("ALLEGRO_HALO_CAP_SCALE")) D.cap_scale = std::atof(e);  // test hook
   D.rank = p.rank;
   D.size = p.world_size;
   int P[3] = {p.grid[0], p.grid[1], p.grid[2]};
@@ -690,7 +693,11 @@ void migrate(allegro_ctx* c) {
   cudaStream_t st = c->stream;
   const int64_t n0 = c->n;
   // leavers per face per step: a few atoms; the capacity (identical on every rank) is generous
-  const int64_t cap = 256 + c->n_global / (16 * std::max(D.size, 1));
+  static const int64_t cap_env = [] {  // test hook (the fallback path): ALLEGRO_MIG_CAP overrides
+    const char* e = std::getenv("ALLEGRO_MIG_CAP");
+    return e ? (int64_t)std::atoll(e) : (int64_t)-1;
+  }();
+  const int64_t cap = cap_env >= 0 ? cap_env : 256 + c->n_global / (16 * std::max(D.size, 1));
   const size_t mbytes = kMsgHdr + (size_t)cap * sizeof(MigAtom);
   {  // room for the owned set to grow by two messages per axis (content kept; grows once)
     const int64_t want = n0 + 6 * cap + 64;
@@ -731,7 +738,11 @@ void migrate(allegro_ctx* c) {
   ALG_CUDA(cudaMemcpyAsync(h, D.ms.p, sizeof(h), cudaMemcpyDeviceToHost, st));
   ALG_CUDA(cudaStreamSynchronize(st));  // the one host read of the migration
   c->n = h[0];
-  if (h[2] != 0) migrate_counted(c);  // a message overflowed somewhere (then every rank is here)
+  if (h[2] != 0) {  // a message overflowed somewhere (then every rank is here)
+    if (std::getenv("ALLEGRO_DOMAIN_LOG"))
+      std::fprintf(stderr, "[rank %d] migration message overflow: exact-count path\n", D.rank);
+    migrate_counted(c);
+  }
 }
 
 // The exact-count path (large domains): per stage one count exchange and one host read.
@@ -825,7 +836,12 @@ int64_t halo_cap(const allegro_ctx* c, int s, double rcp) {
   double area = 1.0;
   for (int d = 0; d < 3; ++d)
     if (d != s) area *= D.w[d] + (d < s ? 2.0 * rcp : 0.0);
-  return (int64_t)std::ceil(2.0 * rho * area * rcp * D.cap_scale) + 512;
+  // test hooks (the overflow / retry path): ALLEGRO_HALO_CAP_MIN replaces the 512 floor
+  static const int64_t floor_ = [] {
+    const char* e = std::getenv("ALLEGRO_HALO_CAP_MIN");
+    return e ? (int64_t)std::atoll(e) : (int64_t)512;
+  }();
+  return (int64_t)std::ceil(2.0 * rho * area * rcp * D.cap_scale) + floor_;
 }
 
 void halo_exchange(allegro_ctx* c) {
@@ -883,6 +899,9 @@ void halo_exchange(allegro_ctx* c) {
     ALG_CUDA(cudaMemcpyAsync(h, D.hs.p, sizeof(h), cudaMemcpyDeviceToHost, st));
     ALG_CUDA(cudaStreamSynchronize(st));
     if (h[1] != 0) {  // a message exceeded its capacity somewhere: widen on every rank and repeat
+      if (std::getenv("ALLEGRO_DOMAIN_LOG"))
+        std::fprintf(stderr, "[rank %d] halo message overflow: capacity scale %g -> %g\n", D.rank, D.cap_scale,
+                     2.0 * D.cap_scale);
       D.cap_scale *= 2.0;
       if (attempt > 8) throw CudaError("halo exchange: message capacity did not converge");
       continue;

@@ -12,17 +12,21 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("cfg,port", [("C2", 29533), ("CP", 29534)])
-def test_two_gpu_decomposition_equals_one_gpu(cfg, port):
+@pytest.mark.parametrize("cfg,port,env", [("C2", 29533, {}), ("CP", 29534, {}),
+                                          ("CP", 29535, {"ALLEGRO_HALO_CAP_SCALE": "0.01", "ALLEGRO_HALO_CAP_MIN": "8",
+                                                         "ALLEGRO_MIG_CAP": "0"})])
+def test_two_gpu_decomposition_equals_one_gpu(cfg, port, env):
     """C2 (the 2-layer l=2 model, unfused TP path) and CP (the paper's 3-layer l=1 model at 6,912
-    atoms, the fused TP + TP-linear kernels)."""
+    atoms, the fused TP + TP-linear kernels); the third case starts the fixed-capacity halo
+    messages far too small (every exchange overflows, every rank doubles and repeats) and gives the
+    migration messages no room (any leaver sends every rank to the exact-count fallback)."""
     import torch
 
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "scripts", "check_multigpu.py"), cfg]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env={**os.environ, **env})
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-2000:]
     res = json.loads(lines[-1])
