@@ -111,7 +111,10 @@ __global__ void __launch_bounds__(NT) k_gemm(GemmArgs g) {
       switch (g.epi) {
         case EPI_STORE: g.C[o] = p; break;
         case EPI_SILU: g.aux[o] = p; g.C[o] = silu(p); break;
-        case EPI_UMUL_SAVE: g.aux[o] = p; g.C[o] = ur * p; break;
+        case EPI_UMUL_SAVE:
+          if (g.aux) g.aux[o] = p;  // (the model passes none: x^0 = u m keeps m recoverable)
+          g.C[o] = ur * p;
+          break;
         case EPI_RESID: g.aux[o] = p; g.C[o] = g.alpha * g.X[o] + g.beta * ur * p; break;
         case EPI_URESID: g.C[o] = g.alpha * g.X[o] + g.beta * ur * p; break;
         case EPI_USCALE: g.C[o] = g.beta * ur * p; break;

@@ -43,6 +43,7 @@ struct GemmArgs {
   const float* dotv = nullptr;  // [M][N]
   float* dot_out = nullptr;     // [M]
   float dot_coef = 0.f;
+  const float* dot_inv_u = nullptr;  // [M] if set: the row-dot of row r is divided by u[r] (0 where u = 0)
   float s = 1.f, alpha = 0.f, beta = 0.f;
   int epi = EPI_STORE;
   int silu_a = 0;  // A holds pre-activations: the contraction multiplies SiLU(A) (applied on load)

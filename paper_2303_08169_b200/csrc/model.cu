@@ -791,13 +791,17 @@ __global__ void k_energy_last(ChunkPtrs ch, const int32_t* __restrict__ row_ptr,
 
 // ubar[e] += coef <P[e], Q[e]> over 128 (warp per edge)
 __global__ void k_rowdot(int64_t E, const float* __restrict__ P, const float* __restrict__ Q, float coef,
-                         float* __restrict__ ubar) {
+                         const float* __restrict__ inv_u, float* __restrict__ ubar) {
   const int lane = threadIdx.x & 31;
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (e >= E) return;
   const float4 p = reinterpret_cast<const float4*>(P + e * kD)[lane];
   const float4 q = reinterpret_cast<const float4*>(Q + e * kD)[lane];
-  const float s = warp_sum(p.x * q.x + p.y * q.y + p.z * q.z + p.w * q.w);
+  float s = warp_sum(p.x * q.x + p.y * q.y + p.z * q.z + p.w * q.w);
+  if (inv_u) {  // x^0 = u m: <x-bar^0, m> = <x-bar^0, x^0> / u (u = 0: u' = 0 there, the term drops)
+    const float ur = inv_u[e];
+    s = ur != 0.f ? s / ur : 0.f;
+  }
   if (lane == 0) ubar[e] += coef * s;
 }
 
@@ -1071,7 +1075,7 @@ void run_gemm(const Model& M, const GemmArgs& g_in, const Wt& w, cudaStream_t st
     if (g.N != kD) throw CudaError("row-dot over N != 128");
     {
       ProfScope ps_(prof, st, PK_ROWDOT, 2.0 * 128 * g.M, (double)g.M * 1024);
-      k_rowdot<<<ceil_div(g.M * 32, 256), 256, 0, st>>>(g.M, g.dotv, g.C, g.dot_coef, g.dot_out);
+      k_rowdot<<<ceil_div(g.M * 32, 256), 256, 0, st>>>(g.M, g.dotv, g.C, g.dot_coef, g.dot_inv_u, g.dot_out);
     }
     ALG_LAUNCH_CHECK();
   }
@@ -1193,10 +1197,10 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     io.w2 = &M.w.tb_w2;
     io.u = w.u.p;
     io.Y = w.Y.p;
-    io.x0 = w.xa.p;
+    io.x0 = w.m.p;  // x^0 = u m in its own buffer (kept for the reverse's row-dot; m is not stored)
     io.a1 = fused_2b_bwd ? nullptr : w.a1.p;  // the fused reverse recomputes a1, a2
     io.a2 = fused_2b_bwd ? nullptr : w.a2.p;
-    io.m = w.m.p;
+    io.m = nullptr;
   }
   if (fused_2b) {
     tb_fwd(tbio, st, &c->prof);
@@ -1207,14 +1211,14 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     GemmArgs g = G(w.a1.p, 32, M.w.tb_w1, 64, 32, w.a2.p, kCSilu / std::sqrt(32.f), EPI_STORE);
     g.silu_a = 1;
     run_gemm(M, g, *last_w, st, &c->prof);
-    g = G(w.a2.p, 64, M.w.tb_w2, 128, 64, w.xa.p, kCSilu / std::sqrt(64.f), EPI_UMUL_SAVE);
+    g = G(w.a2.p, 64, M.w.tb_w2, 128, 64, w.m.p, kCSilu / std::sqrt(64.f), EPI_UMUL_SAVE);
     g.silu_a = 1;
-    g.aux = w.m.p;
+    g.aux = nullptr;
     g.u = w.u.p;
     run_gemm(M, g, *last_w, st, &c->prof);
   }
-  float* x = w.xa.p;
-  float* xn = w.xb.p;
+  float* x = w.m.p;  // x^0 (never overwritten: the latent updates alternate between xa and xb)
+  float* xn = w.xa.p;
   TpArgs tp{};
   tp.ch = ch;
   tp.row_ptr = c->row_ptr.p;
@@ -1280,7 +1284,9 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
     g.alpha = kResA;
     g.beta = kResB;
     run_gemm(M, g, *last_w, st, &c->prof);
-    std::swap(x, xn);
+    float* done = x;
+    x = xn;
+    xn = done == w.m.p ? w.xb.p : done;
   }
   // ---- energies (E7, E8) and the rank-one reverse mode of the last layer ----
   float* xb = w.xbar_a.p;
@@ -1403,7 +1409,8 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
       g.arow_c2 = 1.f / std::sqrt(128.f);
       g.X = xb;
       g.alpha = kResA;
-      g.dotv = k >= 1 ? w.h[k - 1].p : w.m.p;
+      g.dotv = k >= 1 ? w.h[k - 1].p : w.m.p;  // k = 0: x^0, divided by u per row
+      g.dot_inv_u = k >= 1 ? nullptr : w.u.p;
       g.dot_coef = k >= 1 ? kResB : 1.f;
       g.dot_out = w.ubar.p;
       g.dot_part = w.dotp.p;
@@ -1418,7 +1425,8 @@ void run_chunk(allegro_ctx* c, const ChunkPtrs& ch) {
       }
       // xbar^k is complete here: fuse the u-gradient of the update that produced x^k,
       // ubar += (1/sqrt5) <xbar^k, h^{k-1}> (latent resnet) or <xbar^0, m> (two-body x^0 = u m)
-      g.dotv = k >= 1 ? w.h[k - 1].p : w.m.p;
+      g.dotv = k >= 1 ? w.h[k - 1].p : w.m.p;  // k = 0: x^0, divided by u per row
+      g.dot_inv_u = k >= 1 ? nullptr : w.u.p;
       g.dot_coef = k >= 1 ? kResB : 1.f;
       g.dot_out = w.ubar.p;
       run_gemm(M, g, *last_w, st, &c->prof);

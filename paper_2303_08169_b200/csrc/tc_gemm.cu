@@ -613,7 +613,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int64_t rr = row0 + (lane >> 3) + 4 * (lane & 7);
         if (rr < g.M) {
           if (p.n_tiles_total > 1) g.dot_part[rr * p.n_tiles_total + tile] = mine;  // summed by k_dot_parts
-          else g.dot_out[rr] += g.dot_coef * mine;
+          else {
+            if (g.dot_inv_u) {  // x^0 = u m: <x-bar^0, m> from <x-bar^0, x^0> (u = 0: u' = 0 there too)
+              const float ur = g.dot_inv_u[rr];
+              mine = ur != 0.f ? mine / ur : 0.f;
+            }
+            g.dot_out[rr] += g.dot_coef * mine;
+          }
         }
       }
       tc_fence_before();
@@ -634,11 +640,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-__global__ void k_dot_parts(int64_t M, int nt, const float* __restrict__ part, float coef, float* __restrict__ out) {
+__global__ void k_dot_parts(int64_t M, int nt, const float* __restrict__ part, float coef, const float* __restrict__ inv_u,
+                            float* __restrict__ out) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= M) return;
   float sdot = part[r * nt];
   for (int t = 1; t < nt; ++t) sdot += part[r * nt + t];
+  if (inv_u) {
+    const float ur = inv_u[r];
+    sdot = ur != 0.f ? sdot / ur : 0.f;
+  }
   out[r] += coef * sdot;
 }
 
@@ -903,7 +914,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   }
   if (g.dotv && w.n_tiles > 1 && !pair) {  // dot_out[r] += coef (partial_0 + partial_1 + ...), fixed order
     ProfScope ps(prof, st, PK_ROWDOT, (double)g.M * w.n_tiles, 4.0 * (double)g.M * (w.n_tiles + 2));
-    k_dot_parts<<<ceil_div(g.M, 256), 256, 0, st>>>(g.M, w.n_tiles, g.dot_part, g.dot_coef, g.dot_out);
+    k_dot_parts<<<ceil_div(g.M, 256), 256, 0, st>>>(g.M, w.n_tiles, g.dot_part, g.dot_coef, g.dot_inv_u, g.dot_out);
     ALG_LAUNCH_CHECK();
   }
 }
