@@ -873,6 +873,154 @@ __global__ void __launch_bounds__(32 * kTb2Warps, 1) k_tb_bwd2(const __grid_cons
   }
 }
 
+// k_tb_fwd2: the forward with each row's columns over two warps per lane quarter (16 row warps,
+// 2 groups x 8; see k_tb_bwd2): warp (q, hf) computes the geometry, a1 columns 16 hf .. + 15, a2
+// columns 32 hf .. + 31 and x^0 columns 64 hf .. + 63; hf = 0 writes u, hf = 1 writes Y.  Used when
+// nothing but u, Y and x^0 is stored (the fused reverse recomputes a1, a2); bit-identical to k_tb_fwd.
+__global__ void __launch_bounds__(32 * 16, 1) k_tb_fwd2(const __grid_constant__ TbMaps maps, const TbParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_dyn[];
+  unsigned char* base = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
+  unsigned char* w1s = base;
+  unsigned char* w2s = w1s + ((p.w1bytes + 1023u) & ~1023u);
+  unsigned char* slots = w2s + ((p.w2bytes + 1023u) & ~1023u);  // [16 warps][2][4 KB]
+  float(*sw)[32] = reinterpret_cast<float(*)[32]>(slots + 32 * kBox);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + 32 * kBox + 12 * 32 * 4 + 512);
+  uint64_t* a1_full = bars;      // [2]
+  uint64_t* d1_full = bars + 2;  // [2]
+  uint64_t* a2_full = bars + 4;  // [2]
+  uint64_t* d2_full = bars + 6;  // [2]
+  uint64_t* w_full = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = threadIdx.x; t < 12 * 32; t += blockDim.x) sw[t / 32][t % 32] = p.w0[t];
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < 2; ++g)
+      mbar_init(a1_full + g, 8), mbar_init(d1_full + g, 1), mbar_init(a2_full + g, 8), mbar_init(d2_full + g, 1);
+    mbar_init(w_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_my = p.n_tiles > (int)blockIdx.x ? (p.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  if (warp == 0 && lane == 0) {
+    mbar_expect_tx(w_full, p.w1bytes + p.w2bytes);
+    bulk_load(w1s, p.w1img, p.w1bytes, w_full);
+    bulk_load(w2s, p.w2img, p.w2bytes, w_full);
+  }
+  const int g = warp >> 3, j8 = warp & 7, q = j8 & 3, hf = j8 >> 2;
+  const bool issuer = j8 == 0;
+  const uint32_t bm = tmem + 256u * g;
+  const uint32_t b = bm + ((uint32_t)(q * 32) << 16);
+  uint32_t L = 0;
+  if (issuer) {
+    mbar_wait(w_full, 0);
+    tc_fence_after();
+    __syncwarp();
+    L = elect_leader();
+  }
+  const uint64_t dw1 = sdesc(smem_u32(w1s)), dw2 = sdesc(smem_u32(w2s));
+  int n_st = 0;
+  unsigned char* slot0 = slots + (size_t)(2 * warp) * kBox;
+  NextIdx nx;
+  if (g < n_my) nx.load(p, tile_row(g, q, lane));
+  for (int t = g; t < n_my; t += 2) {
+    const uint32_t ph = (uint32_t)(t >> 1) & 1u;
+    const int64_t e0 = (int64_t)((int)blockIdx.x + t * (int)gridDim.x) * kRows;
+    const int64_t e = e0 + q * 32 + lane;
+    const bool valid = e < p.ch.n_e;
+    const int32_t ci = nx.i, ca = nx.a;
+    if (t + 2 < n_my) nx.load(p, tile_row(t + 2, q, lane));
+    float uu = 0.f, a[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) a[c] = 0.f;
+    if (valid) {
+      float r[3], zb[kNB];
+      int zi, zj;
+      geom_core(p, ci, ca, r, uu, zb, zi, zj);
+      a1_half(p, reinterpret_cast<const float4*>(&sw[0][0]), hf, zb, zi, zj, a);
+      if (hf == 0) {
+        p.u[e] = uu;
+      } else {  // Y(r_hat), as geom_row
+        const float d = sqrtf(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+        const float inv = 1.f / d;
+        const float nv[3] = {r[0] * inv, r[1] * inv, r[2] * inv};
+        float y[9];
+        sh_eval(nv, y, p.gp.lmax);
+        if (p.gp.dsh == 4) reinterpret_cast<float4*>(p.Y)[e] = make_float4(y[0], y[1], y[2], y[3]);
+        else
+#pragma unroll
+          for (int k = 0; k < 9; ++k)
+            if (k < p.gp.dsh) p.Y[e * p.gp.dsh + k] = y[k];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) a[c] = silu_tb(a[c]);
+    tc_fence_after();
+    split_store16(b + 16 * hf, b + 32 + 16 * hf, a);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(a1_full + g);
+    if (issuer) {
+      mbar_wait(a1_full + g, ph);
+      tc_fence_after();
+      mma_kblock(L, bm + 64, bm, dw1, 64, idesc_n(64), true);
+      mma_commit_w(L, d1_full + g);
+    }
+    if (t + 2 < n_my) nx.prefetch(p);
+    // a2 columns 32 hf .. + 31 = s1 D1; A2 K-block hf = SiLU(a2)
+    mbar_wait(d1_full + g, ph);
+    tc_fence_after();
+#pragma unroll
+    for (int hc = 0; hc < 2; ++hc) {
+      float v[16];
+      tmem_ld16(b + 64 + 32 * hf + 16 * hc, v);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = silu_tb(p.s1 * v[c]);
+      split_store16(b + 128 + 64 * hf + 16 * hc, b + 128 + 64 * hf + 32 + 16 * hc, v);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(a2_full + g);
+    if (issuer) {
+      mbar_wait(a2_full + g, ph);
+      tc_fence_after();
+      mma_kblock(L, bm, bm + 128, dw2, 128, idesc_n(128), true);
+      mma_kblock(L, bm, bm + 192, dw2 + (uint64_t)((2 * 128 * 128) >> 4), 128, idesc_n(128), false);
+      mma_commit_w(L, d2_full + g);
+    }
+    // x^0 columns 64 hf .. + 63 = u (s2 D2)
+    mbar_wait(d2_full + g, ph);
+    tc_fence_after();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float v[32];
+      tmem_ld32(b + 64 * hf + 32 * h, v);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = uu * (p.s2 * v[c]);
+      unsigned char* sl = slot0 + (size_t)(n_st & 1) * kBox;  // the slot used two stores ago has been read
+      if (n_st >= 2) {
+        if (lane == 0) bulk_wait_read1();
+        __syncwarp();
+      }
+      ++n_st;
+      store_box(sl, &maps.x0, 64 * hf + 32 * h, (int)(e0 + q * 32), v, lane);
+    }
+    tc_fence_before();
+    __syncwarp();
+  }
+  if (lane == 0) bulk_wait0();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 CUtensorMap map_rows(const float* ptr, int64_t rows, int cols) {
   const uint64_t dims[2] = {(uint64_t)cols, (uint64_t)rows};
   const uint64_t strides[1] = {(uint64_t)cols * 4};
@@ -919,12 +1067,23 @@ void tb_fwd(const TbIO& io, cudaStream_t st, Profiler* prof) {
   if (io.m) maps.m = map_rows(io.m, E, 128);
   const size_t smem = 1024 + ((p.w1bytes + 1023) & ~1023u) + ((p.w2bytes + 1023) & ~1023u) + 16 * kBox + 12 * 32 * 4 +
                       512 + 256;
+  const size_t smem2 = 1024 + ((p.w1bytes + 1023) & ~1023u) + ((p.w2bytes + 1023) & ~1023u) + 32 * kBox +
+                       12 * 32 * 4 + 512 + 256;
+  // two warps per lane quarter when only u, Y and x^0 leave the kernel (A/B: ALLEGRO_TB_FWD_SPLIT=1;
+  // off: 11.8-12.0 vs 10.4-10.5 ms per C5 step same box, the duplicated geometry costs more than the
+  // extra warps win here)
+  static const bool split_env = [] {
+    const char* e = std::getenv("ALLEGRO_TB_FWD_SPLIT");
+    return e && std::atoi(e) != 0;
+  }();
+  const bool split2 = split_env && !io.a1 && !io.a2 && !io.m;
   int dev = 0;
   ALG_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};
   static int nsm[64] = {};
   if (!attr[dev]) {
     ALG_CUDA(cudaFuncSetAttribute(k_tb_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    ALG_CUDA(cudaFuncSetAttribute(k_tb_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
     attr[dev] = true;
   }
@@ -936,7 +1095,8 @@ void tb_fwd(const TbIO& io, cudaStream_t st, Profiler* prof) {
     const double bytes = (double)E * (8 + 2 * 24 + 4 + 4.0 * p.gp.dsh + 512 + (io.a1 ? 128 : 0) + (io.a2 ? 256 : 0) +
                                       (io.m ? 512 : 0));
     ProfScope ps_(prof, st, PK_TWOBODY, flops, bytes, "two-body fwd (fused)");
-    k_tb_fwd<<<grid, kTbThreads, smem, st>>>(maps, p);
+    if (split2) k_tb_fwd2<<<grid, 32 * 16, smem2, st>>>(maps, p);
+    else k_tb_fwd<<<grid, kTbThreads, smem, st>>>(maps, p);
   }
   ALG_LAUNCH_CHECK();
   if (std::getenv("ALLEGRO_SYNC_CHECK")) {
