@@ -410,7 +410,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if (PAIR) mbar_arrive_cluster(a_full + j, 0);  // the leader CTA's MMA warp waits for both
+          if (PAIR) {  // the leader CTA's MMA warp waits for both
+#ifndef ALG_PAIR_RELEASE
+            mbar_arrive_cluster_relaxed(a_full + j, 0);  // TMEM stores ordered by wait::st + tcgen05 fence
+#else
+            mbar_arrive_cluster(a_full + j, 0);
+#endif
+          }
           else mbar_arrive(a_full + j);
         }
         if (++j == p.a_stages) j = 0, aph ^= 1;
@@ -625,7 +631,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (PAIR) mbar_arrive_cluster(acc_empty + a, 0);  // the leader reuses it once both CTAs read it
+        if (PAIR) {  // the leader reuses it once both CTAs read it
+#ifndef ALG_PAIR_RELEASE
+          mbar_arrive_cluster_relaxed(acc_empty + a, 0);  // TMEM loads completed (wait::ld) + tcgen05 fence
+#else
+          mbar_arrive_cluster(acc_empty + a, 0);
+#endif
+        }
         else mbar_arrive(acc_empty + a);
       }
     }
@@ -813,9 +825,9 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   // CTA pair (cta_group::2) for a contraction split into two N-tiles: each CTA of a cluster pair
   // holds one N-half of W and splits only its own A rows (instead of two sibling CTAs splitting the
   // same rows); A/B switch ALLEGRO_TC_PAIR
-  static const bool pair_on = [] {  // off by default: measured slower
+  static const bool pair_on = [] {  // on by default (with relaxed remote arrivals)
     const char* e = std::getenv("ALLEGRO_TC_PAIR");
-    return e && std::atoi(e) != 0;
+    return !e || std::atoi(e) != 0;
   }();
   const bool pair = pair_on && w.n_tiles == 2 && (g.epi == EPI_RESID || g.epi == EPI_ACCX) && !g.single_pass &&
                     g_tc_tuning.diag == 0 && (w.N_t * 2) % 32 == 0;

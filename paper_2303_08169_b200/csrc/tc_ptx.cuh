@@ -114,6 +114,15 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* b, uint32_t rank) 
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(b)), "r"(rank));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// relaxed variant: no release fence (a .release.cluster arrive compiles to MEMBAR + ERRBAR, 13-22 %
+// of the pair GEMM's stall samples) -- for arrivals whose only payload is TMEM data already
+// completed (tcgen05.wait::st / ::ld) and ordered by tcgen05.fence::before_thread_sync
+// (build-time A/B: ALG_PAIR_RELEASE restores the release form)
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint64_t* b, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(b)), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
 // wait with cluster-scope acquire (the barrier receives arrivals from the peer CTA)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
