@@ -260,6 +260,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
       // staged rows, or (a tile spanning more than GA atoms: atoms without edges in between) L2
       const unsigned char* gb = ga < F::GA ? st + F::g_off() + (size_t)ga * DSH * 128
                                            : reinterpret_cast<const unsigned char*>(p.G + (int64_t)(hdr[33] + ga) * DSH * 32);
+      // layer 0: this row's Y (DSH = 4) as one 16-B load (scalar loads at a 16-B lane stride were
+      // 4-way shared-memory bank conflicts: 8 % of the kernel's shared wavefronts)
+      [[maybe_unused]] float yrow[4] = {0.f, 0.f, 0.f, 0.f};
+      if constexpr (K == 0) {
+        static_assert(DSH == 4, "the fused TP forward is built for lmax = 1");
+        const float4 y4 = *reinterpret_cast<const float4*>(st + F::y_off() + e * 16);
+        yrow[0] = y4.x, yrow[1] = y4.y, yrow[2] = y4.z, yrow[3] = y4.w;
+      }
       static_for<NO>([&](auto O) {
         constexpr int o = decltype(O)::value;
         constexpr int D3 = F::dim(o);
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tpl_fwd(const __grid_constant__
                     const unsigned char* grow = gb + (A.sh_off[q] + m2) * 128;
                     if constexpr (K == 0) {
                       constexpr int mv = A.in_off[q] + m1;  // V0[m] = w_edge[l(m)] Y[m]
-                      const float yv = reinterpret_cast<const float*>(st + F::y_off())[e * DSH + mv];
+                      const float yv = yrow[mv];
                       const unsigned char* vrow = st + lm_l(mv) * kBoxBytes + e * 128;
 #pragma unroll
                       for (int h = 0; h < 2; ++h) {
