@@ -321,6 +321,8 @@ def main():
     ev0.record(stream)
     rep = m.md_step(n_prof, DT_FS)
     edges_prof = int(rep.n_edges)
+    evp = torch.cuda.Event(enable_timing=True)  # the profiled steps' own span (kernel sum + gaps)
+    evp.record(stream)
     m.profile(False)
     if args.steps > n_prof:
         rep = m.md_step(args.steps - n_prof, DT_FS)
@@ -328,6 +330,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     ms = ev0.elapsed_time(ev1)
+    ms_prof_span = ev0.elapsed_time(evp) / n_prof
     launches = m.launch_count()
     prof = m.profile_read()
     detail = sorted(m.profile_detail(), key=lambda x: -x[1])
@@ -448,6 +451,7 @@ def main():
         "shapes": [{"tag": t, "ms_per_step": round(ms_ / n_prof, 3), "gbs": round(by / max(ms_, 1e-9) / 1e6, 1),
                     "launches_per_step": n_ / n_prof} for t, ms_, by, n_ in detail[:40]],
         "profiled_steps": n_prof,
+        "profiled_step_span_ms": round(ms_prof_span, 3),  # device span of a profiled step (kernels + gaps)
         "edges": {"first": edges_first, "profiled": edges_prof, "last": edges_last,
                   "edges_per_s": round(0.5 * (edges_first + edges_last) * args.steps / (ms_max / 1e3), 1)},
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
