@@ -129,7 +129,12 @@ int allegro_create(const allegro_params* p, allegro_ctx** out) {
     domain_setup(c, p->nccl_unique_id);
     size_t free_b = 0, total_b = 0;
     ALG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    c->ws_budget_bytes = std::min<size_t>(free_b / 2, (size_t)64 << 30);
+    // per-chunk activation workspace: half the free memory, capped (ALLEGRO_WS_GB overrides the cap)
+    static const size_t ws_cap = [] {
+      const char* e = std::getenv("ALLEGRO_WS_GB");
+      return (size_t)(e ? std::atof(e) : 80.0) << 30;  // 80 GB: two C5-size ctxs still fit one B200
+    }();
+    c->ws_budget_bytes = std::min<size_t>(free_b / 2, ws_cap);
     if (p->n_atoms_global > 0) reserve_atoms(c, p->n_atoms_global);
     return ALLEGRO_OK;
   });
