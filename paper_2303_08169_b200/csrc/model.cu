@@ -191,6 +191,15 @@ __device__ __forceinline__ void fetch_env(const TpArgs& t, int64_t e, int lane, 
 // a fixed number of edges ahead of the register pipeline, holds no registers.  Measured on C5
 // (profiles/r01_tp_prefetch_ab.jsonl): k_tp_fwd 46.9 -> 44.6 ms per step at distance 2; in
 // k_tp_bwd it raises the register count (72 -> 96) and nets nothing, so it is off there.
+#ifndef ALG_ENV_BATCH
+#define ALG_ENV_BATCH 4  // environment adjoint: edges per batch of loads in flight (1 = one edge ahead)
+#endif
+#ifndef ALG_GBAR_BATCH
+#define ALG_GBAR_BATCH 8  // Gamma-bar row sum in k_env_adj: edges per batch (1 = one edge ahead)
+#endif
+#ifndef ALG_GAMMA_BATCH
+#define ALG_GAMMA_BATCH 8  // Gamma_i: edges per batch of loads in flight (1 = the one-edge-ahead pipeline)
+#endif
 #ifndef ALG_TP_PFD_FWD
 #define ALG_TP_PFD_FWD 2
 #endif
@@ -294,6 +303,31 @@ __global__ void __launch_bounds__(128) k_tp_fwd(TpArgs t) {
 #pragma unroll
   for (int m = 0; m < AR::DSH; ++m) G[m] = 0.f;
   if (r1 > r0) {
+#if ALG_GAMMA_BATCH > 1
+    // ALG_GAMMA_BATCH edges' loads in flight at once (the row's edges are summed in edge order as
+    // before): the one-edge-ahead pipeline left the warp waiting one L2 round trip per edge
+    for (int64_t e0 = r0; e0 < r1; e0 += ALG_GAMMA_BATCH) {
+      EnvIn<NL, LMAX, K> buf[ALG_GAMMA_BATCH];
+#pragma unroll
+      for (int j = 0; j < ALG_GAMMA_BATCH; ++j)
+        if (e0 + j < r1) fetch_env<NL, LMAX, K>(t, e0 + j, lane, buf[j]);
+      {  // warm L2 with the next batch: lane -> (edge, line), NENV w lines + the Y line per edge
+        constexpr int kL = AR::NENV + 1;
+        const int j = lane / kL, part = lane % kL;
+        const int64_t en = e0 + ALG_GAMMA_BATCH + j;
+        if (j < ALG_GAMMA_BATCH && en < r1) {
+          const float* pf = part < AR::NENV ? t.w + en * AR::NW + AR::ENV_OFF + part * kC : t.Y + en * AR::DSH;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < ALG_GAMMA_BATCH; ++j)
+        if (e0 + j < r1) {
+#pragma unroll
+          for (int m = 0; m < AR::DSH; ++m) G[m] = fmaf(buf[j].we[lm_l(m)], buf[j].y[m], G[m]);
+        }
+    }
+#else
     EnvIn<NL, LMAX, K> nx;
     fetch_env<NL, LMAX, K>(t, r0, lane, nx);
     for (int64_t e = r1 - 1 < r0 + ALG_ROW_PFD ? r1 - 1 : r0 + ALG_ROW_PFD; e > r0; --e)
@@ -305,6 +339,7 @@ __global__ void __launch_bounds__(128) k_tp_fwd(TpArgs t) {
 #pragma unroll
       for (int m = 0; m < AR::DSH; ++m) G[m] = fmaf(cur.we[lm_l(m)], cur.y[m], G[m]);
     }
+#endif
   }
 #pragma unroll
   for (int m = 0; m < AR::DSH; ++m) {
@@ -390,14 +425,7 @@ __device__ __forceinline__ void env_adjoint(const TpArgs& t, int64_t r0, int64_t
     fetch_env<NL, LMAX, K>(t, e, lane, in.env);
     in.yb_old = owns_total<AR::DSH>(lane, mm) ? t.ybar[e * AR::DSH + mm] : 0.f;
   };
-  EnvB en;
-  fetch_envb(r0, en);
-  for (int64_t e = r1 - 1 < r0 + ALG_ROW_PFD ? r1 - 1 : r0 + ALG_ROW_PFD; e > r0; --e)
-    prefetch_env<NL, LMAX, K>(t, e, lane, true);
-  for (int64_t e = r0; e < r1; ++e) {
-    const EnvB cur = en;
-    fetch_envb(e + 1 < r1 ? e + 1 : e, en);
-    if (e + 1 + ALG_ROW_PFD < r1) prefetch_env<NL, LMAX, K>(t, e + 1 + ALG_ROW_PFD, lane, true);
+  auto adjoint_edge = [&](int64_t e, const EnvB& cur) {  // w_env-bar and Y-bar of one edge
     float wb[AR::NENV];
 #pragma unroll
     for (int l = 0; l < AR::NENV; ++l) wb[l] = 0.f;
@@ -412,7 +440,40 @@ __device__ __forceinline__ void env_adjoint(const TpArgs& t, int64_t r0, int64_t
 #pragma unroll
     for (int l = 0; l < AR::NENV; ++l) t.wbar[e * AR::NW + AR::ENV_OFF + l * kC + lane] = t.inv_sqrt_nbar * wb[l];
     if (owns_total<AR::DSH>(lane, mm)) t.ybar[e * AR::DSH + mm] = cur.yb_old + t.inv_sqrt_nbar * s;
+  };
+#if ALG_ENV_BATCH > 1
+  // ALG_ENV_BATCH edges' inputs in flight at once (each edge's outputs depend on that edge only)
+  for (int64_t e0 = r0; e0 < r1; e0 += ALG_ENV_BATCH) {
+    EnvB buf[ALG_ENV_BATCH];
+#pragma unroll
+    for (int j = 0; j < ALG_ENV_BATCH; ++j)
+      if (e0 + j < r1) fetch_envb(e0 + j, buf[j]);
+    {  // warm L2 with the next batch: lane -> (edge, line): NENV w lines, Y, Y-bar
+      constexpr int kL = AR::NENV + 2;
+      const int j = lane / kL, part = lane % kL;
+      const int64_t en2 = e0 + ALG_ENV_BATCH + j;
+      if (j < ALG_ENV_BATCH && en2 < r1) {
+        const float* pf = part < AR::NENV ? t.w + en2 * AR::NW + AR::ENV_OFF + part * kC
+                                          : (part == AR::NENV ? t.Y + en2 * AR::DSH : t.ybar + en2 * AR::DSH);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < ALG_ENV_BATCH; ++j)
+      if (e0 + j < r1) adjoint_edge(e0 + j, buf[j]);
   }
+#else
+  EnvB en;
+  fetch_envb(r0, en);
+  for (int64_t e = r1 - 1 < r0 + ALG_ROW_PFD ? r1 - 1 : r0 + ALG_ROW_PFD; e > r0; --e)
+    prefetch_env<NL, LMAX, K>(t, e, lane, true);
+  for (int64_t e = r0; e < r1; ++e) {  // pipelined one edge ahead (+ L2 prefetch further ahead)
+    const EnvB cur = en;
+    fetch_envb(e + 1 < r1 ? e + 1 : e, en);
+    if (e + 1 + ALG_ROW_PFD < r1) prefetch_env<NL, LMAX, K>(t, e + 1 + ALG_ROW_PFD, lane, true);
+    adjoint_edge(e, cur);
+  }
+#endif
 }
 
 template <int NL, int LMAX, int K>
@@ -505,9 +566,32 @@ __global__ void __launch_bounds__(128) k_env_adj(TpArgs t) {
   if (r1 <= r0) return;
   constexpr int LP = AR::DSH <= 1 ? 0 : AR::DSH <= 2 ? 1 : AR::DSH <= 4 ? 2 : AR::DSH <= 8 ? 3 : 4;
   const int mm = lane >> (5 - LP);
-  float Gb[AR::DSH], nx[AR::DSH];
+  float Gb[AR::DSH];
 #pragma unroll
-  for (int m = 0; m < AR::DSH; ++m) Gb[m] = 0.f, nx[m] = t.gp[(r0 * AR::DSH + m) * kC + lane];
+  for (int m = 0; m < AR::DSH; ++m) Gb[m] = 0.f;
+#if ALG_GBAR_BATCH > 1
+  for (int64_t e0 = r0; e0 < r1; e0 += ALG_GBAR_BATCH) {  // loads of ALG_GBAR_BATCH edges in flight
+    float buf[ALG_GBAR_BATCH][AR::DSH];
+#pragma unroll
+    for (int j = 0; j < ALG_GBAR_BATCH; ++j)
+#pragma unroll
+      for (int m = 0; m < AR::DSH; ++m) buf[j][m] = e0 + j < r1 ? t.gp[((e0 + j) * AR::DSH + m) * kC + lane] : 0.f;
+    {  // warm L2 with the next batch: lane -> (edge, m line)
+      const int j = lane / AR::DSH, m = lane % AR::DSH;
+      const int64_t en2 = e0 + ALG_GBAR_BATCH + j;
+      if (j < ALG_GBAR_BATCH && en2 < r1) asm volatile("prefetch.global.L2 [%0];" ::"l"(t.gp + (en2 * AR::DSH + m) * kC));
+    }
+#pragma unroll
+    for (int j = 0; j < ALG_GBAR_BATCH; ++j)
+      if (e0 + j < r1) {  // the row's edges in order, as before
+#pragma unroll
+        for (int m = 0; m < AR::DSH; ++m) Gb[m] += buf[j][m];
+      }
+  }
+#else
+  float nx[AR::DSH];
+#pragma unroll
+  for (int m = 0; m < AR::DSH; ++m) nx[m] = t.gp[(r0 * AR::DSH + m) * kC + lane];
   for (int64_t e = r0 + 1; e < r1 && e <= r0 + ALG_ROW_PFD; ++e)
     if (lane < AR::DSH) asm volatile("prefetch.global.L2 [%0];" ::"l"(t.gp + (e * AR::DSH + lane) * kC));
   for (int64_t e = r0; e < r1; ++e) {  // pipelined one edge ahead (+ L2 prefetch further ahead)
@@ -522,6 +606,7 @@ __global__ void __launch_bounds__(128) k_env_adj(TpArgs t) {
 #pragma unroll
     for (int m = 0; m < AR::DSH; ++m) Gb[m] += cur[m];
   }
+#endif
   env_adjoint<NL, LMAX, K>(t, r0, r1, lane, mm, Gb);
 }
 
