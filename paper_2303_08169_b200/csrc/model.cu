@@ -191,6 +191,9 @@ __device__ __forceinline__ void fetch_env(const TpArgs& t, int64_t e, int lane, 
 // a fixed number of edges ahead of the register pipeline, holds no registers.  Measured on C5
 // (profiles/r01_tp_prefetch_ab.jsonl): k_tp_fwd 46.9 -> 44.6 ms per step at distance 2; in
 // k_tp_bwd it raises the register count (72 -> 96) and nets nothing, so it is off there.
+#ifndef ALG_LAST_BATCH
+#define ALG_LAST_BATCH 4  // k_last's per-edge loop: edges per batch of loads in flight
+#endif
 #ifndef ALG_ENV_BATCH
 #define ALG_ENV_BATCH 4  // environment adjoint: edges per batch of loads in flight (1 = one edge ahead)
 #endif
@@ -655,15 +658,17 @@ __global__ void __launch_bounds__(128) k_last(LastArgs a) {
   float G[AR::DSH];
 #pragma unroll
   for (int m = 0; m < AR::DSH; ++m) G[m] = 0.f;
-  {
-    EnvIn<NL, LMAX, K> nx;
-    fetch_env<NL, LMAX, K>(t, r0, lane, nx);
-    for (int64_t e = r0; e < r1; ++e) {
-      const EnvIn<NL, LMAX, K> cur = nx;
-      fetch_env<NL, LMAX, K>(t, e + 1 < r1 ? e + 1 : e, lane, nx);
+  for (int64_t e0 = r0; e0 < r1; e0 += ALG_GAMMA_BATCH) {  // batches of loads in flight, edge order kept
+    EnvIn<NL, LMAX, K> buf[ALG_GAMMA_BATCH];
 #pragma unroll
-      for (int m = 0; m < AR::DSH; ++m) G[m] = fmaf(cur.we[lm_l(m)], cur.y[m], G[m]);
-    }
+    for (int j = 0; j < ALG_GAMMA_BATCH; ++j)
+      if (e0 + j < r1) fetch_env<NL, LMAX, K>(t, e0 + j, lane, buf[j]);
+#pragma unroll
+    for (int j = 0; j < ALG_GAMMA_BATCH; ++j)
+      if (e0 + j < r1) {
+#pragma unroll
+        for (int m = 0; m < AR::DSH; ++m) G[m] = fmaf(buf[j].we[lm_l(m)], buf[j].y[m], G[m]);
+      }
   }
 #pragma unroll
   for (int m = 0; m < AR::DSH; ++m) G[m] *= t.inv_sqrt_nbar;
@@ -687,8 +692,6 @@ __global__ void __launch_bounds__(128) k_last(LastArgs a) {
     in.x4 = reinterpret_cast<const float4*>(a.x + e * kD)[lane];
     in.ue = a.u[e];
   };
-  In nx;
-  fetch(r0, nx);
   auto pf = [&](int64_t e) {  // V rows (lanes 0 .. DIN-1) and the x row (4 lines) of edge e
     const float* q = nullptr;
     if (lane < AR::DIN) {
@@ -704,11 +707,8 @@ __global__ void __launch_bounds__(128) k_last(LastArgs a) {
     }
     if (q) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
   };
-  for (int64_t e = r0 + 1; e < r1 && e <= r0 + ALG_ROW_PFD; ++e) pf(e);
-  for (int64_t e = r0; e < r1; ++e) {
-    const In cur = nx;
-    fetch(e + 1 < r1 ? e + 1 : e, nx);
-    if (e + 1 + ALG_ROW_PFD < r1) pf(e + 1 + ALG_ROW_PFD);
+  // the row's edges in order (E_e sum, Gamma-bar), ALG_LAST_BATCH edges' inputs in flight at once
+  auto process = [&](int64_t e, const In& cur) {
     float v[AR::DIN];
     expand_v<NL, LMAX, K>(cur.v, v);
     // T = s (scalar outputs only)
@@ -782,6 +782,19 @@ __global__ void __launch_bounds__(128) k_last(LastArgs a) {
 #pragma unroll
       for (int m = 0; m < dim; ++m) dst[m * kC] = vb[off + m];
     });
+  };
+  for (int64_t e = r0 + ALG_LAST_BATCH; e < r1 && e < r0 + 2 * ALG_LAST_BATCH; ++e) pf(e);
+  for (int64_t e0 = r0; e0 < r1; e0 += ALG_LAST_BATCH) {
+    In buf[ALG_LAST_BATCH];
+#pragma unroll
+    for (int j = 0; j < ALG_LAST_BATCH; ++j)
+      if (e0 + j < r1) fetch(e0 + j, buf[j]);
+#pragma unroll
+    for (int j = 0; j < ALG_LAST_BATCH; ++j)  // warm L2 two batches ahead
+      if (e0 + 2 * ALG_LAST_BATCH + j < r1) pf(e0 + 2 * ALG_LAST_BATCH + j);
+#pragma unroll
+    for (int j = 0; j < ALG_LAST_BATCH; ++j)
+      if (e0 + j < r1) process(e0 + j, buf[j]);
   }
   if (lane == 0) a.e_atom[at] = sig * (double)t.inv_sqrt_nbar * (double)acc + (z == 0 ? a.mu0 : a.mu1);
   constexpr int LP = AR::DSH <= 1 ? 0 : AR::DSH <= 2 ? 1 : AR::DSH <= 4 ? 2 : AR::DSH <= 8 ? 3 : 4;
