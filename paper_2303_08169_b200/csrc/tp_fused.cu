@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "ctx.cuh"
@@ -41,6 +42,8 @@
 
 namespace allegro {
 namespace {
+
+std::mutex g_attr_mu;  // guards the per-device attribute tables of the launchers below
 
 constexpr int kTile = 32;           // edges per tile
 constexpr int kTpWarps = 16;        // TP warps: 4 lane quarters x 4 channel groups
@@ -506,10 +509,14 @@ void launch(const TplIO& io, cudaStream_t st, Profiler* prof) {
   ALG_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};
   static int nsm[64] = {};
-  if (!attr[dev]) {
-    ALG_CUDA(cudaFuncSetAttribute(k_tpl_fwd<NL, LMAX, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
-    ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
-    attr[dev] = true;
+  if (dev < 0 || dev >= 64) throw CudaError("device ordinal out of range");
+  {
+    std::lock_guard<std::mutex> lk_(g_attr_mu);  // per-device function attributes, set once (thread-safe)
+    if (!attr[dev]) {
+      ALG_CUDA(cudaFuncSetAttribute(k_tpl_fwd<NL, LMAX, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
+      ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
+      attr[dev] = true;
+    }
   }
   const int grid = std::max(1, std::min(p.n_tiles, nsm[dev]));
   {
@@ -1098,10 +1105,14 @@ void launch_bwd(const TpbIO& io, cudaStream_t st, Profiler* prof) {
   ALG_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};
   static int nsm[64] = {};
-  if (!attr[dev]) {
-    ALG_CUDA(cudaFuncSetAttribute(k_tpl_bwd<NL, LMAX, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
-    ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
-    attr[dev] = true;
+  if (dev < 0 || dev >= 64) throw CudaError("device ordinal out of range");
+  {
+    std::lock_guard<std::mutex> lk_(g_attr_mu);  // per-device function attributes, set once (thread-safe)
+    if (!attr[dev]) {
+      ALG_CUDA(cudaFuncSetAttribute(k_tpl_bwd<NL, LMAX, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
+      ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
+      attr[dev] = true;
+    }
   }
   const int grid = std::max(1, std::min(p.n_tiles, nsm[dev]));
   {

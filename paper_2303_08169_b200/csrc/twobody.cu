@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "ctx.cuh"
@@ -29,6 +30,8 @@
 
 namespace allegro {
 namespace {
+
+std::mutex g_attr_mu;  // guards the per-device attribute tables of the launchers below
 
 constexpr int kRows = 128;
 constexpr int kTbThreads = 32 * 9;
@@ -1081,11 +1084,15 @@ void tb_fwd(const TbIO& io, cudaStream_t st, Profiler* prof) {
   ALG_CUDA(cudaGetDevice(&dev));
   static bool attr[64] = {};
   static int nsm[64] = {};
-  if (!attr[dev]) {
-    ALG_CUDA(cudaFuncSetAttribute(k_tb_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    ALG_CUDA(cudaFuncSetAttribute(k_tb_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
-    attr[dev] = true;
+  if (dev < 0 || dev >= 64) throw CudaError("device ordinal out of range");
+  {
+    std::lock_guard<std::mutex> lk_(g_attr_mu);  // per-device function attributes, set once (thread-safe)
+    if (!attr[dev]) {
+      ALG_CUDA(cudaFuncSetAttribute(k_tb_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      ALG_CUDA(cudaFuncSetAttribute(k_tb_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
+      attr[dev] = true;
+    }
   }
   const int grid = std::max(1, std::min(p.n_tiles, nsm[dev]));
   {
@@ -1149,11 +1156,15 @@ void tb_bwd(const TbIO& io, const TbbIO& bo, cudaStream_t st, Profiler* prof) {
   }();
   static bool attr[64] = {};
   static int nsm[64] = {};
-  if (!attr[dev]) {
-    ALG_CUDA(cudaFuncSetAttribute(k_tb_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ALG_CUDA(cudaFuncSetAttribute(k_tb_bwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
-    attr[dev] = true;
+  if (dev < 0 || dev >= 64) throw CudaError("device ordinal out of range");
+  {
+    std::lock_guard<std::mutex> lk_(g_attr_mu);  // per-device function attributes, set once (thread-safe)
+    if (!attr[dev]) {
+      ALG_CUDA(cudaFuncSetAttribute(k_tb_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ALG_CUDA(cudaFuncSetAttribute(k_tb_bwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ALG_CUDA(cudaDeviceGetAttribute(&nsm[dev], cudaDevAttrMultiProcessorCount, dev));
+      attr[dev] = true;
+    }
   }
   const int grid = std::max(1, std::min(p.n_tiles, nsm[dev]));
   {
