@@ -94,6 +94,7 @@ struct TcParams {
   int tma_store;       // the output C (and aux) leave by TMA stores of [32 x 32] boxes (no row-dot)
   int store_hint;      // TMA stores carry an L2 evict_first policy
   int out_slots;       // output staging slots per epilogue warp (2, or 4: two C + aux groups in flight)
+  int dot_x;           // EPI_R2: the row-dot operand arrives through the X ring (thread = row sums)
 };
 
 // v <- s v (the saved pre-activation "aux"); out <- epilogue(v, xin) (xin = X, or old C for EPI_ACC)
@@ -443,6 +444,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // ---------------- epilogue warpgroup (warps 4..7) ----------------
     const int q = warp & 3;  // TMEM lane quarter
+    const bool dotx = EPI == EPI_R2 && p.dot_x != 0;  // compile-time false for the other epilogues
     const GemmArgs& g = p.g;
     constexpr bool kX = EPI == EPI_RESID || EPI == EPI_URESID || EPI == EPI_ADDX || EPI == EPI_DSILU || EPI == EPI_ACCX;
     constexpr bool kAuxEpi = EPI == EPI_SILU || EPI == EPI_UMUL_SAVE || EPI == EPI_RESID;
@@ -469,16 +471,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const float ur = u_next, e2_row = rs2_next;
       u_next = row_u(t + 1);
       rs2_next = row_rs2(t + 1);
+      const int64_t row0 = (int64_t)mt(t) * ROWS + q * 32;
+      // the row-dot's read-modify-write target (and 1/u) of this warp's 32 rows (one 128-B line
+      // each): warmed in L2 now, so the tile's last step is not a dependent DRAM round trip
+      if ((EPI == EPI_ACCX || EPI == EPI_R2 || EPI == EPI_ACC) && g.dotv != nullptr && p.n_tiles_total == 1 &&
+          lane == 0 && row0 < g.M) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(g.dot_out + row0));
+        if (g.dot_inv_u) asm volatile("prefetch.global.L2 [%0];" ::"l"(g.dot_inv_u + row0));
+      }
       mbar_wait(acc_full + a, acph);
       tc_fence_after();
-      const int64_t row0 = (int64_t)mt(t) * ROWS + q * 32;
       const int64_t r = row0 + lane;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * p.acc_cols);
       float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // row-dot partials, rows (lane>>3)+4i
+      float dsum = 0.f;  // dot_x: this thread's row-dot
       for (int c0 = 0; c0 < p.N_t; c0 += 32) {
         float v[32], out[32], xin[32];
         float4 dq[8];
-        if (g.dotv != nullptr) {  // row-dot operand, coalesced like the stores; in flight during the waits
+        if (g.dotv != nullptr && !dotx) {  // row-dot operand, coalesced like the stores; in flight during the waits
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int64_t rr = row0 + (lane >> 3) + 4 * i;
@@ -542,7 +552,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int64_t col = col0 + c0;
         const int nc = (p.N_t - c0) >= 32 ? 8 : (p.N_t - c0) / 4;
         epi_apply<32, EPI>(g, v, xin, ur, out);
-        if (g.dotv != nullptr && !p.tma_store) {
+        if (dotx) {
+          // this thread's row of the TMA-loaded [128 x 32] row-dot operand box: sum in column order
+          mbar_wait(x_full + xs, xph);
+          const unsigned char* xb = x_stage + (size_t)xs * X_STAGE_BYTES;
+          const int row = q * 32 + lane;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 d4 = *reinterpret_cast<const float4*>(xb + row * 128 + ((c ^ (row & 7)) << 4));
+            dsum = fmaf(out[4 * c], d4.x, dsum);
+            dsum = fmaf(out[4 * c + 1], d4.y, dsum);
+            dsum = fmaf(out[4 * c + 2], d4.z, dsum);
+            dsum = fmaf(out[4 * c + 3], d4.w, dsum);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(x_empty + xs);
+          if (++xs == X_STAGES) xs = 0, xph ^= 1;
+        }
+        if (g.dotv != nullptr && !p.tma_store && !dotx) {
           scatter_rows_dot(buf, g.C + col, g.N, row0, g.M, lane, out, nc, dq, acc8);
         } else if (p.tma_store) {  // [32 rows x 32 cols] boxes through this warp's two SMEM slots
           if (want_aux) {  // C and aux in one group; wait until the previous group has read both slots
@@ -591,7 +619,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               else tma_store_2d(&mapC, (int)col, (int)row0, tb);
               bulk_commit();
             }
-            if (g.dotv != nullptr) {  // fused row-dot on the transposed (coalesced) view of the slot
+            if (g.dotv != nullptr && !dotx) {  // fused row-dot on the transposed (coalesced) view of the slot
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 const float4 o4 = *tile_at(tb, (lane >> 3) + 4 * i, lane & 7);
@@ -607,16 +635,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (want_aux) scatter_rows(buf, g.aux + col, g.N, row0, g.M, lane, v, nc);
       }
       if (g.dotv != nullptr) {  // reduce the 8 lanes of each row; lane (lane & 7) == i writes row (lane>>3)+4i
-        float mine = 0.f;
+        float mine = dsum;
+        if (!dotx) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float t8 = acc8[i];
-          t8 += __shfl_xor_sync(0xffffffffu, t8, 1);
-          t8 += __shfl_xor_sync(0xffffffffu, t8, 2);
-          t8 += __shfl_xor_sync(0xffffffffu, t8, 4);
-          if ((lane & 7) == i) mine = t8;
+          for (int i = 0; i < 8; ++i) {
+            float t8 = acc8[i];
+            t8 += __shfl_xor_sync(0xffffffffu, t8, 1);
+            t8 += __shfl_xor_sync(0xffffffffu, t8, 2);
+            t8 += __shfl_xor_sync(0xffffffffu, t8, 4);
+            if ((lane & 7) == i) mine = t8;
+          }
         }
-        const int64_t rr = row0 + (lane >> 3) + 4 * (lane & 7);
+        const int64_t rr = dotx ? row0 + lane : row0 + (lane >> 3) + 4 * (lane & 7);
         if (rr < g.M) {
           if (p.n_tiles_total > 1) g.dot_part[rr * p.n_tiles_total + tile] = mine;  // summed by k_dot_parts
           else {
@@ -795,8 +825,15 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const CUtensorMap mA2 = g.A2 ? make_map(g.A2, g.M, g.K - g.K1, g.lda2) : mA;
   const size_t w_bytes = w.tile_bytes;
   const size_t w_round = (w_bytes + 1023) & ~(size_t)1023;
+  // EPI_R2 has no [M][N] input: its X ring carries the row-dot operand instead (A/B ALLEGRO_TC_DOTX=0:
+  // per-lane global loads of the operand, transposed sums)
+  static const bool dotx_on = [] {
+    const char* e = std::getenv("ALLEGRO_TC_DOTX");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool dot_x = dotx_on && g.epi == EPI_R2 && g.dotv != nullptr && g.N % 32 == 0;
   const bool has_x = g.epi == EPI_RESID || g.epi == EPI_URESID || g.epi == EPI_ADDX || g.epi == EPI_DSILU ||
-                     g.epi == EPI_ACC || g.epi == EPI_ACCX;
+                     g.epi == EPI_ACC || g.epi == EPI_ACCX || dot_x;
   const bool aux_epi0 = g.aux && (g.epi == EPI_SILU || g.epi == EPI_UMUL_SAVE || g.epi == EPI_RESID);
   // A/B (ALLEGRO_TC_OUTSLOTS=4): two (C, aux) store groups in flight per epilogue warp
   static const int outslots_env = [] {
@@ -863,7 +900,8 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   p.tmem_cols = cols;
   p.diag = g_tc_tuning.diag;
   p.has_x = has_x ? 1 : 0;
-  const float* xsrc = g.epi == EPI_ACC ? g.C : g.X;
+  const float* xsrc = dot_x ? g.dotv : (g.epi == EPI_ACC ? g.C : g.X);
+  p.dot_x = dot_x ? 1 : 0;
   const CUtensorMap mX = has_x ? make_map(xsrc, g.M, g.N, g.N) : mA;
   const bool aux_epi = g.aux && (g.epi == EPI_SILU || g.epi == EPI_UMUL_SAVE || g.epi == EPI_RESID);
   p.tma_store = (g_tc_tuning.tma_store && w.N_t % 32 == 0 && (p.diag & 2) == 0) ? 1 : 0;
