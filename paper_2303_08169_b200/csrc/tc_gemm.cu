@@ -53,6 +53,11 @@ constexpr int A_TMEM_COLS = 64;              // one TMEM A stage: hi (32 cols) +
 constexpr size_t SMEM_LIMIT = 227 * 1024;
 constexpr size_t SMEM_RESERVE = 2048;        // barriers + alignment slack
 constexpr int STAGE_OUT_BYTES = 32 * 128;    // per epilogue warp: [32 rows x 32 fp32] transpose tile
+// per-row epilogue scalars: L1 prefetch a tile ahead + load at the tile start (1), or a register
+// loaded a tile ahead (0, the round-2 form; build-time A/B)
+#ifndef ALG_TC_ROWPF
+#define ALG_TC_ROWPF 1
+#endif
 constexpr int X_STAGES = 2;                  // epilogue input ring: [128 rows x 32 fp32] TMA boxes
 constexpr int X_STAGE_BYTES = ROWS * 128;
 
@@ -444,7 +449,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // ---------------- epilogue warpgroup (warps 4..7) ----------------
     const int q = warp & 3;  // TMEM lane quarter
-    const bool dotx = EPI == EPI_R2 && p.dot_x != 0;  // compile-time false for the other epilogues
+    // EPI_R2's row-dot operand arrives through the X ring (compile-time: the per-lane operand
+    // registers of the other epilogues' row-dot would spill this instantiation)
+    constexpr bool kDotX = EPI == EPI_R2;
+    const bool dotx = kDotX && p.g.dotv != nullptr;
     const GemmArgs& g = p.g;
     constexpr bool kX = EPI == EPI_RESID || EPI == EPI_URESID || EPI == EPI_ADDX || EPI == EPI_DSILU || EPI == EPI_ACCX;
     constexpr bool kAuxEpi = EPI == EPI_SILU || EPI == EPI_UMUL_SAVE || EPI == EPI_RESID;
@@ -453,8 +461,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     constexpr bool kIn = kX || EPI == EPI_ACC;  // epilogue reads a [M][N] input (X or old C)
     int xs = 0;
     uint32_t xph = 0;
-    // per-row scalars (u, and rs2 for EPI_R2) are loaded one tile ahead: a load issued at the
-    // tile start would stall the epilogue warps for a full DRAM round trip every tile
+    // per-row scalars (u, and rs2 for EPI_R2): their 128-B lines are prefetched into L1 one tile
+    // ahead and loaded at the tile start (a register loaded a tile ahead was spilled at once by
+    // the register-capped epilogues -- the spill store waited a DRAM round trip every tile)
     auto row_u = [&](int tt) -> float {
       const int64_t rr = (int64_t)mt(tt) * ROWS + q * 32 + lane;
       return (tt < n_my && rr < g.M && g.u != nullptr) ? __ldg(g.u + rr) : 1.f;
@@ -463,14 +472,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int64_t rr = (int64_t)mt(tt) * ROWS + q * 32 + lane;
       return (EPI == EPI_R2 && tt < n_my && rr < g.M) ? __ldg(g.rs2 + rr) : 0.f;
     };
+#if ALG_TC_ROWPF
+    auto pf_rows = [&](int tt) {
+      const int64_t r0 = (int64_t)mt(tt) * ROWS + q * 32;
+      if (lane == 0 && tt < n_my && r0 < g.M) {
+        if (g.u != nullptr) asm volatile("prefetch.global.L1 [%0];" ::"l"(g.u + r0));
+        if (EPI == EPI_R2) asm volatile("prefetch.global.L1 [%0];" ::"l"(g.rs2 + r0));
+      }
+    };
+    pf_rows(0);
+#else
     float u_next = row_u(0), rs2_next = row_rs2(0);
+#endif
     int n_st = 0;  // TMA stores issued by this warp
     for (int t = 0; t < n_my; ++t) {
       const int a = t % p.n_acc;
       const uint32_t acph = (uint32_t)(t / p.n_acc) & 1u;
+#if ALG_TC_ROWPF
+      const float ur = row_u(t), e2_row = row_rs2(t);
+      pf_rows(t + 1);
+#else
       const float ur = u_next, e2_row = rs2_next;
       u_next = row_u(t + 1);
       rs2_next = row_rs2(t + 1);
+#endif
       const int64_t row0 = (int64_t)mt(t) * ROWS + q * 32;
       // the row-dot's read-modify-write target (and 1/u) of this warp's 32 rows (one 128-B line
       // each): warmed in L2 now, so the tile's last step is not a dependent DRAM round trip
@@ -481,14 +506,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       mbar_wait(acc_full + a, acph);
       tc_fence_after();
-      const int64_t r = row0 + lane;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * p.acc_cols);
       float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // row-dot partials, rows (lane>>3)+4i
       float dsum = 0.f;  // dot_x: this thread's row-dot
       for (int c0 = 0; c0 < p.N_t; c0 += 32) {
         float v[32], out[32], xin[32];
         float4 dq[8];
-        if (g.dotv != nullptr && !dotx) {  // row-dot operand, coalesced like the stores; in flight during the waits
+        if (!kDotX && g.dotv != nullptr) {  // row-dot operand, coalesced like the stores; in flight during the waits
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int64_t rr = row0 + (lane >> 3) + 4 * i;
@@ -570,7 +594,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (lane == 0) mbar_arrive(x_empty + xs);
           if (++xs == X_STAGES) xs = 0, xph ^= 1;
         }
-        if (g.dotv != nullptr && !p.tma_store && !dotx) {
+        if (!kDotX && g.dotv != nullptr && !p.tma_store) {
           scatter_rows_dot(buf, g.C + col, g.N, row0, g.M, lane, out, nc, dq, acc8);
         } else if (p.tma_store) {  // [32 rows x 32 cols] boxes through this warp's two SMEM slots
           if (want_aux) {  // C and aux in one group; wait until the previous group has read both slots
@@ -619,7 +643,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               else tma_store_2d(&mapC, (int)col, (int)row0, tb);
               bulk_commit();
             }
-            if (g.dotv != nullptr && !dotx) {  // fused row-dot on the transposed (coalesced) view of the slot
+            if (!kDotX && g.dotv != nullptr) {  // fused row-dot on the transposed (coalesced) view of the slot
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 const float4 o4 = *tile_at(tb, (lane >> 3) + 4 * i, lane & 7);
@@ -636,7 +660,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       if (g.dotv != nullptr) {  // reduce the 8 lanes of each row; lane (lane & 7) == i writes row (lane>>3)+4i
         float mine = dsum;
-        if (!dotx) {
+        if constexpr (!kDotX) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             float t8 = acc8[i];
@@ -646,7 +670,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if ((lane & 7) == i) mine = t8;
           }
         }
-        const int64_t rr = dotx ? row0 + lane : row0 + (lane >> 3) + 4 * (lane & 7);
+        const int64_t rr = kDotX ? row0 + lane : row0 + (lane >> 3) + 4 * (lane & 7);
         if (rr < g.M) {
           if (p.n_tiles_total > 1) g.dot_part[rr * p.n_tiles_total + tile] = mine;  // summed by k_dot_parts
           else {
@@ -825,13 +849,9 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   const CUtensorMap mA2 = g.A2 ? make_map(g.A2, g.M, g.K - g.K1, g.lda2) : mA;
   const size_t w_bytes = w.tile_bytes;
   const size_t w_round = (w_bytes + 1023) & ~(size_t)1023;
-  // EPI_R2 has no [M][N] input: its X ring carries the row-dot operand instead (A/B ALLEGRO_TC_DOTX=0:
-  // per-lane global loads of the operand, transposed sums)
-  static const bool dotx_on = [] {
-    const char* e = std::getenv("ALLEGRO_TC_DOTX");
-    return !e || std::atoi(e) != 0;
-  }();
-  const bool dot_x = dotx_on && g.epi == EPI_R2 && g.dotv != nullptr && g.N % 32 == 0;
+  // EPI_R2 has no [M][N] input: its X ring carries the row-dot operand instead (thread = row sums)
+  const bool dot_x = g.epi == EPI_R2 && g.dotv != nullptr;
+  if (dot_x && g.N % 32 != 0) throw CudaError("tc_gemm: EPI_R2 row-dot needs N % 32 == 0");
   const bool has_x = g.epi == EPI_RESID || g.epi == EPI_URESID || g.epi == EPI_ADDX || g.epi == EPI_DSILU ||
                      g.epi == EPI_ACC || g.epi == EPI_ACCX || dot_x;
   const bool aux_epi0 = g.aux && (g.epi == EPI_SILU || g.epi == EPI_UMUL_SAVE || g.epi == EPI_RESID);
