@@ -15,6 +15,7 @@
 //   Row order: by centre, then (gid_j, nx, ny, nz) ascending.
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 
 #include "ctx.cuh"
 
@@ -416,8 +417,18 @@ void build_neighbors(allegro_ctx* c) {
     c->key_pad.reserve((size_t)n * c->max_nb);
     ALG_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int), st));
     const size_t smem = (size_t)kEdgeWarps * c->max_nb * (sizeof(unsigned long long) + sizeof(int32_t));
-    if (smem > 48 * 1024)
-      ALG_CUDA(cudaFuncSetAttribute(k_edge_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024) {  // the attribute is per device: set once to the limit (the launch passes its own size)
+      int dev = 0;
+      ALG_CUDA(cudaGetDevice(&dev));
+      if (dev < 0 || dev >= 64) throw CudaError("device ordinal out of range");
+      static bool attr[64] = {};
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lk(mu);
+      if (!attr[dev]) {
+        ALG_CUDA(cudaFuncSetAttribute(k_edge_build, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr[dev] = true;
+      }
+    }
     if (n > 0) {
       {
         ProfScope ps_(&c->prof, st, PK_EDGE, 0, 28.0 * n);
