@@ -342,6 +342,17 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(t.item())
     value = s.n * args.steps / (ms_max / 1e3)  # s.n = atoms of the whole (replicated) box
+    ranks = None
+    if ws > 1:  # per-rank view of the same timed region: the max above is set by the slowest device
+        ksum = sum(v[0] for v in prof.values()) / n_prof  # this rank's own kernel time per profiled step
+        mine = torch.tensor([ms / args.steps, ms_prof_span, float((clk or {}).get("sm_mhz") or 0.0), ksum],
+                            device="cuda", dtype=torch.float64)
+        allr = [torch.zeros_like(mine) for _ in range(ws)]
+        torch.distributed.all_gather(allr, mine)
+        ranks = {"ms_per_step": [round(float(x[0]), 3) for x in allr],
+                 "profiled_step_span_ms": [round(float(x[1]), 3) for x in allr],
+                 "sm_mhz": [round(float(x[2]), 1) for x in allr],
+                 "kernel_ms_per_step": [round(float(x[3]), 3) for x in allr]}
 
     # ---- e2e: the SAME K steps (same start state) through md_step_host, state in pinned host memory ----
     m.md_set_state(s.species, pos_w, vel_w)
@@ -457,6 +468,7 @@ def main():
         "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "same_steps_as_value": e2e_same},
         "clocks": clk,
+        "ranks": ranks,
         "md": {"e_pot": rep.e_pot, "e_kin": rep.e_kin, "temperature": rep.temperature,
                "n_outliers_last": rep.n_outliers_last},
     }
