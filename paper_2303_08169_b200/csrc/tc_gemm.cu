@@ -318,11 +318,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   // sibling CTAs (one per N-tile) walk the same M-tiles in step, so A is read from HBM once; a CTA
   // PAIR (cluster of 2) instead walks M-tile pairs: CTA r takes M-tile 2 u + r of pair-unit u and
-  // holds W's N-half r, the pair's M = 256 MMAs produce all N_t columns of both CTAs' rows
-  const int tile = PAIR ? (int)crank : p.tile_base + (int)blockIdx.x % p.n_tiles;
-  const int grp = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x / p.n_tiles;
-  const int n_grp = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x / p.n_tiles;
-  const int col0 = PAIR ? 0 : tile * p.N_t;
+  // holds the N-half r of its pair tile, the pair's M = 256 MMAs produce all N_t columns of both
+  // CTAs' rows.  With more than one pair tile (p.n_tiles of them, N_t columns each; l = 2's merged
+  // x-bar, whose W image leaves room for 32-column halves only) sibling pairs share the M-tiles.
+  const int pu = (int)blockIdx.x / 2;                 // PAIR: cluster index
+  const int pt = PAIR ? pu % p.n_tiles : 0;           // PAIR: pair tile
+  const int tile = PAIR ? 2 * pt + (int)crank : p.tile_base + (int)blockIdx.x % p.n_tiles;  // W image
+  const int grp = PAIR ? pu / p.n_tiles : (int)blockIdx.x / p.n_tiles;
+  const int n_grp = PAIR ? (int)gridDim.x / 2 / p.n_tiles : (int)gridDim.x / p.n_tiles;
+  const int col0 = PAIR ? pt * p.N_t : tile * p.N_t;
+  const int dtile = PAIR ? pt : tile;                 // this CTA's column block of the row-dot partials
   const float* wimg_g = p.wimg + (size_t)tile * p.tile_floats;
   const int n_units = PAIR ? (p.n_mtiles + 1) / 2 : p.n_mtiles;
   const int n_my = n_units > grp ? (n_units - 1 - grp) / n_grp + 1 : 0;
@@ -672,7 +677,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         const int64_t rr = kDotX ? row0 + lane : row0 + (lane >> 3) + 4 * (lane & 7);
         if (rr < g.M) {
-          if (p.n_tiles_total > 1) g.dot_part[rr * p.n_tiles_total + tile] = mine;  // summed by k_dot_parts
+          if (p.n_tiles_total > 1) g.dot_part[rr * p.n_tiles_total + dtile] = mine;  // summed by k_dot_parts
           else {
             if (g.dot_inv_u) {  // x^0 = u m: <x-bar^0, m> from <x-bar^0, x^0> (u = 0: u' = 0 there too)
               const float ur = g.dot_inv_u[rr];
@@ -886,8 +891,15 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
     const char* e = std::getenv("ALLEGRO_TC_PAIR");
     return !e || std::atoi(e) != 0;
   }();
-  const bool pair = pair_on && w.n_tiles == 2 && (g.epi == EPI_RESID || g.epi == EPI_ACCX) && !g.single_pass &&
-                    g_tc_tuning.diag == 0 && (w.N_t * 2) % 32 == 0;
+  // (more than two N-tiles: sibling pairs, ALLEGRO_TC_PAIR_MULTI=0 keeps those on single CTAs)
+  static const bool pair_multi = [] {
+    const char* e = std::getenv("ALLEGRO_TC_PAIR_MULTI");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool pair = pair_on && (w.n_tiles == 2 || (pair_multi && w.n_tiles % 2 == 0)) &&
+                    (g.epi == EPI_RESID || g.epi == EPI_ACCX) && !g.single_pass && g_tc_tuning.diag == 0 &&
+                    (w.N_t * 2) % 32 == 0;
+  const int n_pt = pair ? w.n_tiles / 2 : 1;  // pair tiles
   TcParams p;
   p.g = g;
   p.N_t = pair ? 2 * w.N_t : w.N_t;
@@ -929,7 +941,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
   p.out_slots = out_slots;
   const CUtensorMap mC = p.tma_store ? make_map(g.C, g.M, g.N, g.N, 32) : mA;
   const CUtensorMap mAux = (p.tma_store && aux_epi) ? make_map(g.aux, g.M, g.N, g.N, 32) : mA;
-  if (g.dotv && w.n_tiles != 1 && !pair && !g.dot_part)
+  if (g.dotv && (pair ? n_pt : w.n_tiles) != 1 && !g.dot_part)
     throw CudaError("tc_gemm: a row-dot over N-tiles needs dot_part");
   // one launch; CTA b handles N-tile b % n_tiles of M-tile group b / n_tiles
   // (ALLEGRO_TC_COSCHED=0: one launch per N-tile, for A/B measurements)
@@ -938,13 +950,13 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
     return !e || std::atoi(e) != 0;
   }();
   const int per_launch = pair ? w.n_tiles : (cosched ? w.n_tiles : 1);
-  const int groups = pair ? std::max(1, std::min((p.n_mtiles + 1) / 2, g_num_sms[dev] / 2))
+  const int groups = pair ? std::max(1, std::min((p.n_mtiles + 1) / 2, g_num_sms[dev] / (2 * n_pt)))
                           : std::max(1, std::min(p.n_mtiles, g_num_sms[dev] / per_launch));
-  const int grid = groups * (pair ? 2 : per_launch);
+  const int grid = groups * (pair ? 2 * n_pt : per_launch);
   const double mn = (double)g.M * g.N;
   const int n_io = 1 + (g.aux != nullptr) + (g.X != nullptr) + (g.epi == EPI_ACC);
-  p.n_tiles = pair ? 1 : per_launch;
-  p.n_tiles_total = pair ? 1 : w.n_tiles;  // a pair's row-dot covers all N columns: no partials
+  p.n_tiles = pair ? n_pt : per_launch;
+  p.n_tiles_total = pair ? n_pt : w.n_tiles;  // one pair tile's row-dot covers all N columns: no partials
   p.wimg = w.dev;
   p.tile_floats = w.tile_bytes / 4;
   for (int tb = 0; tb < w.n_tiles; tb += per_launch) {
@@ -982,9 +994,10 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
     }
     ALG_LAUNCH_CHECK();
   }
-  if (g.dotv && w.n_tiles > 1 && !pair) {  // dot_out[r] += coef (partial_0 + partial_1 + ...), fixed order
-    ProfScope ps(prof, st, PK_ROWDOT, (double)g.M * w.n_tiles, 4.0 * (double)g.M * (w.n_tiles + 2));
-    k_dot_parts<<<ceil_div(g.M, 256), 256, 0, st>>>(g.M, w.n_tiles, g.dot_part, g.dot_coef, g.dot_inv_u, g.dot_out);
+  if (g.dotv && p.n_tiles_total > 1) {  // dot_out[r] += coef (partial_0 + partial_1 + ...), fixed order
+    const int nt = p.n_tiles_total;
+    ProfScope ps(prof, st, PK_ROWDOT, (double)g.M * nt, 4.0 * (double)g.M * (nt + 2));
+    k_dot_parts<<<ceil_div(g.M, 256), 256, 0, st>>>(g.M, nt, g.dot_part, g.dot_coef, g.dot_inv_u, g.dot_out);
     ALG_LAUNCH_CHECK();
   }
 }
