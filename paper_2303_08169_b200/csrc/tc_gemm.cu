@@ -880,6 +880,7 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
 #undef ALG_SET
       ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<EPI_RESID, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
       ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<EPI_ACCX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
+      ALG_CUDA(cudaFuncSetAttribute(k_tc_gemm<EPI_STORE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
       ALG_CUDA(cudaDeviceGetAttribute(&g_num_sms[dev], cudaDevAttrMultiProcessorCount, dev));
       g_attr_set[dev] = true;
     }
@@ -896,8 +897,13 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
     const char* e = std::getenv("ALLEGRO_TC_PAIR_MULTI");
     return !e || std::atoi(e) != 0;
   }();
+  static const bool pair_store = [] {  // plain stores split over N-tiles (l = 2's env contraction); A/B
+    const char* e = std::getenv("ALLEGRO_TC_PAIR_STORE");
+    return !e || std::atoi(e) != 0;
+  }();
   const bool pair = pair_on && (w.n_tiles == 2 || (pair_multi && w.n_tiles % 2 == 0)) &&
-                    (g.epi == EPI_RESID || g.epi == EPI_ACCX) && !g.single_pass && g_tc_tuning.diag == 0 &&
+                    (g.epi == EPI_RESID || g.epi == EPI_ACCX || (g.epi == EPI_STORE && pair_store)) && !g.single_pass &&
+                    g_tc_tuning.diag == 0 &&
                     (w.N_t * 2) % 32 == 0;
   const int n_pt = pair ? w.n_tiles / 2 : 1;  // pair tiles
   TcParams p;
@@ -980,7 +986,8 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
       cfg.attrs = at;
       cfg.numAttrs = 1;
       if (g.epi == EPI_RESID) ALG_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<EPI_RESID, 1>, mA, mA2, mX, mC, mAux, p));
-      else ALG_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<EPI_ACCX, 1>, mA, mA2, mX, mC, mAux, p));
+      else if (g.epi == EPI_ACCX) ALG_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<EPI_ACCX, 1>, mA, mA2, mX, mC, mAux, p));
+      else ALG_CUDA(cudaLaunchKernelEx(&cfg, k_tc_gemm<EPI_STORE, 1>, mA, mA2, mX, mC, mAux, p));
       ALG_LAUNCH_CHECK();
       break;
     }
