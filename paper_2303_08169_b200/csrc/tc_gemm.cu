@@ -632,10 +632,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               }
               bulk_commit();
             }
-          } else {  // double-buffered: the slot of chunk n_st - 2 must have been read
-            unsigned char* tb = out_stage + (size_t)(p.out_slots * q + (n_st & 1)) * STAGE_OUT_BYTES;
-            if (n_st >= 2) {
-              if (lane == 0) bulk_wait_read1();
+          } else {  // double- (or quad-) buffered: the slot of chunk n_st - out_slots must have been read
+            unsigned char* tb =
+                out_stage + (size_t)(p.out_slots * q + (n_st & (p.out_slots - 1))) * STAGE_OUT_BYTES;
+            if (n_st >= p.out_slots) {
+              if (lane == 0) {
+                if (p.out_slots == 4) bulk_wait_read3();
+                else bulk_wait_read1();
+              }
               __syncwarp();
             }
 #pragma unroll
@@ -865,7 +869,14 @@ void tc_gemm(const GemmArgs& g, const TcWeight& w, cudaStream_t st, Profiler* pr
     const char* e = std::getenv("ALLEGRO_TC_OUTSLOTS");
     return e ? std::atoi(e) : 2;
   }();
-  const int out_slots = (aux_epi0 && outslots_env == 4) ? 4 : 2;
+  // store-heavy contractions (N >= 2 K: l = 2's TP-linear^T, K = 32) keep four output boxes in flight
+  // per epilogue warp (A/B ALLEGRO_TC_STORE4=0)
+  static const bool store4_on = [] {
+    const char* e = std::getenv("ALLEGRO_TC_STORE4");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool store4 = store4_on && !aux_epi0 && g.dotv == nullptr && g.N >= 2 * g.K;
+  const int out_slots = ((aux_epi0 && outslots_env == 4) || store4) ? 4 : 2;
   const size_t out_bytes = 4 * (size_t)out_slots * STAGE_OUT_BYTES + (has_x ? (size_t)X_STAGES * X_STAGE_BYTES : 0);
   int stages = (int)((SMEM_LIMIT - SMEM_RESERVE - w_round - out_bytes) / STAGE_BYTES);
   stages = std::min(stages, g_tc_tuning.max_stages);
