@@ -4,7 +4,8 @@ of the C2 evaluation agrees with the oracle within D20 and with the default buil
 Each variant runs in its own process because the library reads the switches once:
 ALLEGRO_TC_TMASTORE=0 (STG-scatter epilogue instead of TMA stores), ALLEGRO_FUSE_R2=0 and
 ALLEGRO_FUSE_ROWDOT=0 (standalone row-dot passes), ALLEGRO_TC_STOREHINT=1 (L2 policy on the
-stores), ALLEGRO_TC_PAIR_MULTI=0 / ALLEGRO_TC_PAIR_STORE=0 (single-CTA N-tiles instead of CTA pairs).  Switches that change only where bytes go are bit-identical to the default; the row-dot
+stores), ALLEGRO_TC_PAIR_MULTI=0 / ALLEGRO_TC_PAIR_STORE=0 (single-CTA N-tiles instead of CTA pairs),
+ALLEGRO_TC_STORE4=0 (two output slots per epilogue warp).  Switches that change only where bytes go are bit-identical to the default; the row-dot
 switches change a summation order (tolerance)."""
 import json
 import os
@@ -63,6 +64,7 @@ def reference():
     # partials are summed in a different grouping: tolerance), and the paired plain store
     ("pair_multi0", {"ALLEGRO_TC_PAIR_MULTI": "0"}, False),
     ("pair_store0", {"ALLEGRO_TC_PAIR_STORE": "0"}, True),
+    ("store4_0", {"ALLEGRO_TC_STORE4": "0"}, True),
 ])
 def test_switch_variants(reference, tmp_path, name, env, bitwise):
     s, ref = reference
