@@ -577,7 +577,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] += v2[j];
         }
-        if (p.diag & 2) continue;
+        if (p.diag & 2) {  // diagnostics (no stores): still release the row-dot operand's ring slot
+          if (dotx) {
+            mbar_wait(x_full + xs, xph);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(x_empty + xs);
+            if (++xs == X_STAGES) xs = 0, xph ^= 1;
+          }
+          continue;
+        }
         const int64_t col = col0 + c0;
         const int nc = (p.N_t - c0) >= 32 ? 8 : (p.N_t - c0) / 4;
         epi_apply<32, EPI>(g, v, xin, ur, out);
